@@ -1,0 +1,149 @@
+"""c2 — remap / alloc / free block allocator (oracle). TEST INFRASTRUCTURE ONLY.
+
+Follows PAPER.md:306-308 (Remapping Controller "reclaims a portion of the
+parameter memory to expand KV cache capacity"), :492 ("marks the GPU memory
+previously occupied by parameters as available for KV cache"), :558-564 §6
+("Once parameter tensors are released, the KV cache engine can immediately
+reuse the freed physical memory"), Alg. 1 :509/:529-531, and PagedAttention's
+block tables. Unstated details follow SURVEY.md §8(c) c2 and
+readings #1, #11-#15 (listed in DESIGN.md):
+
+* per recipient model r: native ids [0, N0); reclaimed ids appended
+  monotonically (next_id), runs ascending, never reused;
+* remap(d, r, C, beta): R = sorted(C[beta:]) split into maximal runs of
+  consecutive layer ids; each run of |run| * S_d bytes yields floor(len / BB_r)
+  blocks at byte offsets first*S_d + i*BB_r of the donor's weight arena;
+* alloc(r, seq, n): the n lowest free ids, ascending, all-or-nothing;
+* free(r, seq): return all of seq's blocks; unknown seq -> DoubleFree.
+
+Pins: worked examples (toy layer -> 48 blocks; SPEC 2 GB / 16 MB -> 128),
+invariants I1-I4 and an exhaustive comparison against an independent set-based
+model in tests/test_oracle_allocator.py.
+"""
+
+RESIDENT, SLOT, RECLAIMED = 0, 1, 2
+
+
+class StateError(RuntimeError):
+    pass
+
+
+class RangeError(ValueError):
+    pass
+
+
+class NoBlocks(RuntimeError):
+    def __init__(self, shortfall):
+        super().__init__(f"shortfall {shortfall}")
+        self.shortfall = shortfall
+
+
+class DoubleFree(RuntimeError):
+    pass
+
+
+class Model:
+    def __init__(self, n_layers, layer_bytes, block_bytes, n_native):
+        self.n_layers = n_layers
+        self.S = layer_bytes
+        self.BB = block_bytes
+        self.n_native = n_native
+        self.next_id = n_native
+        self.free = set(range(n_native))
+        self.tables = {}
+        self.layer_state = [RESIDENT] * n_layers
+        self.cycle = []
+        self.beta = 0
+        self.reclaimed_bytes = 0          # bytes of R carved into this model's pool
+        self.donated_bytes = 0            # bytes of this model's layers reclaimed
+        self.block_loc = {i: ("native", i * block_bytes) for i in range(n_native)}
+        self.regions = []                 # (donor, first_layer, n_layers, first_id, n_blocks)
+        self.active = True
+
+
+class Allocator:
+    def __init__(self):
+        self.models = []
+
+    def add_model(self, n_layers, layer_bytes, block_bytes, n_native):
+        self.models.append(Model(n_layers, layer_bytes, block_bytes, n_native))
+        return len(self.models) - 1
+
+    def set_active(self, model, active):
+        self.models[model].active = bool(active)
+
+    def remap(self, donor, recipient, C, beta):
+        """Returns the number of blocks added to the recipient's pool."""
+        if not (0 <= donor < len(self.models) and 0 <= recipient < len(self.models)):
+            raise RangeError("model id")
+        d, r = self.models[donor], self.models[recipient]
+        m = len(C)
+        if not (0 <= beta <= m) or any(not (0 <= l < d.n_layers) for l in C):
+            raise RangeError("cycle")
+        if len(set(C)) != m or list(C) != sorted(C):
+            raise RangeError("cycle must be strictly ascending")
+        if any(d.layer_state[l] != RESIDENT for l in C):
+            raise StateError("layer already cycled or reclaimed")
+        if beta == 0 and d.active:
+            raise StateError("beta=0 needs an inactive donor")
+        if beta > 0 and donor != recipient:
+            raise StateError("streaming remap must be a self-remap")
+        if beta > 0 and d.cycle:
+            raise StateError("donor already has a cycle")
+        R = sorted(C[beta:])
+        gained = 0
+        runs = []
+        for l in R:
+            if runs and runs[-1][-1] == l - 1:
+                runs[-1].append(l)
+            else:
+                runs.append([l])
+        for run in runs:
+            off = run[0] * d.S
+            length = len(run) * d.S
+            k = length // r.BB
+            first = r.next_id
+            for i in range(k):
+                bid = r.next_id
+                r.next_id += 1
+                r.free.add(bid)
+                r.block_loc[bid] = (donor, off + i * r.BB)
+            r.regions.append((donor, run[0], len(run), first, k))
+            gained += k
+        r.reclaimed_bytes += len(R) * d.S
+        d.donated_bytes += len(R) * d.S
+        for l in C[:beta]:
+            d.layer_state[l] = SLOT
+        for l in R:
+            d.layer_state[l] = RECLAIMED
+        if beta > 0:
+            d.cycle = list(C)
+            d.beta = beta
+        return gained
+
+    def alloc(self, model, seq, n):
+        r = self.models[model]
+        if n < 0:
+            raise RangeError("n")
+        if n > len(r.free):
+            raise NoBlocks(n - len(r.free))
+        ids = sorted(r.free)[:n]
+        for i in ids:
+            r.free.remove(i)
+        r.tables.setdefault(seq, []).extend(ids)
+        return ids
+
+    def free_seq(self, model, seq):
+        r = self.models[model]
+        if seq not in r.tables:
+            raise DoubleFree(f"seq {seq}")
+        r.free.update(r.tables.pop(seq))
+
+    def table(self, model, seq):
+        return list(self.models[model].tables[seq])
+
+    def n_free(self, model):
+        return len(self.models[model].free)
+
+    def n_total(self, model):
+        return self.models[model].next_id

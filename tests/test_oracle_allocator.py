@@ -1,0 +1,212 @@
+"""Pins for oracle c2 (allocator): worked examples, invariants I1-I4, and an
+exhaustive comparison against an independent set-based model. CPU only."""
+import itertools
+import json
+import os
+import random
+
+import pytest
+
+from oracle import allocator as A
+from synth import models, weights
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
+
+
+def bb(m, block_tokens=16):
+    return m.n_layers * m.n_kv_heads * 2 * block_tokens * m.head_dim * 2
+
+
+def test_toy_layer_gives_48_blocks():
+    m = models.TOY
+    S, BB = weights.layer_bytes(m), bb(m)
+    assert (S, BB) == (1579520, 32768)
+    al = A.Allocator()
+    t = al.add_model(2, S, BB, 32)
+    assert al.remap(t, t, [0, 1], 1) == 48
+    assert al.n_total(t) == 80
+    assert sorted(al.models[t].free) == list(range(80))
+    assert al.models[t].block_loc[32] == (0, 1 * S)
+    assert al.models[t].block_loc[79] == (0, S + 47 * BB)
+    assert al.models[t].reclaimed_bytes == S
+
+
+def test_opt13b_layer_and_llama_donor():
+    o, l = models.OPT_13B, models.LLAMA2_7B
+    assert weights.layer_bytes(o) // bb(o) == 48
+    al = A.Allocator()
+    r = al.add_model(40, weights.layer_bytes(o), bb(o), 604)
+    d = al.add_model(32, weights.layer_bytes(l), bb(l), 0)
+    al.set_active(d, False)
+    got = al.remap(d, r, list(range(32)), 0)
+    assert got == 988                     # coalesced run
+    assert 32 * (weights.layer_bytes(l) // bb(o)) == 960   # per-layer carving would give 960
+    assert al.models[r].reclaimed_bytes == 32 * weights.layer_bytes(l)
+
+
+def test_spec_examples():
+    # SPEC.md:201-202 2 GB reclaimed / 16 MB blocks -> 128 blocks
+    al = A.Allocator()
+    r = al.add_model(1, 1, 16 << 20, 0)
+    d = al.add_model(1, 2 << 30, 16 << 20, 0)
+    al.set_active(d, False)
+    assert al.remap(d, r, [0], 0) == 128
+    with pytest.raises(A.StateError):      # apply twice -> StateError
+        al.remap(d, r, [0], 0)
+    al.alloc(r, 7, 1)
+    al.free_seq(r, 7)
+    with pytest.raises(A.DoubleFree):
+        al.free_seq(r, 7)
+
+
+def test_capacity_arithmetic_paper():
+    ex = GOLD["capacity_h100"]
+    ratio = (ex["kv_gb"] + ex["params_gb"] * ex["fraction_num"] / ex["fraction_den"]) / ex["kv_gb"]
+    assert abs(ratio - ex["ratio"]) < 1e-3
+    assert ex["params_gb"] + ex["kv_gb"] == 80
+
+
+def test_shortfall_is_data_state_unchanged():
+    al = A.Allocator()
+    r = al.add_model(2, 1000, 100, 4)
+    al.alloc(r, 1, 3)
+    with pytest.raises(A.NoBlocks) as e:
+        al.alloc(r, 2, 2)
+    assert e.value.shortfall == 1
+    assert al.n_free(r) == 1 and 2 not in al.models[r].tables
+
+
+def test_errors():
+    al = A.Allocator()
+    r = al.add_model(4, 1000, 100, 4)
+    with pytest.raises(A.StateError):
+        al.remap(r, r, [0, 1], 0)          # active donor with beta=0
+    with pytest.raises(A.RangeError):
+        al.remap(r, r, [2, 1], 1)          # not ascending
+    with pytest.raises(A.RangeError):
+        al.remap(r, r, [0, 9], 1)
+    assert al.remap(r, r, [0, 2], 1) == 10
+    with pytest.raises(A.StateError):
+        al.remap(r, r, [1, 3], 1)          # second cycle
+    with pytest.raises(A.StateError):
+        al.remap(r, r, [2, 3], 1)          # already reclaimed
+
+
+class SetModel:
+    """Independent model of the same rules: ids are assigned by counting, free ids
+    kept as a plain list re-sorted on every alloc, blocks per remap computed from
+    total contiguous byte spans."""
+
+    def __init__(self, n_native, S, BB):
+        self.ids = list(range(n_native))
+        self.owner = {i: None for i in self.ids}
+        self.S, self.BB = S, BB
+        self.reclaimed = set()
+
+    def remap(self, layers):
+        layers = sorted(layers)
+        spans, cur = [], None
+        for l in layers:
+            if cur and cur[1] == l:
+                cur[1] = l + 1
+            else:
+                cur = [l, l + 1]
+                spans.append(cur)
+        for a, b in spans:
+            for _ in range((b - a) * self.S // self.BB):
+                nid = len(self.owner)
+                self.owner[nid] = None
+        self.reclaimed |= set(layers)
+
+    def alloc(self, seq, n):
+        free = [i for i in sorted(self.owner) if self.owner[i] is None]
+        if n > len(free):
+            return None, n - len(free)
+        for i in free[:n]:
+            self.owner[i] = seq
+        return free[:n], 0
+
+    def free(self, seq):
+        mine = [i for i, o in self.owner.items() if o == seq]
+        if not mine and seq not in getattr(self, "live", set()):
+            return False
+        for i in mine:
+            self.owner[i] = None
+        return True
+
+
+def check_invariants(al, r):
+    M = al.models[r]
+    live = set(range(M.next_id))
+    used = [i for t in M.tables.values() for i in t]
+    assert len(used) == len(set(used))                # no double allocation
+    assert M.free.isdisjoint(used)
+    assert M.free | set(used) == live                 # no loss
+
+
+def test_random_ops_vs_set_model():
+    rng = random.Random(1)
+    for trial in range(300):
+        n_layers, S, BB, N0 = 6, rng.choice([250, 300, 512]), 100, rng.randint(0, 6)
+        al = A.Allocator()
+        r = al.add_model(n_layers, S, BB, N0)
+        ref = SetModel(N0, S, BB)
+        live = set()
+        ref.live = live
+        remapped = set()
+        for op in range(20):
+            c = rng.random()
+            if c < 0.15 and len(remapped) < n_layers - 1:
+                cand = [l for l in range(n_layers) if l not in remapped]
+                C = sorted(rng.sample(cand, rng.randint(1, min(3, len(cand)))))
+                if al.models[r].cycle:
+                    continue
+                al.set_active(r, False)
+                al.remap(r, r, C, 0)
+                ref.remap(C)
+                remapped |= set(C)
+            elif c < 0.6:
+                seq, n = rng.randint(0, 4), rng.randint(0, 4)
+                try:
+                    got = al.alloc(r, seq, n)
+                    short = 0
+                except A.NoBlocks as e:
+                    got, short = None, e.shortfall
+                exp, eshort = ref.alloc(seq, n)
+                assert got == exp and short == eshort
+                if got is not None:
+                    live.add(seq)
+            else:
+                seq = rng.randint(0, 4)
+                try:
+                    al.free_seq(r, seq)
+                    ok = True
+                except A.DoubleFree:
+                    ok = False
+                assert ok == (seq in live)
+                if ok:
+                    ref.free(seq)
+                    live.discard(seq)
+            check_invariants(al, r)
+        assert al.n_total(r) == len(ref.owner)
+
+
+def test_bytes_invariants():
+    # I2: reclaimed bytes == |R| * S; I3: blocks per run = floor(len/BB), waste < BB;
+    # I4: resident + slot + reclaimed bytes == n * S
+    for C, beta in [([0, 3, 6], 1), ([1, 2, 3, 7], 2), ([4], 1), ([0, 1, 2, 3, 4, 5, 6, 7], 1)]:
+        al = A.Allocator()
+        S, BB = 1000, 256
+        r = al.add_model(8, S, BB, 2)
+        got = al.remap(r, r, C, beta)
+        R = C[beta:]
+        assert al.models[r].reclaimed_bytes == len(R) * S
+        runs = [list(g) for _, g in itertools.groupby(enumerate(R), lambda t: t[1] - t[0])]
+        assert got == sum(len(run) * S // BB for run in runs)
+        st = al.models[r].layer_state
+        assert sum(S for s in st if s == A.RESIDENT) + sum(S for s in st if s == A.SLOT) + \
+            sum(S for s in st if s == A.RECLAIMED) == 8 * S
+        for bid, (donor, off) in al.models[r].block_loc.items():
+            if donor != "native":
+                l0 = off // S
+                assert st[l0] == A.RECLAIMED and (off + BB - 1) // S in R
