@@ -1,0 +1,267 @@
+/*
+ * mirage.h — C-ABI of the B200-native MIRAGE decode-step hot path
+ * (arXiv 2507.11507, "MIRAGE: ... Dynamic Remapping Engine", PAPER.md in the
+ * reference tree; SURVEY.md §8(b) is the interface contract).
+ *
+ * What the library does (PAPER.md:297-329 §4, :552-564 §6):
+ *   - parameter bytes of chosen layers (or of an inactive tenant's whole model)
+ *     are reclaimed as paged KV-cache blocks       (mirage_remap_layers)
+ *   - per-sequence block tables over one id space that spans the native pool
+ *     and the reclaimed regions                     (mirage_alloc/free_blocks)
+ *   - a decode step whose paged-attention kernel reads through that table and
+ *     whose cycled layers' weights are re-streamed one-way from pinned host
+ *     memory, one layer ahead of use, gated by events (mirage_decode_step)
+ *
+ * Conventions (all functions):
+ *   - extern "C", fixed-width types, no C++ or torch types.
+ *   - Every call returns int32_t status: MIRAGE_OK (0) or a negative code.
+ *     Nothing throws across the ABI. mirage_last_error() gives the message.
+ *   - One mirage_ctx per GPU per process; a ctx is NOT thread-safe.
+ *   - Device work is enqueued on the caller's compute stream and the call
+ *     returns before it finishes. Host metadata (allocator, tables, remap sets,
+ *     slot log) is updated synchronously and deterministically at call time.
+ *   - Ownership: the caller owns and must keep alive, for the ctx's lifetime,
+ *     the device arena, every host weight blob and the compute stream. The
+ *     library owns its metadata, events, the copy stream (unless supplied), the
+ *     cuBLAS handle, pinned staging buffers and everything it carves from the
+ *     arena.
+ *   - Sticky failure: a CUDA error puts the ctx in a failed state; every later
+ *     call returns MIRAGE_ERR_CUDA until mirage_destroy.
+ *   - There is no CPU fallback: every step of the decode path runs in this
+ *     library's sm_100a kernels (GEMMs via cuBLAS).
+ */
+#ifndef MIRAGE_H_
+#define MIRAGE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (SPEC.md error vocabulary) ------------ */
+#define MIRAGE_OK 0
+#define MIRAGE_ERR_CONFIG -1      /* bad configuration (SPEC ConfigError)              */
+#define MIRAGE_ERR_CAPACITY -2    /* arena too small (SPEC CapacityError)              */
+#define MIRAGE_ERR_RANGE -3       /* argument out of range (SPEC RangeError)           */
+#define MIRAGE_ERR_STATE -4       /* illegal in current state (SPEC StateError)        */
+#define MIRAGE_ERR_NO_BLOCKS -5   /* not enough free blocks; shortfall is data         */
+#define MIRAGE_ERR_DOUBLE_FREE -6 /* free of an unknown / already freed sequence       */
+#define MIRAGE_ERR_INFEASIBLE -7  /* no zero-stall plan (SPEC InfeasibleAlpha)         */
+#define MIRAGE_ERR_PRESSURE -8    /* reserved: unremap with live blocks (NEXT-1)       */
+#define MIRAGE_ERR_CUDA -9        /* CUDA / cuBLAS failure (sticky)                     */
+#define MIRAGE_ERR_NCCL -10       /* reserved: NCCL failure (sticky)                    */
+
+/* ---- families and flags -------------------------------------------------- */
+#define MIRAGE_FAMILY_OPT 0   /* pre-LN, ReLU MLP, learned positions (+2), tied head */
+#define MIRAGE_FAMILY_LLAMA 1 /* RMSNorm, rotate-half RoPE, SiLU-gated MLP, GQA      */
+
+#define MIRAGE_BETA_1 1       /* one staging slot          (Eq. 4, :472)  */
+#define MIRAGE_BETA_2 2       /* double buffering          (Eq. 5, :478)  */
+#define MIRAGE_BETA_DYNAMIC 3 /* smallest m with zero predicted stall (reading #6) */
+
+#define MIRAGE_BLOCK_TOKENS 16
+#define MIRAGE_MAX_CYCLE 256
+
+typedef struct mirage_ctx mirage_ctx;
+
+typedef struct mirage_init_cfg {
+  int32_t device;           /* CUDA device ordinal                                  */
+  void* dev_arena;          /* caller-owned device allocation (borrowed)            */
+  uint64_t dev_arena_bytes; /* its size; everything the library needs is carved here */
+  int32_t block_tokens;     /* tokens per KV block; must be 16                      */
+  void* compute_stream;     /* cudaStream_t on which all compute is enqueued        */
+  void* copy_stream;        /* cudaStream_t for H2D re-streaming, NULL -> library's */
+  int32_t max_batch;        /* max sequences per decode step                        */
+  int32_t max_ctx;          /* max tokens per sequence                              */
+  uint32_t flags;           /* reserved, 0                                          */
+  int32_t tp_rank, tp_size; /* tensor parallel rank/size; this version: 0 / 1        */
+  void* nccl_comm;          /* reserved, NULL                                       */
+} mirage_init_cfg;
+
+typedef struct mirage_model_cfg {
+  int32_t family;     /* MIRAGE_FAMILY_*                                           */
+  int32_t n_layers;   /* hidden layers n                                           */
+  int32_t d_model;    /* d; multiple of 128                                        */
+  int32_t n_heads;    /* H                                                         */
+  int32_t n_kv_heads; /* H_kv; H % H_kv == 0, H/H_kv in {1,2,4,8}                  */
+  int32_t head_dim;   /* D in {64, 128}                                            */
+  int32_t ffn_dim;    /* multiple of 128                                           */
+  int32_t vocab;
+  int32_t max_pos;    /* OPT: learned position table has max_pos + 2 rows          */
+  float norm_eps;
+  float rope_theta;   /* Llama only                                                */
+} mirage_model_cfg;
+
+/*
+ * Weight blob layout (host, bf16, little-endian; the device copy is identical):
+ *   [layer 0][layer 1] ... [layer n-1][globals]
+ * Each layer occupies exactly S = mirage_layer_bytes bytes (a multiple of 256),
+ * tensors back to back in this order (row-major, PyTorch Linear [out, in]):
+ *   OPT  : w_qkv[3d,d] w_o[d,d] w_fc1[f,d] w_fc2[d,f] b_qkv[3d] b_o[d] b_fc1[f]
+ *          b_fc2[d] ln1_g[d] ln1_b[d] ln2_g[d] ln2_b[d]
+ *   Llama: w_qkv[(H+2H_kv)D,d] w_o[d,HD] w_gateup[2f,d] (gate rows, then up rows)
+ *          w_down[d,f] rms1_g[d] rms2_g[d]
+ *   w_qkv rows are [q heads | k heads | v heads], head h at rows h*D..h*D+D-1.
+ * Globals: OPT: embed[V,d] pos_embed[max_pos+2,d] lnf_g[d] lnf_b[d]
+ *          Llama: embed[V,d] normf_g[d] lm_head[V,d]
+ *
+ * KV block layout (device): one physical block holds 16 tokens of ALL layers:
+ *   [L][H_kv][2 (K,V)][16][D] bf16, BB = L*H_kv*2*16*D*2 bytes.
+ * Block ids [0, N0) are the native pool; reclaimed ids are appended after.
+ */
+
+/* Sizes of one model: S (one hidden layer), globals, and BB (one KV block). */
+int32_t mirage_model_sizes(const mirage_model_cfg* m, uint64_t* layer_bytes,
+                           uint64_t* global_bytes, uint64_t* block_bytes);
+
+/* Arena bytes mirage_add_model will carve for a model with n_native blocks
+ * under the given init limits (weights + native pool + workspace). */
+int32_t mirage_model_arena_bytes(const mirage_model_cfg* m, int64_t native_kv_blocks,
+                                 int32_t max_batch, int32_t max_ctx, uint64_t* bytes);
+
+/* Bind device and streams; create events, the cuBLAS handle and staging.
+ * Errors: CONFIG (block_tokens != 16, tp_size != 1, null arena/stream), CUDA. */
+int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out);
+
+/* Synchronise the compute and copy streams, release everything the library
+ * owns. Borrowed pointers are not freed. Safe on NULL. */
+void mirage_destroy(mirage_ctx* ctx);
+
+/* Message of the last failing call on this ctx ("" if none). Never NULL. */
+const char* mirage_last_error(const mirage_ctx* ctx);
+
+/* Add a tenant model. host_blob (pinned, caller-owned, must outlive ctx) holds
+ * the layout above and is copied once H2D into the arena; it stays the
+ * authoritative copy re-streamed for cycled layers (PAPER.md:555 footnote: the
+ * serving framework keeps a complete host copy of the parameters). The native
+ * KV pool gets ids [0, native_kv_blocks). Model ids are 0,1,2,... in call order.
+ * Errors: CONFIG (shape constraints, host_bytes mismatch, blob not pinned),
+ * CAPACITY (arena exhausted), CUDA. */
+int32_t mirage_add_model(mirage_ctx* ctx, const mirage_model_cfg* m, const void* host_blob,
+                         uint64_t host_bytes, int64_t native_kv_blocks, int32_t* model_id);
+
+/* Pure planner (§5.3-5.4, Eqs. 1-5). Writes the
+ * cycle C (ascending, m entries; cycle_out capacity >= n_layers), m and beta.
+ * Slot holders are C[0..beta), reclaimed layers R = C[beta..m).
+ * Errors: RANGE (bad arguments, alpha + beta > n), INFEASIBLE (dynamic policy
+ * found no zero-stall plan). */
+int32_t mirage_plan(int32_t n_layers, int32_t alpha, int32_t beta_policy,
+                    uint64_t t_transfer_ns, uint64_t t_compute_layer_ns, int32_t anchor,
+                    int32_t* cycle_out, int32_t* m_out, int32_t* beta_out);
+
+/* Reclaim the parameter memory of R = cycle[beta..m) of `donor` as KV blocks of
+ * `recipient`. R is split into maximal runs
+ * of consecutive layers; each run yields floor(run_bytes / BB_recipient) blocks
+ * at byte offsets first*S + i*BB of the donor's weights, appended to the
+ * recipient's id space and usable at once. beta > 0 (self-remap of an active
+ * model) also installs the cycle: the beta slot holders' storage becomes the
+ * staging slots through which all m cycled layers rotate (PAPER.md:411-413,
+ * :463-482); the change takes effect at the next decode step. beta == 0
+ * requires an inactive donor (its layers are never executed). Eqs. 4/5 are not
+ * enforced here (speed, not correctness). KV writes into reclaimed bytes are
+ * stream-ordered after every previously enqueued kernel that read them.
+ * Errors: RANGE (ids, cycle not strictly ascending, beta > m), STATE (layer
+ * already cycled/reclaimed, active donor with beta 0, beta > 0 with donor !=
+ * recipient or a cycle already installed), CUDA. */
+int32_t mirage_remap_layers(mirage_ctx* ctx, int32_t donor, int32_t recipient,
+                            const int32_t* cycle, int32_t m, int32_t beta,
+                            int64_t* blocks_gained, uint64_t* reclaimed_bytes);
+
+/* Mark a tenant active (1) or inactive (0) (temporal sharing).
+ * Errors: RANGE; STATE (activating a model with reclaimed layers: needs
+ * unremap, not in this version). */
+int32_t mirage_set_active(mirage_ctx* ctx, int32_t model, int32_t active);
+
+/* Allocate n blocks for seq_id: the n lowest free ids, ascending, appended to
+ * its table; all-or-nothing (reading #14). ids_out (capacity n, may be NULL).
+ * Errors: RANGE; NO_BLOCKS with *shortfall_out = n - free (state unchanged). */
+int32_t mirage_alloc_blocks(mirage_ctx* ctx, int32_t model, int64_t seq_id, int32_t n,
+                            int32_t* ids_out, int32_t* shortfall_out);
+
+/* Return all blocks of seq_id and forget the sequence (reading #15).
+ * Errors: RANGE; DOUBLE_FREE for an unknown or already freed sequence. */
+int32_t mirage_free_blocks(mirage_ctx* ctx, int32_t model, int64_t seq_id);
+
+/* Copy of the host block table of seq_id. Errors: RANGE (unknown seq, cap too
+ * small; *n_out still receives the length). */
+int32_t mirage_get_block_table(mirage_ctx* ctx, int32_t model, int64_t seq_id, int32_t* out,
+                               int32_t cap, int32_t* n_out);
+
+/* Where block `block_id` of `model` lives: donor = -1 for the native pool
+ * (offset from the pool start), else the donor model id and the byte offset
+ * from the start of the donor's layer-0 weights. Errors: RANGE. */
+int32_t mirage_block_location(mirage_ctx* ctx, int32_t model, int32_t block_id, int32_t* donor,
+                              uint64_t* offset);
+
+/* Tokens cached for seq_id (0 if unknown). */
+int32_t mirage_seq_len(mirage_ctx* ctx, int32_t model, int64_t seq_id, int32_t* len_out);
+
+/* One decode step for `batch` sequences (Alg. 1 line 13
+ * "GPU LLM Kernel(enable_remap, remapped_layer_list)"). positions[i] must equal
+ * the tokens already cached for seq_ids[i]; the step appends the new token's
+ * K/V at that position and attends over positions[i]+1 tokens, so seq i needs
+ * >= ceil((positions[i]+1)/16) blocks. tokens are teacher-forced by the caller.
+ * hidden_out: device bf16 [batch, d] (final normalised hidden) or NULL.
+ * argmax_out: host int32 [batch] (greedy token, lowest index on ties) or NULL;
+ * valid after the compute stream is synchronised.
+ * Errors: RANGE (batch, ids), NO_BLOCKS (a missing block, checked before any
+ * enqueue), STATE (position != cached length, model inactive or fully
+ * reclaimed), CUDA. */
+int32_t mirage_decode_step(mirage_ctx* ctx, int32_t model, int32_t batch, const int64_t* seq_ids,
+                           const int32_t* tokens, const int32_t* positions, void* hidden_out,
+                           int32_t* argmax_out);
+
+typedef struct mirage_stats {
+  int64_t native_blocks, total_blocks, free_blocks;
+  uint64_t layer_bytes, block_bytes;
+  uint64_t reclaimed_bytes; /* bytes of R carved into this model's pool           */
+  uint64_t donated_bytes;   /* bytes of this model's layers reclaimed            */
+  int32_t m, beta, active, n_seqs;
+  int32_t cycle[MIRAGE_MAX_CYCLE];
+  uint64_t uses;            /* cycled-layer uses enqueued so far                 */
+  uint64_t h2d_copies, h2d_bytes;
+  double h2d_ms;            /* summed event time of completed H2D copies         */
+  double last_step_ms;      /* event time of the last completed decode step      */
+  int64_t steps;
+} mirage_stats;
+
+int32_t mirage_query(mirage_ctx* ctx, int32_t model, mirage_stats* out);
+
+/* Slot-assignment log of `model` since its cycle was installed: rows of
+ * (k, step, layer, slot, copied) as int64, row-major [n][5]; equals the
+ * oracle's c5 log. Errors: RANGE (cap too small; *n_out gets the length). */
+int32_t mirage_slot_log(mirage_ctx* ctx, int32_t model, int64_t* out, int32_t cap, int32_t* n_out);
+
+/* Block until all work enqueued by this ctx has finished; reports sticky errors. */
+int32_t mirage_sync(mirage_ctx* ctx);
+
+/* ---- test / bench hooks --------------------------------------------------- */
+
+/* Paged attention of one layer only (a8+a9), over the sequences' current
+ * cached lengths. q_dev: device fp32 [batch, H, D]; out_dev: device [batch, H,
+ * D] fp32 (out_fp32 = 1) or bf16. split_tokens_override > 0 forces the split
+ * size (multiple of 16). Errors: RANGE, STATE (a sequence with 0 tokens). */
+int32_t mirage_attn_only(mirage_ctx* ctx, int32_t model, int32_t layer, int32_t batch,
+                         const int64_t* seq_ids, const float* q_dev, void* out_dev,
+                         int32_t out_fp32, int32_t split_tokens_override);
+
+/* Append n_tokens synthetic tokens of KV to seq_id (all layers), values from
+ * the counter-based generator documented in oracle/kvgen.py's header (the
+ * kernel implements it independently). Needs the blocks. Errors: RANGE,
+ * NO_BLOCKS. */
+int32_t mirage_fill_kv(mirage_ctx* ctx, int32_t model, int64_t seq_id, int32_t n_tokens,
+                       uint64_t seed);
+
+/* Append n_tokens of caller KV to seq_id: host_kv bf16 [L][H_kv][2][n][D]
+ * (any host memory; copied synchronously). Errors: RANGE, NO_BLOCKS. */
+int32_t mirage_write_kv(mirage_ctx* ctx, int32_t model, int64_t seq_id, int32_t n_tokens,
+                        const void* host_kv);
+
+/* Number of kernels this ctx has launched (its own kernels, not cuBLAS). */
+int64_t mirage_kernel_launches(const mirage_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MIRAGE_H_ */

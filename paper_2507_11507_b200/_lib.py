@@ -1,0 +1,304 @@
+"""ctypes binding of libmirage.so — argument marshalling only.
+
+Every function here forwards to the C-ABI declared in include/mirage.h with the
+same name (without the ``mirage_`` prefix on methods). Device memory, pinned
+host memory and streams come from PyTorch (plumbing); every step of the decode
+path runs inside libmirage's kernels. There is no fallback: if the shared
+library is missing or fails to load, importing this module raises.
+"""
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmirage.so")
+
+OK, ERR_CONFIG, ERR_CAPACITY, ERR_RANGE, ERR_STATE = 0, -1, -2, -3, -4
+ERR_NO_BLOCKS, ERR_DOUBLE_FREE, ERR_INFEASIBLE, ERR_PRESSURE, ERR_CUDA, ERR_NCCL = -5, -6, -7, -8, -9, -10
+FAMILY_OPT, FAMILY_LLAMA = 0, 1
+BETA_1, BETA_2, BETA_DYNAMIC = 1, 2, 3
+BLOCK_TOKENS = 16
+MAX_CYCLE = 256
+
+_NAMES = {ERR_CONFIG: "CONFIG", ERR_CAPACITY: "CAPACITY", ERR_RANGE: "RANGE", ERR_STATE: "STATE",
+          ERR_NO_BLOCKS: "NO_BLOCKS", ERR_DOUBLE_FREE: "DOUBLE_FREE", ERR_INFEASIBLE: "INFEASIBLE",
+          ERR_PRESSURE: "PRESSURE", ERR_CUDA: "CUDA", ERR_NCCL: "NCCL"}
+
+
+class MirageError(RuntimeError):
+    def __init__(self, code, msg, shortfall=0):
+        super().__init__(f"mirage {_NAMES.get(code, code)}: {msg}")
+        self.code = code
+        self.shortfall = shortfall
+
+
+class InitCfg(C.Structure):
+    _fields_ = [("device", C.c_int32), ("dev_arena", C.c_void_p), ("dev_arena_bytes", C.c_uint64),
+                ("block_tokens", C.c_int32), ("compute_stream", C.c_void_p), ("copy_stream", C.c_void_p),
+                ("max_batch", C.c_int32), ("max_ctx", C.c_int32), ("flags", C.c_uint32),
+                ("tp_rank", C.c_int32), ("tp_size", C.c_int32), ("nccl_comm", C.c_void_p)]
+
+
+class ModelCfg(C.Structure):
+    _fields_ = [("family", C.c_int32), ("n_layers", C.c_int32), ("d_model", C.c_int32),
+                ("n_heads", C.c_int32), ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("ffn_dim", C.c_int32), ("vocab", C.c_int32), ("max_pos", C.c_int32),
+                ("norm_eps", C.c_float), ("rope_theta", C.c_float)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("native_blocks", C.c_int64), ("total_blocks", C.c_int64), ("free_blocks", C.c_int64),
+                ("layer_bytes", C.c_uint64), ("block_bytes", C.c_uint64),
+                ("reclaimed_bytes", C.c_uint64), ("donated_bytes", C.c_uint64),
+                ("m", C.c_int32), ("beta", C.c_int32), ("active", C.c_int32), ("n_seqs", C.c_int32),
+                ("cycle", C.c_int32 * MAX_CYCLE), ("uses", C.c_uint64), ("h2d_copies", C.c_uint64),
+                ("h2d_bytes", C.c_uint64), ("h2d_ms", C.c_double), ("last_step_ms", C.c_double),
+                ("steps", C.c_int64)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "cycle"}
+        d["cycle"] = list(self.cycle[: self.m])
+        return d
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(LIB_PATH)
+    P, I32, I64, U64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64
+    pI32, pI64, pU64 = C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_uint64)
+    sig = {
+        "mirage_model_sizes": (I32, [C.POINTER(ModelCfg), pU64, pU64, pU64]),
+        "mirage_model_arena_bytes": (I32, [C.POINTER(ModelCfg), I64, I32, I32, pU64]),
+        "mirage_init": (I32, [C.POINTER(InitCfg), C.POINTER(P)]),
+        "mirage_destroy": (None, [P]),
+        "mirage_last_error": (C.c_char_p, [P]),
+        "mirage_add_model": (I32, [P, C.POINTER(ModelCfg), P, U64, I64, pI32]),
+        "mirage_plan": (I32, [I32, I32, I32, U64, U64, I32, pI32, pI32, pI32]),
+        "mirage_remap_layers": (I32, [P, I32, I32, pI32, I32, I32, pI64, pU64]),
+        "mirage_set_active": (I32, [P, I32, I32]),
+        "mirage_alloc_blocks": (I32, [P, I32, I64, I32, pI32, pI32]),
+        "mirage_free_blocks": (I32, [P, I32, I64]),
+        "mirage_get_block_table": (I32, [P, I32, I64, pI32, I32, pI32]),
+        "mirage_block_location": (I32, [P, I32, I32, pI32, pU64]),
+        "mirage_seq_len": (I32, [P, I32, I64, pI32]),
+        "mirage_decode_step": (I32, [P, I32, I32, pI64, pI32, pI32, P, pI32]),
+        "mirage_query": (I32, [P, I32, C.POINTER(Stats)]),
+        "mirage_slot_log": (I32, [P, I32, pI64, I32, pI32]),
+        "mirage_sync": (I32, [P]),
+        "mirage_attn_only": (I32, [P, I32, I32, I32, pI64, P, P, I32, I32]),
+        "mirage_fill_kv": (I32, [P, I32, I64, I32, U64]),
+        "mirage_write_kv": (I32, [P, I32, I64, I32, P]),
+        "mirage_kernel_launches": (I64, [P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+LIB = _load()
+EXPORTED = [
+    "mirage_model_sizes", "mirage_model_arena_bytes", "mirage_init", "mirage_destroy", "mirage_last_error",
+    "mirage_add_model", "mirage_plan", "mirage_remap_layers", "mirage_set_active", "mirage_alloc_blocks",
+    "mirage_free_blocks", "mirage_get_block_table", "mirage_block_location", "mirage_seq_len",
+    "mirage_decode_step", "mirage_query", "mirage_slot_log", "mirage_sync", "mirage_attn_only",
+    "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches"]
+
+
+def model_cfg(shape):
+    """mirage_model_cfg from any object with the synth.models.ModelShape fields."""
+    return ModelCfg(shape.family, shape.n_layers, shape.d_model, shape.n_heads, shape.n_kv_heads,
+                    shape.head_dim, shape.ffn_dim, shape.vocab, shape.max_pos, shape.norm_eps,
+                    shape.rope_theta)
+
+
+def model_sizes(shape):
+    S, G, BB = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    cfg = model_cfg(shape)
+    rc = LIB.mirage_model_sizes(C.byref(cfg), C.byref(S), C.byref(G), C.byref(BB))
+    if rc:
+        raise MirageError(rc, "model_sizes")
+    return S.value, G.value, BB.value
+
+
+def model_arena_bytes(shape, native_blocks, max_batch, max_ctx):
+    out = C.c_uint64()
+    cfg = model_cfg(shape)
+    rc = LIB.mirage_model_arena_bytes(C.byref(cfg), native_blocks, max_batch, max_ctx, C.byref(out))
+    if rc:
+        raise MirageError(rc, "model_arena_bytes")
+    return out.value
+
+
+def plan(n_layers, alpha, beta_policy, t_transfer_ns, t_compute_layer_ns, anchor=0):
+    cyc = (C.c_int32 * max(n_layers, 1))()
+    m, beta = C.c_int32(), C.c_int32()
+    rc = LIB.mirage_plan(n_layers, alpha, beta_policy, int(t_transfer_ns), int(t_compute_layer_ns), anchor,
+                         cyc, C.byref(m), C.byref(beta))
+    if rc:
+        raise MirageError(rc, "plan")
+    return list(cyc[: m.value]), m.value, beta.value
+
+
+def _i32(seq):
+    return (C.c_int32 * len(seq))(*[int(x) for x in seq])
+
+
+def _i64(seq):
+    return (C.c_int64 * len(seq))(*[int(x) for x in seq])
+
+
+def pack_blob(layers_bytes, global_bytes):
+    """Pinned host blob = concatenation of per-layer byte images + globals
+    (include/mirage.h "Weight blob layout"). Inputs are uint8 CPU tensors."""
+    total = sum(int(t.numel()) for t in layers_bytes) + int(global_bytes.numel())
+    blob = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+    off = 0
+    for t in list(layers_bytes) + [global_bytes]:
+        n = int(t.numel())
+        blob[off: off + n].copy_(t)
+        off += n
+    return blob
+
+
+def tensors_to_bytes(named, order):
+    """Concatenate bf16 tensors in the documented order into one uint8 tensor."""
+    return torch.cat([named[n].contiguous().view(torch.uint8).reshape(-1) for n in order])
+
+
+class Context:
+    """One mirage_ctx on one GPU. Owns (keeps alive) the arena, the streams and
+    the host blobs it was given."""
+
+    def __init__(self, arena_bytes, max_batch, max_ctx, device=0, stream=None):
+        self.device = torch.device("cuda", device)
+        self.arena = torch.empty(int(arena_bytes) + 256, dtype=torch.uint8, device=self.device)
+        base = self.arena.data_ptr()
+        self._arena_ptr = (base + 255) // 256 * 256
+        self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
+        self._blobs = []
+        cfg = InitCfg(device, self._arena_ptr, int(arena_bytes), BLOCK_TOKENS, self.stream.cuda_stream,
+                      None, max_batch, max_ctx, 0, 0, 1, None)
+        self._ctx = C.c_void_p()
+        rc = LIB.mirage_init(C.byref(cfg), C.byref(self._ctx))
+        if rc:
+            raise MirageError(rc, "init")
+        self.max_batch, self.max_ctx = max_batch, max_ctx
+
+    # -- errors ---------------------------------------------------------------
+    def _check(self, rc, what, shortfall=0):
+        if rc:
+            raise MirageError(rc, f"{what}: {LIB.mirage_last_error(self._ctx).decode()}", shortfall)
+
+    def close(self):
+        if self._ctx:
+            LIB.mirage_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- API ------------------------------------------------------------------
+    def add_model(self, shape, host_blob, native_blocks):
+        assert host_blob.is_pinned(), "host blob must be pinned"
+        self._blobs.append(host_blob)
+        cfg = model_cfg(shape)
+        mid = C.c_int32()
+        rc = LIB.mirage_add_model(self._ctx, C.byref(cfg), host_blob.data_ptr(), host_blob.numel(),
+                                  int(native_blocks), C.byref(mid))
+        self._check(rc, "add_model")
+        return mid.value
+
+    def remap_layers(self, donor, recipient, cycle, beta):
+        gained, rb = C.c_int64(), C.c_uint64()
+        rc = LIB.mirage_remap_layers(self._ctx, donor, recipient, _i32(cycle), len(cycle), beta,
+                                     C.byref(gained), C.byref(rb))
+        self._check(rc, "remap_layers")
+        return gained.value, rb.value
+
+    def set_active(self, model, active):
+        self._check(LIB.mirage_set_active(self._ctx, model, int(active)), "set_active")
+
+    def alloc_blocks(self, model, seq_id, n):
+        ids = (C.c_int32 * max(n, 1))()
+        short = C.c_int32()
+        rc = LIB.mirage_alloc_blocks(self._ctx, model, int(seq_id), int(n), ids, C.byref(short))
+        self._check(rc, "alloc_blocks", short.value)
+        return list(ids[:n])
+
+    def free_blocks(self, model, seq_id):
+        self._check(LIB.mirage_free_blocks(self._ctx, model, int(seq_id)), "free_blocks")
+
+    def block_table(self, model, seq_id):
+        n = C.c_int32()
+        LIB.mirage_get_block_table(self._ctx, model, int(seq_id), None, 0, C.byref(n))
+        buf = (C.c_int32 * max(n.value, 1))()
+        rc = LIB.mirage_get_block_table(self._ctx, model, int(seq_id), buf, n.value, C.byref(n))
+        self._check(rc, "get_block_table")
+        return list(buf[: n.value])
+
+    def block_location(self, model, block_id):
+        d, off = C.c_int32(), C.c_uint64()
+        self._check(LIB.mirage_block_location(self._ctx, model, block_id, C.byref(d), C.byref(off)),
+                    "block_location")
+        return d.value, off.value
+
+    def seq_len(self, model, seq_id):
+        n = C.c_int32()
+        self._check(LIB.mirage_seq_len(self._ctx, model, int(seq_id), C.byref(n)), "seq_len")
+        return n.value
+
+    def decode_step(self, model, seq_ids, tokens, positions, hidden_out=None, argmax=True):
+        B = len(seq_ids)
+        am = (C.c_int32 * B)() if argmax else None
+        hp = hidden_out.data_ptr() if hidden_out is not None else None
+        rc = LIB.mirage_decode_step(self._ctx, model, B, _i64(seq_ids), _i32(tokens), _i32(positions),
+                                    hp, am)
+        self._check(rc, "decode_step")
+        return am
+
+    def decode_step_raw(self, model, B, seq_ids_c, tokens_c, positions_c, hidden_ptr, argmax_c):
+        """Pre-marshalled variant (ctypes arrays) for timed loops."""
+        rc = LIB.mirage_decode_step(self._ctx, model, B, seq_ids_c, tokens_c, positions_c, hidden_ptr,
+                                    argmax_c)
+        self._check(rc, "decode_step")
+
+    def query(self, model):
+        st = Stats()
+        self._check(LIB.mirage_query(self._ctx, model, C.byref(st)), "query")
+        return st.as_dict()
+
+    def slot_log(self, model):
+        n = C.c_int32()
+        LIB.mirage_slot_log(self._ctx, model, None, 0, C.byref(n))
+        buf = (C.c_int64 * max(5 * n.value, 1))()
+        self._check(LIB.mirage_slot_log(self._ctx, model, buf, n.value, C.byref(n)), "slot_log")
+        v = list(buf[: 5 * n.value])
+        return [tuple(v[i: i + 5]) for i in range(0, len(v), 5)]
+
+    def sync(self):
+        self._check(LIB.mirage_sync(self._ctx), "sync")
+
+    def attn_only(self, model, layer, seq_ids, q, out, split_tokens=0):
+        assert q.dtype == torch.float32 and q.is_cuda and q.is_contiguous()
+        rc = LIB.mirage_attn_only(self._ctx, model, layer, len(seq_ids), _i64(seq_ids), q.data_ptr(),
+                                  out.data_ptr(), int(out.dtype == torch.float32), int(split_tokens))
+        self._check(rc, "attn_only")
+
+    def fill_kv(self, model, seq_id, n_tokens, seed):
+        self._check(LIB.mirage_fill_kv(self._ctx, model, int(seq_id), int(n_tokens), int(seed)), "fill_kv")
+
+    def write_kv(self, model, seq_id, kv):
+        """kv: bf16 CPU tensor [L][H_kv][2][n][D]."""
+        kv = kv.contiguous()
+        self._check(LIB.mirage_write_kv(self._ctx, model, int(seq_id), int(kv.shape[3]), kv.data_ptr()),
+                    "write_kv")
+
+    def kernel_launches(self):
+        return LIB.mirage_kernel_launches(self._ctx)

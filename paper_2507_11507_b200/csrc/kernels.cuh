@@ -1,0 +1,68 @@
+// Internal kernel launch API of libmirage (not part of the C-ABI).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mirage {
+
+// One attention work unit: a (sequence, split) pair; blockIdx.y is the KV head.
+struct AttnUnit {
+  int32_t seq;     // row in the step's batch
+  int32_t split;   // split index within the sequence
+  int32_t nsplit;  // number of splits of this sequence
+  int32_t pbase;   // first partial record of this sequence (valid if nsplit > 1)
+};
+
+struct AttnParams {
+  const float* q;              // [B][H][D] fp32 (unscaled)
+  const int32_t* tables;       // [B][tbl_pitch] block ids
+  int32_t tbl_pitch;
+  const int32_t* ctx_len;      // [B] tokens attended (incl. the new one)
+  const uint64_t* block_base;  // [ids] device address of each physical block
+  uint64_t layer_off;          // layer * H_kv * 2 * 16 * D * 2 bytes
+  const AttnUnit* units;       // [n_units]
+  int32_t n_units;
+  int32_t split_blocks;        // 16-token blocks per split
+  int32_t H, H_kv, D;
+  float scale_log2;            // log2(e) / sqrt(D)
+  float* partial;              // [(pbase + split) * H + h][D + 2]
+  int32_t* tickets;            // [B * H_kv], zero between launches
+  void* out;                   // [B][H][D] fp32 or bf16
+  int32_t out_fp32;
+};
+
+cudaError_t launch_paged_attention(const AttnParams& p, cudaStream_t s);
+
+// ---- dense-layer support kernels -------------------------------------------
+// h[b] = E[tok] (+ P[pos + 2] for OPT); x[b] = bf16(norm(h[b])).
+cudaError_t launch_embed_norm(int family, int B, int d, const int32_t* tokens,
+                              const int32_t* positions, const __nv_bfloat16* embed,
+                              const __nv_bfloat16* pos_embed, const __nv_bfloat16* g,
+                              const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
+                              cudaStream_t s);
+// h[b] += y[b] (+ bias); x[b] = bf16(norm(h[b])). y row stride ldy.
+cudaError_t launch_residual_norm(int family, int B, int d, const float* y, int ldy,
+                                 const __nv_bfloat16* bias, const __nv_bfloat16* g,
+                                 const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
+                                 cudaStream_t s);
+// qkv [B][(H+2Hk)D] fp32 (+bias, +RoPE) -> q fp32 [B][H][D]; K/V bf16 appended to
+// the paged cache at positions[b].
+cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float* qkv,
+                            const __nv_bfloat16* bias, const int32_t* positions,
+                            const int32_t* tables, int tbl_pitch, const uint64_t* block_base,
+                            uint64_t layer_off, float rope_theta, float* q, cudaStream_t s);
+// OPT: f = bf16(relu(y + b)); Llama: f = bf16(silu(y[:, :f]) * y[:, f:]).
+cudaError_t launch_act(int family, int B, int f, const float* y, const __nv_bfloat16* bias,
+                       __nv_bfloat16* out, cudaStream_t s);
+// argmax over each row of logits [B][V] (lowest index on ties).
+cudaError_t launch_argmax(int B, int V, const float* logits, int32_t* out, cudaStream_t s);
+
+// ---- KV hooks ----------------------------------------------------------------
+cudaError_t launch_fill_kv(uint64_t seed, int64_t seq_id, int L, int Hk, int D, int p0, int n,
+                           const int32_t* table, const uint64_t* block_base, cudaStream_t s);
+// src: device bf16 [L][Hk][2][n][D] -> paged blocks at positions p0..p0+n-1.
+cudaError_t launch_write_kv(int L, int Hk, int D, int p0, int n, const __nv_bfloat16* src,
+                            const int32_t* table, const uint64_t* block_base, cudaStream_t s);
+
+}  // namespace mirage

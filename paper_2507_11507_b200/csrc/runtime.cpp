@@ -1,0 +1,1105 @@
+// libmirage host runtime: context, arena carving, block allocator with remap
+// (a2, a3), copy-engine prefetcher with event-gated layer handoff (a4, a5) and
+// the decode-step executor (a0, a6-a9). See include/mirage.h for the contract
+// and DESIGN.md for the readings of the paper this follows.
+#include <cublas_v2.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/mirage.h"
+#include "kernels.cuh"
+
+namespace mirage {
+std::vector<int32_t> uniform_placement(int32_t n, int32_t m, int32_t anchor);
+}
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+constexpr int kBlockTokens = MIRAGE_BLOCK_TOKENS;
+constexpr int kMaxSplits = 64;
+constexpr int kTargetCtas = 148 * 8;
+constexpr uint64_t kAlign = 256;
+constexpr size_t kCublasWs = 32u << 20;
+
+enum LayerState { RESIDENT = 0, SLOT = 1, RECLAIMED = 2 };
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+struct Shape {
+  int family, n, d, H, Hk, D, f, V, max_pos;
+  float eps, theta;
+};
+
+struct Sizes {
+  uint64_t S, G, BB;
+};
+
+uint64_t layer_params(const Shape& m) {
+  const uint64_t d = m.d, f = m.f;
+  if (m.family == MIRAGE_FAMILY_OPT) return 4 * d * d + 2 * d * f + 9 * d + f;
+  const uint64_t qkv = (uint64_t)(m.H + 2 * m.Hk) * m.D;
+  return qkv * d + d * (uint64_t)m.H * m.D + 3 * f * d + 2 * d;
+}
+
+uint64_t global_params(const Shape& m) {
+  const uint64_t d = m.d, V = m.V;
+  if (m.family == MIRAGE_FAMILY_OPT) return V * d + (uint64_t)(m.max_pos + 2) * d + 2 * d;
+  return 2 * V * d + d;
+}
+
+Sizes sizes_of(const Shape& m) {
+  Sizes z;
+  z.S = 2 * layer_params(m);
+  z.G = 2 * global_params(m);
+  z.BB = (uint64_t)m.n * m.Hk * 2 * kBlockTokens * m.D * 2;
+  return z;
+}
+
+// Per-layer tensor pointers (blob order documented in include/mirage.h).
+struct LayerW {
+  const bf16 *w_qkv, *w_o, *w_1, *w_2;  // w_1 = fc1 / gateup, w_2 = fc2 / down
+  const bf16 *b_qkv, *b_o, *b_1, *b_2;  // OPT only
+  const bf16 *n1_g, *n1_b, *n2_g, *n2_b;
+};
+
+LayerW layer_ptrs(const Shape& m, const char* base) {
+  LayerW w{};
+  const bf16* p = reinterpret_cast<const bf16*>(base);
+  const size_t d = m.d, f = m.f;
+  if (m.family == MIRAGE_FAMILY_OPT) {
+    w.w_qkv = p; p += 3 * d * d;
+    w.w_o = p; p += d * d;
+    w.w_1 = p; p += f * d;
+    w.w_2 = p; p += d * f;
+    w.b_qkv = p; p += 3 * d;
+    w.b_o = p; p += d;
+    w.b_1 = p; p += f;
+    w.b_2 = p; p += d;
+    w.n1_g = p; p += d;
+    w.n1_b = p; p += d;
+    w.n2_g = p; p += d;
+    w.n2_b = p; p += d;
+  } else {
+    const size_t qkv = (size_t)(m.H + 2 * m.Hk) * m.D;
+    w.w_qkv = p; p += qkv * d;
+    w.w_o = p; p += d * (size_t)m.H * m.D;
+    w.w_1 = p; p += 2 * f * d;
+    w.w_2 = p; p += d * f;
+    w.n1_g = p; p += d;
+    w.n2_g = p; p += d;
+  }
+  return w;
+}
+
+struct GlobalW {
+  const bf16 *embed, *pos_embed, *nf_g, *nf_b, *lm_head;
+};
+
+GlobalW global_ptrs(const Shape& m, const char* base) {
+  GlobalW g{};
+  const bf16* p = reinterpret_cast<const bf16*>(base);
+  const size_t d = m.d, V = m.V;
+  g.embed = p; p += V * d;
+  if (m.family == MIRAGE_FAMILY_OPT) {
+    g.pos_embed = p; p += (size_t)(m.max_pos + 2) * d;
+    g.nf_g = p; p += d;
+    g.nf_b = p; p += d;
+    g.lm_head = g.embed;  // tied
+  } else {
+    g.nf_g = p; p += d;
+    g.lm_head = p; p += V * d;
+  }
+  return g;
+}
+
+struct CopyTiming {
+  cudaEvent_t t0, t1;
+  uint64_t bytes;
+};
+
+struct Model {
+  Shape shp;
+  Sizes sz;
+  int id = 0;
+  char* w_dev = nullptr;      // layer 0 of the device weights
+  const char* host = nullptr; // pinned host blob
+  char* pool = nullptr;       // native KV pool
+  int64_t n_native = 0;
+  bool active = true;
+  // ---- allocator (a2, a3) ----
+  int32_t next_id = 0;
+  std::set<int32_t> free_ids;
+  std::unordered_map<int64_t, std::vector<int32_t>> tables;
+  std::unordered_map<int64_t, int32_t> lens;
+  std::vector<int32_t> loc_donor;  // -1 native
+  std::vector<uint64_t> loc_off;
+  std::vector<uint64_t> bbase_host;
+  uint64_t* bbase_dev = nullptr;
+  int64_t bbase_cap = 0;
+  uint64_t reclaimed_bytes = 0, donated_bytes = 0;
+  std::vector<int> layer_state;
+  // ---- prefetcher (a4, a5) ----
+  std::vector<int32_t> cycle;
+  int32_t beta = 0;
+  std::vector<int> cyc_index;  // layer -> index in cycle or -1
+  uint64_t uses = 0;           // cycled uses enqueued since install
+  int64_t cyc_steps = 0;
+  std::vector<int64_t> slot_log;  // rows of 5
+  std::vector<cudaEvent_t> ready_ev, free_ev;
+  std::deque<CopyTiming> pending;
+  uint64_t h2d_copies = 0, h2d_bytes = 0;
+  double h2d_ms = 0;
+  // ---- workspace (arena) ----
+  float* h = nullptr;
+  bf16* x = nullptr;
+  float* y = nullptr;
+  float* q = nullptr;
+  bf16* f = nullptr;
+  float* partial = nullptr;
+  int32_t* tickets = nullptr;
+  int32_t* argmax = nullptr;
+  int y_ld_max = 0;
+  // ---- step timing ----
+  cudaEvent_t st0 = nullptr, st1 = nullptr;
+  bool step_timed = false;
+  double last_step_ms = 0;
+  int64_t steps = 0;
+};
+
+}  // namespace
+
+struct mirage_ctx {
+  mirage_init_cfg cfg{};
+  cudaStream_t cs = nullptr, xs = nullptr;
+  bool own_xs = false;
+  char* arena = nullptr;
+  uint64_t arena_used = 0;
+  std::vector<Model*> models;
+  cublasHandle_t blas = nullptr;
+  void* blas_ws = nullptr;
+  // step metadata: pinned staging ring -> device
+  size_t meta_bytes = 0;
+  char* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  int stage_i = 0;
+  char* meta_dev = nullptr;
+  int max_units = 0;
+  int max_blk = 0;
+  std::string err;
+  int32_t sticky = MIRAGE_OK;
+  int64_t launches = 0;
+};
+
+namespace {
+
+int32_t fail(mirage_ctx* c, int32_t code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (code == MIRAGE_ERR_CUDA || code == MIRAGE_ERR_NCCL) c->sticky = code;
+  }
+  return code;
+}
+
+#define CK(ctx, expr)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(ctx, MIRAGE_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+#define CKB(ctx, expr)                                                                        \
+  do {                                                                                        \
+    cublasStatus_t e_ = (expr);                                                               \
+    if (e_ != CUBLAS_STATUS_SUCCESS)                                                          \
+      return fail(ctx, MIRAGE_ERR_CUDA, "%s: cublas status %d (%s:%d)", #expr, (int)e_, __FILE__, \
+                  __LINE__);                                                                  \
+  } while (0)
+
+#define KL(ctx, expr)      \
+  do {                     \
+    ++(ctx)->launches;     \
+    CK(ctx, (expr));       \
+  } while (0)
+
+#define GUARD(ctx)                                                      \
+  do {                                                                  \
+    if (!(ctx)) return MIRAGE_ERR_CONFIG;                               \
+    if ((ctx)->sticky) return (ctx)->sticky;                            \
+  } while (0)
+
+Shape shape_of(const mirage_model_cfg* m) {
+  Shape s;
+  s.family = m->family;
+  s.n = m->n_layers;
+  s.d = m->d_model;
+  s.H = m->n_heads;
+  s.Hk = m->n_kv_heads;
+  s.D = m->head_dim;
+  s.f = m->ffn_dim;
+  s.V = m->vocab;
+  s.max_pos = m->max_pos;
+  s.eps = m->norm_eps;
+  s.theta = m->rope_theta;
+  return s;
+}
+
+const char* check_shape(const Shape& s) {
+  if (s.family != MIRAGE_FAMILY_OPT && s.family != MIRAGE_FAMILY_LLAMA) return "family";
+  if (s.n <= 0 || s.n > MIRAGE_MAX_CYCLE) return "n_layers";
+  if (s.d <= 0 || s.d % 128 || s.d > 8192) return "d_model (multiple of 128, <= 8192)";
+  if (s.D != 64 && s.D != 128) return "head_dim (64 or 128)";
+  if (s.H <= 0 || s.Hk <= 0 || s.H % s.Hk) return "n_heads % n_kv_heads";
+  const int g = s.H / s.Hk;
+  if (g != 1 && g != 2 && g != 4 && g != 8) return "group size (1,2,4,8)";
+  if (s.family == MIRAGE_FAMILY_OPT && (s.H * s.D != s.d || s.Hk != s.H)) return "OPT: H*D == d, MHA";
+  if (s.f <= 0 || s.f % 128) return "ffn_dim (multiple of 128)";
+  if (s.V <= 0 || s.max_pos <= 0) return "vocab/max_pos";
+  return nullptr;
+}
+
+// workspace element counts of a model under the ctx limits
+struct WsPlan {
+  uint64_t h, x, y, q, f, partial, tickets, argmax;
+  int y_ld;
+};
+
+WsPlan ws_plan(const Shape& s, int Bm, int max_units) {
+  WsPlan w;
+  const int qkv = (s.H + 2 * s.Hk) * s.D;
+  const int ffn_out = s.family == MIRAGE_FAMILY_LLAMA ? 2 * s.f : s.f;
+  w.y_ld = std::max(std::max(qkv, ffn_out), std::max(s.V, s.d));
+  w.h = (uint64_t)Bm * s.d * 4;
+  w.x = (uint64_t)Bm * std::max(s.d, s.H * s.D) * 2;
+  w.y = (uint64_t)Bm * w.y_ld * 4;
+  w.q = (uint64_t)Bm * s.H * s.D * 4;
+  w.f = (uint64_t)Bm * s.f * 2;
+  w.partial = (uint64_t)max_units * s.H * (s.D + 2) * 4;
+  w.tickets = (uint64_t)Bm * s.Hk * 4;
+  w.argmax = (uint64_t)Bm * 4;
+  return w;
+}
+
+uint64_t model_arena(const Shape& s, int64_t n_native, int Bm, int max_units) {
+  const Sizes z = sizes_of(s);
+  const WsPlan w = ws_plan(s, Bm, max_units);
+  uint64_t t = 0;
+  t += align_up((uint64_t)s.n * z.S + z.G, kAlign);
+  t += align_up((uint64_t)n_native * z.BB, kAlign);
+  for (uint64_t b : {w.h, w.x, w.y, w.q, w.f, w.partial, w.tickets, w.argmax}) t += align_up(b, kAlign);
+  return t;
+}
+
+int units_cap(int Bm) { return 2 * Bm + 2 * kTargetCtas; }
+
+char* carve(mirage_ctx* c, uint64_t bytes) {
+  const uint64_t off = align_up(c->arena_used, kAlign);
+  if (off + bytes > c->cfg.dev_arena_bytes) return nullptr;
+  c->arena_used = off + bytes;
+  return c->arena + off;
+}
+
+Model* get_model(mirage_ctx* c, int32_t id) {
+  if (id < 0 || id >= (int32_t)c->models.size()) return nullptr;
+  return c->models[id];
+}
+
+// ---- step metadata packing ---------------------------------------------------
+struct MetaView {
+  int32_t *tokens, *pos, *len, *tables;
+  mirage::AttnUnit* units;
+};
+
+MetaView meta_view(mirage_ctx* c, char* base) {
+  MetaView v;
+  const int Bm = c->cfg.max_batch;
+  char* p = base;
+  v.tokens = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
+  v.pos = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
+  v.len = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
+  v.units = reinterpret_cast<mirage::AttnUnit*>(p); p += align_up((uint64_t)c->max_units * 16, 16);
+  v.tables = reinterpret_cast<int32_t*>(p);
+  return v;
+}
+
+size_t meta_size(mirage_ctx* c) {
+  const int Bm = c->cfg.max_batch;
+  return 3 * align_up((uint64_t)Bm * 4, 16) + align_up((uint64_t)c->max_units * 16, 16) +
+         (uint64_t)Bm * c->max_blk * 4;
+}
+
+int32_t acquire_stage(mirage_ctx* c, char** host) {
+  c->stage_i ^= 1;
+  CK(c, cudaEventSynchronize(c->stage_ev[c->stage_i]));
+  *host = c->stage[c->stage_i];
+  return MIRAGE_OK;
+}
+
+// Build attention units for lens[] (logical lengths only -> placement
+// independent splits). Returns the unit count and split size in blocks.
+int build_units(const int32_t* lens, int B, int Hk, int override_blocks, mirage::AttnUnit* units,
+                int max_units, int* split_blocks) {
+  int64_t work = 0;
+  int max_nb = 0;
+  for (int b = 0; b < B; ++b) {
+    const int nb = (lens[b] + kBlockTokens - 1) / kBlockTokens;
+    work += (int64_t)nb * Hk;
+    max_nb = std::max(max_nb, nb);
+  }
+  int P;
+  if (override_blocks > 0) {
+    P = override_blocks;
+  } else {
+    P = (int)std::max<int64_t>(1, (work + kTargetCtas - 1) / kTargetCtas);
+    P = std::max(P, (max_nb + kMaxSplits - 1) / kMaxSplits);
+  }
+  int n = 0, pbase = 0;
+  for (int b = 0; b < B; ++b) {
+    const int nb = (lens[b] + kBlockTokens - 1) / kBlockTokens;
+    const int ns = std::max(1, (nb + P - 1) / P);
+    if (n + ns > max_units) return -1;
+    for (int i = 0; i < ns; ++i) units[n++] = mirage::AttnUnit{b, i, ns, ns > 1 ? pbase : 0};
+    if (ns > 1) pbase += ns;
+  }
+  *split_blocks = P;
+  return n;
+}
+
+void harvest_copy_times(Model* M) {
+  while (!M->pending.empty()) {
+    CopyTiming& t = M->pending.front();
+    if (cudaEventQuery(t.t1) != cudaSuccess) break;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t.t0, t.t1);
+    M->h2d_ms += ms;
+    M->h2d_bytes += t.bytes;
+    M->h2d_copies += 1;
+    cudaEventDestroy(t.t0);
+    cudaEventDestroy(t.t1);
+    M->pending.pop_front();
+  }
+  (void)cudaGetLastError();
+}
+
+void harvest_step_time(Model* M) {
+  if (M->step_timed && cudaEventQuery(M->st1) == cudaSuccess) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, M->st0, M->st1);
+    M->last_step_ms = ms;
+    M->step_timed = false;
+  }
+  (void)cudaGetLastError();
+}
+
+int32_t gemm(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf16* x, float* y, int ldy) {
+  const float one = 1.f, zero = 0.f;
+  CKB(c, cublasGemmEx(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, N, B, K, &one, W, CUDA_R_16BF, K, x,
+                      CUDA_R_16BF, K, &zero, y, CUDA_R_32F, ldy, CUBLAS_COMPUTE_32F,
+                      CUBLAS_GEMM_DEFAULT));
+  return MIRAGE_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int32_t mirage_model_sizes(const mirage_model_cfg* m, uint64_t* layer_bytes, uint64_t* global_bytes,
+                           uint64_t* block_bytes) {
+  if (!m) return MIRAGE_ERR_CONFIG;
+  const Shape s = shape_of(m);
+  if (check_shape(s)) return MIRAGE_ERR_CONFIG;
+  const Sizes z = sizes_of(s);
+  if (layer_bytes) *layer_bytes = z.S;
+  if (global_bytes) *global_bytes = z.G;
+  if (block_bytes) *block_bytes = z.BB;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_model_arena_bytes(const mirage_model_cfg* m, int64_t native_kv_blocks,
+                                 int32_t max_batch, int32_t max_ctx, uint64_t* bytes) {
+  if (!m || !bytes || native_kv_blocks < 0 || max_batch <= 0 || max_ctx <= 0)
+    return MIRAGE_ERR_CONFIG;
+  const Shape s = shape_of(m);
+  if (check_shape(s)) return MIRAGE_ERR_CONFIG;
+  *bytes = model_arena(s, native_kv_blocks, max_batch, units_cap(max_batch)) + kAlign;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
+  if (!cfg || !out) return MIRAGE_ERR_CONFIG;
+  *out = nullptr;
+  if (cfg->block_tokens != kBlockTokens || cfg->tp_size != 1 || cfg->tp_rank != 0 ||
+      !cfg->dev_arena || !cfg->compute_stream || cfg->max_batch <= 0 || cfg->max_ctx <= 0 ||
+      (reinterpret_cast<uintptr_t>(cfg->dev_arena) % kAlign))
+    return MIRAGE_ERR_CONFIG;
+  mirage_ctx* c = new mirage_ctx();
+  c->cfg = *cfg;
+  c->arena = reinterpret_cast<char*>(cfg->dev_arena);
+  c->cs = reinterpret_cast<cudaStream_t>(cfg->compute_stream);
+  c->max_units = units_cap(cfg->max_batch);
+  c->max_blk = (cfg->max_ctx + kBlockTokens - 1) / kBlockTokens;
+  auto bail = [&](int32_t code) {
+    mirage_destroy(c);
+    return code;
+  };
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return bail(MIRAGE_ERR_CUDA);
+  if (cfg->copy_stream) {
+    c->xs = reinterpret_cast<cudaStream_t>(cfg->copy_stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&c->xs, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(MIRAGE_ERR_CUDA);
+    c->own_xs = true;
+  }
+  if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return bail(MIRAGE_ERR_CUDA);
+  if (cudaMalloc(&c->blas_ws, kCublasWs) != cudaSuccess) return bail(MIRAGE_ERR_CUDA);
+  if (cublasSetWorkspace(c->blas, c->blas_ws, kCublasWs) != CUBLAS_STATUS_SUCCESS ||
+      cublasSetStream(c->blas, c->cs) != CUBLAS_STATUS_SUCCESS)
+    return bail(MIRAGE_ERR_CUDA);
+  c->meta_bytes = meta_size(c);
+  for (int i = 0; i < 2; ++i) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&c->stage[i]), c->meta_bytes, cudaHostAllocDefault) !=
+            cudaSuccess ||
+        cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming) != cudaSuccess)
+      return bail(MIRAGE_ERR_CUDA);
+  }
+  if (cudaMalloc(reinterpret_cast<void**>(&c->meta_dev), c->meta_bytes) != cudaSuccess)
+    return bail(MIRAGE_ERR_CUDA);
+  *out = c;
+  return MIRAGE_OK;
+}
+
+void mirage_destroy(mirage_ctx* c) {
+  if (!c) return;
+  if (c->cs) cudaStreamSynchronize(c->cs);
+  if (c->xs) cudaStreamSynchronize(c->xs);
+  for (Model* M : c->models) {
+    for (auto e : M->ready_ev) cudaEventDestroy(e);
+    for (auto e : M->free_ev) cudaEventDestroy(e);
+    for (auto& t : M->pending) {
+      cudaEventDestroy(t.t0);
+      cudaEventDestroy(t.t1);
+    }
+    if (M->st0) cudaEventDestroy(M->st0);
+    if (M->st1) cudaEventDestroy(M->st1);
+    if (M->bbase_dev) cudaFree(M->bbase_dev);
+    delete M;
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (c->stage[i]) cudaFreeHost(c->stage[i]);
+    if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
+  }
+  if (c->meta_dev) cudaFree(c->meta_dev);
+  if (c->blas) cublasDestroy(c->blas);
+  if (c->blas_ws) cudaFree(c->blas_ws);
+  if (c->own_xs && c->xs) cudaStreamDestroy(c->xs);
+  (void)cudaGetLastError();
+  delete c;
+}
+
+const char* mirage_last_error(const mirage_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+
+int64_t mirage_kernel_launches(const mirage_ctx* c) { return c ? c->launches : 0; }
+
+int32_t mirage_add_model(mirage_ctx* c, const mirage_model_cfg* mc, const void* host_blob,
+                         uint64_t host_bytes, int64_t native_kv_blocks, int32_t* model_id) {
+  GUARD(c);
+  if (!mc || !host_blob || !model_id || native_kv_blocks < 0)
+    return fail(c, MIRAGE_ERR_CONFIG, "add_model: null argument or negative pool");
+  const Shape s = shape_of(mc);
+  if (const char* why = check_shape(s)) return fail(c, MIRAGE_ERR_CONFIG, "add_model: bad %s", why);
+  const Sizes z = sizes_of(s);
+  if (host_bytes != (uint64_t)s.n * z.S + z.G)
+    return fail(c, MIRAGE_ERR_CONFIG, "add_model: host_bytes %llu != n*S+G %llu",
+                (unsigned long long)host_bytes, (unsigned long long)((uint64_t)s.n * z.S + z.G));
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, host_blob) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+    (void)cudaGetLastError();
+    return fail(c, MIRAGE_ERR_CONFIG, "add_model: host blob must be pinned host memory");
+  }
+  Model* M = new Model();
+  M->shp = s;
+  M->sz = z;
+  M->host = reinterpret_cast<const char*>(host_blob);
+  M->n_native = native_kv_blocks;
+  const int Bm = c->cfg.max_batch;
+  const WsPlan w = ws_plan(s, Bm, c->max_units);
+  auto C = [&](uint64_t b) { return carve(c, b); };
+  M->w_dev = C((uint64_t)s.n * z.S + z.G);
+  M->pool = native_kv_blocks ? C((uint64_t)native_kv_blocks * z.BB) : c->arena;
+  M->h = reinterpret_cast<float*>(C(w.h));
+  M->x = reinterpret_cast<bf16*>(C(w.x));
+  M->y = reinterpret_cast<float*>(C(w.y));
+  M->q = reinterpret_cast<float*>(C(w.q));
+  M->f = reinterpret_cast<bf16*>(C(w.f));
+  M->partial = reinterpret_cast<float*>(C(w.partial));
+  M->tickets = reinterpret_cast<int32_t*>(C(w.tickets));
+  M->argmax = reinterpret_cast<int32_t*>(C(w.argmax));
+  M->y_ld_max = w.y_ld;
+  if (!M->w_dev || !M->pool || !M->h || !M->x || !M->y || !M->q || !M->f || !M->partial ||
+      !M->tickets || !M->argmax) {
+    delete M;
+    return fail(c, MIRAGE_ERR_CAPACITY, "add_model: arena exhausted (%llu of %llu bytes used)",
+                (unsigned long long)c->arena_used, (unsigned long long)c->cfg.dev_arena_bytes);
+  }
+  // block_base (library-owned): native ids + everything the arena could donate
+  const uint64_t cap = (uint64_t)native_kv_blocks + c->cfg.dev_arena_bytes / z.BB + 16;
+  if (cudaMalloc(reinterpret_cast<void**>(&M->bbase_dev), cap * 8) != cudaSuccess) {
+    delete M;
+    return fail(c, MIRAGE_ERR_CUDA, "add_model: block_base allocation");
+  }
+  M->bbase_cap = (int64_t)cap;
+  M->next_id = (int32_t)native_kv_blocks;
+  for (int32_t i = 0; i < native_kv_blocks; ++i) {
+    M->free_ids.insert(M->free_ids.end(), i);
+    M->loc_donor.push_back(-1);
+    M->loc_off.push_back((uint64_t)i * z.BB);
+    M->bbase_host.push_back(reinterpret_cast<uint64_t>(M->pool) + (uint64_t)i * z.BB);
+  }
+  M->layer_state.assign(s.n, RESIDENT);
+  M->cyc_index.assign(s.n, -1);
+  CK(c, cudaMemcpyAsync(M->w_dev, host_blob, host_bytes, cudaMemcpyHostToDevice, c->cs));
+  if (native_kv_blocks)
+    CK(c, cudaMemcpyAsync(M->bbase_dev, M->bbase_host.data(), native_kv_blocks * 8,
+                          cudaMemcpyHostToDevice, c->cs));
+  CK(c, cudaMemsetAsync(M->tickets, 0, w.tickets, c->cs));
+  CK(c, cudaEventCreate(&M->st0));
+  CK(c, cudaEventCreate(&M->st1));
+  CK(c, cudaStreamSynchronize(c->cs));
+  M->id = (int32_t)c->models.size();
+  c->models.push_back(M);
+  *model_id = M->id;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_set_active(mirage_ctx* c, int32_t model, int32_t active) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M) return fail(c, MIRAGE_ERR_RANGE, "set_active: model %d", model);
+  if (active && !M->active) {
+    for (int st : M->layer_state)
+      if (st == RECLAIMED && M->cycle.empty())
+        return fail(c, MIRAGE_ERR_STATE, "set_active: model %d has reclaimed layers", model);
+  }
+  M->active = active != 0;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_remap_layers(mirage_ctx* c, int32_t donor, int32_t recipient, const int32_t* cycle,
+                            int32_t m, int32_t beta, int64_t* blocks_gained,
+                            uint64_t* reclaimed_bytes) {
+  GUARD(c);
+  Model* D = get_model(c, donor);
+  Model* R = get_model(c, recipient);
+  if (!D || !R) return fail(c, MIRAGE_ERR_RANGE, "remap: model id");
+  if (m <= 0 || m > D->shp.n || !cycle || beta < 0 || beta > m)
+    return fail(c, MIRAGE_ERR_RANGE, "remap: m=%d beta=%d", m, beta);
+  for (int i = 0; i < m; ++i) {
+    if (cycle[i] < 0 || cycle[i] >= D->shp.n) return fail(c, MIRAGE_ERR_RANGE, "remap: layer %d", cycle[i]);
+    if (i && cycle[i] <= cycle[i - 1])
+      return fail(c, MIRAGE_ERR_RANGE, "remap: cycle must be strictly ascending");
+  }
+  for (int i = 0; i < m; ++i)
+    if (D->layer_state[cycle[i]] != RESIDENT)
+      return fail(c, MIRAGE_ERR_STATE, "remap: layer %d already cycled or reclaimed", cycle[i]);
+  if (beta == 0 && D->active) return fail(c, MIRAGE_ERR_STATE, "remap: beta=0 needs an inactive donor");
+  if (beta > 0 && donor != recipient)
+    return fail(c, MIRAGE_ERR_STATE, "remap: streaming remap must be a self-remap");
+  if (beta > 0 && !D->cycle.empty()) return fail(c, MIRAGE_ERR_STATE, "remap: donor already has a cycle");
+  // carve R = cycle[beta:] into runs of consecutive layers
+  std::vector<int32_t> Rl(cycle + beta, cycle + m);
+  int64_t gained = 0;
+  std::vector<std::pair<int32_t, int32_t>> runs;  // (first, count)
+  for (int32_t l : Rl) {
+    if (!runs.empty() && runs.back().first + runs.back().second == l) runs.back().second++;
+    else runs.push_back({l, 1});
+  }
+  int64_t total_new = 0;
+  for (auto& r : runs) total_new += (int64_t)((uint64_t)r.second * D->sz.S / R->sz.BB);
+  if ((int64_t)R->next_id + total_new > R->bbase_cap)
+    return fail(c, MIRAGE_ERR_CAPACITY, "remap: block table capacity %lld exceeded", (long long)R->bbase_cap);
+  const int32_t first_new = R->next_id;
+  for (auto& r : runs) {
+    const uint64_t off = (uint64_t)r.first * D->sz.S;
+    const uint64_t len = (uint64_t)r.second * D->sz.S;
+    const int64_t k = (int64_t)(len / R->sz.BB);
+    for (int64_t i = 0; i < k; ++i) {
+      const int32_t id = R->next_id++;
+      R->free_ids.insert(id);
+      R->loc_donor.push_back(donor);
+      R->loc_off.push_back(off + (uint64_t)i * R->sz.BB);
+      R->bbase_host.push_back(reinterpret_cast<uint64_t>(D->w_dev) + off + (uint64_t)i * R->sz.BB);
+    }
+    gained += k;
+  }
+  R->reclaimed_bytes += (uint64_t)Rl.size() * D->sz.S;
+  D->donated_bytes += (uint64_t)Rl.size() * D->sz.S;
+  for (int i = 0; i < beta; ++i) D->layer_state[cycle[i]] = SLOT;
+  for (int32_t l : Rl) D->layer_state[l] = RECLAIMED;
+  if (gained)  // stream-ordered after every kernel that read these bytes as weights
+    CK(c, cudaMemcpyAsync(R->bbase_dev + first_new, R->bbase_host.data() + first_new, gained * 8,
+                          cudaMemcpyHostToDevice, c->cs));
+  if (beta > 0) {
+    D->cycle.assign(cycle, cycle + m);
+    D->beta = beta;
+    for (int i = 0; i < m; ++i) D->cyc_index[cycle[i]] = i;
+    D->uses = 0;
+    D->cyc_steps = 0;
+    D->slot_log.clear();
+    for (int j = 0; j < beta; ++j) {
+      cudaEvent_t a, b;
+      CK(c, cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      CK(c, cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      D->ready_ev.push_back(a);
+      D->free_ev.push_back(b);
+    }
+  }
+  if (gained) CK(c, cudaStreamSynchronize(c->cs));  // the host staging above is a pageable vector
+  if (blocks_gained) *blocks_gained = gained;
+  if (reclaimed_bytes) *reclaimed_bytes = (uint64_t)Rl.size() * D->sz.S;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_alloc_blocks(mirage_ctx* c, int32_t model, int64_t seq_id, int32_t n, int32_t* ids_out,
+                            int32_t* shortfall_out) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || n < 0) return fail(c, MIRAGE_ERR_RANGE, "alloc: model %d n %d", model, n);
+  if (shortfall_out) *shortfall_out = 0;
+  if ((size_t)n > M->free_ids.size()) {
+    if (shortfall_out) *shortfall_out = n - (int32_t)M->free_ids.size();
+    return fail(c, MIRAGE_ERR_NO_BLOCKS, "alloc: shortfall %d", n - (int32_t)M->free_ids.size());
+  }
+  auto& t = M->tables[seq_id];
+  if ((int64_t)t.size() + n > c->max_blk)
+    return fail(c, MIRAGE_ERR_RANGE, "alloc: table of seq %lld would exceed max_ctx", (long long)seq_id);
+  for (int i = 0; i < n; ++i) {
+    const int32_t id = *M->free_ids.begin();
+    M->free_ids.erase(M->free_ids.begin());
+    t.push_back(id);
+    if (ids_out) ids_out[i] = id;
+  }
+  M->lens.emplace(seq_id, 0);
+  return MIRAGE_OK;
+}
+
+int32_t mirage_free_blocks(mirage_ctx* c, int32_t model, int64_t seq_id) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M) return fail(c, MIRAGE_ERR_RANGE, "free: model %d", model);
+  auto it = M->tables.find(seq_id);
+  if (it == M->tables.end()) return fail(c, MIRAGE_ERR_DOUBLE_FREE, "free: seq %lld", (long long)seq_id);
+  for (int32_t id : it->second) M->free_ids.insert(id);
+  M->tables.erase(it);
+  M->lens.erase(seq_id);
+  return MIRAGE_OK;
+}
+
+int32_t mirage_get_block_table(mirage_ctx* c, int32_t model, int64_t seq_id, int32_t* out, int32_t cap,
+                               int32_t* n_out) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M) return fail(c, MIRAGE_ERR_RANGE, "table: model %d", model);
+  auto it = M->tables.find(seq_id);
+  if (it == M->tables.end()) {
+    if (n_out) *n_out = 0;
+    return fail(c, MIRAGE_ERR_RANGE, "table: unknown seq %lld", (long long)seq_id);
+  }
+  if (n_out) *n_out = (int32_t)it->second.size();
+  if ((int32_t)it->second.size() > cap || (!out && !it->second.empty()))
+    return fail(c, MIRAGE_ERR_RANGE, "table: cap %d < %zu", cap, it->second.size());
+  std::copy(it->second.begin(), it->second.end(), out);
+  return MIRAGE_OK;
+}
+
+int32_t mirage_block_location(mirage_ctx* c, int32_t model, int32_t block_id, int32_t* donor,
+                              uint64_t* offset) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || block_id < 0 || block_id >= M->next_id)
+    return fail(c, MIRAGE_ERR_RANGE, "location: model %d block %d", model, block_id);
+  if (donor) *donor = M->loc_donor[block_id];
+  if (offset) *offset = M->loc_off[block_id];
+  return MIRAGE_OK;
+}
+
+int32_t mirage_seq_len(mirage_ctx* c, int32_t model, int64_t seq_id, int32_t* len_out) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || !len_out) return fail(c, MIRAGE_ERR_RANGE, "seq_len: model %d", model);
+  auto it = M->lens.find(seq_id);
+  *len_out = it == M->lens.end() ? 0 : it->second;
+  return MIRAGE_OK;
+}
+
+// ---- decode step -------------------------------------------------------------
+int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_t* seq_ids,
+                           const int32_t* tokens, const int32_t* positions, void* hidden_out,
+                           int32_t* argmax_out) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M) return fail(c, MIRAGE_ERR_RANGE, "step: model %d", model);
+  if (B <= 0 || B > c->cfg.max_batch || !seq_ids || !tokens || !positions)
+    return fail(c, MIRAGE_ERR_RANGE, "step: batch %d", B);
+  const Shape& s = M->shp;
+  if (!M->active) return fail(c, MIRAGE_ERR_STATE, "step: model %d inactive", model);
+  for (int st : M->layer_state)
+    if (st == RECLAIMED && M->cycle.empty())
+      return fail(c, MIRAGE_ERR_STATE, "step: model %d has reclaimed layers and no cycle", model);
+  // ---- validate (before any enqueue) ----
+  std::vector<const std::vector<int32_t>*> rows(B);
+  int pitch = 1;
+  for (int i = 0; i < B; ++i) {
+    auto it = M->tables.find(seq_ids[i]);
+    const int32_t len = M->lens.count(seq_ids[i]) ? M->lens[seq_ids[i]] : 0;
+    if (positions[i] != len)
+      return fail(c, MIRAGE_ERR_STATE, "step: seq %lld position %d != cached %d",
+                  (long long)seq_ids[i], positions[i], len);
+    if (positions[i] + 1 > c->cfg.max_ctx || positions[i] + 1 > s.max_pos)
+      return fail(c, MIRAGE_ERR_RANGE, "step: seq %lld exceeds max_ctx", (long long)seq_ids[i]);
+    if (tokens[i] < 0 || tokens[i] >= s.V) return fail(c, MIRAGE_ERR_RANGE, "step: token %d", tokens[i]);
+    const int need = (positions[i] + 1 + kBlockTokens - 1) / kBlockTokens;
+    if (it == M->tables.end() || (int)it->second.size() < need)
+      return fail(c, MIRAGE_ERR_NO_BLOCKS, "step: seq %lld needs %d blocks", (long long)seq_ids[i], need);
+    rows[i] = &it->second;
+    pitch = std::max(pitch, need);
+  }
+  for (int i = 0; i < B; ++i)
+    for (int j = 0; j < i; ++j)
+      if (seq_ids[i] == seq_ids[j]) return fail(c, MIRAGE_ERR_RANGE, "step: duplicate seq");
+  harvest_copy_times(M);
+  harvest_step_time(M);
+  // ---- pack metadata ----
+  char* host;
+  if (int32_t e = acquire_stage(c, &host)) return e;
+  MetaView hv = meta_view(c, host), dv = meta_view(c, c->meta_dev);
+  for (int i = 0; i < B; ++i) {
+    hv.tokens[i] = tokens[i];
+    hv.pos[i] = positions[i];
+    hv.len[i] = positions[i] + 1;
+    std::copy(rows[i]->begin(), rows[i]->begin() + std::min<size_t>(rows[i]->size(), pitch),
+              hv.tables + (size_t)i * pitch);
+  }
+  int split_blocks = 1;
+  const int n_units = build_units(hv.len, B, s.Hk, 0, hv.units, c->max_units, &split_blocks);
+  if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "step: too many attention units");
+  const size_t tbl_bytes = (size_t)B * pitch * 4;
+  const size_t head = reinterpret_cast<char*>(hv.tables) - host;
+  cudaStream_t cs = c->cs;
+  const bool timed = !M->step_timed;
+  if (timed) CK(c, cudaEventRecord(M->st0, cs));
+  CK(c, cudaMemcpyAsync(c->meta_dev, host, head + tbl_bytes, cudaMemcpyHostToDevice, cs));
+  CK(c, cudaEventRecord(c->stage_ev[c->stage_i], cs));
+
+  const GlobalW gw = global_ptrs(s, M->w_dev + (uint64_t)s.n * M->sz.S);
+  const int d = s.d, H = s.H, Hk = s.Hk, D = s.D, qkvN = (H + 2 * Hk) * D;
+  const bool opt = s.family == MIRAGE_FAMILY_OPT;
+  const int m = (int)M->cycle.size();
+  const int beta = M->beta;
+  // weights of layer l for this step (slot if cycled) and its use index
+  std::vector<const char*> wptr(s.n);
+  std::vector<int64_t> use_of(s.n, -1);
+  uint64_t k = M->uses;
+  for (int l = 0; l < s.n; ++l) {
+    if (M->cyc_index[l] >= 0) {
+      use_of[l] = (int64_t)k;
+      const int slot = (int)(k % beta);
+      wptr[l] = M->w_dev + (uint64_t)M->cycle[slot] * M->sz.S;
+      ++k;
+    } else {
+      wptr[l] = M->w_dev + (uint64_t)l * M->sz.S;
+    }
+  }
+  auto gate = [&](int l) -> int32_t {  // wait until layer l's weights are in its slot
+    if (l < s.n && use_of[l] >= beta && use_of[l] >= 0)
+      CK(c, cudaStreamWaitEvent(cs, M->ready_ev[use_of[l] % beta], 0));
+    return MIRAGE_OK;
+  };
+  auto release = [&](int l) -> int32_t {  // layer l done reading its slot; prefetch use+beta
+    if (use_of[l] < 0) return MIRAGE_OK;
+    const uint64_t u = (uint64_t)use_of[l];
+    const int slot = (int)(u % beta);
+    M->slot_log.insert(M->slot_log.end(),
+                       {(int64_t)u, M->cyc_steps, l, slot, (int64_t)(u >= (uint64_t)beta)});
+    CK(c, cudaEventRecord(M->free_ev[slot], cs));
+    const uint64_t nu = u + beta;
+    const int nl = M->cycle[nu % m];
+    CK(c, cudaStreamWaitEvent(c->xs, M->free_ev[slot], 0));
+    CopyTiming t{};
+    CK(c, cudaEventCreate(&t.t0));
+    CK(c, cudaEventCreate(&t.t1));
+    t.bytes = M->sz.S;
+    CK(c, cudaEventRecord(t.t0, c->xs));
+    CK(c, cudaMemcpyAsync(M->w_dev + (uint64_t)M->cycle[slot] * M->sz.S,
+                          M->host + (uint64_t)nl * M->sz.S, M->sz.S, cudaMemcpyHostToDevice, c->xs));
+    CK(c, cudaEventRecord(t.t1, c->xs));
+    CK(c, cudaEventRecord(M->ready_ev[slot], c->xs));
+    M->pending.push_back(t);
+    return MIRAGE_OK;
+  };
+
+  // embedding + layer 0's first norm
+  if (int32_t e = gate(0)) return e;
+  {
+    const LayerW w0 = layer_ptrs(s, wptr[0]);
+    KL(c, mirage::launch_embed_norm(s.family, B, d, dv.tokens, dv.pos, gw.embed, gw.pos_embed, w0.n1_g,
+                                   w0.n1_b, s.eps, M->h, M->x, cs));
+  }
+  mirage::AttnParams ap{};
+  ap.q = M->q;
+  ap.tables = dv.tables;
+  ap.tbl_pitch = pitch;
+  ap.ctx_len = dv.len;
+  ap.block_base = M->bbase_dev;
+  ap.units = dv.units;
+  ap.n_units = n_units;
+  ap.split_blocks = split_blocks;
+  ap.H = H;
+  ap.H_kv = Hk;
+  ap.D = D;
+  ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+  ap.partial = M->partial;
+  ap.tickets = M->tickets;
+  ap.out = M->x;  // bf16 [B][H*D]: the O-projection input
+  ap.out_fp32 = 0;
+  for (int l = 0; l < s.n; ++l) {
+    const LayerW w = layer_ptrs(s, wptr[l]);
+    const uint64_t layer_off = (uint64_t)l * Hk * 2 * kBlockTokens * D * 2;
+    if (int32_t e = gemm(c, B, qkvN, d, w.w_qkv, M->x, M->y, qkvN)) return e;
+    KL(c, mirage::launch_qkv_post(s.family, B, H, Hk, D, M->y, opt ? w.b_qkv : nullptr, dv.pos,
+                                 dv.tables, pitch, M->bbase_dev, layer_off, s.theta, M->q, cs));
+    ap.layer_off = layer_off;
+    KL(c, mirage::launch_paged_attention(ap, cs));
+    if (int32_t e = gemm(c, B, d, H * D, w.w_o, M->x, M->y, d)) return e;
+    KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_o : nullptr, w.n2_g,
+                                      opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs));
+    if (opt) {
+      if (int32_t e = gemm(c, B, s.f, d, w.w_1, M->x, M->y, s.f)) return e;
+      KL(c, mirage::launch_act(s.family, B, s.f, M->y, w.b_1, M->f, cs));
+    } else {
+      if (int32_t e = gemm(c, B, 2 * s.f, d, w.w_1, M->x, M->y, 2 * s.f)) return e;
+      KL(c, mirage::launch_act(s.family, B, s.f, M->y, nullptr, M->f, cs));
+    }
+    if (int32_t e = gemm(c, B, d, s.f, w.w_2, M->f, M->y, d)) return e;
+    // residual, then the next layer's first norm (or the final norm)
+    const bool last = l + 1 == s.n;
+    const bf16* ng = last ? gw.nf_g : nullptr;
+    const bf16* nb = last ? gw.nf_b : nullptr;
+    const bool split_gate = !last && use_of[l] >= 0 && use_of[l + 1] >= 0 && beta == 1;
+    if (split_gate) {
+      // l and l+1 share the single slot: finish l, hand the slot over, then norm
+      KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_2 : nullptr, nullptr,
+                                        nullptr, s.eps, M->h, M->x, cs));
+      if (int32_t e = release(l)) return e;
+      if (int32_t e = gate(l + 1)) return e;
+      const LayerW wn = layer_ptrs(s, wptr[l + 1]);
+      KL(c, mirage::launch_residual_norm(s.family, B, d, nullptr, d, nullptr, wn.n1_g,
+                                        opt ? wn.n1_b : nullptr, s.eps, M->h, M->x, cs));
+    } else {
+      if (!last) {
+        if (int32_t e = gate(l + 1)) return e;
+        const LayerW wn = layer_ptrs(s, wptr[l + 1]);
+        ng = wn.n1_g;
+        nb = opt ? wn.n1_b : nullptr;
+      }
+      KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_2 : nullptr, ng,
+                                        opt ? nb : nullptr, s.eps, M->h, M->x, cs));
+      if (int32_t e = release(l)) return e;
+    }
+  }
+  // LM head + argmax
+  if (int32_t e = gemm(c, B, s.V, d, gw.lm_head, M->x, M->y, s.V)) return e;
+  KL(c, mirage::launch_argmax(B, s.V, M->y, M->argmax, cs));
+  if (hidden_out)
+    CK(c, cudaMemcpyAsync(hidden_out, M->x, (size_t)B * d * 2, cudaMemcpyDeviceToDevice, cs));
+  if (argmax_out) CK(c, cudaMemcpyAsync(argmax_out, M->argmax, (size_t)B * 4, cudaMemcpyDeviceToHost, cs));
+  if (timed) {
+    CK(c, cudaEventRecord(M->st1, cs));
+    M->step_timed = true;
+  }
+  // commit host state
+  M->uses = k;
+  if (m) M->cyc_steps++;
+  M->steps++;
+  for (int i = 0; i < B; ++i) M->lens[seq_ids[i]] = positions[i] + 1;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B, const int64_t* seq_ids,
+                         const float* q_dev, void* out_dev, int32_t out_fp32,
+                         int32_t split_tokens_override) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || layer < 0 || layer >= M->shp.n || B <= 0 || B > c->cfg.max_batch || !seq_ids || !q_dev ||
+      !out_dev || split_tokens_override < 0 || split_tokens_override % kBlockTokens)
+    return fail(c, MIRAGE_ERR_RANGE, "attn_only: arguments");
+  std::vector<const std::vector<int32_t>*> rows(B);
+  int pitch = 1;
+  char* host;
+  if (int32_t e = acquire_stage(c, &host)) return e;
+  MetaView hv = meta_view(c, host), dv = meta_view(c, c->meta_dev);
+  for (int i = 0; i < B; ++i) {
+    auto it = M->tables.find(seq_ids[i]);
+    const int32_t len = M->lens.count(seq_ids[i]) ? M->lens[seq_ids[i]] : 0;
+    if (it == M->tables.end() || len <= 0)
+      return fail(c, MIRAGE_ERR_STATE, "attn_only: seq %lld has no tokens", (long long)seq_ids[i]);
+    rows[i] = &it->second;
+    hv.len[i] = len;
+    pitch = std::max(pitch, (len + kBlockTokens - 1) / kBlockTokens);
+  }
+  for (int i = 0; i < B; ++i) {
+    const size_t nb = (hv.len[i] + kBlockTokens - 1) / kBlockTokens;
+    std::copy(rows[i]->begin(), rows[i]->begin() + nb, hv.tables + (size_t)i * pitch);
+  }
+  int split_blocks = 1;
+  const int n_units = build_units(hv.len, B, M->shp.Hk, split_tokens_override / kBlockTokens,
+                                  hv.units, c->max_units, &split_blocks);
+  if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "attn_only: too many units for the split override");
+  const size_t head = reinterpret_cast<char*>(hv.tables) - host;
+  CK(c, cudaMemcpyAsync(c->meta_dev, host, head + (size_t)B * pitch * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(c, cudaEventRecord(c->stage_ev[c->stage_i], c->cs));
+  const Shape& s = M->shp;
+  mirage::AttnParams ap{};
+  ap.q = q_dev;
+  ap.tables = dv.tables;
+  ap.tbl_pitch = pitch;
+  ap.ctx_len = dv.len;
+  ap.block_base = M->bbase_dev;
+  ap.layer_off = (uint64_t)layer * s.Hk * 2 * kBlockTokens * s.D * 2;
+  ap.units = dv.units;
+  ap.n_units = n_units;
+  ap.split_blocks = split_blocks;
+  ap.H = s.H;
+  ap.H_kv = s.Hk;
+  ap.D = s.D;
+  ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)s.D));
+  ap.partial = M->partial;
+  ap.tickets = M->tickets;
+  ap.out = out_dev;
+  ap.out_fp32 = out_fp32;
+  KL(c, mirage::launch_paged_attention(ap, c->cs));
+  return MIRAGE_OK;
+}
+
+static int32_t kv_hook_prepare(mirage_ctx* c, Model* M, int64_t seq_id, int32_t n, int32_t* p0) {
+  auto it = M->tables.find(seq_id);
+  const int32_t len = M->lens.count(seq_id) ? M->lens[seq_id] : 0;
+  const int need = (len + n + kBlockTokens - 1) / kBlockTokens;
+  if (it == M->tables.end() || (int)it->second.size() < need)
+    return fail(c, MIRAGE_ERR_NO_BLOCKS, "kv: seq %lld needs %d blocks", (long long)seq_id, need);
+  if (len + n > c->cfg.max_ctx) return fail(c, MIRAGE_ERR_RANGE, "kv: exceeds max_ctx");
+  char* host;
+  if (int32_t e = acquire_stage(c, &host)) return e;
+  MetaView hv = meta_view(c, host);
+  std::copy(it->second.begin(), it->second.begin() + need, hv.tables);
+  const size_t head = reinterpret_cast<char*>(hv.tables) - host;
+  CK(c, cudaMemcpyAsync(c->meta_dev + head, host + head, (size_t)need * 4, cudaMemcpyHostToDevice, c->cs));
+  CK(c, cudaEventRecord(c->stage_ev[c->stage_i], c->cs));
+  *p0 = len;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_fill_kv(mirage_ctx* c, int32_t model, int64_t seq_id, int32_t n, uint64_t seed) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || n < 0) return fail(c, MIRAGE_ERR_RANGE, "fill_kv: arguments");
+  int32_t p0 = 0;
+  if (int32_t e = kv_hook_prepare(c, M, seq_id, n, &p0)) return e;
+  MetaView dv = meta_view(c, c->meta_dev);
+  const Shape& s = M->shp;
+  KL(c, mirage::launch_fill_kv(seed, seq_id, s.n, s.Hk, s.D, p0, n, dv.tables, M->bbase_dev, c->cs));
+  M->lens[seq_id] = p0 + n;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_write_kv(mirage_ctx* c, int32_t model, int64_t seq_id, int32_t n, const void* host_kv) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || n < 0 || (!host_kv && n)) return fail(c, MIRAGE_ERR_RANGE, "write_kv: arguments");
+  int32_t p0 = 0;
+  if (int32_t e = kv_hook_prepare(c, M, seq_id, n, &p0)) return e;
+  const Shape& s = M->shp;
+  const size_t bytes = (size_t)s.n * s.Hk * 2 * n * s.D * 2;
+  void* tmp = nullptr;
+  if (bytes) {
+    CK(c, cudaMalloc(&tmp, bytes));
+    CK(c, cudaMemcpyAsync(tmp, host_kv, bytes, cudaMemcpyHostToDevice, c->cs));
+    MetaView dv = meta_view(c, c->meta_dev);
+    ++c->launches;
+    cudaError_t e = mirage::launch_write_kv(s.n, s.Hk, s.D, p0, n, reinterpret_cast<const bf16*>(tmp),
+                                            dv.tables, M->bbase_dev, c->cs);
+    cudaError_t e2 = cudaStreamSynchronize(c->cs);
+    cudaFree(tmp);
+    CK(c, e);
+    CK(c, e2);
+  }
+  M->lens[seq_id] = p0 + n;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_query(mirage_ctx* c, int32_t model, mirage_stats* o) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || !o) return fail(c, MIRAGE_ERR_RANGE, "query: model %d", model);
+  harvest_copy_times(M);
+  harvest_step_time(M);
+  std::memset(o, 0, sizeof *o);
+  o->native_blocks = M->n_native;
+  o->total_blocks = M->next_id;
+  o->free_blocks = (int64_t)M->free_ids.size();
+  o->layer_bytes = M->sz.S;
+  o->block_bytes = M->sz.BB;
+  o->reclaimed_bytes = M->reclaimed_bytes;
+  o->donated_bytes = M->donated_bytes;
+  o->m = (int32_t)M->cycle.size();
+  o->beta = M->beta;
+  o->active = M->active;
+  o->n_seqs = (int32_t)M->tables.size();
+  for (size_t i = 0; i < M->cycle.size() && i < MIRAGE_MAX_CYCLE; ++i) o->cycle[i] = M->cycle[i];
+  o->uses = M->uses;
+  o->h2d_copies = M->h2d_copies;
+  o->h2d_bytes = M->h2d_bytes;
+  o->h2d_ms = M->h2d_ms;
+  o->last_step_ms = M->last_step_ms;
+  o->steps = M->steps;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_slot_log(mirage_ctx* c, int32_t model, int64_t* out, int32_t cap, int32_t* n_out) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M) return fail(c, MIRAGE_ERR_RANGE, "slot_log: model %d", model);
+  const int32_t n = (int32_t)(M->slot_log.size() / 5);
+  if (n_out) *n_out = n;
+  if (n > cap || (!out && n)) return fail(c, MIRAGE_ERR_RANGE, "slot_log: cap %d < %d", cap, n);
+  std::copy(M->slot_log.begin(), M->slot_log.end(), out);
+  return MIRAGE_OK;
+}
+
+int32_t mirage_sync(mirage_ctx* c) {
+  GUARD(c);
+  CK(c, cudaStreamSynchronize(c->cs));
+  CK(c, cudaStreamSynchronize(c->xs));
+  CK(c, cudaGetLastError());
+  return MIRAGE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+"""End-to-end decode-step parity (a0-a9) through the C-ABI against oracle c4,
+remap invariance (bit-exact), slot-log parity with oracle c5, error paths.
+GPU only."""
+import numpy as np
+import pytest
+import torch
+
+import harness
+from oracle import timeline as OT
+from oracle.decode import Decoder
+from synth import models, weights, workload
+
+pytestmark = pytest.mark.gpu
+
+REL_RMS, MAX_ABS = 1e-2, 5e-2     # DESIGN.md reading #19 (end-to-end bf16 decode)
+
+
+def run_gpu(shape, steps, B, n_native, remap=None, seed=3, max_ctx=256):
+    """remap = (step, cycle, beta). Returns hidden [steps][B,d] (float32 numpy),
+    argmax [steps][B], ctx, model id."""
+    from paper_2507_11507_b200 import Context
+    arena = harness.arena_for([(shape, n_native)], B, max_ctx)
+    ctx = Context(arena, B, max_ctx)
+    mid = ctx.add_model(shape, harness.make_blob(shape, seed=seed), n_native)
+    hid = torch.empty((B, shape.d_model), dtype=torch.bfloat16, device="cuda")
+    H, A = [], []
+    for t in range(steps):
+        if remap and remap[0] == t:
+            ctx.remap_layers(mid, mid, remap[1], remap[2])
+        for s in range(B):
+            if t % 16 == 0:
+                ctx.alloc_blocks(mid, s, 1)
+        toks = [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)]
+        am = ctx.decode_step(mid, list(range(B)), toks, [t] * B, hidden_out=hid)
+        ctx.sync()
+        H.append(hid.float().cpu().numpy().copy())
+        A.append(list(am))
+    return H, A, ctx, mid
+
+
+def run_oracle(shape, steps, B, seed=3):
+    layers = [weights.layer_tensors(shape, l, seed) for l in range(shape.n_layers)]
+    dec = Decoder(shape, layers, weights.global_tensors(shape, seed), round_points=True)
+    H, A, M = [], [], []
+    for t in range(steps):
+        toks = [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)]
+        h, logits, am = dec.step(list(range(B)), toks, [t] * B)
+        srt = np.sort(logits, axis=1)
+        H.append(h)
+        A.append(am)
+        M.append(srt[:, -1] - srt[:, -2])
+    return H, A, M
+
+
+@pytest.mark.parametrize("shape,remap", [
+    (models.TOY, (0, [0, 1], 1)),                  # C1: layer 1 reclaimed, layer 0 is the slot
+    (models.TOY_LLAMA, (5, [0, 1], 2)),            # double buffering, prefetch only (m == beta)
+    (models.TOY_LLAMA, (3, [0, 1], 1)),
+])
+def test_decode_matches_oracle_and_remap_is_invisible(shape, remap):
+    steps, B = 48, 8
+    Hg, Ag, ctx, mid = run_gpu(shape, steps, B, n_native=32, remap=remap)
+    Hn, An, _, _ = run_gpu(shape, steps, B, n_native=64, remap=None)
+    for t in range(steps):   # remapping moves memory, never math
+        assert np.array_equal(Hg[t], Hn[t]), t
+        assert Ag[t] == An[t]
+    Ho, Ao, Mo = run_oracle(shape, steps, B)
+    for t in range(steps):
+        ref = Ho[t]
+        rel = np.sqrt(((Hg[t] - ref) ** 2).mean() / (ref ** 2).mean())
+        assert rel <= REL_RMS and np.abs(Hg[t] - ref).max() <= MAX_ABS, (t, rel)
+        for s in range(B):
+            if Mo[t][s] > 0.5:
+                assert Ag[t][s] == Ao[t][s], (t, s)
+    # slot-assignment log == oracle c5 schedule
+    C, beta = remap[1], remap[2]
+    log = ctx.slot_log(mid)
+    exp = [(k, st, l, sl, int(cp)) for k, st, l, sl, cp in OT.slot_log(C, beta, steps - remap[0])]
+    assert log == exp
+    st = ctx.query(mid)
+    assert st["m"] == len(C) and st["beta"] == beta
+    assert st["reclaimed_bytes"] == (len(C) - beta) * weights.layer_bytes(shape)
+    assert st["h2d_copies"] + 2 >= (steps - remap[0]) * len(C) - beta
+
+
+def test_c1_blocks_and_capacity():
+    shape = models.TOY
+    from paper_2507_11507_b200 import Context
+    ctx = Context(harness.arena_for([(shape, 32)], 8, 256), 8, 256)
+    mid = ctx.add_model(shape, harness.make_blob(shape), 32)
+    gained, rb = ctx.remap_layers(mid, mid, [0, 1], 1)
+    assert gained == 48 and rb == weights.layer_bytes(shape)
+    assert ctx.query(mid)["total_blocks"] == 80
+    ids = [i for s in range(10) for i in ctx.alloc_blocks(mid, s, 8)]
+    assert ids == list(range(80))
+    don, off = ctx.block_location(mid, 32)
+    assert (don, off) == (mid, weights.layer_bytes(shape))
+
+
+def test_error_paths():
+    from paper_2507_11507_b200 import Context, MirageError, _lib
+    shape = models.TOY
+    ctx = Context(harness.arena_for([(shape, 4)], 4, 256), 4, 256)
+    mid = ctx.add_model(shape, harness.make_blob(shape), 4)
+    with pytest.raises(MirageError) as e:
+        ctx.decode_step(mid, [0], [1], [0])               # no blocks: refused before enqueue
+    assert e.value.code == _lib.ERR_NO_BLOCKS
+    ctx.alloc_blocks(mid, 0, 1)
+    with pytest.raises(MirageError) as e:
+        ctx.decode_step(mid, [0], [1], [3])               # position != cached length
+    assert e.value.code == _lib.ERR_STATE
+    with pytest.raises(MirageError) as e:
+        ctx.alloc_blocks(mid, 1, 9)
+    assert e.value.code == _lib.ERR_NO_BLOCKS and e.value.shortfall == 6
+    ctx.free_blocks(mid, 0)
+    with pytest.raises(MirageError) as e:
+        ctx.free_blocks(mid, 0)
+    assert e.value.code == _lib.ERR_DOUBLE_FREE
+    with pytest.raises(MirageError) as e:
+        ctx.remap_layers(mid, mid, [0, 1], 0)             # active donor, beta 0
+    assert e.value.code == _lib.ERR_STATE
+    ctx.sync()
