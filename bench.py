@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""bench.py — MIRAGE decode-step hot path on B200 (BASELINE.json configs[1]).
+
+Workload: OPT-13B-shaped decoder, random-init bf16
+weights, a batch of B sequences caught mid-generation with ShareGPT-shaped
+context lengths, under KV pressure: the native KV pool is sized so the batch
+fits only with the blocks reclaimed from the remapped layers' parameter bytes.
+alpha layers are remapped with the planner's uniform-interval placement
+(§5.4) and beta staging slots; their weights are re-streamed from the
+pinned host copy every step. One step = one mirage_decode_step (all §8(a)
+rows) over the batch. Inputs (weights, KV) exceed the 126 MB L2 many times over.
+
+Default: N=1, --steps 30 --warmup 5. N>1 under torchrun: every rank runs its own
+tenant replica on its GPU (weak scaling, no data-path collective).
+--impl reference: the CPU oracle on the host cores (bounded samples), same metric.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode tok/s & p99 TBT under KV pressure; paged-attn HBM GB/s vs peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mirage", choices=["mirage", "reference"])
+    ap.add_argument("--batch", type=int, default=400)
+    ap.add_argument("--alpha", type=int, default=1)
+    ap.add_argument("--beta", type=int, default=1)
+    ap.add_argument("--placement", default="uniform", choices=["uniform", "last"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-resident-arm", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+def nearest_rank(xs, p):
+    s = sorted(xs)
+    return s[max(0, math.ceil(p / 100.0 * len(s)) - 1)]
+
+
+# ---------------------------------------------------------------- clocks ----
+class ClockSampler:
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 9]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------ cpu oracle ----
+def oracle_leg(n_seqs=2, seed=0, steps=1, batch=400):
+    """Time the CPU oracle (oracle/, as it stands) on a bounded sample of the C2
+    workload: one OPT-13B-shaped layer + the LM head for `n_seqs` sequences of the
+    same ShareGPT-shaped context mix, KV from the counter-based generator.
+    Scaled to tok/s of the full 40-layer model:
+      t_token = 40 * (t_layer_step - t_head) / n + t_head / n."""
+    import numpy as np
+    import torch
+    from oracle import kvgen
+    from oracle.decode import Decoder
+    from synth import models, weights, workload
+    shape = models.OPT_13B
+    one = shape.with_layers(1)
+    ctxs = workload.mid_generation_contexts(batch, seed=seed)[:n_seqs]
+    t0 = time.perf_counter()
+    dec = Decoder(one, [weights.layer_tensors(one, 0, seed)], weights.global_tensors(one, seed))
+    for i, L in enumerate(ctxs):
+        K = np.stack([kvgen.kv_values(seed, i, shape.n_layers, 40, 128, 0, h, 0, range(L)) for h in range(40)])
+        V = np.stack([kvgen.kv_values(seed, i, shape.n_layers, 40, 128, 0, h, 1, range(L)) for h in range(40)])
+        dec.set_kv(i, [(K, V)])
+    setup = time.perf_counter() - t0
+    threads = torch.get_num_threads()
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([threads] + [i.get("num_threads", 0) for i in threadpool_info()])
+    except Exception:
+        pass
+    per_step = []
+    for s in range(steps):
+        pos = [int(L) + s for L in ctxs]
+        toks = [workload.teacher_tokens(i, p, shape.vocab) for i, p in enumerate(pos)]
+        t1 = time.perf_counter()
+        dec.step(list(range(n_seqs)), toks, pos)
+        t_step = time.perf_counter() - t1
+        x = np.ones(shape.d_model)
+        t2 = time.perf_counter()
+        for _ in range(n_seqs):
+            dec.G["embed"] @ x
+        t_head = time.perf_counter() - t2
+        t_tok = (shape.n_layers * (t_step - t_head) + t_head) / n_seqs
+        per_step.append(t_tok)
+    return {"tok_s": 1.0 / statistics.median(per_step), "t_token_s": statistics.median(per_step),
+            "cores": threads, "setup_s": setup, "per_step_token_s": per_step,
+            "sample": (f"oracle c4 decode of {n_seqs} seqs (ctx {list(map(int, ctxs))}) through 1 OPT-13B "
+                       f"layer + LM head, fp64 numpy, scaled x{shape.n_layers} layers to tok/s")}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    res = oracle_leg(n_seqs=2, seed=args.seed, steps=args.warmup + args.steps, batch=args.batch)
+    times = res["per_step_token_s"][args.warmup:]
+    tok_s = 1.0 / statistics.median(times)
+    line = {"impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tok/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded random-init weights, counter-based KV, ShareGPT-shaped lengths)",
+            "config": {"workload": "C2 OPT-13B-shaped decode, ShareGPT-shaped contexts (bounded oracle sample)"},
+            "cpu_baseline": {"value": tok_s, "unit": "tok/s", "cores": res["cores"], "kind": "oracle",
+                             "sample": res["sample"]},
+            "e2e": {"value": tok_s, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- mirage arm ---
+def measure_h2d_peak(torch, dev, nbytes=1 << 30):
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s = torch.cuda.Stream(dev)
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record()
+            d.copy_(h, non_blocking=True)
+            e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del h, d
+    return nbytes / best / 1e6
+
+
+def build_workload(args, rank, total_steps):
+    from paper_2507_11507_b200 import _lib
+    from synth import models, workload
+    shape = models.OPT_13B
+    S, G, BB = _lib.model_sizes(shape)
+    max_ctx = shape.max_pos
+    ctxs = workload.mid_generation_contexts(args.batch, seed=args.seed + 1000 * rank, max_ctx=max_ctx)
+    ctxs = [int(min(c, max_ctx - total_steps - 1)) for c in ctxs]
+    need = sum((c + total_steps + 15) // 16 for c in ctxs)
+    if args.alpha:
+        if args.placement == "uniform":
+            cycle, m, beta = _lib.plan(shape.n_layers, args.alpha, args.beta, 0, 1)
+        else:   # last alpha layers reclaimed, the beta layers just before them are the slots
+            m, beta = args.alpha + args.beta, args.beta
+            cycle = list(range(shape.n_layers - m, shape.n_layers))
+        R = cycle[beta:]
+        runs, cur = [], None
+        for l in R:
+            if cur and cur[-1] == l - 1:
+                cur.append(l)
+            else:
+                cur = [l]
+                runs.append(cur)
+        reclaimed = sum(len(r) * S // BB for r in runs)
+    else:
+        cycle, beta, reclaimed = [], 0, 0
+    return shape, ctxs, need, cycle, beta, reclaimed, (S, G, BB)
+
+
+def run_arm(args, torch, dev, shape, blob, ctxs, n_native, cycle, beta, steps, warmup, e2e_steps,
+            clock=None, record=True):
+    """One context: fill KV, warm up, time `steps` decode steps on the device,
+    then `e2e_steps` end-to-end steps (host sync + argmax read-back each step)."""
+    import ctypes as C
+    import harness
+    from paper_2507_11507_b200 import _lib
+    B = len(ctxs)
+    max_ctx = shape.max_pos
+    arena = harness.arena_for([(shape, n_native)], B, max_ctx)
+    ctx = _lib.Context(arena, B, max_ctx, device=dev.index, flags=_lib.FLAG_TIME_ATTN)
+    mid = ctx.add_model(shape, blob, n_native)
+    if cycle:
+        ctx.remap_layers(mid, mid, cycle, beta)
+    for i, L in enumerate(ctxs):
+        ctx.alloc_blocks(mid, i, harness.blocks_for(L))
+        ctx.fill_kv(mid, i, L, seed=args.seed * 7919 + i)
+    ctx.sync()
+    pos = list(ctxs)
+    seq_c = (C.c_int64 * B)(*range(B))
+    tok_c = (C.c_int32 * B)()
+    pos_c = (C.c_int32 * B)()
+    am_c = (C.c_int32 * B)()
+    from synth import workload
+
+    def step(read_back):
+        for i in range(B):
+            if pos[i] % 16 == 0:
+                ctx.alloc_blocks(mid, i, 1)
+            tok_c[i] = workload.teacher_tokens(i, pos[i], shape.vocab)
+            pos_c[i] = pos[i]
+        ctx.decode_step_raw(mid, B, seq_c, tok_c, pos_c, None, am_c if read_back else None)
+        for i in range(B):
+            pos[i] += 1
+
+    for _ in range(warmup):
+        step(False)
+    ctx.sync()
+    st0 = ctx.query(mid)
+    l0 = ctx.kernel_launches()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    if torch.distributed.is_initialized():
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    if clock:
+        clock.start()
+    cs = ctx.stream
+    evs[0].record(cs)
+    for k in range(steps):
+        step(False)
+        evs[k + 1].record(cs)
+    ctx.sync()
+    torch.cuda.synchronize(dev)
+    clocks = clock.stop() if clock else None
+    step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(steps)]
+    total_ms = evs[0].elapsed_time(evs[steps])
+    launches = ctx.kernel_launches() - l0
+    st1 = ctx.query(mid)
+    # end-to-end: host arrays in, argmax read back to host every step
+    e2e_ms = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        step(True)
+        ctx.sync()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    st2 = ctx.query(mid)
+    out = dict(step_ms=step_ms, total_ms=total_ms, launches=launches, clocks=clocks, e2e_ms=e2e_ms,
+               attn_ms=st1["attn_ms"] - st0["attn_ms"], attn_launches=st1["attn_launches"] - st0["attn_launches"],
+               attn_bytes=st1["attn_bytes"] - st0["attn_bytes"],
+               h2d_ms=st1["h2d_ms"] - st0["h2d_ms"], h2d_bytes=st1["h2d_bytes"] - st0["h2d_bytes"],
+               h2d_copies=st1["h2d_copies"] - st0["h2d_copies"], meta_bytes=st2["last_meta_h2d_bytes"],
+               units=st1["last_attn_units"], split_blocks=st1["last_split_blocks"], stats=st1)
+    ctx.close()
+    del ctx
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_mirage(args, rank, world):
+    import torch
+    import harness
+    lr = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", lr)
+    torch.cuda.set_device(dev)
+    total = args.warmup + args.steps + args.e2e_steps + 1
+    shape, ctxs, need, cycle, beta, reclaimed, (S, G, BB) = build_workload(args, rank, total)
+    n_native = need - reclaimed
+    assert n_native > 0
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    h2d_peak = measure_h2d_peak(torch, dev)
+    t0 = time.time()
+    blob = harness.make_blob(shape, seed=args.seed, model_idx=rank, gen_device=dev)
+    setup_blob_s = time.time() - t0
+    clock = ClockSampler(lr)
+    res = run_arm(args, torch, dev, shape, blob, ctxs, n_native, cycle, beta, args.steps, args.warmup,
+                  args.e2e_steps, clock)
+    resident = None
+    if not args.no_resident_arm and cycle and world == 1:
+        # the same batch with every layer resident (pool grown by the reclaimed blocks)
+        r2 = run_arm(args, torch, dev, shape, blob, ctxs, n_native + reclaimed, [], 0,
+                     max(5, args.steps // 2), 3, 0)
+        resident = statistics.median(r2["step_ms"])
+    B = len(ctxs)
+    t_local = res["total_ms"]
+    t_all = t_local
+    if world > 1:
+        t = torch.tensor([t_local], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_all = float(t.item())
+    tokens = B * args.steps * world
+    value = tokens / (t_all / 1e3)
+    e2e_med = statistics.median(res["e2e_ms"]) if res["e2e_ms"] else None
+    attn_avg_ms = res["attn_ms"] / max(1, res["attn_launches"])
+    attn_bytes_launch = res["attn_bytes"] / max(1, res["attn_launches"])
+    achieved = attn_bytes_launch / (attn_avg_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "attention_traffic.json")))
+        traffic = tr.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            o = oracle_leg(n_seqs=2, seed=args.seed, steps=1, batch=args.batch)
+            cpu = {"value": o["tok_s"], "unit": "tok/s", "cores": o["cores"], "kind": "oracle", "sample": o["sample"]}
+        except Exception as e:  # the CPU leg must not hide the GPU number
+            cpu = {"value": None, "unit": "tok/s", "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {e}"}
+    step_med = statistics.median(res["step_ms"])
+    h2d_gbs = res["h2d_bytes"] / (res["h2d_ms"] * 1e-3) / 1e9 if res["h2d_ms"] else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_all / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: seeded random-init bf16 weights (torch CUDA generator), counter-based KV, ShareGPT-shaped lengths",
+        "config": {"workload": "C2: OPT-13B-shaped decode, 1xB200 per rank, ShareGPT-shaped contexts, "
+                               f"{args.alpha} layer(s) remapped to KV ({args.placement} placement, beta={beta}), "
+                               "native pool sized so the batch fits only with the reclaimed blocks",
+                   "batch_per_gpu": B, "ctx_mean": sum(ctxs) / B, "ctx_max": max(ctxs), "cycle": cycle, "beta": beta,
+                   "native_blocks": n_native, "reclaimed_blocks": reclaimed, "block_bytes": BB, "layer_bytes": S,
+                   "l2": "inputs larger than L2 (weights 26.7 GB + KV per step)", "parallelism": f"tenant-replica x{world}"},
+        "p99_tbt_ms": nearest_rank(res["step_ms"], 99), "p50_tbt_ms": nearest_rank(res["step_ms"], 50),
+        "roofline": {"kernel": "paged_attention_kernel<128,1>", "bound": "hbm", "achieved": achieved,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": attn_bytes_launch, "avg_launch_ms": attn_avg_ms,
+                     "launches": res["attn_launches"], "share_of_step": res["attn_ms"] / t_local,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, of measured)"},
+        "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": h2d_peak, "frac": (h2d_gbs / h2d_peak) if h2d_gbs else None,
+                "bytes_per_step": res["h2d_bytes"] / args.steps, "copies": res["h2d_copies"],
+                "peak_source": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this run"},
+        "remap": {"step_ms_remapped": step_med, "step_ms_all_resident": resident,
+                  "ratio": (step_med / resident) if resident else None},
+        "cpu_baseline": cpu, "clocks": res["clocks"],
+        "e2e": {"value": B / (e2e_med / 1e3) * world if e2e_med else None, "unit": "tok/s",
+                "h2d_bytes_per_step": res["meta_bytes"], "d2h_bytes_per_step": 4 * B,
+                "ms_per_step": e2e_med, "how": "host-timed mirage_decode_step with host token/position arrays, "
+                                               "argmax read back to host and stream sync every step"},
+        "gpu_launches": res["launches"], "setup_blob_s": setup_blob_s,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "mirage":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+            dist.init_process_group("nccl")
+        else:
+            dist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_mirage(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

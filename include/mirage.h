@@ -60,6 +60,8 @@ extern "C" {
 #define MIRAGE_BETA_2 2       /* double buffering          (Eq. 5, :478)  */
 #define MIRAGE_BETA_DYNAMIC 3 /* smallest m with zero predicted stall (reading #6) */
 
+#define MIRAGE_FLAG_TIME_ATTN 1u /* init flag: time every attention launch with events */
+
 #define MIRAGE_BLOCK_TOKENS 16
 #define MIRAGE_MAX_CYCLE 256
 
@@ -74,7 +76,7 @@ typedef struct mirage_init_cfg {
   void* copy_stream;        /* cudaStream_t for H2D re-streaming, NULL -> library's */
   int32_t max_batch;        /* max sequences per decode step                        */
   int32_t max_ctx;          /* max tokens per sequence                              */
-  uint32_t flags;           /* reserved, 0                                          */
+  uint32_t flags;           /* MIRAGE_FLAG_* bits                                   */
   int32_t tp_rank, tp_size; /* tensor parallel rank/size; this version: 0 / 1        */
   void* nccl_comm;          /* reserved, NULL                                       */
 } mirage_init_cfg;
@@ -224,6 +226,14 @@ typedef struct mirage_stats {
   double h2d_ms;            /* summed event time of completed H2D copies         */
   double last_step_ms;      /* event time of the last completed decode step      */
   int64_t steps;
+  /* with MIRAGE_FLAG_TIME_ATTN: completed attention launches, their summed event
+   * time and algorithmic KV bytes (sum over sequences of ctx_len * 2 * H_kv * D * 2) */
+  int64_t attn_launches;
+  double attn_ms;
+  uint64_t attn_bytes;
+  uint64_t last_meta_h2d_bytes; /* step metadata uploaded by the last decode step    */
+  int32_t last_attn_units;      /* attention work units of the last decode step      */
+  int32_t last_split_blocks;    /* blocks per split-K partition of the last step     */
 } mirage_stats;
 
 int32_t mirage_query(mirage_ctx* ctx, int32_t model, mirage_stats* out);

@@ -19,6 +19,7 @@ ERR_NO_BLOCKS, ERR_DOUBLE_FREE, ERR_INFEASIBLE, ERR_PRESSURE, ERR_CUDA, ERR_NCCL
 FAMILY_OPT, FAMILY_LLAMA = 0, 1
 BETA_1, BETA_2, BETA_DYNAMIC = 1, 2, 3
 BLOCK_TOKENS = 16
+FLAG_TIME_ATTN = 1
 MAX_CYCLE = 256
 
 _NAMES = {ERR_CONFIG: "CONFIG", ERR_CAPACITY: "CAPACITY", ERR_RANGE: "RANGE", ERR_STATE: "STATE",
@@ -54,7 +55,9 @@ class Stats(C.Structure):
                 ("m", C.c_int32), ("beta", C.c_int32), ("active", C.c_int32), ("n_seqs", C.c_int32),
                 ("cycle", C.c_int32 * MAX_CYCLE), ("uses", C.c_uint64), ("h2d_copies", C.c_uint64),
                 ("h2d_bytes", C.c_uint64), ("h2d_ms", C.c_double), ("last_step_ms", C.c_double),
-                ("steps", C.c_int64)]
+                ("steps", C.c_int64), ("attn_launches", C.c_int64), ("attn_ms", C.c_double),
+                ("attn_bytes", C.c_uint64), ("last_meta_h2d_bytes", C.c_uint64),
+                ("last_attn_units", C.c_int32), ("last_split_blocks", C.c_int32)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "cycle"}
@@ -173,7 +176,7 @@ class Context:
     """One mirage_ctx on one GPU. Owns (keeps alive) the arena, the streams and
     the host blobs it was given."""
 
-    def __init__(self, arena_bytes, max_batch, max_ctx, device=0, stream=None):
+    def __init__(self, arena_bytes, max_batch, max_ctx, device=0, stream=None, flags=0):
         self.device = torch.device("cuda", device)
         self.arena = torch.empty(int(arena_bytes) + 256, dtype=torch.uint8, device=self.device)
         base = self.arena.data_ptr()
@@ -181,7 +184,7 @@ class Context:
         self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
         self._blobs = []
         cfg = InitCfg(device, self._arena_ptr, int(arena_bytes), BLOCK_TOKENS, self.stream.cuda_stream,
-                      None, max_batch, max_ctx, 0, 0, 1, None)
+                      None, max_batch, max_ctx, flags, 0, 1, None)
         self._ctx = C.c_void_p()
         rc = LIB.mirage_init(C.byref(cfg), C.byref(self._ctx))
         if rc:

@@ -254,31 +254,41 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+// one thread per (row, 8-element chunk); a row is one token of one
+// (layer, kv head, K|V). Writes 16 bytes.
 __global__ void fill_kv_kernel(uint64_t seed, int64_t seq_id, int L, int Hk, int D, int p0,
                                int n, const int32_t* table, const uint64_t* block_base) {
-  const size_t total = (size_t)L * Hk * 2 * n * D;
+  const int cpr = D / 8;
+  const size_t total = (size_t)L * Hk * 2 * n * cpr;
   const uint64_t key = seed * 0x9E3779B97F4A7C15ull;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
        e += (size_t)gridDim.x * blockDim.x) {
-    const int d = (int)(e % D);
-    size_t r = e / D;
-    const int t = (int)(r % n);
-    r /= n;
-    const int kv = (int)(r % 2);
-    r /= 2;
-    const int hk = (int)(r % Hk);
-    const int layer = (int)(r / Hk);
+    const int ch = (int)(e % cpr);
+    uint32_t r = (uint32_t)(e / cpr);
+    const int t = (int)(r % (uint32_t)n);
+    r /= (uint32_t)n;
+    const int kv = (int)(r & 1);
+    r >>= 1;
+    const int hk = (int)(r % (uint32_t)Hk);
+    const int layer = (int)(r / (uint32_t)Hk);
     const int pos = p0 + t;
     const uint64_t base = (((uint64_t)seq_id * L + layer) * Hk + hk) * 2 + kv;
-    const uint64_t idx = (base * (1ull << 20) + (uint64_t)pos) * (uint64_t)D + (uint64_t)d;
-    const uint64_t hsh = splitmix64(idx ^ key);
-    const float u = (float)(uint32_t)(hsh >> 40) * 5.9604644775390625e-08f;  // 2^-24
-    float x = __fsub_rn(__fmul_rn(2.0f, u), 1.0f);
-    if (kv == 0) x = __fmul_rn(x, 1.7320508f);
+    const uint64_t idx0 = (base * (1ull << 20) + (uint64_t)pos) * (uint64_t)D + (uint64_t)(ch * 8);
+    uint32_t packed[4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t hsh = splitmix64((idx0 + j) ^ key);
+      const float u = (float)(uint32_t)(hsh >> 40) * 5.9604644775390625e-08f;  // 2^-24
+      float x = __fsub_rn(__fmul_rn(2.0f, u), 1.0f);
+      if (kv == 0) x = __fmul_rn(x, 1.7320508f);
+      const uint32_t b = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x));
+      if (j & 1) packed[j >> 1] |= b << 16;
+      else packed[j >> 1] = b;
+    }
     const int32_t blk = table[pos >> 4];
-    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(
-        block_base[blk] + ((((uint64_t)layer * Hk + hk) * 2 + kv) * 16 + (pos & 15)) * D * 2);
-    dst[d] = __float2bfloat16_rn(x);
+    uint4* dst = reinterpret_cast<uint4*>(
+        block_base[blk] + ((((uint64_t)layer * Hk + hk) * 2 + kv) * 16 + (pos & 15)) * D * 2 + ch * 16);
+    *dst = make_uint4(packed[0], packed[1], packed[2], packed[3]);
   }
 }
 
@@ -355,7 +365,7 @@ cudaError_t launch_argmax(int B, int V, const float* logits, int32_t* out, cudaS
 
 cudaError_t launch_fill_kv(uint64_t seed, int64_t seq_id, int L, int Hk, int D, int p0, int n,
                            const int32_t* table, const uint64_t* block_base, cudaStream_t s) {
-  const size_t total = (size_t)L * Hk * 2 * n * D;
+  const size_t total = (size_t)L * Hk * 2 * n * (D / 8);
   if (!total) return cudaSuccess;
   fill_kv_kernel<<<grid_for(total, 256), 256, 0, s>>>(seed, seq_id, L, Hk, D, p0, n, table,
                                                      block_base);

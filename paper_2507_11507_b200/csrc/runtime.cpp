@@ -172,6 +172,18 @@ struct Model {
   int32_t* tickets = nullptr;
   int32_t* argmax = nullptr;
   int y_ld_max = 0;
+  // ---- attention kernel timing (MIRAGE_FLAG_TIME_ATTN) ----
+  struct AttnTiming {
+    cudaEvent_t t0, t1;
+    uint64_t bytes;
+  };
+  std::deque<AttnTiming> attn_pending;
+  std::vector<cudaEvent_t> ev_pool;
+  int64_t attn_launches = 0;
+  double attn_ms = 0;
+  uint64_t attn_bytes = 0;
+  uint64_t last_meta = 0;
+  int32_t last_units = 0, last_split = 0;
   // ---- step timing ----
   cudaEvent_t st0 = nullptr, st1 = nullptr;
   bool step_timed = false;
@@ -399,6 +411,33 @@ void harvest_copy_times(Model* M) {
   (void)cudaGetLastError();
 }
 
+void harvest_attn_times(Model* M) {
+  while (!M->attn_pending.empty()) {
+    auto& t = M->attn_pending.front();
+    if (cudaEventQuery(t.t1) != cudaSuccess) break;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t.t0, t.t1);
+    M->attn_ms += ms;
+    M->attn_bytes += t.bytes;
+    M->attn_launches += 1;
+    M->ev_pool.push_back(t.t0);
+    M->ev_pool.push_back(t.t1);
+    M->attn_pending.pop_front();
+  }
+  (void)cudaGetLastError();
+}
+
+cudaEvent_t pool_event(Model* M) {
+  if (!M->ev_pool.empty()) {
+    cudaEvent_t e = M->ev_pool.back();
+    M->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
 void harvest_step_time(Model* M) {
   if (M->step_timed && cudaEventQuery(M->st1) == cudaSuccess) {
     float ms = 0;
@@ -501,6 +540,11 @@ void mirage_destroy(mirage_ctx* c) {
     if (M->st0) cudaEventDestroy(M->st0);
     if (M->st1) cudaEventDestroy(M->st1);
     if (M->bbase_dev) cudaFree(M->bbase_dev);
+    for (auto& t : M->attn_pending) {
+      cudaEventDestroy(t.t0);
+      cudaEventDestroy(t.t1);
+    }
+    for (auto e : M->ev_pool) cudaEventDestroy(e);
     delete M;
   }
   for (int i = 0; i < 2; ++i) {
@@ -808,6 +852,9 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   if (timed) CK(c, cudaEventRecord(M->st0, cs));
   CK(c, cudaMemcpyAsync(c->meta_dev, host, head + tbl_bytes, cudaMemcpyHostToDevice, cs));
   CK(c, cudaEventRecord(c->stage_ev[c->stage_i], cs));
+  M->last_meta = head + tbl_bytes;
+  M->last_units = n_units;
+  M->last_split = split_blocks;
 
   const GlobalW gw = global_ptrs(s, M->w_dev + (uint64_t)s.n * M->sz.S);
   const int d = s.d, H = s.H, Hk = s.Hk, D = s.D, qkvN = (H + 2 * Hk) * D;
@@ -880,6 +927,10 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   ap.tickets = M->tickets;
   ap.out = M->x;  // bf16 [B][H*D]: the O-projection input
   ap.out_fp32 = 0;
+  const bool time_attn = c->cfg.flags & MIRAGE_FLAG_TIME_ATTN;
+  uint64_t attn_bytes = 0;
+  for (int i = 0; i < B; ++i) attn_bytes += (uint64_t)hv.len[i] * 2 * Hk * D * 2;
+  if (time_attn) harvest_attn_times(M);
   for (int l = 0; l < s.n; ++l) {
     const LayerW w = layer_ptrs(s, wptr[l]);
     const uint64_t layer_off = (uint64_t)l * Hk * 2 * kBlockTokens * D * 2;
@@ -887,7 +938,15 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     KL(c, mirage::launch_qkv_post(s.family, B, H, Hk, D, M->y, opt ? w.b_qkv : nullptr, dv.pos,
                                  dv.tables, pitch, M->bbase_dev, layer_off, s.theta, M->q, cs));
     ap.layer_off = layer_off;
-    KL(c, mirage::launch_paged_attention(ap, cs));
+    if (time_attn) {
+      Model::AttnTiming at{pool_event(M), pool_event(M), attn_bytes};
+      CK(c, cudaEventRecord(at.t0, cs));
+      KL(c, mirage::launch_paged_attention(ap, cs));
+      CK(c, cudaEventRecord(at.t1, cs));
+      M->attn_pending.push_back(at);
+    } else {
+      KL(c, mirage::launch_paged_attention(ap, cs));
+    }
     if (int32_t e = gemm(c, B, d, H * D, w.w_o, M->x, M->y, d)) return e;
     KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_o : nullptr, w.n2_g,
                                       opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs));
@@ -1061,6 +1120,7 @@ int32_t mirage_query(mirage_ctx* c, int32_t model, mirage_stats* o) {
   if (!M || !o) return fail(c, MIRAGE_ERR_RANGE, "query: model %d", model);
   harvest_copy_times(M);
   harvest_step_time(M);
+  harvest_attn_times(M);
   std::memset(o, 0, sizeof *o);
   o->native_blocks = M->n_native;
   o->total_blocks = M->next_id;
@@ -1080,6 +1140,12 @@ int32_t mirage_query(mirage_ctx* c, int32_t model, mirage_stats* o) {
   o->h2d_ms = M->h2d_ms;
   o->last_step_ms = M->last_step_ms;
   o->steps = M->steps;
+  o->attn_launches = M->attn_launches;
+  o->attn_ms = M->attn_ms;
+  o->attn_bytes = M->attn_bytes;
+  o->last_meta_h2d_bytes = M->last_meta;
+  o->last_attn_units = M->last_units;
+  o->last_split_blocks = M->last_split;
   return MIRAGE_OK;
 }
 
