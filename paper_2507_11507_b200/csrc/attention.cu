@@ -11,8 +11,10 @@
 //   * grid = (units, H_kv); a unit is one (sequence, split) pair; CTA = 4 warps;
 //     warp w handles blocks w, w+4, ... of the split (placement independent).
 //   * one 16-token block of one (layer, kv-head) is a contiguous 2*16*D*2-byte
-//     K|V tile; a warp fetches it with 16-byte coalesced ld.global.nc (512 B per
-//     instruction), software-prefetching the next block.
+//     K|V tile, fetched whole by one cp.async.bulk (TMA engine) into shared
+//     memory; every warp runs its own NS-deep ring (mbarrier complete_tx), so
+//     NS tiles per warp are in flight while it computes; block addresses
+//     (table -> block_base) are resolved 32 at a time, one per lane.
 //   * lane owns 8 head dims (dims fixed per lane); QK partial dots are reduced
 //     with a transpose-reduction (D/16 values across D/8 lanes in D/16 + 1
 //     shuffles); online softmax in base 2; PV accumulates in registers.
@@ -21,21 +23,13 @@
 //     only on logical lengths, so outputs are bit-identical under any physical
 //     placement of the blocks (remap invariance).
 #include <math_constants.h>
+#include <stdlib.h>
 
 #include "kernels.cuh"
 
 namespace mirage {
 namespace {
 
-constexpr int kWarps = 4;
-
-__device__ __forceinline__ uint4 ldg_stream(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
@@ -47,13 +41,59 @@ __device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
   f[6] = bf_lo(v.w); f[7] = bf_hi(v.w);
 }
 
-template <int D, int G>
-__global__ void __launch_bounds__(kWarps * 32)
+// ---- mbarrier / bulk-copy (TMA engine) helpers ------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// 1-D bulk copy global -> shared, completion counted on `bar` (cp.async.bulk).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+
+constexpr int kMaxSplitsDev = 64;  // split-K partitions per (sequence, kv head)
+
+template <int D, int W, int NS>
+constexpr int smem_bytes() { return W * NS * 2 * (16 * D * 2); }
+
+// W warps per CTA; every warp runs its own NS-deep ring of K|V tiles.
+template <int D, int G, int W, int NS>
+__global__ void __launch_bounds__(W * 32)
 paged_attention_kernel(const AttnParams p) {
+  constexpr int kWarps = W;
   constexpr int CPR = D / 8;        // 16-byte chunks per token row
-  constexpr int TPI = 32 / CPR;     // token rows per warp-wide load
-  constexpr int ITERS = 16 / TPI;   // loads per 16-token tile (== CPR / 2)
+  constexpr int TPI = 32 / CPR;     // token rows per warp-wide chunk sweep
+  constexpr int ITERS = 16 / TPI;   // chunk sweeps per 16-token tile (== CPR / 2)
   constexpr int TILE = 16 * D * 2;  // bytes of K (or V) of one block/layer/head
+
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[kWarps][NS];
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -67,6 +107,35 @@ paged_attention_kernel(const AttnParams p) {
   const int dim0 = (lane % CPR) * 8;
   const int32_t* tbl = p.tables + (size_t)s * p.tbl_pitch;
   const uint64_t head_off = p.layer_off + (uint64_t)hk * (2 * TILE);
+  uint8_t* ring = smem + (size_t)warp * NS * 2 * TILE;
+  // this warp's blocks: b0 + warp + kWarps * it, it < n_it
+  const int first = b0 + warp;
+  const int n_it = first < b1 ? (b1 - first + kWarps - 1) / kWarps : 0;
+
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) mbar_init(&bars[warp][i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // block addresses of iterations [base, base + 32) live one per lane
+  int addr_base = 0;
+  uint64_t my_addr = 0;
+  if (lane < n_it) my_addr = p.block_base[tbl[first + kWarps * lane]] + head_off;
+  auto addr_of = [&](int it) -> uint64_t {  // warp-uniform it within [addr_base, addr_base+32)
+    return __shfl_sync(0xffffffffu, my_addr, it - addr_base);
+  };
+  // prologue: fill the ring
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    if (i < n_it) {
+      const uint64_t a = addr_of(i);
+      if (lane == 0) {
+        mbar_expect_tx(&bars[warp][i], 2 * TILE);
+        bulk_g2s(ring + i * 2 * TILE, reinterpret_cast<const void*>(a), 2 * TILE, &bars[warp][i]);
+      }
+    }
+  }
 
   float qr[G][8];
 #pragma unroll
@@ -89,47 +158,36 @@ paged_attention_kernel(const AttnParams p) {
   }
 
   // token held (after the transpose-reduction) by this lane, and the lane that
-  // holds the score of the token whose V row this lane owns in load i.
+  // holds the score of the token whose V row this lane owns in sweep i.
   const int my_i = (lane >> 1) & (ITERS - 1);
   const int my_tok = my_i * TPI + lane / CPR;
   const int src_base = (lane / CPR) * CPR;
 
-  uint4 kr[ITERS], vr[ITERS];
-  int blk = b0 + warp;
-  if (blk < b1) {
-    const char* base = reinterpret_cast<const char*>(p.block_base[tbl[blk]] + head_off);
-#pragma unroll
-    for (int i = 0; i < ITERS; ++i) {
-      kr[i] = ldg_stream(base + (size_t)(i * 32 + lane) * 16);
-      vr[i] = ldg_stream(base + TILE + (size_t)(i * 32 + lane) * 16);
-    }
-  }
-  for (; blk < b1; blk += kWarps) {
-    // prefetch the next block of this warp
-    uint4 nk[ITERS], nv[ITERS];
-    const int nb = blk + kWarps;
-    if (nb < b1) {
-      const char* base = reinterpret_cast<const char*>(p.block_base[tbl[nb]] + head_off);
-#pragma unroll
-      for (int i = 0; i < ITERS; ++i) {
-        nk[i] = ldg_stream(base + (size_t)(i * 32 + lane) * 16);
-        nv[i] = ldg_stream(base + TILE + (size_t)(i * 32 + lane) * 16);
-      }
-    }
+  for (int it = 0; it < n_it; ++it) {
+    const int st = it % NS;
+    const uint32_t phase = (it / NS) & 1;
+    const int blk = first + kWarps * it;
+    mbar_wait(&bars[warp][st], phase);
+    const uint8_t* tile = ring + st * 2 * TILE;
     const bool valid = blk * 16 + my_tok < L;
     const bool tail = blk * 16 + 16 > L;
+    float part[G][ITERS];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float v[ITERS];
+    for (int i = 0; i < ITERS; ++i) {
+      float kf[8];
+      unpack8(lds128(tile + (i * 32 + lane) * 16), kf);
 #pragma unroll
-      for (int i = 0; i < ITERS; ++i) {
-        float kf[8];
-        unpack8(kr[i], kf);
+      for (int g = 0; g < G; ++g) {
         float a = 0.f;
 #pragma unroll
         for (int j = 0; j < 8; ++j) a = fmaf(qr[g][j], kf[j], a);
-        v[i] = a;
+        part[g][i] = a;
       }
+    }
+    float pr[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float* v = part[g];
       // transpose-reduction over the CPR lanes sharing a token row
       int n = ITERS;
 #pragma unroll
@@ -156,30 +214,43 @@ paged_attention_kernel(const AttnParams p) {
       for (int mask = 1; mask < 32; mask <<= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, mask));
       const float m_new = fmaxf(m[g], bm);
       const float alpha = exp2f(m[g] - m_new);
-      const float pr = valid ? exp2f(sc - m_new) : 0.f;
-      float ps = pr;
+      pr[g] = valid ? exp2f(sc - m_new) : 0.f;
+      float ps = pr[g];
 #pragma unroll
       for (int mask = 2; mask < 32; mask <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, mask);
       l[g] = l[g] * alpha + ps;
       m[g] = m_new;
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[g][j] *= alpha;
-#pragma unroll
-      for (int i = 0; i < ITERS; ++i) {
-        const float pi = __shfl_sync(0xffffffffu, pr, src_base + (i << 1));
-        // rows past the context may hold any bytes (NaN/Inf): skip, don't multiply by 0
-        if (tail && blk * 16 + i * TPI + lane / CPR >= L) continue;
-        float vf[8];
-        unpack8(vr[i], vf);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[g][j] = fmaf(pi, vf[j], acc[g][j]);
-      }
     }
-    if (nb < b1) {
 #pragma unroll
-      for (int i = 0; i < ITERS; ++i) {
-        kr[i] = nk[i];
-        vr[i] = nv[i];
+    for (int i = 0; i < ITERS; ++i) {
+      float pi[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) pi[g] = __shfl_sync(0xffffffffu, pr[g], src_base + (i << 1));
+      // rows past the context may hold any bytes (NaN/Inf): skip, don't multiply by 0
+      if (tail && blk * 16 + i * TPI + lane / CPR >= L) continue;
+      float vf[8];
+      unpack8(lds128(tile + TILE + (i * 32 + lane) * 16), vf);
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[g][j] = fmaf(pi[g], vf[j], acc[g][j]);
+    }
+    // refill this stage with iteration it + NS (all lanes are done reading it)
+    const int nx = it + NS;
+    if (nx < n_it) {
+      if (nx - addr_base >= 32) {  // next window of 32 block addresses
+        addr_base += 32;
+        const int j = addr_base + lane;
+        my_addr = j < n_it ? p.block_base[tbl[first + kWarps * j]] + head_off : 0;
+      }
+      const uint64_t a = addr_of(nx);
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bars[warp][st], 2 * TILE);
+        bulk_g2s(ring + st * 2 * TILE, reinterpret_cast<const void*>(a), 2 * TILE, &bars[warp][st]);
       }
     }
   }
@@ -253,39 +324,97 @@ paged_attention_kernel(const AttnParams p) {
   __syncthreads();
   if (!am_last) return;
   __threadfence();
+  // split weights w_i = 2^(m_i - M), Lambda = sum_i w_i l_i (fixed order i = 0..S-1)
+  __shared__ float sw[kMaxSplitsDev][G];
+  __shared__ float sL[G];
+  const size_t stride = (size_t)p.H * (D + 2);
+  const float* rec0 = p.partial + ((size_t)u.pbase * p.H + hk * G) * (D + 2);
+  for (int e = threadIdx.x; e < u.nsplit * G; e += kWarps * 32) {
+    const int i = e / G, g = e % G;
+    sw[i][g] = __ldcg(rec0 + i * stride + g * (D + 2) + D);
+  }
+  __syncthreads();
+  if (threadIdx.x < G) {
+    const int g = threadIdx.x;
+    float M = -CUDART_INF_F;
+    for (int i = 0; i < u.nsplit; ++i) M = fmaxf(M, sw[i][g]);
+    float Ls = 0.f;
+    for (int i = 0; i < u.nsplit; ++i) {
+      const float w = exp2f(sw[i][g] - M);
+      Ls += w * __ldcg(rec0 + i * stride + g * (D + 2) + D + 1);
+      sw[i][g] = w;
+    }
+    sL[g] = Ls;
+  }
+  __syncthreads();
   for (int e = threadIdx.x; e < G * D; e += kWarps * 32) {
     const int g = e / D, d = e % D;
-    const int h = hk * G + g;
-    const float* rec0 = p.partial + ((size_t)u.pbase * p.H + h) * (D + 2);
-    const size_t stride = (size_t)p.H * (D + 2);
-    float M = -CUDART_INF_F;
-    for (int i = 0; i < u.nsplit; ++i) M = fmaxf(M, __ldcg(rec0 + i * stride + D));
-    float Ls = 0.f, o = 0.f;
-    for (int i = 0; i < u.nsplit; ++i) {
-      const float* rec = rec0 + i * stride;
-      const float f = exp2f(__ldcg(rec + D) - M);
-      Ls += f * __ldcg(rec + D + 1);
-      o += f * __ldcg(rec + d);
+    const float* rec = rec0 + g * (D + 2) + d;
+    float o = 0.f;
+    int i = 0;
+    for (; i + 4 <= u.nsplit; i += 4) {  // independent loads in flight
+      const float a0 = __ldcg(rec + (i + 0) * stride), a1 = __ldcg(rec + (i + 1) * stride);
+      const float a2 = __ldcg(rec + (i + 2) * stride), a3 = __ldcg(rec + (i + 3) * stride);
+      o += sw[i][g] * a0;
+      o += sw[i + 1][g] * a1;
+      o += sw[i + 2][g] * a2;
+      o += sw[i + 3][g] * a3;
     }
-    const float r = o / Ls;
-    const size_t oi = ((size_t)s * p.H + h) * D + d;
+    for (; i < u.nsplit; ++i) o += sw[i][g] * __ldcg(rec + i * stride);
+    const float r = o / sL[g];
+    const size_t oi = ((size_t)s * p.H + hk * G + g) * D + d;
     if (p.out_fp32) reinterpret_cast<float*>(p.out)[oi] = r;
     else reinterpret_cast<__nv_bfloat16*>(p.out)[oi] = __float2bfloat16_rn(r);
   }
 }
 
+template <int D, int G, int W, int NS>
+cudaError_t launch_v(const AttnParams& p, cudaStream_t s) {
+  constexpr int SMEM = smem_bytes<D, W, NS>();
+  static bool configured = false;  // opt in to > 48 KB dynamic shared memory once
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(paged_attention_kernel<D, G, W, NS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid(p.n_units, p.H_kv);
+  paged_attention_kernel<D, G, W, NS><<<grid, W * 32, SMEM, s>>>(p);
+  return cudaGetLastError();
+}
+
+// tuning hook: MIRAGE_ATTN_VARIANT=0..3 selects (warps, stages) for D=128, G=1
+int variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MIRAGE_ATTN_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <int D, int G>
+cudaError_t launch_dg(const AttnParams& p, cudaStream_t s) {
+  if (D == 128 && G == 1) {
+    switch (variant()) {
+      case 1: return launch_v<D, G, 4, 3>(p, s);
+      case 2: return launch_v<D, G, 8, 2>(p, s);
+      case 3: return launch_v<D, G, 2, 4>(p, s);
+      default: break;
+    }
+  }
+  return launch_v<D, G, 4, D == 128 ? 2 : 4>(p, s);
+}
+
 template <int D>
 cudaError_t launch_d(const AttnParams& p, cudaStream_t s) {
-  dim3 grid(p.n_units, p.H_kv);
-  const int G = p.H / p.H_kv;
-  switch (G) {
-    case 1: paged_attention_kernel<D, 1><<<grid, kWarps * 32, 0, s>>>(p); break;
-    case 2: paged_attention_kernel<D, 2><<<grid, kWarps * 32, 0, s>>>(p); break;
-    case 4: paged_attention_kernel<D, 4><<<grid, kWarps * 32, 0, s>>>(p); break;
-    case 8: paged_attention_kernel<D, 8><<<grid, kWarps * 32, 0, s>>>(p); break;
+  switch (p.H / p.H_kv) {
+    case 1: return launch_dg<D, 1>(p, s);
+    case 2: return launch_dg<D, 2>(p, s);
+    case 4: return launch_dg<D, 4>(p, s);
+    case 8: return launch_dg<D, 8>(p, s);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace

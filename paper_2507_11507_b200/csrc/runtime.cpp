@@ -387,7 +387,7 @@ int build_units(const int32_t* lens, int B, int Hk, int override_blocks, mirage:
   for (int b = 0; b < B; ++b) {
     const int nb = (lens[b] + kBlockTokens - 1) / kBlockTokens;
     const int ns = std::max(1, (nb + P - 1) / P);
-    if (n + ns > max_units) return -1;
+    if (n + ns > max_units || ns > kMaxSplits) return -1;
     for (int i = 0; i < ns; ++i) units[n++] = mirage::AttnUnit{b, i, ns, ns > 1 ? pbase : 0};
     if (ns > 1) pbase += ns;
   }

@@ -1,0 +1,76 @@
+"""Attention-kernel microbenchmark through the C-ABI hook mirage_attn_only.
+
+Shapes keep the KV geometry of the bench configs (layers, H, H_kv, D) with
+minimal weights (the kernel never reads them). Times back-to-back launches with
+CUDA events on the library's compute stream; every launch reads > L2.
+Usage: python tools/attn_bench.py [--case NAME ...] [--reps N]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import harness  # noqa: E402
+from paper_2507_11507_b200 import _lib  # noqa: E402
+from synth import models, workload  # noqa: E402
+
+CASES = {
+    # name: (n_layers, H, Hk, D, batch, contexts)
+    "opt13b_b400": (40, 40, 40, 128, 400, "sharegpt"),
+    "opt13b_b64": (40, 40, 40, 128, 64, "sharegpt"),
+    "opt13b_b29": (40, 40, 40, 128, 29, "sharegpt"),
+    "llama3_8b_32x8k": (32, 32, 8, 128, 32, 8192),
+    "llama3_8b_1x32k": (32, 32, 8, 128, 1, 32768),
+    "llama3_8b_4x16k": (32, 32, 8, 128, 4, 16384),
+    "llama70b_tp8_64x4k": (80, 8, 1, 128, 64, 4096),
+}
+
+
+def run(name, reps, seed=0):
+    L, H, Hk, D, B, ctx = CASES[name]
+    shape = models.ModelShape(f"attn-{name}", models.LLAMA, L, 128, H, Hk, D, 128, 128, 65536)
+    lens = ([int(c) for c in workload.mid_generation_contexts(B, seed=seed)] if ctx == "sharegpt" else [ctx] * B)
+    need = sum(harness.blocks_for(x) for x in lens)
+    max_ctx = max(lens) + 16
+    arena = harness.arena_for([(shape, need)], B, max_ctx)
+    ctx_ = _lib.Context(arena, B, max_ctx)
+    mid = ctx_.add_model(shape, harness.make_blob(shape), need)
+    for i, x in enumerate(lens):
+        ctx_.alloc_blocks(mid, i, harness.blocks_for(x))
+        ctx_.fill_kv(mid, i, x, seed=i)
+    q = workload.queries(B, H, D, seed=1).cuda()
+    out = torch.empty((B, H, D), dtype=torch.bfloat16, device="cuda")
+    ctx_.sync()
+    layers = list(range(L))
+    for w in range(3):
+        ctx_.attn_only(mid, layers[w % L], list(range(B)), q, out)
+    ctx_.sync()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    ev[0].record(ctx_.stream)
+    for r in range(reps):
+        ctx_.attn_only(mid, layers[r % L], list(range(B)), q, out)
+        ev[r + 1].record(ctx_.stream)
+    ctx_.sync()
+    ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(reps)]
+    ms.sort()
+    med = ms[len(ms) // 2]
+    nbytes = sum(lens) * 2 * Hk * D * 2
+    st = ctx_.query(mid)
+    ctx_.close()
+    return {"case": name, "batch": B, "ctx_sum": sum(lens), "bytes": nbytes, "median_ms": med, "best_ms": ms[0],
+            "gbs_median": nbytes / med / 1e6, "gbs_best": nbytes / ms[0] / 1e6}
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", nargs="*", default=list(CASES))
+    ap.add_argument("--reps", type=int, default=20)
+    a = ap.parse_args()
+    for c in a.case:
+        print(json.dumps(run(c, a.reps)), flush=True)
