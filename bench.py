@@ -251,11 +251,13 @@ def run_arm(args, torch, dev, shape, blob, ctxs, n_native, cycle, beta, steps, w
     if clock:
         clock.start()
     cs = ctx.stream
+    torch.cuda.nvtx.range_push("timed")
     evs[0].record(cs)
     for k in range(steps):
         step(False)
         evs[k + 1].record(cs)
     ctx.sync()
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize(dev)
     clocks = clock.stop() if clock else None
     step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(steps)]

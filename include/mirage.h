@@ -109,7 +109,10 @@ typedef struct mirage_model_cfg {
  *          Llama: embed[V,d] normf_g[d] lm_head[V,d]
  *
  * KV block layout (device): one physical block holds 16 tokens of ALL layers:
- *   [L][H_kv][2 (K,V)][16][D] bf16, BB = L*H_kv*2*16*D*2 bytes.
+ *   [L][H_kv][2 (K,V)][16 rows][D] bf16, BB = L*H_kv*2*16*D*2 bytes. Within a
+ *   row r (token pos % 16), element c is stored at position
+ *   ((c / 8) ^ (r % 8)) * 8 + c % 8 (16-byte chunks XOR-swizzled by row) so the
+ *   attention kernel's tensor-core fragment loads are bank-conflict free.
  * Block ids [0, N0) are the native pool; reclaimed ids are appended after.
  */
 

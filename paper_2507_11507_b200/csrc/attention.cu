@@ -7,7 +7,7 @@
 // block may sit in the native pool or in reclaimed parameter memory
 // (PAPER.md:161 PagedAttention; :558-564 reclaimed memory reused as KV).
 //
-// Design (HBM-bound gather, AI = G flop/B — CUDA cores, no tensor cores):
+// Design (HBM-bound gather; AI = G flop/B):
 //   * grid = (units, H_kv); a unit is one (sequence, split) pair; CTA = 4 warps;
 //     warp w handles blocks w, w+4, ... of the split (placement independent).
 //   * one 16-token block of one (layer, kv-head) is a contiguous 2*16*D*2-byte
@@ -15,9 +15,11 @@
 //     memory; every warp runs its own NS-deep ring (mbarrier complete_tx), so
 //     NS tiles per warp are in flight while it computes; block addresses
 //     (table -> block_base) are resolved 32 at a time, one per lane.
-//   * lane owns 8 head dims (dims fixed per lane); QK partial dots are reduced
-//     with a transpose-reduction (D/16 values across D/8 lanes in D/16 + 1
-//     shuffles); online softmax in base 2; PV accumulates in registers.
+//   * QK^T and PV run on the tensor cores (mma.sync m16n8k16 bf16 -> fp32) with
+//     q and p carried as bf16 hi+lo column pairs (near-fp32 accuracy); this cuts
+//     the per-tile instruction count ~6x versus CUDA-core dot products so the
+//     kernel stays memory-bound for every group size G in {1, 2, 4, 8}.
+//     Online softmax in base 2 on the accumulator fragments.
 //   * deterministic: fixed block->warp map, fixed warp merge order, fixed split
 //     combine order by the last-arriving CTA (atomic ticket). Split sizes depend
 //     only on logical lengths, so outputs are bit-identical under any physical
@@ -30,16 +32,6 @@
 namespace mirage {
 namespace {
 
-
-__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
-
-__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
-  f[0] = bf_lo(v.x); f[1] = bf_hi(v.x);
-  f[2] = bf_lo(v.y); f[3] = bf_hi(v.y);
-  f[4] = bf_lo(v.z); f[5] = bf_hi(v.z);
-  f[6] = bf_lo(v.w); f[7] = bf_hi(v.w);
-}
 
 // ---- mbarrier / bulk-copy (TMA engine) helpers ------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -69,12 +61,34 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ uint4 lds128(const void* p) {
-  uint4 r;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(smem_u32(p)));
-  return r;
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+// D[16x8] += A[16x16] * B[16x8], bf16 in, fp32 accumulate (tensor cores)
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+// x = hi + lo with hi = bf16(x), lo = bf16(x - hi): the pair carries ~16 mantissa bits
+__device__ __forceinline__ float bf16_part(float x, int part) {
+  const float hi = __bfloat162float(__float2bfloat16_rn(x));
+  return part ? x - hi : hi;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
+  const uint32_t a = __bfloat16_as_ushort(__float2bfloat16_rn(lo_elem));
+  const uint32_t b = __bfloat16_as_ushort(__float2bfloat16_rn(hi_elem));
+  return a | (b << 16);
 }
 
 constexpr int kMaxSplitsDev = 64;  // split-K partitions per (sequence, kv head)
@@ -82,21 +96,30 @@ constexpr int kMaxSplitsDev = 64;  // split-K partitions per (sequence, kv head)
 template <int D, int W, int NS>
 constexpr int smem_bytes() { return W * NS * 2 * (16 * D * 2); }
 
-// W warps per CTA; every warp runs its own NS-deep ring of K|V tiles.
+// Tensor-core formulation per 16-token tile (one warp):
+//   S[16 tok x 8 col] = K[16 x D] * Qc[D x 8]      (D/16 mma.m16n8k16 per n-tile)
+//   O^T[D x 8]       += V^T[D x 16] * P[16 x 8]    (D/16 mma per n-tile)
+// where column n = 2*head + part holds the bf16 hi (part 0) or lo (part 1) half
+// of q (resp. p), so the fp32 accumulators see q and p to ~16 mantissa bits
+// while K and V stay exact bf16. G <= 4 heads fill one n8 tile, G = 8 two.
+// The KV tile is stored XOR-swizzled in 16-byte chunks (chunk ^ (row & 7), see
+// include/mirage.h), which makes every ldmatrix below bank-conflict free.
 template <int D, int G, int W, int NS>
 __global__ void __launch_bounds__(W * 32)
 paged_attention_kernel(const AttnParams p) {
   constexpr int kWarps = W;
-  constexpr int CPR = D / 8;        // 16-byte chunks per token row
-  constexpr int TPI = 32 / CPR;     // token rows per warp-wide chunk sweep
-  constexpr int ITERS = 16 / TPI;   // chunk sweeps per 16-token tile (== CPR / 2)
-  constexpr int TILE = 16 * D * 2;  // bytes of K (or V) of one block/layer/head
+  constexpr int TILE = 16 * D * 2;    // bytes of K (or V) of one block/layer/head
+  constexpr int ROW = 2 * D;          // bytes per token row
+  constexpr int KS = D / 16;          // k-slices (QK) == dim tiles (PV)
+  constexpr int NT = (2 * G + 7) / 8; // n8 tiles of (head, part) columns
 
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[kWarps][NS];
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  const int gq = lane >> 2;  // mma group id (row / column index)
+  const int tq = lane & 3;   // thread in group
   const AttnUnit u = p.units[blockIdx.x];
   const int hk = blockIdx.y;
   const int s = u.seq;
@@ -104,12 +127,10 @@ paged_attention_kernel(const AttnParams p) {
   const int nblk = (L + 15) >> 4;
   const int b0 = u.split * p.split_blocks;
   const int b1 = min(b0 + p.split_blocks, nblk);
-  const int dim0 = (lane % CPR) * 8;
   const int32_t* tbl = p.tables + (size_t)s * p.tbl_pitch;
   const uint64_t head_off = p.layer_off + (uint64_t)hk * (2 * TILE);
   uint8_t* ring = smem + (size_t)warp * NS * 2 * TILE;
-  // this warp's blocks: b0 + warp + kWarps * it, it < n_it
-  const int first = b0 + warp;
+  const int first = b0 + warp;  // this warp's blocks: first + W * it
   const int n_it = first < b1 ? (b1 - first + kWarps - 1) / kWarps : 0;
 
   if (lane == 0) {
@@ -118,14 +139,10 @@ paged_attention_kernel(const AttnParams p) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  // block addresses of iterations [base, base + 32) live one per lane
   int addr_base = 0;
   uint64_t my_addr = 0;
   if (lane < n_it) my_addr = p.block_base[tbl[first + kWarps * lane]] + head_off;
-  auto addr_of = [&](int it) -> uint64_t {  // warp-uniform it within [addr_base, addr_base+32)
-    return __shfl_sync(0xffffffffu, my_addr, it - addr_base);
-  };
-  // prologue: fill the ring
+  auto addr_of = [&](int it) -> uint64_t { return __shfl_sync(0xffffffffu, my_addr, it - addr_base); };
 #pragma unroll
   for (int i = 0; i < NS; ++i) {
     if (i < n_it) {
@@ -137,105 +154,113 @@ paged_attention_kernel(const AttnParams p) {
     }
   }
 
-  float qr[G][8];
+  // B fragments of the query columns: column n = gq (+8 nt): head nt*4 + gq/2, part gq&1
+  uint32_t qb[NT][KS][2];
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const float* qp = p.q + ((size_t)s * p.H + hk * G + g) * D + dim0;
-    float4 a = *reinterpret_cast<const float4*>(qp);
-    float4 b = *reinterpret_cast<const float4*>(qp + 4);
-    qr[g][0] = a.x * p.scale_log2; qr[g][1] = a.y * p.scale_log2;
-    qr[g][2] = a.z * p.scale_log2; qr[g][3] = a.w * p.scale_log2;
-    qr[g][4] = b.x * p.scale_log2; qr[g][5] = b.y * p.scale_log2;
-    qr[g][6] = b.z * p.scale_log2; qr[g][7] = b.w * p.scale_log2;
+  for (int nt = 0; nt < NT; ++nt) {
+    const int hh = nt * 4 + (gq >> 1);
+    const int part = gq & 1;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      if (hh < G) {
+        const float* qp = p.q + ((size_t)s * p.H + hk * G + hh) * D + ks * 16 + 2 * tq;
+        const float sc = p.scale_log2;
+        qb[nt][ks][0] = pack_bf16(bf16_part(qp[0] * sc, part), bf16_part(qp[1] * sc, part));
+        qb[nt][ks][1] = pack_bf16(bf16_part(qp[8] * sc, part), bf16_part(qp[9] * sc, part));
+      } else {
+        qb[nt][ks][0] = qb[nt][ks][1] = 0u;
+      }
+    }
   }
-  float m[G], l[G], acc[G][8];
+  // per lane: softmax state of head nt*4 + tq; O^T accumulators (dims ks*16+gq,+8)
+  float m[NT], l[NT], o[NT][KS][4];
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    m[g] = -CUDART_INF_F;
-    l[g] = 0.f;
+  for (int nt = 0; nt < NT; ++nt) {
+    m[nt] = -CUDART_INF_F;
+    l[nt] = 0.f;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[g][j] = 0.f;
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[nt][ks][j] = 0.f;
   }
-
-  // token held (after the transpose-reduction) by this lane, and the lane that
-  // holds the score of the token whose V row this lane owns in sweep i.
-  const int my_i = (lane >> 1) & (ITERS - 1);
-  const int my_tok = my_i * TPI + lane / CPR;
-  const int src_base = (lane / CPR) * CPR;
+  // ldmatrix row addresses (byte offsets within a tile, before the swizzle)
+  const int k_row = (lane & 7) + ((lane >> 3) & 1) * 8, k_cadd = lane >> 4;
+  const int v_row = (lane & 7) + (lane >> 4) * 8, v_cadd = (lane >> 3) & 1;
 
   for (int it = 0; it < n_it; ++it) {
     const int st = it % NS;
     const uint32_t phase = (it / NS) & 1;
     const int blk = first + kWarps * it;
     mbar_wait(&bars[warp][st], phase);
-    const uint8_t* tile = ring + st * 2 * TILE;
-    const bool valid = blk * 16 + my_tok < L;
-    const bool tail = blk * 16 + 16 > L;
-    float part[G][ITERS];
+    uint8_t* tile = ring + st * 2 * TILE;
+    const int valid_rows = min(16, L - blk * 16);
+    if (valid_rows < 16) {  // rows past the context may hold any bytes: zero V there
+      for (int e = lane; e < (16 - valid_rows) * (ROW / 16); e += 32) {
+        const int r = valid_rows + e / (ROW / 16), c = e % (ROW / 16);
+        *reinterpret_cast<uint4*>(tile + TILE + r * ROW + c * 16) = make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+    }
+    // ---- S = K Qc ----
+    float sacc[NT][4];
 #pragma unroll
-    for (int i = 0; i < ITERS; ++i) {
-      float kf[8];
-      unpack8(lds128(tile + (i * 32 + lane) * 16), kf);
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        float a = 0.f;
+      for (int j = 0; j < 4; ++j) sacc[nt][j] = 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) a = fmaf(qr[g][j], kf[j], a);
-        part[g][i] = a;
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t a[4];
+      const int c = 2 * ks + k_cadd;
+      ldsm_x4(a, tile + k_row * ROW + ((c ^ (k_row & 7)) << 4));
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) mma_bf16(sacc[nt], a, qb[nt][ks]);
+    }
+    // ---- online softmax (base 2) per head nt*4+tq; rows gq and gq+8 ----
+    float pA[NT], pB[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const float s0 = (gq < valid_rows) ? sacc[nt][0] + sacc[nt][1] : -CUDART_INF_F;
+      const float s1 = (gq + 8 < valid_rows) ? sacc[nt][2] + sacc[nt][3] : -CUDART_INF_F;
+      float bm = fmaxf(s0, s1);
+      bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 4));
+      bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
+      bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
+      const float m_new = fmaxf(m[nt], bm);
+      const float alpha = exp2f(m[nt] - m_new);
+      pA[nt] = exp2f(s0 - m_new);
+      pB[nt] = exp2f(s1 - m_new);
+      l[nt] = l[nt] * alpha + pA[nt] + pB[nt];
+      m[nt] = m_new;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[nt][ks][j] *= alpha;
+    }
+    // ---- P as B fragments: lane needs P[2tq, 2tq+1, 2tq+8, 2tq+9][column gq] ----
+    uint32_t pb[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int src0 = 8 * tq + (gq >> 1), src1 = src0 + 4;
+      const float a0 = __shfl_sync(0xffffffffu, pA[nt], src0);  // P[2tq]
+      const float a8 = __shfl_sync(0xffffffffu, pB[nt], src0);  // P[2tq+8]
+      const float c0 = __shfl_sync(0xffffffffu, pA[nt], src1);  // P[2tq+1]
+      const float c8 = __shfl_sync(0xffffffffu, pB[nt], src1);  // P[2tq+9]
+      const int part = gq & 1;
+      if (nt * 4 + (gq >> 1) < G) {
+        pb[nt][0] = pack_bf16(bf16_part(a0, part), bf16_part(c0, part));
+        pb[nt][1] = pack_bf16(bf16_part(a8, part), bf16_part(c8, part));
+      } else {
+        pb[nt][0] = pb[nt][1] = 0u;
       }
     }
-    float pr[G];
+    // ---- O^T += V^T P ----
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float* v = part[g];
-      // transpose-reduction over the CPR lanes sharing a token row
-      int n = ITERS;
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t a[4];
+      const int c = 2 * ks + v_cadd;
+      ldsm_x4_t(a, tile + TILE + v_row * ROW + ((c ^ (v_row & 7)) << 4));
 #pragma unroll
-      for (int mask = CPR / 2; mask >= 1; mask >>= 1) {
-        if (n > 1) {
-          const bool up = lane & mask;
-          const int half = n / 2;
-#pragma unroll
-          for (int j = 0; j < ITERS / 2; ++j) {
-            if (j < half) {
-              const float keep = up ? v[j + half] : v[j];
-              const float send = up ? v[j] : v[j + half];
-              v[j] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
-            }
-          }
-          n = half;
-        } else {
-          v[0] += __shfl_xor_sync(0xffffffffu, v[0], mask);
-        }
-      }
-      const float sc = valid ? v[0] : -CUDART_INF_F;
-      float bm = sc;
-#pragma unroll
-      for (int mask = 1; mask < 32; mask <<= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, mask));
-      const float m_new = fmaxf(m[g], bm);
-      const float alpha = exp2f(m[g] - m_new);
-      pr[g] = valid ? exp2f(sc - m_new) : 0.f;
-      float ps = pr[g];
-#pragma unroll
-      for (int mask = 2; mask < 32; mask <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, mask);
-      l[g] = l[g] * alpha + ps;
-      m[g] = m_new;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc[g][j] *= alpha;
-    }
-#pragma unroll
-    for (int i = 0; i < ITERS; ++i) {
-      float pi[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) pi[g] = __shfl_sync(0xffffffffu, pr[g], src_base + (i << 1));
-      // rows past the context may hold any bytes (NaN/Inf): skip, don't multiply by 0
-      if (tail && blk * 16 + i * TPI + lane / CPR >= L) continue;
-      float vf[8];
-      unpack8(lds128(tile + TILE + (i * 32 + lane) * 16), vf);
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[g][j] = fmaf(pi[g], vf[j], acc[g][j]);
+      for (int nt = 0; nt < NT; ++nt) mma_bf16(o[nt][ks], a, pb[nt]);
     }
     // refill this stage with iteration it + NS (all lanes are done reading it)
     const int nx = it + NS;
@@ -254,28 +279,29 @@ paged_attention_kernel(const AttnParams p) {
       }
     }
   }
-  // lanes with equal lane % CPR hold the same dims for different token rows
+  // l: sum the lane partials over the 8 token groups
 #pragma unroll
-  for (int g = 0; g < G; ++g)
-#pragma unroll
-    for (int mask = CPR; mask < 32; mask <<= 1)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc[g][j] += __shfl_xor_sync(0xffffffffu, acc[g][j], mask);
+  for (int nt = 0; nt < NT; ++nt) {
+    l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 4);
+    l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 8);
+    l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 16);
+  }
 
   __shared__ float sm_m[kWarps][G], sm_l[kWarps][G];
   __shared__ __align__(16) float sm_acc[kWarps][G][D];
-  if (lane < CPR) {
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
+  for (int nt = 0; nt < NT; ++nt) {
+    const int hh = nt * 4 + tq;
+    if (hh < G) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sm_acc[warp][g][dim0 + j] = acc[g][j];
-    }
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      sm_m[warp][g] = m[g];
-      sm_l[warp][g] = l[g];
+      for (int ks = 0; ks < KS; ++ks) {
+        sm_acc[warp][hh][ks * 16 + gq] = o[nt][ks][0] + o[nt][ks][1];
+        sm_acc[warp][hh][ks * 16 + gq + 8] = o[nt][ks][2] + o[nt][ks][3];
+      }
+      if (gq == 0) {
+        sm_m[warp][hh] = m[nt];
+        sm_l[warp][hh] = l[nt];
+      }
     }
   }
   __syncthreads();

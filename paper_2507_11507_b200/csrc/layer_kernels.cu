@@ -16,6 +16,11 @@ constexpr int kMaxPerThread = 32;  // d <= 8192
 
 __device__ __forceinline__ float bf(const __nv_bfloat16* p, int i) { return __bfloat162float(p[i]); }
 
+// KV tile row layout (include/mirage.h): element c of token row r sits in
+// 16-byte chunk (c / 8) ^ (r & 7) -- the swizzle the attention kernel's
+// ldmatrix reads are conflict-free under.
+__device__ __forceinline__ int swz(int c, int r) { return (((c >> 3) ^ (r & 7)) << 3) | (c & 7); }
+
 template <int NT>
 __device__ __forceinline__ float block_sum(float v, float* red) {
 #pragma unroll
@@ -174,8 +179,8 @@ __global__ void qkv_post_kernel(int family, int H, int Hk, int D, const float* q
       const int kh = hh - H;
       __nv_bfloat16* dst =
           reinterpret_cast<__nv_bfloat16*>(kvbase + ((size_t)(kh * 2 + 0) * 16 + r) * D * 2);
-      dst[i] = __float2bfloat16_rn(y0);
-      dst[i + half] = __float2bfloat16_rn(y1);
+      dst[swz(i, r)] = __float2bfloat16_rn(y0);
+      dst[swz(i + half, r)] = __float2bfloat16_rn(y1);
     }
   }
   for (int e = threadIdx.x; e < Hk * D; e += blockDim.x) {
@@ -185,7 +190,7 @@ __global__ void qkv_post_kernel(int family, int H, int Hk, int D, const float* q
     if (bias) x0 += bf(bias, c);
     __nv_bfloat16* dst =
         reinterpret_cast<__nv_bfloat16*>(kvbase + ((size_t)(kh * 2 + 1) * 16 + r) * D * 2);
-    dst[i] = __float2bfloat16_rn(x0);
+    dst[swz(i, r)] = __float2bfloat16_rn(x0);
   }
 }
 
@@ -286,8 +291,9 @@ __global__ void fill_kv_kernel(uint64_t seed, int64_t seq_id, int L, int Hk, int
       else packed[j >> 1] = b;
     }
     const int32_t blk = table[pos >> 4];
-    uint4* dst = reinterpret_cast<uint4*>(
-        block_base[blk] + ((((uint64_t)layer * Hk + hk) * 2 + kv) * 16 + (pos & 15)) * D * 2 + ch * 16);
+    uint4* dst = reinterpret_cast<uint4*>(block_base[blk] +
+                                          ((((uint64_t)layer * Hk + hk) * 2 + kv) * 16 + (pos & 15)) * D * 2 +
+                                          ((ch ^ (pos & 7)) * 16));
     *dst = make_uint4(packed[0], packed[1], packed[2], packed[3]);
   }
 }
@@ -309,7 +315,7 @@ __global__ void write_kv_kernel(int L, int Hk, int D, int p0, int n, const __nv_
     const int32_t blk = table[pos >> 4];
     __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(
         block_base[blk] + ((((uint64_t)layer * Hk + hk) * 2 + kv) * 16 + (pos & 15)) * D * 2);
-    dst[d] = src[e];
+    dst[swz(d, pos & 15)] = src[e];
   }
 }
 

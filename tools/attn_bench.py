@@ -24,6 +24,9 @@ CASES = {
     # name: (n_layers, H, Hk, D, batch, contexts)
     "opt13b_b400": (40, 40, 40, 128, 400, "sharegpt"),
     "opt13b_b64": (40, 40, 40, 128, 64, "sharegpt"),
+    "opt13b_uni400x305": (40, 40, 40, 128, 400, 305),
+    "opt13b_b100x1220": (40, 40, 40, 128, 100, 1220),
+    "opt13b_b25x1900": (40, 40, 40, 128, 25, 1900),
     "opt13b_b29": (40, 40, 40, 128, 29, "sharegpt"),
     "llama3_8b_32x8k": (32, 32, 8, 128, 32, 8192),
     "llama3_8b_1x32k": (32, 32, 8, 128, 1, 32768),
