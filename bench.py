@@ -307,11 +307,12 @@ def run_mirage(args, rank, world):
     clock = ClockSampler(lr)
     res = run_arm(args, torch, dev, shape, blob, ctxs, n_native, cycle, beta, args.steps, args.warmup,
                   args.e2e_steps, clock)
-    resident = None
+    resident, r2 = None, None
     if not args.no_resident_arm and cycle and world == 1:
         # the same batch with every layer resident (pool grown by the reclaimed blocks)
+        # same warm-up and step count, so both arms time the same context lengths
         r2 = run_arm(args, torch, dev, shape, blob, ctxs, n_native + reclaimed, [], 0,
-                     max(5, args.steps // 2), 3, 0)
+                     args.steps, args.warmup, 0)
         resident = statistics.median(r2["step_ms"])
     B = len(ctxs)
     t_local = res["total_ms"]
@@ -364,7 +365,9 @@ def run_mirage(args, rank, world):
                 "bytes_per_step": res["h2d_bytes"] / args.steps, "copies": res["h2d_copies"],
                 "peak_source": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this run"},
         "remap": {"step_ms_remapped": step_med, "step_ms_all_resident": resident,
-                  "ratio": (step_med / resident) if resident else None},
+                  "ratio": (step_med / resident) if resident else None,
+                  "steps_ms_remapped": [round(x, 3) for x in res["step_ms"]],
+                  "steps_ms_resident": [round(x, 3) for x in r2["step_ms"]] if resident else None},
         "cpu_baseline": cpu, "clocks": res["clocks"],
         "e2e": {"value": B / (e2e_med / 1e3) * world if e2e_med else None, "unit": "tok/s",
                 "h2d_bytes_per_step": res["meta_bytes"], "d2h_bytes_per_step": 4 * B,

@@ -61,6 +61,11 @@ extern "C" {
 #define MIRAGE_BETA_DYNAMIC 3 /* smallest m with zero predicted stall (reading #6) */
 
 #define MIRAGE_FLAG_TIME_ATTN 1u /* init flag: time every attention launch with events */
+#define MIRAGE_FLAG_HOST_ONLY 2u /* init flag: no device; allocator/remap/table/query
+                                  * calls only (the arena pointer is used for address
+                                  * arithmetic, never dereferenced); device calls
+                                  * return MIRAGE_ERR_STATE. For CPU-only replay,
+                                  * fuzzing and multi-rank allocator checks.       */
 
 #define MIRAGE_BLOCK_TOKENS 16
 #define MIRAGE_MAX_CYCLE 256

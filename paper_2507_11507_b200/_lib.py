@@ -20,6 +20,7 @@ FAMILY_OPT, FAMILY_LLAMA = 0, 1
 BETA_1, BETA_2, BETA_DYNAMIC = 1, 2, 3
 BLOCK_TOKENS = 16
 FLAG_TIME_ATTN = 1
+FLAG_HOST_ONLY = 2
 MAX_CYCLE = 256
 
 _NAMES = {ERR_CONFIG: "CONFIG", ERR_CAPACITY: "CAPACITY", ERR_RANGE: "RANGE", ERR_STATE: "STATE",
@@ -175,6 +176,33 @@ def tensors_to_bytes(named, order):
 class Context:
     """One mirage_ctx on one GPU. Owns (keeps alive) the arena, the streams and
     the host blobs it was given."""
+
+    @classmethod
+    def host_only(cls, arena_bytes, max_batch, max_ctx, arena_base=1 << 40):
+        """A device-less context (MIRAGE_FLAG_HOST_ONLY): allocator, remap and
+        tables only; the arena is a virtual address range never dereferenced."""
+        self = cls.__new__(cls)
+        self.device, self.arena, self.stream, self._blobs = None, None, None, []
+        self._arena_ptr = arena_base
+        cfg = InitCfg(0, arena_base, int(arena_bytes), BLOCK_TOKENS, None, None, max_batch, max_ctx,
+                      FLAG_HOST_ONLY, 0, 1, None)
+        self._ctx = C.c_void_p()
+        rc = LIB.mirage_init(C.byref(cfg), C.byref(self._ctx))
+        if rc:
+            raise MirageError(rc, "init(host_only)")
+        self.max_batch, self.max_ctx = max_batch, max_ctx
+        return self
+
+    def add_model_host_only(self, shape, native_blocks):
+        """add_model on a host-only context (no blob is read)."""
+        S, G, _ = model_sizes(shape)
+        cfg = model_cfg(shape)
+        mid = C.c_int32()
+        dummy = C.create_string_buffer(1)
+        rc = LIB.mirage_add_model(self._ctx, C.byref(cfg), C.addressof(dummy), shape.n_layers * S + G,
+                                  int(native_blocks), C.byref(mid))
+        self._check(rc, "add_model")
+        return mid.value
 
     def __init__(self, arena_bytes, max_batch, max_ctx, device=0, stream=None, flags=0):
         self.device = torch.device("cuda", device)

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -213,6 +214,7 @@ struct mirage_ctx {
   std::string err;
   int32_t sticky = MIRAGE_OK;
   int64_t launches = 0;
+  bool host_only = false;  // MIRAGE_FLAG_HOST_ONLY: allocator/planner state only, no device
 };
 
 namespace {
@@ -487,7 +489,8 @@ int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
   if (!cfg || !out) return MIRAGE_ERR_CONFIG;
   *out = nullptr;
   if (cfg->block_tokens != kBlockTokens || cfg->tp_size != 1 || cfg->tp_rank != 0 ||
-      !cfg->dev_arena || !cfg->compute_stream || cfg->max_batch <= 0 || cfg->max_ctx <= 0 ||
+      !cfg->dev_arena || (!cfg->compute_stream && !(cfg->flags & MIRAGE_FLAG_HOST_ONLY)) ||
+      cfg->max_batch <= 0 || cfg->max_ctx <= 0 ||
       (reinterpret_cast<uintptr_t>(cfg->dev_arena) % kAlign))
     return MIRAGE_ERR_CONFIG;
   mirage_ctx* c = new mirage_ctx();
@@ -500,6 +503,12 @@ int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
     mirage_destroy(c);
     return code;
   };
+  if (cfg->flags & MIRAGE_FLAG_HOST_ONLY) {  // no CUDA calls at all
+    c->host_only = true;
+    c->cs = nullptr;
+    *out = c;
+    return MIRAGE_OK;
+  }
   if (cudaSetDevice(cfg->device) != cudaSuccess) return bail(MIRAGE_ERR_CUDA);
   if (cfg->copy_stream) {
     c->xs = reinterpret_cast<cudaStream_t>(cfg->copy_stream);
@@ -528,6 +537,11 @@ int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
 
 void mirage_destroy(mirage_ctx* c) {
   if (!c) return;
+  if (c->host_only) {
+    for (Model* M : c->models) delete M;
+    delete c;
+    return;
+  }
   if (c->cs) cudaStreamSynchronize(c->cs);
   if (c->xs) cudaStreamSynchronize(c->xs);
   for (Model* M : c->models) {
@@ -575,7 +589,8 @@ int32_t mirage_add_model(mirage_ctx* c, const mirage_model_cfg* mc, const void* 
     return fail(c, MIRAGE_ERR_CONFIG, "add_model: host_bytes %llu != n*S+G %llu",
                 (unsigned long long)host_bytes, (unsigned long long)((uint64_t)s.n * z.S + z.G));
   cudaPointerAttributes attr;
-  if (cudaPointerGetAttributes(&attr, host_blob) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+  if (!c->host_only &&
+      (cudaPointerGetAttributes(&attr, host_blob) != cudaSuccess || attr.type != cudaMemoryTypeHost)) {
     (void)cudaGetLastError();
     return fail(c, MIRAGE_ERR_CONFIG, "add_model: host blob must be pinned host memory");
   }
@@ -606,7 +621,7 @@ int32_t mirage_add_model(mirage_ctx* c, const mirage_model_cfg* mc, const void* 
   }
   // block_base (library-owned): native ids + everything the arena could donate
   const uint64_t cap = (uint64_t)native_kv_blocks + c->cfg.dev_arena_bytes / z.BB + 16;
-  if (cudaMalloc(reinterpret_cast<void**>(&M->bbase_dev), cap * 8) != cudaSuccess) {
+  if (!c->host_only && cudaMalloc(reinterpret_cast<void**>(&M->bbase_dev), cap * 8) != cudaSuccess) {
     delete M;
     return fail(c, MIRAGE_ERR_CUDA, "add_model: block_base allocation");
   }
@@ -620,6 +635,12 @@ int32_t mirage_add_model(mirage_ctx* c, const mirage_model_cfg* mc, const void* 
   }
   M->layer_state.assign(s.n, RESIDENT);
   M->cyc_index.assign(s.n, -1);
+  if (c->host_only) {
+    M->id = (int32_t)c->models.size();
+    c->models.push_back(M);
+    *model_id = M->id;
+    return MIRAGE_OK;
+  }
   CK(c, cudaMemcpyAsync(M->w_dev, host_blob, host_bytes, cudaMemcpyHostToDevice, c->cs));
   if (native_kv_blocks)
     CK(c, cudaMemcpyAsync(M->bbase_dev, M->bbase_host.data(), native_kv_blocks * 8,
@@ -698,7 +719,7 @@ int32_t mirage_remap_layers(mirage_ctx* c, int32_t donor, int32_t recipient, con
   D->donated_bytes += (uint64_t)Rl.size() * D->sz.S;
   for (int i = 0; i < beta; ++i) D->layer_state[cycle[i]] = SLOT;
   for (int32_t l : Rl) D->layer_state[l] = RECLAIMED;
-  if (gained)  // stream-ordered after every kernel that read these bytes as weights
+  if (gained && !c->host_only)  // stream-ordered after every kernel that read these bytes as weights
     CK(c, cudaMemcpyAsync(R->bbase_dev + first_new, R->bbase_host.data() + first_new, gained * 8,
                           cudaMemcpyHostToDevice, c->cs));
   if (beta > 0) {
@@ -708,7 +729,7 @@ int32_t mirage_remap_layers(mirage_ctx* c, int32_t donor, int32_t recipient, con
     D->uses = 0;
     D->cyc_steps = 0;
     D->slot_log.clear();
-    for (int j = 0; j < beta; ++j) {
+    for (int j = 0; j < beta && !c->host_only; ++j) {
       cudaEvent_t a, b;
       CK(c, cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
       CK(c, cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
@@ -716,7 +737,7 @@ int32_t mirage_remap_layers(mirage_ctx* c, int32_t donor, int32_t recipient, con
       D->free_ev.push_back(b);
     }
   }
-  if (gained) CK(c, cudaStreamSynchronize(c->cs));  // the host staging above is a pageable vector
+  if (gained && !c->host_only) CK(c, cudaStreamSynchronize(c->cs));  // the host staging above is a pageable vector
   if (blocks_gained) *blocks_gained = gained;
   if (reclaimed_bytes) *reclaimed_bytes = (uint64_t)Rl.size() * D->sz.S;
   return MIRAGE_OK;
@@ -799,6 +820,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
                            const int32_t* tokens, const int32_t* positions, void* hidden_out,
                            int32_t* argmax_out) {
   GUARD(c);
+  if (c->host_only) return fail(c, MIRAGE_ERR_STATE, "host-only context has no device");
   Model* M = get_model(c, model);
   if (!M) return fail(c, MIRAGE_ERR_RANGE, "step: model %d", model);
   if (B <= 0 || B > c->cfg.max_batch || !seq_ids || !tokens || !positions)
@@ -875,8 +897,9 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
       wptr[l] = M->w_dev + (uint64_t)l * M->sz.S;
     }
   }
+  static const int dbg_nowait = getenv("MIRAGE_PREFETCH_DEBUG") && atoi(getenv("MIRAGE_PREFETCH_DEBUG")) == 2;
   auto gate = [&](int l) -> int32_t {  // wait until layer l's weights are in its slot
-    if (l < s.n && use_of[l] >= beta && use_of[l] >= 0)
+    if (!dbg_nowait && l < s.n && use_of[l] >= beta && use_of[l] >= 0)
       CK(c, cudaStreamWaitEvent(cs, M->ready_ev[use_of[l] % beta], 0));
     return MIRAGE_OK;
   };
@@ -895,8 +918,10 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     CK(c, cudaEventCreate(&t.t1));
     t.bytes = M->sz.S;
     CK(c, cudaEventRecord(t.t0, c->xs));
-    CK(c, cudaMemcpyAsync(M->w_dev + (uint64_t)M->cycle[slot] * M->sz.S,
-                          M->host + (uint64_t)nl * M->sz.S, M->sz.S, cudaMemcpyHostToDevice, c->xs));
+    static const int dbg_mode = getenv("MIRAGE_PREFETCH_DEBUG") ? atoi(getenv("MIRAGE_PREFETCH_DEBUG")) : 0;
+    if (dbg_mode != 1)  // experiment hook: 1 = events only, no DMA
+      CK(c, cudaMemcpyAsync(M->w_dev + (uint64_t)M->cycle[slot] * M->sz.S,
+                            M->host + (uint64_t)nl * M->sz.S, M->sz.S, cudaMemcpyHostToDevice, c->xs));
     CK(c, cudaEventRecord(t.t1, c->xs));
     CK(c, cudaEventRecord(M->ready_ev[slot], c->xs));
     M->pending.push_back(t);
@@ -1006,6 +1031,7 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
                          const float* q_dev, void* out_dev, int32_t out_fp32,
                          int32_t split_tokens_override) {
   GUARD(c);
+  if (c->host_only) return fail(c, MIRAGE_ERR_STATE, "host-only context has no device");
   Model* M = get_model(c, model);
   if (!M || layer < 0 || layer >= M->shp.n || B <= 0 || B > c->cfg.max_batch || !seq_ids || !q_dev ||
       !out_dev || split_tokens_override < 0 || split_tokens_override % kBlockTokens)
@@ -1078,6 +1104,7 @@ static int32_t kv_hook_prepare(mirage_ctx* c, Model* M, int64_t seq_id, int32_t 
 
 int32_t mirage_fill_kv(mirage_ctx* c, int32_t model, int64_t seq_id, int32_t n, uint64_t seed) {
   GUARD(c);
+  if (c->host_only) return fail(c, MIRAGE_ERR_STATE, "host-only context has no device");
   Model* M = get_model(c, model);
   if (!M || n < 0) return fail(c, MIRAGE_ERR_RANGE, "fill_kv: arguments");
   int32_t p0 = 0;
@@ -1091,6 +1118,7 @@ int32_t mirage_fill_kv(mirage_ctx* c, int32_t model, int64_t seq_id, int32_t n, 
 
 int32_t mirage_write_kv(mirage_ctx* c, int32_t model, int64_t seq_id, int32_t n, const void* host_kv) {
   GUARD(c);
+  if (c->host_only) return fail(c, MIRAGE_ERR_STATE, "host-only context has no device");
   Model* M = get_model(c, model);
   if (!M || n < 0 || (!host_kv && n)) return fail(c, MIRAGE_ERR_RANGE, "write_kv: arguments");
   int32_t p0 = 0;
@@ -1118,9 +1146,11 @@ int32_t mirage_query(mirage_ctx* c, int32_t model, mirage_stats* o) {
   GUARD(c);
   Model* M = get_model(c, model);
   if (!M || !o) return fail(c, MIRAGE_ERR_RANGE, "query: model %d", model);
-  harvest_copy_times(M);
-  harvest_step_time(M);
-  harvest_attn_times(M);
+  if (!c->host_only) {
+    harvest_copy_times(M);
+    harvest_step_time(M);
+    harvest_attn_times(M);
+  }
   std::memset(o, 0, sizeof *o);
   o->native_blocks = M->n_native;
   o->total_blocks = M->next_id;
@@ -1162,6 +1192,7 @@ int32_t mirage_slot_log(mirage_ctx* c, int32_t model, int64_t* out, int32_t cap,
 
 int32_t mirage_sync(mirage_ctx* c) {
   GUARD(c);
+  if (c->host_only) return MIRAGE_OK;
   CK(c, cudaStreamSynchronize(c->cs));
   CK(c, cudaStreamSynchronize(c->xs));
   CK(c, cudaGetLastError());
