@@ -40,7 +40,7 @@ def build(verbose=False):
             sys.stderr.write(log)
     if not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC] + ARCH + ["-shared", "-o", OUT] + objs + [
-            "-L/usr/local/cuda/lib64", "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+            "-L/usr/local/cuda/lib64", "-lcublas", "-lcublasLt", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(f"link failed:\n{r.stderr}")

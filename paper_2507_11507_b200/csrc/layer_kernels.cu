@@ -11,137 +11,155 @@
 namespace mirage {
 namespace {
 
-constexpr int kNormThreads = 256;
-constexpr int kMaxPerThread = 32;  // d <= 8192
-
-__device__ __forceinline__ float bf(const __nv_bfloat16* p, int i) { return __bfloat162float(p[i]); }
-
 // KV tile row layout (include/mirage.h): element c of token row r sits in
 // 16-byte chunk (c / 8) ^ (r & 7) -- the swizzle the attention kernel's
 // ldmatrix reads are conflict-free under.
 __device__ __forceinline__ int swz(int c, int r) { return (((c >> 3) ^ (r & 7)) << 3) | (c & 7); }
 
-template <int NT>
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void load8bf(const __nv_bfloat16* p, float (&v)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[2 * k] = __uint_as_float(w[k] << 16);
+    v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+  }
+}
+__device__ __forceinline__ uint4 pack8bf(const float (&v)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    w[k] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v[2 * k])) |
+           ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v[2 * k + 1])) << 16);
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// block-wide sum, fixed order (deterministic); blockDim.x is a multiple of 32
 __device__ __forceinline__ float block_sum(float v, float* red) {
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   __syncthreads();
   if (lane == 0) red[w] = v;
   __syncthreads();
   float t = 0.f;
-#pragma unroll
-  for (int i = 0; i < NT / 32; ++i) t += red[i];  // fixed order: deterministic
+  for (int i = 0; i < nw; ++i) t += red[i];
   return t;
 }
 
-// normalise the row held in v[] (fp32) and write bf16 x. family 0: LayerNorm
-// (two-pass mean/var), 1: RMSNorm.
-__device__ __forceinline__ void norm_row(int family, int d, float (&v)[kMaxPerThread], int cnt,
-                                         const __nv_bfloat16* g, const __nv_bfloat16* bta,
-                                         float eps, __nv_bfloat16* x, float* red) {
-  const int tid = threadIdx.x;
+// Normalise one row held 8 elements per thread (thread t owns elements
+// 8t..8t+7, t < d/8) and write bf16 x. family 0: LayerNorm (two-pass
+// mean/var), 1: RMSNorm.
+__device__ __forceinline__ void norm_row8(int family, int d, bool own, float (&v)[8],
+                                          const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps,
+                                          __nv_bfloat16* x, float* red) {
+  const int e0 = threadIdx.x * 8;
+  float gv[8], bv[8], out[8];
   if (family == 0) {
-    float s = 0.f;
+    float sm = 0.f;
+    if (own)
 #pragma unroll
-    for (int k = 0; k < kMaxPerThread; ++k)
-      if (k < cnt) s += v[k];
-    const float mean = block_sum<kNormThreads>(s, red) / d;
+      for (int k = 0; k < 8; ++k) sm += v[k];
+    const float mean = block_sum(sm, red) / d;
     float q = 0.f;
+    if (own)
 #pragma unroll
-    for (int k = 0; k < kMaxPerThread; ++k) {
-      if (k < cnt) {
-        const float c = v[k] - mean;
-        q += c * c;
-      }
-    }
-    const float var = block_sum<kNormThreads>(q, red) / d;
-    const float r = rsqrtf(var + eps);
+      for (int k = 0; k < 8; ++k) q += (v[k] - mean) * (v[k] - mean);
+    const float r = rsqrtf(block_sum(q, red) / d + eps);
+    if (own) {
+      load8bf(g + e0, gv);
+      load8bf(bta + e0, bv);
 #pragma unroll
-    for (int k = 0; k < kMaxPerThread; ++k) {
-      if (k < cnt) {
-        const int i = tid + k * kNormThreads;
-        x[i] = __float2bfloat16_rn((v[k] - mean) * r * bf(g, i) + bf(bta, i));
-      }
+      for (int k = 0; k < 8; ++k) out[k] = (v[k] - mean) * r * gv[k] + bv[k];
+      *reinterpret_cast<uint4*>(x + e0) = pack8bf(out);
     }
   } else {
     float q = 0.f;
+    if (own)
 #pragma unroll
-    for (int k = 0; k < kMaxPerThread; ++k)
-      if (k < cnt) q += v[k] * v[k];
-    const float ms = block_sum<kNormThreads>(q, red) / d;
-    const float r = rsqrtf(ms + eps);
+      for (int k = 0; k < 8; ++k) q += v[k] * v[k];
+    const float r = rsqrtf(block_sum(q, red) / d + eps);
+    if (own) {
+      load8bf(g + e0, gv);
 #pragma unroll
-    for (int k = 0; k < kMaxPerThread; ++k) {
-      if (k < cnt) {
-        const int i = tid + k * kNormThreads;
-        x[i] = __float2bfloat16_rn(v[k] * r * bf(g, i));
-      }
+      for (int k = 0; k < 8; ++k) out[k] = v[k] * r * gv[k];
+      *reinterpret_cast<uint4*>(x + e0) = pack8bf(out);
     }
   }
 }
 
-__global__ void __launch_bounds__(kNormThreads)
+__global__ void __launch_bounds__(1024)
 embed_norm_kernel(int family, int d, const int32_t* tokens, const int32_t* positions,
                   const __nv_bfloat16* embed, const __nv_bfloat16* pos_embed,
                   const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps, float* h,
                   __nv_bfloat16* x) {
-  __shared__ float red[kNormThreads / 32];
+  __shared__ float red[32];
   const int b = blockIdx.x;
-  const int tid = threadIdx.x;
-  const __nv_bfloat16* e = embed + (size_t)tokens[b] * d;
-  const __nv_bfloat16* pe = family == 0 ? pos_embed + (size_t)(positions[b] + 2) * d : nullptr;
-  float v[kMaxPerThread];
-  const int cnt = (d - tid + kNormThreads - 1) / kNormThreads;
+  const int e0 = threadIdx.x * 8;
+  const bool own = e0 < d;
+  float v[8];
+  if (own) {
+    load8bf(embed + (size_t)tokens[b] * d + e0, v);
+    if (family == 0) {
+      float pv[8];
+      load8bf(pos_embed + (size_t)(positions[b] + 2) * d + e0, pv);
 #pragma unroll
-  for (int k = 0; k < kMaxPerThread; ++k) {
-    if (k < cnt) {
-      const int i = tid + k * kNormThreads;
-      float t = bf(e, i);
-      if (pe) t += bf(pe, i);
-      v[k] = t;
-      h[(size_t)b * d + i] = t;
+      for (int k = 0; k < 8; ++k) v[k] += pv[k];
     }
+    store8(h + (size_t)b * d + e0, v);
   }
-  norm_row(family, d, v, cnt, g, bta, eps, x + (size_t)b * d, red);
+  norm_row8(family, d, own, v, g, bta, eps, x + (size_t)b * d, red);
 }
 
-__global__ void __launch_bounds__(kNormThreads)
+// h[b] += y[b] (+ bias) if y != nullptr; then x[b] = bf16(norm(h[b])) if g != nullptr.
+__global__ void __launch_bounds__(1024)
 residual_norm_kernel(int family, int d, const float* y, int ldy, const __nv_bfloat16* bias,
                      const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps, float* h,
                      __nv_bfloat16* x) {
-  __shared__ float red[kNormThreads / 32];
+  __shared__ float red[32];
   const int b = blockIdx.x;
-  const int tid = threadIdx.x;
-  float v[kMaxPerThread];
-  const int cnt = (d - tid + kNormThreads - 1) / kNormThreads;
+  const int e0 = threadIdx.x * 8;
+  const bool own = e0 < d;
+  float v[8];
+  if (own) {
+    load8(h + (size_t)b * d + e0, v);
+    if (y) {
+      float yv[8];
+      load8(y + (size_t)b * ldy + e0, yv);
 #pragma unroll
-  for (int k = 0; k < kMaxPerThread; ++k) {
-    if (k < cnt) {
-      const int i = tid + k * kNormThreads;
-      float t = h[(size_t)b * d + i];
-      if (y) {  // y == nullptr: norm only
-        t += y[(size_t)b * ldy + i];
-        if (bias) t += bf(bias, i);
-        h[(size_t)b * d + i] = t;
+      for (int k = 0; k < 8; ++k) v[k] += yv[k];
+      if (bias) {
+        float bv[8];
+        load8bf(bias + e0, bv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] += bv[k];
       }
-      v[k] = t;
+      store8(h + (size_t)b * d + e0, v);
     }
   }
-  if (g) norm_row(family, d, v, cnt, g, bta, eps, x + (size_t)b * d, red);  // g == nullptr: add only
+  if (g) norm_row8(family, d, own, v, g, bta, eps, x + (size_t)b * d, red);
 }
 
 // One CTA per sequence. Adds the bias, applies rotate-half RoPE (Llama) with the
 // angle pos * theta^(-2i/D) evaluated in fp64, writes q (fp32) and appends k, v
-// (bf16) into the paged cache row of position pos.
-__global__ void qkv_post_kernel(int family, int H, int Hk, int D, const float* qkv,
-                                const __nv_bfloat16* bias, const int32_t* positions,
-                                const int32_t* tables, int tbl_pitch, const uint64_t* block_base,
-                                uint64_t layer_off, float rope_theta, float* q) {
+// (bf16) into the paged cache row of position pos. Work items are 8-element
+// chunks: (head, chunk pair c, c + D/16) for q/k, (kv head, chunk) for v.
+__global__ void __launch_bounds__(256)
+qkv_post_kernel(int family, int H, int Hk, int D, const float* qkv, const __nv_bfloat16* bias,
+                const int32_t* positions, const int32_t* tables, int tbl_pitch,
+                const uint64_t* block_base, uint64_t layer_off, float rope_theta, float* q) {
   extern __shared__ float cs[];  // [D/2] cos, [D/2] sin
   const int b = blockIdx.x;
   const int pos = positions[b];
-  const int half = D / 2;
+  const int half = D / 2, hc = D / 16;  // chunks per half row
   const int W = (H + 2 * Hk) * D;
   const float* row = qkv + (size_t)b * W;
   if (family == 1) {
@@ -157,57 +175,83 @@ __global__ void qkv_post_kernel(int family, int H, int Hk, int D, const float* q
   const int32_t blk = tables[(size_t)b * tbl_pitch + (pos >> 4)];
   char* kvbase = reinterpret_cast<char*>(block_base[blk] + layer_off);
   const int r = pos & 15;
-  // q and k heads: pairs (i, i + D/2)
-  for (int e = threadIdx.x; e < (H + Hk) * half; e += blockDim.x) {
-    const int hh = e / half, i = e % half;
-    const int c0 = hh * D + i, c1 = c0 + half;
-    float x0 = row[c0], x1 = row[c1];
-    if (bias) {
-      x0 += bf(bias, c0);
-      x1 += bf(bias, c1);
-    }
-    float y0 = x0, y1 = x1;
-    if (family == 1) {
-      const float c = cs[i], s = cs[half + i];
-      y0 = x0 * c - x1 * s;
-      y1 = x1 * c + x0 * s;
-    }
-    if (hh < H) {
-      q[((size_t)b * H + hh) * D + i] = y0;
-      q[((size_t)b * H + hh) * D + i + half] = y1;
+  const int n_qk = (H + Hk) * hc, n_v = Hk * (D / 8);
+  for (int e = threadIdx.x; e < n_qk + n_v; e += blockDim.x) {
+    if (e < n_qk) {
+      const int hh = e / hc, c = e % hc;
+      const int c0 = hh * D + c * 8, c1 = c0 + half;
+      float x0[8], x1[8];
+      load8(row + c0, x0);
+      load8(row + c1, x1);
+      if (bias) {
+        float b0[8], b1[8];
+        load8bf(bias + c0, b0);
+        load8bf(bias + c1, b1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          x0[k] += b0[k];
+          x1[k] += b1[k];
+        }
+      }
+      if (family == 1) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float co = cs[c * 8 + k], si = cs[half + c * 8 + k];
+          const float y0 = x0[k] * co - x1[k] * si, y1 = x1[k] * co + x0[k] * si;
+          x0[k] = y0;
+          x1[k] = y1;
+        }
+      }
+      if (hh < H) {
+        float* qd = q + ((size_t)b * H + hh) * D + c * 8;
+        store8(qd, x0);
+        store8(qd + half, x1);
+      } else {
+        char* dst = kvbase + ((size_t)((hh - H) * 2 + 0) * 16 + r) * D * 2;
+        *reinterpret_cast<uint4*>(dst + ((c ^ (r & 7)) << 4)) = pack8bf(x0);
+        *reinterpret_cast<uint4*>(dst + (((c + hc) ^ (r & 7)) << 4)) = pack8bf(x1);
+      }
     } else {
-      const int kh = hh - H;
-      __nv_bfloat16* dst =
-          reinterpret_cast<__nv_bfloat16*>(kvbase + ((size_t)(kh * 2 + 0) * 16 + r) * D * 2);
-      dst[swz(i, r)] = __float2bfloat16_rn(y0);
-      dst[swz(i + half, r)] = __float2bfloat16_rn(y1);
+      const int e2 = e - n_qk;
+      const int kh = e2 / (D / 8), c = e2 % (D / 8);
+      const int col = (H + Hk) * D + kh * D + c * 8;
+      float x0[8];
+      load8(row + col, x0);
+      if (bias) {
+        float b0[8];
+        load8bf(bias + col, b0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x0[k] += b0[k];
+      }
+      char* dst = kvbase + ((size_t)(kh * 2 + 1) * 16 + r) * D * 2;
+      *reinterpret_cast<uint4*>(dst + ((c ^ (r & 7)) << 4)) = pack8bf(x0);
     }
-  }
-  for (int e = threadIdx.x; e < Hk * D; e += blockDim.x) {
-    const int kh = e / D, i = e % D;
-    const int c = (H + Hk) * D + e;
-    float x0 = row[c];
-    if (bias) x0 += bf(bias, c);
-    __nv_bfloat16* dst =
-        reinterpret_cast<__nv_bfloat16*>(kvbase + ((size_t)(kh * 2 + 1) * 16 + r) * D * 2);
-    dst[swz(i, r)] = __float2bfloat16_rn(x0);
   }
 }
 
+// 8 elements per thread. OPT: f = bf16(relu(y + b)); Llama: f = bf16(silu(g) * u),
+// y = [gate | up] per row.
 __global__ void act_kernel(int family, int B, int f, const float* y, const __nv_bfloat16* bias,
                            __nv_bfloat16* out) {
-  const size_t n = (size_t)B * f;
+  const size_t n = (size_t)B * f / 8;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
        e += (size_t)gridDim.x * blockDim.x) {
-    const size_t b = e / f, i = e % f;
-    float r;
+    const size_t b = e * 8 / f, i = e * 8 % f;
+    float r[8];
     if (family == 0) {
-      r = fmaxf(y[b * f + i] + bf(bias, (int)i), 0.f);
+      float bv[8];
+      load8(y + b * f + i, r);
+      load8bf(bias + i, bv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = fmaxf(r[k] + bv[k], 0.f);
     } else {
-      const float gt = y[b * 2 * f + i], up = y[b * 2 * f + f + i];
-      r = gt / (1.f + expf(-gt)) * up;
+      float gt[8], up[8];
+      load8(y + b * 2 * f + i, gt);
+      load8(y + b * 2 * f + f + i, up);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = gt[k] / (1.f + __expf(-gt[k])) * up[k];
     }
-    out[e] = __float2bfloat16_rn(r);
+    *reinterpret_cast<uint4*>(out + e * 8) = pack8bf(r);
   }
 }
 
@@ -332,8 +376,8 @@ cudaError_t launch_embed_norm(int family, int B, int d, const int32_t* tokens,
                               const __nv_bfloat16* pos_embed, const __nv_bfloat16* g,
                               const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
                               cudaStream_t s) {
-  if (d > kNormThreads * kMaxPerThread) return cudaErrorInvalidValue;
-  embed_norm_kernel<<<B, kNormThreads, 0, s>>>(family, d, tokens, positions, embed, pos_embed, g,
+  if (d % 8 || d > 8192) return cudaErrorInvalidValue;
+  embed_norm_kernel<<<B, ((d / 8 + 31) / 32) * 32, 0, s>>>(family, d, tokens, positions, embed, pos_embed, g,
                                                bta, eps, h, x);
   return cudaGetLastError();
 }
@@ -342,8 +386,8 @@ cudaError_t launch_residual_norm(int family, int B, int d, const float* y, int l
                                  const __nv_bfloat16* bias, const __nv_bfloat16* g,
                                  const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
                                  cudaStream_t s) {
-  if (d > kNormThreads * kMaxPerThread) return cudaErrorInvalidValue;
-  residual_norm_kernel<<<B, kNormThreads, 0, s>>>(family, d, y, ldy, bias, g, bta, eps, h, x);
+  if (d % 8 || d > 8192) return cudaErrorInvalidValue;
+  residual_norm_kernel<<<B, ((d / 8 + 31) / 32) * 32, 0, s>>>(family, d, y, ldy, bias, g, bta, eps, h, x);
   return cudaGetLastError();
 }
 
@@ -359,7 +403,7 @@ cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float
 
 cudaError_t launch_act(int family, int B, int f, const float* y, const __nv_bfloat16* bias,
                        __nv_bfloat16* out, cudaStream_t s) {
-  const size_t n = (size_t)B * f;
+  const size_t n = (size_t)B * f / 8;
   act_kernel<<<grid_for(n, 256), 256, 0, s>>>(family, B, f, y, bias, out);
   return cudaGetLastError();
 }

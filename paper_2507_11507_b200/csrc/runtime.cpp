@@ -2,6 +2,7 @@
 // (a2, a3), copy-engine prefetcher with event-gated layer handoff (a4, a5) and
 // the decode-step executor (a0, a6-a9). See include/mirage.h for the contract
 // and DESIGN.md for the readings of the paper this follows.
+#include <cublasLt.h>
 #include <cublas_v2.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -14,6 +15,7 @@
 #include <cstring>
 #include <deque>
 #include <map>
+#include <tuple>
 #include <set>
 #include <string>
 #include <unordered_map>
@@ -202,7 +204,15 @@ struct mirage_ctx {
   uint64_t arena_used = 0;
   std::vector<Model*> models;
   cublasHandle_t blas = nullptr;
+  cublasLtHandle_t lt = nullptr;
   void* blas_ws = nullptr;
+  struct LtPlan {
+    cublasLtMatmulDesc_t op = nullptr;
+    cublasLtMatrixLayout_t a = nullptr, b = nullptr, d = nullptr;
+    cublasLtMatmulAlgo_t algo{};
+    bool has_algo = false;
+  };
+  std::map<std::tuple<int, int, int, int, int>, LtPlan> lt_plans;  // (B, N, K, out_bf16, epi)
   // step metadata: pinned staging ring -> device
   size_t meta_bytes = 0;
   char* stage[2] = {nullptr, nullptr};
@@ -450,11 +460,48 @@ void harvest_step_time(Model* M) {
   (void)cudaGetLastError();
 }
 
-int32_t gemm(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf16* x, float* y, int ldy) {
+// y[B][N] = epilogue(x[B][K] W[N][K]^T (+ bias[N])), fp32 accumulate, via cuBLASLt.
+// epi: 0 none, 1 bias, 2 relu(+bias). out_bf16 selects the output type.
+int32_t gemm_lt(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf16* x, void* y, int out_bf16,
+                const bf16* bias, int epi) {
+  auto key = std::make_tuple(B, N, K, out_bf16, epi);
+  auto it = c->lt_plans.find(key);
+  if (it == c->lt_plans.end()) {
+    mirage_ctx::LtPlan pl;
+    CKB(c, cublasLtMatmulDescCreate(&pl.op, CUBLAS_COMPUTE_32F, CUDA_R_32F));
+    const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
+    CKB(c, cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof ta));
+    CKB(c, cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof tb));
+    cublasLtEpilogue_t e = epi == 2 ? CUBLASLT_EPILOGUE_RELU_BIAS
+                           : epi == 1 ? CUBLASLT_EPILOGUE_BIAS : CUBLASLT_EPILOGUE_DEFAULT;
+    CKB(c, cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_EPILOGUE, &e, sizeof e));
+    if (epi) {
+      const cudaDataType_t bt = CUDA_R_16BF;
+      CKB(c, cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &bt, sizeof bt));
+    }
+    CKB(c, cublasLtMatrixLayoutCreate(&pl.a, CUDA_R_16BF, K, N, K));
+    CKB(c, cublasLtMatrixLayoutCreate(&pl.b, CUDA_R_16BF, K, B, K));
+    CKB(c, cublasLtMatrixLayoutCreate(&pl.d, out_bf16 ? CUDA_R_16BF : CUDA_R_32F, N, B, N));
+    cublasLtMatmulPreference_t pref;
+    CKB(c, cublasLtMatmulPreferenceCreate(&pref));
+    const uint64_t ws = kCublasWs;
+    CKB(c, cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws, sizeof ws));
+    cublasLtMatmulHeuristicResult_t res[1];
+    int n = 0;
+    cublasLtMatmulAlgoGetHeuristic(c->lt, pl.op, pl.a, pl.b, pl.d, pl.d, pref, 1, res, &n);
+    cublasLtMatmulPreferenceDestroy(pref);
+    if (n > 0) {
+      pl.algo = res[0].algo;
+      pl.has_algo = true;
+    }
+    it = c->lt_plans.emplace(key, pl).first;
+  }
+  const mirage_ctx::LtPlan& pl = it->second;
+  if (epi)
+    CKB(c, cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof bias));
   const float one = 1.f, zero = 0.f;
-  CKB(c, cublasGemmEx(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, N, B, K, &one, W, CUDA_R_16BF, K, x,
-                      CUDA_R_16BF, K, &zero, y, CUDA_R_32F, ldy, CUBLAS_COMPUTE_32F,
-                      CUBLAS_GEMM_DEFAULT));
+  CKB(c, cublasLtMatmul(c->lt, pl.op, &one, W, pl.a, x, pl.b, &zero, y, pl.d, y, pl.d,
+                        pl.has_algo ? &pl.algo : nullptr, c->blas_ws, kCublasWs, c->cs));
   return MIRAGE_OK;
 }
 
@@ -518,6 +565,7 @@ int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
     c->own_xs = true;
   }
   if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return bail(MIRAGE_ERR_CUDA);
+  if (cublasLtCreate(&c->lt) != CUBLAS_STATUS_SUCCESS) return bail(MIRAGE_ERR_CUDA);
   if (cudaMalloc(&c->blas_ws, kCublasWs) != cudaSuccess) return bail(MIRAGE_ERR_CUDA);
   if (cublasSetWorkspace(c->blas, c->blas_ws, kCublasWs) != CUBLAS_STATUS_SUCCESS ||
       cublasSetStream(c->blas, c->cs) != CUBLAS_STATUS_SUCCESS)
@@ -567,6 +615,13 @@ void mirage_destroy(mirage_ctx* c) {
   }
   if (c->meta_dev) cudaFree(c->meta_dev);
   if (c->blas) cublasDestroy(c->blas);
+  for (auto& kv : c->lt_plans) {
+    cublasLtMatmulDescDestroy(kv.second.op);
+    cublasLtMatrixLayoutDestroy(kv.second.a);
+    cublasLtMatrixLayoutDestroy(kv.second.b);
+    cublasLtMatrixLayoutDestroy(kv.second.d);
+  }
+  if (c->lt) cublasLtDestroy(c->lt);
   if (c->blas_ws) cudaFree(c->blas_ws);
   if (c->own_xs && c->xs) cudaStreamDestroy(c->xs);
   (void)cudaGetLastError();
@@ -959,7 +1014,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   for (int l = 0; l < s.n; ++l) {
     const LayerW w = layer_ptrs(s, wptr[l]);
     const uint64_t layer_off = (uint64_t)l * Hk * 2 * kBlockTokens * D * 2;
-    if (int32_t e = gemm(c, B, qkvN, d, w.w_qkv, M->x, M->y, qkvN)) return e;
+    if (int32_t e = gemm_lt(c, B, qkvN, d, w.w_qkv, M->x, M->y, 0, nullptr, 0)) return e;
     KL(c, mirage::launch_qkv_post(s.family, B, H, Hk, D, M->y, opt ? w.b_qkv : nullptr, dv.pos,
                                  dv.tables, pitch, M->bbase_dev, layer_off, s.theta, M->q, cs));
     ap.layer_off = layer_off;
@@ -972,17 +1027,17 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     } else {
       KL(c, mirage::launch_paged_attention(ap, cs));
     }
-    if (int32_t e = gemm(c, B, d, H * D, w.w_o, M->x, M->y, d)) return e;
+    if (int32_t e = gemm_lt(c, B, d, H * D, w.w_o, M->x, M->y, 0, nullptr, 0)) return e;
     KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_o : nullptr, w.n2_g,
                                       opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs));
     if (opt) {
-      if (int32_t e = gemm(c, B, s.f, d, w.w_1, M->x, M->y, s.f)) return e;
-      KL(c, mirage::launch_act(s.family, B, s.f, M->y, w.b_1, M->f, cs));
+      // FC1 + bias + ReLU fused in the GEMM epilogue, bf16 out (one rounding, as before)
+      if (int32_t e = gemm_lt(c, B, s.f, d, w.w_1, M->x, M->f, 1, w.b_1, 2)) return e;
     } else {
-      if (int32_t e = gemm(c, B, 2 * s.f, d, w.w_1, M->x, M->y, 2 * s.f)) return e;
+      if (int32_t e = gemm_lt(c, B, 2 * s.f, d, w.w_1, M->x, M->y, 0, nullptr, 0)) return e;
       KL(c, mirage::launch_act(s.family, B, s.f, M->y, nullptr, M->f, cs));
     }
-    if (int32_t e = gemm(c, B, d, s.f, w.w_2, M->f, M->y, d)) return e;
+    if (int32_t e = gemm_lt(c, B, d, s.f, w.w_2, M->f, M->y, 0, nullptr, 0)) return e;
     // residual, then the next layer's first norm (or the final norm)
     const bool last = l + 1 == s.n;
     const bf16* ng = last ? gw.nf_g : nullptr;
@@ -1010,7 +1065,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     }
   }
   // LM head + argmax
-  if (int32_t e = gemm(c, B, s.V, d, gw.lm_head, M->x, M->y, s.V)) return e;
+  if (int32_t e = gemm_lt(c, B, s.V, d, gw.lm_head, M->x, M->y, 0, nullptr, 0)) return e;
   KL(c, mirage::launch_argmax(B, s.V, M->y, M->argmax, cs));
   if (hidden_out)
     CK(c, cudaMemcpyAsync(hidden_out, M->x, (size_t)B * d * 2, cudaMemcpyDeviceToDevice, cs));
