@@ -8,8 +8,11 @@
 // (PAPER.md:161 PagedAttention; :558-564 reclaimed memory reused as KV).
 //
 // Design (HBM-bound gather; AI = G flop/B):
-//   * grid = (units, H_kv); a unit is one (sequence, split) pair; CTA = 4 warps;
-//     warp w handles blocks w, w+4, ... of the split (placement independent).
+//   * a work item is (sequence, split, kv head); a CTA = 4 warps, warp w takes
+//     blocks w, w+4, ... of the item (placement independent). The grid is
+//     persistent (one wave of CTAs); CTA c takes items c, c + grid, ... in the
+//     host's longest-first order, and each warp's TMA ring streams straight
+//     across item boundaries, so no CTA launch/prologue bubbles remain.
 //   * one 16-token block of one (layer, kv-head) is a contiguous 2*16*D*2-byte
 //     K|V tile, fetched whole by one cp.async.bulk (TMA engine) into shared
 //     memory; every warp runs its own NS-deep ring (mbarrier complete_tx), so
@@ -26,6 +29,8 @@
 //     placement of the blocks (remap invariance).
 #include <math_constants.h>
 #include <stdlib.h>
+
+#include <algorithm>
 
 #include "kernels.cuh"
 
@@ -91,10 +96,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
   return a | (b << 16);
 }
 
-constexpr int kMaxSplitsDev = 64;  // split-K partitions per (sequence, kv head)
+constexpr int kMaxSplitsDev = 128;  // split-K partitions per (sequence, kv head); runtime agrees
 
-template <int D, int W, int NS>
-constexpr int smem_bytes() { return W * NS * 2 * (16 * D * 2); }
+template <int D, int G, int W, int NS>
+constexpr int smem_bytes() { return W * NS * 2 * (16 * D * 2) + (NS + 1) * G * D * 4; }
 
 // Tensor-core formulation per 16-token tile (one warp):
 //   S[16 tok x 8 col] = K[16 x D] * Qc[D x 8]      (D/16 mma.m16n8k16 per n-tile)
@@ -113,303 +118,367 @@ paged_attention_kernel(const AttnParams p) {
   constexpr int KS = D / 16;          // k-slices (QK) == dim tiles (PV)
   constexpr int NT = (2 * G + 7) / 8; // n8 tiles of (head, part) columns
 
+  constexpr int QB = NS + 1;           // q staging buffers per CTA (warp 0's producer runs ahead)
+
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[kWarps][NS];
+  __shared__ __align__(8) uint64_t qbars[QB];
+  __shared__ float sm_m[kWarps][G], sm_l[kWarps][G];
+  constexpr int ACC = (kWarps * D > 2 * kMaxSplitsDev ? kWarps * D : 2 * kMaxSplitsDev) * G;
+  __shared__ __align__(16) float sm_accf[ACC];
+  float(*sm_acc)[G][D] = reinterpret_cast<float(*)[G][D]>(sm_accf);
+  __shared__ int am_last;
+  __shared__ float sLam[G];
+  // split-combine scratch aliases sm_acc (free once the partials are written)
+  float(*sw)[G] = reinterpret_cast<float(*)[G]>(sm_accf);
+  float(*sl)[G] = reinterpret_cast<float(*)[G]>(sm_accf + kMaxSplitsDev * G);
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int gq = lane >> 2;  // mma group id (row / column index)
   const int tq = lane & 3;   // thread in group
-  const AttnUnit u = p.units[blockIdx.x];
-  const int hk = blockIdx.y;
-  const int s = u.seq;
-  const int L = p.ctx_len[s];
-  const int nblk = (L + 15) >> 4;
-  const int b0 = u.split * p.split_blocks;
-  const int b1 = min(b0 + p.split_blocks, nblk);
-  const int32_t* tbl = p.tables + (size_t)s * p.tbl_pitch;
-  const uint64_t head_off = p.layer_off + (uint64_t)hk * (2 * TILE);
+  const int n_flat = p.n_units * p.H_kv;  // work item f = unit * H_kv + kv head
   uint8_t* ring = smem + (size_t)warp * NS * 2 * TILE;
-  const int first = b0 + warp;  // this warp's blocks: first + W * it
-  const int n_it = first < b1 ? (b1 - first + kWarps - 1) / kWarps : 0;
+  // q staging (dynamic smem after the rings): [QB][G*D] fp32, one copy per CTA item
+  float(*qbuf)[G * D] = reinterpret_cast<float(*)[G * D]>(smem + (size_t)kWarps * NS * 2 * TILE);
 
   if (lane == 0) {
 #pragma unroll
     for (int i = 0; i < NS; ++i) mbar_init(&bars[warp][i], 1);
+    if (warp == 0)
+#pragma unroll
+      for (int i = 0; i < QB; ++i) mbar_init(&qbars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncwarp();
-  int addr_base = 0;
-  uint64_t my_addr = 0;
-  if (lane < n_it) my_addr = p.block_base[tbl[first + kWarps * lane]] + head_off;
-  auto addr_of = [&](int it) -> uint64_t { return __shfl_sync(0xffffffffu, my_addr, it - addr_base); };
-#pragma unroll
-  for (int i = 0; i < NS; ++i) {
-    if (i < n_it) {
-      const uint64_t a = addr_of(i);
-      if (lane == 0) {
-        mbar_expect_tx(&bars[warp][i], 2 * TILE);
-        bulk_g2s(ring + i * 2 * TILE, reinterpret_cast<const void*>(a), 2 * TILE, &bars[warp][i]);
-      }
-    }
-  }
+  __syncthreads();  // q barriers are shared by the CTA
 
-  // B fragments of the query columns: column n = gq (+8 nt): head nt*4 + gq/2, part gq&1
-  uint32_t qb[NT][KS][2];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int hh = nt * 4 + (gq >> 1);
-    const int part = gq & 1;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      if (hh < G) {
-        const float* qp = p.q + ((size_t)s * p.H + hk * G + hh) * D + ks * 16 + 2 * tq;
-        const float sc = p.scale_log2;
-        qb[nt][ks][0] = pack_bf16(bf16_part(qp[0] * sc, part), bf16_part(qp[1] * sc, part));
-        qb[nt][ks][1] = pack_bf16(bf16_part(qp[8] * sc, part), bf16_part(qp[9] * sc, part));
-      } else {
-        qb[nt][ks][0] = qb[nt][ks][1] = 0u;
+  // ---- producer: walks this warp's tile stream (items blockIdx.x, +gridDim.x, ...,
+  // blocks warp, warp+W, ... of each) NS tiles ahead of the consumer, across
+  // item boundaries, so the ring never drains between work items ----
+  int pf = (int)blockIdx.x - (int)gridDim.x, p_it = 0, p_n = 0, addr_base = 0;
+  uint32_t pq = 0;  // items whose q warp 0's producer has staged
+  const int32_t* p_tbl = nullptr;
+  uint64_t p_off = 0, my_addr = 0;
+  auto produce = [&](int stage) {
+    while (p_it >= p_n) {
+      pf += gridDim.x;
+      if (pf >= n_flat) return;
+      const AttnUnit u = p.units[pf / p.H_kv];
+      const int L = p.ctx_len[u.seq];
+      const int b0 = u.split * p.split_blocks;
+      const int b1 = min(b0 + p.split_blocks, (L + 15) >> 4);
+      const int first = b0 + warp;
+      p_n = first < b1 ? (b1 - first + kWarps - 1) / kWarps : 0;
+      p_it = 0;
+      p_tbl = p.tables + (size_t)u.seq * p.tbl_pitch + first;
+      p_off = p.layer_off + (uint64_t)(pf % p.H_kv) * (2 * TILE);
+      addr_base = 0;
+      my_addr = lane < p_n ? p.block_base[p_tbl[kWarps * lane]] + p_off : 0;
+      if (warp == 0) {  // stage this item's q rows (G heads x D fp32) for the whole CTA;
+        // warp 0 owns the first block of every item, so it visits every item in order
+        __syncwarp();
+        if (lane == 0) {
+          const int qi = pq % QB;
+          const float* src = p.q + ((size_t)u.seq * p.H + (pf % p.H_kv) * G) * D;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&qbars[qi], G * D * 4);
+          bulk_g2s(&qbuf[qi][0], src, G * D * 4, &qbars[qi]);
+        }
+        ++pq;
       }
     }
-  }
-  // per lane: softmax state of head nt*4 + tq; O^T accumulators (dims ks*16+gq,+8)
-  float m[NT], l[NT], o[NT][KS][4];
+    if (p_it - addr_base >= 32) {  // next window of 32 block addresses
+      addr_base += 32;
+      const int j = addr_base + lane;
+      my_addr = j < p_n ? p.block_base[p_tbl[kWarps * j]] + p_off : 0;
+    }
+    const uint64_t a = __shfl_sync(0xffffffffu, my_addr, p_it - addr_base);
+    ++p_it;
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bars[warp][stage], 2 * TILE);
+      bulk_g2s(ring + stage * 2 * TILE, reinterpret_cast<const void*>(a), 2 * TILE, &bars[warp][stage]);
+    }
+  };
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    m[nt] = -CUDART_INF_F;
-    l[nt] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) o[nt][ks][j] = 0.f;
-  }
+  for (int i = 0; i < NS; ++i) produce(i);
+
   // ldmatrix row addresses (byte offsets within a tile, before the swizzle)
   const int k_row = (lane & 7) + ((lane >> 3) & 1) * 8, k_cadd = lane >> 4;
   const int v_row = (lane & 7) + (lane >> 4) * 8, v_cadd = (lane >> 3) & 1;
+  uint32_t rc = 0;  // consumer ring counter
+  uint32_t cq = 0;  // consumer item counter (indexes the q ring)
 
-  for (int it = 0; it < n_it; ++it) {
-    const int st = it % NS;
-    const uint32_t phase = (it / NS) & 1;
-    const int blk = first + kWarps * it;
-    mbar_wait(&bars[warp][st], phase);
-    uint8_t* tile = ring + st * 2 * TILE;
-    const int valid_rows = min(16, L - blk * 16);
-    if (valid_rows < 16) {  // rows past the context may hold any bytes: zero V there
-      for (int e = lane; e < (16 - valid_rows) * (ROW / 16); e += 32) {
-        const int r = valid_rows + e / (ROW / 16), c = e % (ROW / 16);
-        *reinterpret_cast<uint4*>(tile + TILE + r * ROW + c * 16) = make_uint4(0, 0, 0, 0);
-      }
-      __syncwarp();
-    }
-    // ---- S = K Qc ----
-    float sacc[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) sacc[nt][j] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      uint32_t a[4];
-      const int c = 2 * ks + k_cadd;
-      ldsm_x4(a, tile + k_row * ROW + ((c ^ (k_row & 7)) << 4));
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) mma_bf16(sacc[nt], a, qb[nt][ks]);
-    }
-    // ---- online softmax (base 2) per head nt*4+tq; rows gq and gq+8 ----
-    float pA[NT], pB[NT];
+  for (int f = blockIdx.x; f < n_flat; f += gridDim.x) {
+    const AttnUnit u = p.units[f / p.H_kv];
+    const int hk = f % p.H_kv;
+    const int s = u.seq;
+    const int L = p.ctx_len[s];
+    const int b0 = u.split * p.split_blocks;
+    const int b1 = min(b0 + p.split_blocks, (L + 15) >> 4);
+    const int first = b0 + warp;
+    const int n_it = first < b1 ? (b1 - first + kWarps - 1) / kWarps : 0;
+
+    // B fragments of the query columns: column n = gq (+8 nt): head nt*4 + gq/2, part gq&1
+    uint32_t qb[NT][KS][2];
+    const float* qs = &qbuf[cq % QB][0];
+    if (n_it > 0) mbar_wait(&qbars[cq % QB], (cq / QB) & 1);
+    ++cq;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      const float s0 = (gq < valid_rows) ? sacc[nt][0] + sacc[nt][1] : -CUDART_INF_F;
-      const float s1 = (gq + 8 < valid_rows) ? sacc[nt][2] + sacc[nt][3] : -CUDART_INF_F;
-      float bm = fmaxf(s0, s1);
-      bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 4));
-      bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
-      bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
-      const float m_new = fmaxf(m[nt], bm);
-      const float alpha = exp2f(m[nt] - m_new);
-      pA[nt] = exp2f(s0 - m_new);
-      pB[nt] = exp2f(s1 - m_new);
-      l[nt] = l[nt] * alpha + pA[nt] + pB[nt];
-      m[nt] = m_new;
+      const int hh = nt * 4 + (gq >> 1);
+      const int part = gq & 1;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        if (hh < G && n_it > 0) {
+          const float* qp = qs + hh * D + ks * 16 + 2 * tq;
+          const float sc = p.scale_log2;
+          qb[nt][ks][0] = pack_bf16(bf16_part(qp[0] * sc, part), bf16_part(qp[1] * sc, part));
+          qb[nt][ks][1] = pack_bf16(bf16_part(qp[8] * sc, part), bf16_part(qp[9] * sc, part));
+        } else {
+          qb[nt][ks][0] = qb[nt][ks][1] = 0u;
+        }
+      }
+    }
+    // per lane: softmax state of head nt*4 + tq; O^T accumulators (dims ks*16+gq,+8)
+    float m[NT], l[NT], o[NT][KS][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      m[nt] = -CUDART_INF_F;
+      l[nt] = 0.f;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) o[nt][ks][j] *= alpha;
+        for (int j = 0; j < 4; ++j) o[nt][ks][j] = 0.f;
     }
-    // ---- P as B fragments: lane needs P[2tq, 2tq+1, 2tq+8, 2tq+9][column gq] ----
-    uint32_t pb[NT][2];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int src0 = 8 * tq + (gq >> 1), src1 = src0 + 4;
-      const float a0 = __shfl_sync(0xffffffffu, pA[nt], src0);  // P[2tq]
-      const float a8 = __shfl_sync(0xffffffffu, pB[nt], src0);  // P[2tq+8]
-      const float c0 = __shfl_sync(0xffffffffu, pA[nt], src1);  // P[2tq+1]
-      const float c8 = __shfl_sync(0xffffffffu, pB[nt], src1);  // P[2tq+9]
-      const int part = gq & 1;
-      if (nt * 4 + (gq >> 1) < G) {
-        pb[nt][0] = pack_bf16(bf16_part(a0, part), bf16_part(c0, part));
-        pb[nt][1] = pack_bf16(bf16_part(a8, part), bf16_part(c8, part));
-      } else {
-        pb[nt][0] = pb[nt][1] = 0u;
-      }
-    }
-    // ---- O^T += V^T P ----
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      uint32_t a[4];
-      const int c = 2 * ks + v_cadd;
-      ldsm_x4_t(a, tile + TILE + v_row * ROW + ((c ^ (v_row & 7)) << 4));
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) mma_bf16(o[nt][ks], a, pb[nt]);
-    }
-    // refill this stage with iteration it + NS (all lanes are done reading it)
-    const int nx = it + NS;
-    if (nx < n_it) {
-      if (nx - addr_base >= 32) {  // next window of 32 block addresses
-        addr_base += 32;
-        const int j = addr_base + lane;
-        my_addr = j < n_it ? p.block_base[tbl[first + kWarps * j]] + head_off : 0;
-      }
-      const uint64_t a = addr_of(nx);
-      __syncwarp();
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bars[warp][st], 2 * TILE);
-        bulk_g2s(ring + st * 2 * TILE, reinterpret_cast<const void*>(a), 2 * TILE, &bars[warp][st]);
-      }
-    }
-  }
-  // l: sum the lane partials over the 8 token groups
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 4);
-    l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 8);
-    l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 16);
-  }
 
-  __shared__ float sm_m[kWarps][G], sm_l[kWarps][G];
-  __shared__ __align__(16) float sm_acc[kWarps][G][D];
+    for (int it = 0; it < n_it; ++it, ++rc) {
+      const int st = rc % NS;
+      const uint32_t phase = (rc / NS) & 1;
+      const int blk = first + kWarps * it;
+      mbar_wait(&bars[warp][st], phase);
+      uint8_t* tile = ring + st * 2 * TILE;
+      const int valid_rows = min(16, L - blk * 16);
+      if (valid_rows < 16) {  // rows past the context may hold any bytes: zero V there
+        for (int e = lane; e < (16 - valid_rows) * (ROW / 16); e += 32) {
+          const int r = valid_rows + e / (ROW / 16), c = e % (ROW / 16);
+          *reinterpret_cast<uint4*>(tile + TILE + r * ROW + c * 16) = make_uint4(0, 0, 0, 0);
+        }
+        __syncwarp();
+      }
+      // ---- S = K Qc ----
+      float sacc[NT][4];
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int hh = nt * 4 + tq;
-    if (hh < G) {
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sacc[nt][j] = 0.f;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
-        sm_acc[warp][hh][ks * 16 + gq] = o[nt][ks][0] + o[nt][ks][1];
-        sm_acc[warp][hh][ks * 16 + gq + 8] = o[nt][ks][2] + o[nt][ks][3];
+        uint32_t a[4];
+        const int c = 2 * ks + k_cadd;
+        ldsm_x4(a, tile + k_row * ROW + ((c ^ (k_row & 7)) << 4));
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mma_bf16(sacc[nt], a, qb[nt][ks]);
       }
-      if (gq == 0) {
-        sm_m[warp][hh] = m[nt];
-        sm_l[warp][hh] = l[nt];
+      // ---- online softmax (base 2) per head nt*4+tq; rows gq and gq+8 ----
+      float pA[NT], pB[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const float s0 = (gq < valid_rows) ? sacc[nt][0] + sacc[nt][1] : -CUDART_INF_F;
+        const float s1 = (gq + 8 < valid_rows) ? sacc[nt][2] + sacc[nt][3] : -CUDART_INF_F;
+        float bm = fmaxf(s0, s1);
+        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 4));
+        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
+        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
+        const float m_new = fmaxf(m[nt], bm);
+        const float alpha = exp2f(m[nt] - m_new);
+        pA[nt] = exp2f(s0 - m_new);
+        pB[nt] = exp2f(s1 - m_new);
+        l[nt] = l[nt] * alpha + pA[nt] + pB[nt];
+        m[nt] = m_new;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o[nt][ks][j] *= alpha;
       }
+      // ---- P as B fragments: lane needs P[2tq, 2tq+1, 2tq+8, 2tq+9][column gq] ----
+      uint32_t pb[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int src0 = 8 * tq + (gq >> 1), src1 = src0 + 4;
+        const float a0 = __shfl_sync(0xffffffffu, pA[nt], src0);  // P[2tq]
+        const float a8 = __shfl_sync(0xffffffffu, pB[nt], src0);  // P[2tq+8]
+        const float c0 = __shfl_sync(0xffffffffu, pA[nt], src1);  // P[2tq+1]
+        const float c8 = __shfl_sync(0xffffffffu, pB[nt], src1);  // P[2tq+9]
+        const int part = gq & 1;
+        if (nt * 4 + (gq >> 1) < G) {
+          pb[nt][0] = pack_bf16(bf16_part(a0, part), bf16_part(c0, part));
+          pb[nt][1] = pack_bf16(bf16_part(a8, part), bf16_part(c8, part));
+        } else {
+          pb[nt][0] = pb[nt][1] = 0u;
+        }
+      }
+      // ---- O^T += V^T P ----
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        uint32_t a[4];
+        const int c = 2 * ks + v_cadd;
+        ldsm_x4_t(a, tile + TILE + v_row * ROW + ((c ^ (v_row & 7)) << 4));
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mma_bf16(o[nt][ks], a, pb[nt]);
+      }
+      produce(st);  // refill this stage with the tile NS ahead in the stream
     }
-  }
-  __syncthreads();
+    // l: sum the lane partials over the 8 token groups
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 4);
+      l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 8);
+      l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 16);
+    }
 
-  // merge the warps in fixed order; thread t handles (g, d) pairs
-  const bool split = u.nsplit > 1;
-  for (int e = threadIdx.x; e < G * D; e += kWarps * 32) {
-    const int g = e / D, d = e % D;
-    float M = sm_m[0][g];
+    __syncthreads();  // the previous item's merge has finished reading sm_*
 #pragma unroll
-    for (int w = 1; w < kWarps; ++w) M = fmaxf(M, sm_m[w][g]);
-    float Ls = 0.f, o = 0.f;
+    for (int nt = 0; nt < NT; ++nt) {
+      const int hh = nt * 4 + tq;
+      if (hh < G) {
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const float f = (sm_m[w][g] == -CUDART_INF_F) ? 0.f : exp2f(sm_m[w][g] - M);
-      Ls += f * sm_l[w][g];
-      o += f * sm_acc[w][g][d];
+        for (int ks = 0; ks < KS; ++ks) {
+          sm_acc[warp][hh][ks * 16 + gq] = o[nt][ks][0] + o[nt][ks][1];
+          sm_acc[warp][hh][ks * 16 + gq + 8] = o[nt][ks][2] + o[nt][ks][3];
+        }
+        if (gq == 0) {
+          sm_m[warp][hh] = m[nt];
+          sm_l[warp][hh] = l[nt];
+        }
+      }
     }
-    const int h = hk * G + g;
-    if (!split) {
-      const float r = o / Ls;
-      const size_t oi = ((size_t)s * p.H + h) * D + d;
+    __syncthreads();
+
+    // merge the warps in fixed order; thread t handles (g, d) pairs
+    const bool split = u.nsplit > 1;
+    for (int e = threadIdx.x; e < G * D; e += kWarps * 32) {
+      const int g = e / D, d = e % D;
+      float M = sm_m[0][g];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) M = fmaxf(M, sm_m[w][g]);
+      float Ls = 0.f, ov = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const float fw = (sm_m[w][g] == -CUDART_INF_F) ? 0.f : exp2f(sm_m[w][g] - M);
+        Ls += fw * sm_l[w][g];
+        ov += fw * sm_acc[w][g][d];
+      }
+      const int h = hk * G + g;
+      if (!split) {
+        const float r = ov / Ls;
+        const size_t oi = ((size_t)s * p.H + h) * D + d;
+        if (p.out_fp32) reinterpret_cast<float*>(p.out)[oi] = r;
+        else reinterpret_cast<__nv_bfloat16*>(p.out)[oi] = __float2bfloat16_rn(r);
+      } else {
+        float* rec = p.partial + ((size_t)(u.pbase + u.split) * p.H + h) * (D + 2);
+        rec[d] = ov;
+        if (d == 0) {
+          rec[D] = M;
+          rec[D + 1] = Ls;
+        }
+      }
+    }
+    if (!split) continue;
+
+    // ---- split-K combine by the last-arriving CTA of this (seq, kv head) ----
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int* t = p.tickets + (size_t)s * p.H_kv + hk;
+      const int prev = atomicAdd(t, 1);
+      am_last = (prev == u.nsplit - 1);
+      if (am_last) *t = 0;  // reset for the next launch
+    }
+    __syncthreads();
+    if (!am_last) continue;
+    __threadfence();
+    const size_t rstride = (size_t)p.H * (D + 2);
+    const float* rec0 = p.partial + ((size_t)u.pbase * p.H + hk * G) * (D + 2);
+    const int ns = u.nsplit;  // <= kMaxSplitsDev
+    // (1) stage every split's (m, l) in shared memory
+    for (int e = threadIdx.x; e < ns * G; e += kWarps * 32) {
+      const int i = e / G, g = e % G;
+      sw[i][g] = __ldcg(rec0 + i * rstride + g * (D + 2) + D);
+      sl[i][g] = __ldcg(rec0 + i * rstride + g * (D + 2) + D + 1);
+    }
+    __syncthreads();
+    // (2) per head: M = max_i m_i, w_i = 2^(m_i - M), Lambda = sum_i w_i l_i (fixed order)
+    if (threadIdx.x < G) {
+      const int g = threadIdx.x;
+      float M = -CUDART_INF_F;
+      for (int i = 0; i < ns; ++i) M = fmaxf(M, sw[i][g]);
+      float Ls = 0.f;
+      for (int i = 0; i < ns; ++i) {
+        const float w = exp2f(sw[i][g] - M);
+        sw[i][g] = w;
+        Ls += w * sl[i][g];
+      }
+      sLam[g] = Ls;
+    }
+    __syncthreads();
+    // (3) o = sum_i w_i o_i / Lambda, 8 independent loads in flight per thread
+    for (int e = threadIdx.x; e < G * D; e += kWarps * 32) {
+      const int g = e / D, d = e % D;
+      const float* rg = rec0 + g * (D + 2) + d;
+      float acc = 0.f;
+      int i = 0;
+      for (; i + 8 <= ns; i += 8) {
+        float ov[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ov[k] = __ldcg(rg + (i + k) * rstride);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc += sw[i + k][g] * ov[k];
+      }
+      for (; i < ns; ++i) acc += sw[i][g] * __ldcg(rg + i * rstride);
+      const float r = acc / sLam[g];
+      const size_t oi = ((size_t)s * p.H + hk * G + g) * D + d;
       if (p.out_fp32) reinterpret_cast<float*>(p.out)[oi] = r;
       else reinterpret_cast<__nv_bfloat16*>(p.out)[oi] = __float2bfloat16_rn(r);
-    } else {
-      float* rec = p.partial + ((size_t)(u.pbase + u.split) * p.H + h) * (D + 2);
-      rec[d] = o;
-      if (d == 0) {
-        rec[D] = M;
-        rec[D + 1] = Ls;
-      }
     }
-  }
-  if (!split) return;
-
-  // ---- split-K combine by the last-arriving CTA of this (seq, kv-head) ----
-  __shared__ int am_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int* t = p.tickets + (size_t)s * p.H_kv + hk;
-    const int prev = atomicAdd(t, 1);
-    am_last = (prev == u.nsplit - 1);
-    if (am_last) *t = 0;  // reset for the next launch
-  }
-  __syncthreads();
-  if (!am_last) return;
-  __threadfence();
-  // split weights w_i = 2^(m_i - M), Lambda = sum_i w_i l_i (fixed order i = 0..S-1)
-  __shared__ float sw[kMaxSplitsDev][G];
-  __shared__ float sL[G];
-  const size_t stride = (size_t)p.H * (D + 2);
-  const float* rec0 = p.partial + ((size_t)u.pbase * p.H + hk * G) * (D + 2);
-  for (int e = threadIdx.x; e < u.nsplit * G; e += kWarps * 32) {
-    const int i = e / G, g = e % G;
-    sw[i][g] = __ldcg(rec0 + i * stride + g * (D + 2) + D);
-  }
-  __syncthreads();
-  if (threadIdx.x < G) {
-    const int g = threadIdx.x;
-    float M = -CUDART_INF_F;
-    for (int i = 0; i < u.nsplit; ++i) M = fmaxf(M, sw[i][g]);
-    float Ls = 0.f;
-    for (int i = 0; i < u.nsplit; ++i) {
-      const float w = exp2f(sw[i][g] - M);
-      Ls += w * __ldcg(rec0 + i * stride + g * (D + 2) + D + 1);
-      sw[i][g] = w;
-    }
-    sL[g] = Ls;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < G * D; e += kWarps * 32) {
-    const int g = e / D, d = e % D;
-    const float* rec = rec0 + g * (D + 2) + d;
-    float o = 0.f;
-    int i = 0;
-    for (; i + 4 <= u.nsplit; i += 4) {  // independent loads in flight
-      const float a0 = __ldcg(rec + (i + 0) * stride), a1 = __ldcg(rec + (i + 1) * stride);
-      const float a2 = __ldcg(rec + (i + 2) * stride), a3 = __ldcg(rec + (i + 3) * stride);
-      o += sw[i][g] * a0;
-      o += sw[i + 1][g] * a1;
-      o += sw[i + 2][g] * a2;
-      o += sw[i + 3][g] * a3;
-    }
-    for (; i < u.nsplit; ++i) o += sw[i][g] * __ldcg(rec + i * stride);
-    const float r = o / sL[g];
-    const size_t oi = ((size_t)s * p.H + hk * G + g) * D + d;
-    if (p.out_fp32) reinterpret_cast<float*>(p.out)[oi] = r;
-    else reinterpret_cast<__nv_bfloat16*>(p.out)[oi] = __float2bfloat16_rn(r);
   }
 }
 
 template <int D, int G, int W, int NS>
-cudaError_t launch_v(const AttnParams& p, cudaStream_t s) {
-  constexpr int SMEM = smem_bytes<D, W, NS>();
-  static bool configured = false;  // opt in to > 48 KB dynamic shared memory once
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(paged_attention_kernel<D, G, W, NS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
+int grid_ctas() {  // persistent grid: as many CTAs as fit on the GPU at once
+  constexpr int SMEM = smem_bytes<D, G, W, NS>();
+  static int ctas = 0;
+  if (!ctas) {
+    if (cudaFuncSetAttribute(paged_attention_kernel<D, G, W, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM) != cudaSuccess)
+      return -1;
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, paged_attention_kernel<D, G, W, NS>, W * 32,
+                                                      SMEM) != cudaSuccess)
+      return -1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    ctas = std::max(1, per_sm) * sms;
   }
-  dim3 grid(p.n_units, p.H_kv);
-  paged_attention_kernel<D, G, W, NS><<<grid, W * 32, SMEM, s>>>(p);
+  return ctas;
+}
+
+template <int D, int G, int W, int NS>
+cudaError_t launch_v(const AttnParams& p, cudaStream_t s, bool query, int* grid_out) {
+  const int ctas = grid_ctas<D, G, W, NS>();
+  if (ctas < 0) return cudaErrorInvalidValue;
+  if (query) {
+    *grid_out = ctas;
+    return cudaSuccess;
+  }
+  const long items = (long)p.n_units * p.H_kv;
+  const int grid = (int)std::min<long>(items, ctas);
+  paged_attention_kernel<D, G, W, NS><<<grid, W * 32, smem_bytes<D, G, W, NS>(), s>>>(p);
   return cudaGetLastError();
 }
 
-// tuning hook: MIRAGE_ATTN_VARIANT=0..3 selects (warps, stages) for D=128, G=1
+// tuning hook: MIRAGE_ATTN_VARIANT selects (warps, stages) alternatives
 int variant() {
   static int v = -1;
   if (v < 0) {
@@ -420,25 +489,23 @@ int variant() {
 }
 
 template <int D, int G>
-cudaError_t launch_dg(const AttnParams& p, cudaStream_t s) {
-  if (D == 128 && G == 1) {
-    switch (variant()) {
-      case 1: return launch_v<D, G, 4, 3>(p, s);
-      case 2: return launch_v<D, G, 8, 2>(p, s);
-      case 3: return launch_v<D, G, 2, 4>(p, s);
-      default: break;
-    }
+cudaError_t launch_dg(const AttnParams& p, cudaStream_t s, bool query, int* grid_out) {
+  constexpr int NS = D == 128 ? 2 : 4;
+  if (p.H_kv % 4 == 0) {
+    if (D == 128 && variant() == 1) return launch_v<D, G, 4, 3>(p, s, query, grid_out);
+    return launch_v<D, G, 4, NS>(p, s, query, grid_out);
   }
-  return launch_v<D, G, 4, D == 128 ? 2 : 4>(p, s);
+  if (p.H_kv % 2 == 0) return launch_v<D, G, 2, NS>(p, s, query, grid_out);
+  return launch_v<D, G, 1, NS>(p, s, query, grid_out);
 }
 
 template <int D>
-cudaError_t launch_d(const AttnParams& p, cudaStream_t s) {
+cudaError_t launch_d(const AttnParams& p, cudaStream_t s, bool query, int* grid_out) {
   switch (p.H / p.H_kv) {
-    case 1: return launch_dg<D, 1>(p, s);
-    case 2: return launch_dg<D, 2>(p, s);
-    case 4: return launch_dg<D, 4>(p, s);
-    case 8: return launch_dg<D, 8>(p, s);
+    case 1: return launch_dg<D, 1>(p, s, query, grid_out);
+    case 2: return launch_dg<D, 2>(p, s, query, grid_out);
+    case 4: return launch_dg<D, 4>(p, s, query, grid_out);
+    case 8: return launch_dg<D, 8>(p, s, query, grid_out);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -447,9 +514,22 @@ cudaError_t launch_d(const AttnParams& p, cudaStream_t s) {
 
 cudaError_t launch_paged_attention(const AttnParams& p, cudaStream_t s) {
   if (p.n_units == 0) return cudaSuccess;
-  if (p.D == 128) return launch_d<128>(p, s);
-  if (p.D == 64) return launch_d<64>(p, s);
+  if (p.D == 128) return launch_d<128>(p, s, false, nullptr);
+  if (p.D == 64) return launch_d<64>(p, s, false, nullptr);
   return cudaErrorInvalidValue;
 }
+
+int attention_grid_ctas(int H, int H_kv, int D) {
+  AttnParams p{};
+  p.H = H;
+  p.H_kv = H_kv;
+  p.D = D;
+  int g = -1;
+  if (D == 128) launch_d<128>(p, nullptr, true, &g);
+  if (D == 64) launch_d<64>(p, nullptr, true, &g);
+  return g;
+}
+
+int attention_cta_warps(int H_kv) { return H_kv % 4 == 0 ? 4 : H_kv % 2 == 0 ? 2 : 1; }
 
 }  // namespace mirage

@@ -33,6 +33,10 @@ struct AttnParams {
 };
 
 cudaError_t launch_paged_attention(const AttnParams& p, cudaStream_t s);
+// CTAs of the persistent attention grid on this device (for split planning), and
+// warps per CTA (blocks of one work item are spread over them).
+int attention_grid_ctas(int H, int H_kv, int D);
+int attention_cta_warps(int H_kv);
 
 // ---- dense-layer support kernels -------------------------------------------
 // h[b] = E[tok] (+ P[pos + 2] for OPT); x[b] = bf16(norm(h[b])).

@@ -32,8 +32,8 @@ namespace {
 
 using bf16 = __nv_bfloat16;
 constexpr int kBlockTokens = MIRAGE_BLOCK_TOKENS;
-constexpr int kMaxSplits = 64;
-constexpr int kTargetCtas = 148 * 8;
+constexpr int kMaxSplits = 128;        // split-K partitions per (sequence, kv head) (kernel agrees)
+constexpr int kTargetCtas = 148 * 16;     // sizing bound for the attention work-item list
 constexpr uint64_t kAlign = 256;
 constexpr size_t kCublasWs = 32u << 20;
 
@@ -379,22 +379,65 @@ int32_t acquire_stage(mirage_ctx* c, char** host) {
 
 // Build attention units for lens[] (logical lengths only -> placement
 // independent splits). Returns the unit count and split size in blocks.
-int build_units(const int32_t* lens, int B, int Hk, int override_blocks, mirage::AttnUnit* units,
-                int max_units, int* split_blocks) {
-  int64_t work = 0;
+// Split-K planning for the persistent attention kernel (a9). Work items are
+// (sequence, split, kv head); `grid` CTAs take items round-robin in longest-first
+// order, each spreading an item's blocks over `warps` warps. The split size P
+// (blocks) is chosen from logical lengths only -- never from block placement --
+// by minimising the estimated makespan of CTA 0 (it receives the largest item of
+// every round): sum over rounds of ceil(size / warps) + 1 tile times, plus the
+// last CTA's combine read of the largest split count.
+int choose_split(const int32_t* lens, int B, int Hk, int G, int grid, int warps, int* max_nb_out) {
   int max_nb = 0;
+  int64_t work = 0;
+  std::vector<int> nbs(B);
   for (int b = 0; b < B; ++b) {
-    const int nb = (lens[b] + kBlockTokens - 1) / kBlockTokens;
-    work += (int64_t)nb * Hk;
-    max_nb = std::max(max_nb, nb);
+    nbs[b] = (lens[b] + kBlockTokens - 1) / kBlockTokens;
+    max_nb = std::max(max_nb, nbs[b]);
+    work += (int64_t)nbs[b] * Hk;
   }
-  int P;
-  if (override_blocks > 0) {
-    P = override_blocks;
-  } else {
-    P = (int)std::max<int64_t>(1, (work + kTargetCtas - 1) / kTargetCtas);
-    P = std::max(P, (max_nb + kMaxSplits - 1) / kMaxSplits);
+  *max_nb_out = max_nb;
+  const int p_lo = std::max(1, (max_nb + kMaxSplits - 1) / kMaxSplits);
+  if (grid <= 0 || (int64_t)B * Hk >= 16LL * grid) return std::max(p_lo, max_nb);  // many items: no split
+  std::vector<int64_t> cnt;
+  int best_p = max_nb;
+  double best = 1e300;
+  for (int P = max_nb; P >= p_lo;) {
+    // item sizes histogram (per kv head multiplicity Hk)
+    cnt.assign(P + 1, 0);
+    int max_ns = 1;
+    for (int b = 0; b < B; ++b) {
+      const int full = nbs[b] / P, rem = nbs[b] % P;
+      cnt[P] += (int64_t)full * Hk;
+      if (rem) cnt[rem] += Hk;
+      max_ns = std::max(max_ns, full + (rem ? 1 : 0));
+    }
+    // CTA 0 takes sorted items 0, grid, 2*grid, ...
+    double t = 0;
+    int64_t pos = 0;  // index of the first item of the current size bucket
+    for (int sz = P; sz >= 1; --sz) {
+      if (!cnt[sz]) continue;
+      const int64_t first_k = (pos + grid - 1) / grid;           // first k with k*grid >= pos
+      const int64_t last_k = (pos + cnt[sz] - 1) / grid;          // last k with k*grid < pos+cnt
+      if (last_k >= first_k) t += (double)(last_k - first_k + 1) * ((sz + warps - 1) / warps + 1);
+      pos += cnt[sz];
+    }
+    if (max_ns > 1) t += (double)max_ns * G / 16.0;
+    if (t < best - 1e-9) {
+      best = t;
+      best_p = P;
+    }
+    const int next = (int)(P * 0.9);
+    P = next < P ? next : P - 1;
   }
+  (void)work;
+  return best_p;
+}
+
+int build_units(const int32_t* lens, int B, int Hk, int G, int grid, int warps, int override_blocks,
+                mirage::AttnUnit* units, int max_units, int* split_blocks) {
+  int max_nb = 0;
+  int P = choose_split(lens, B, Hk, G, grid, warps, &max_nb);
+  if (override_blocks > 0) P = override_blocks;
   int n = 0, pbase = 0;
   for (int b = 0; b < B; ++b) {
     const int nb = (lens[b] + kBlockTokens - 1) / kBlockTokens;
@@ -403,6 +446,14 @@ int build_units(const int32_t* lens, int B, int Hk, int override_blocks, mirage:
     for (int i = 0; i < ns; ++i) units[n++] = mirage::AttnUnit{b, i, ns, ns > 1 ? pbase : 0};
     if (ns > 1) pbase += ns;
   }
+  // longest-first order for the persistent kernel's round-robin item assignment
+  auto size_of = [&](const mirage::AttnUnit& u) {
+    const int nb = (lens[u.seq] + kBlockTokens - 1) / kBlockTokens;
+    return std::min(P, nb - u.split * P);
+  };
+  std::stable_sort(units, units + n, [&](const mirage::AttnUnit& a, const mirage::AttnUnit& b) {
+    return size_of(a) > size_of(b);
+  });
   *split_blocks = P;
   return n;
 }
@@ -920,7 +971,8 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
               hv.tables + (size_t)i * pitch);
   }
   int split_blocks = 1;
-  const int n_units = build_units(hv.len, B, s.Hk, 0, hv.units, c->max_units, &split_blocks);
+  const int n_units = build_units(hv.len, B, s.Hk, s.H / s.Hk, mirage::attention_grid_ctas(s.H, s.Hk, s.D),
+                                  mirage::attention_cta_warps(s.Hk), 0, hv.units, c->max_units, &split_blocks);
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "step: too many attention units");
   const size_t tbl_bytes = (size_t)B * pitch * 4;
   const size_t head = reinterpret_cast<char*>(hv.tables) - host;
@@ -1110,7 +1162,9 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
     std::copy(rows[i]->begin(), rows[i]->begin() + nb, hv.tables + (size_t)i * pitch);
   }
   int split_blocks = 1;
-  const int n_units = build_units(hv.len, B, M->shp.Hk, split_tokens_override / kBlockTokens,
+  const int n_units = build_units(hv.len, B, M->shp.Hk, M->shp.H / M->shp.Hk,
+                                  mirage::attention_grid_ctas(M->shp.H, M->shp.Hk, M->shp.D),
+                                  mirage::attention_cta_warps(M->shp.Hk), split_tokens_override / kBlockTokens,
                                   hv.units, c->max_units, &split_blocks);
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "attn_only: too many units for the split override");
   const size_t head = reinterpret_cast<char*>(hv.tables) - host;
