@@ -3,7 +3,7 @@
 //
 // Computes, for sequence s and query head h (KV head h' = h / G):
 //   o = softmax(q K^T / sqrt(D)) V over the s's first ctx_len tokens,
-// reading K/V through the block table and the block_base indirection, so a
+// reading K/V through the block table (resolved per step to block addresses), so a
 // block may sit in the native pool or in reclaimed parameter memory
 // (PAPER.md:161 PagedAttention; :558-564 reclaimed memory reused as KV).
 //
@@ -128,6 +128,8 @@ paged_attention_kernel(const AttnParams p) {
   __shared__ __align__(16) float sm_accf[ACC];
   float(*sm_acc)[G][D] = reinterpret_cast<float(*)[G][D]>(sm_accf);
   __shared__ int am_last;
+  // dynamic item queue: CTA item k (in claim order) lives in slot k % QB
+  __shared__ int slot_item[QB], slot_gen[QB], slot_claim[QB];
   __shared__ float sLam[G];
   // split-combine scratch aliases sm_acc (free once the partials are written)
   float(*sw)[G] = reinterpret_cast<float(*)[G]>(sm_accf);
@@ -147,84 +149,112 @@ paged_attention_kernel(const AttnParams p) {
     for (int i = 0; i < NS; ++i) mbar_init(&bars[warp][i], 1);
     if (warp == 0)
 #pragma unroll
-      for (int i = 0; i < QB; ++i) mbar_init(&qbars[i], 1);
+      for (int i = 0; i < QB; ++i) {
+        mbar_init(&qbars[i], 1);
+        slot_gen[i] = -1;
+        slot_claim[i] = i - QB;
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();  // q barriers are shared by the CTA
+  __syncthreads();  // q barriers and item slots are shared by the CTA
 
-  // ---- producer: walks this warp's tile stream (items blockIdx.x, +gridDim.x, ...,
-  // blocks warp, warp+W, ... of each) NS tiles ahead of the consumer, across
-  // item boundaries, so the ring never drains between work items ----
-  int pf = (int)blockIdx.x - (int)gridDim.x, p_it = 0, p_n = 0, addr_base = 0;
-  uint32_t pq = 0;  // items whose q warp 0's producer has staged
-  const int32_t* p_tbl = nullptr;
-  uint64_t p_off = 0, my_addr = 0;
-  auto produce = [&](int stage) {
-    while (p_it >= p_n) {
-      pf += gridDim.x;
-      if (pf >= n_flat) return;
-      const AttnUnit u = p.units[pf / p.H_kv];
-      const int L = p.ctx_len[u.seq];
-      const int b0 = u.split * p.split_blocks;
-      const int b1 = min(b0 + p.split_blocks, (L + 15) >> 4);
-      const int first = b0 + warp;
-      p_n = first < b1 ? (b1 - first + kWarps - 1) / kWarps : 0;
-      p_it = 0;
-      p_tbl = p.tables + (size_t)u.seq * p.tbl_pitch + first;
-      p_off = p.layer_off + (uint64_t)(pf % p.H_kv) * (2 * TILE);
-      addr_base = 0;
-      my_addr = lane < p_n ? p.block_base[p_tbl[kWarps * lane]] + p_off : 0;
-      if (warp == 0) {  // stage this item's q rows (G heads x D fp32) for the whole CTA;
-        // warp 0 owns the first block of every item, so it visits every item in order
-        __syncwarp();
-        if (lane == 0) {
-          const int qi = pq % QB;
-          const float* src = p.q + ((size_t)u.seq * p.H + (pf % p.H_kv) * G) * D;
+  // ---- work items are claimed dynamically from a global counter (items are in
+  // longest-first order, so this is greedy LPT). The first warp of the CTA to
+  // need the CTA's k-th item claims it, stages its q rows by bulk copy and
+  // publishes it in slot k % QB; the other warps read the slot. ----
+  auto get_item = [&](int k) -> int {
+    const int sl = k % QB;
+    int item = 0;
+    if (lane == 0) {
+      if (atomicCAS(&slot_claim[sl], k - QB, k) == k - QB) {
+        item = atomicAdd(p.sched, 1);
+        if (item < n_flat) {
+          const AttnUnit u = p.units[item / p.H_kv];
+          const float* src = p.q + ((size_t)u.seq * p.H + (item % p.H_kv) * G) * D;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_expect_tx(&qbars[qi], G * D * 4);
-          bulk_g2s(&qbuf[qi][0], src, G * D * 4, &qbars[qi]);
+          mbar_expect_tx(&qbars[sl], G * D * 4);
+          bulk_g2s(&qbuf[sl][0], src, G * D * 4, &qbars[sl]);
         }
-        ++pq;
+        *reinterpret_cast<volatile int*>(&slot_item[sl]) = item;
+        __threadfence_block();
+        atomicExch(&slot_gen[sl], k);
+      } else {
+        while (*reinterpret_cast<volatile int*>(&slot_gen[sl]) != k) __nanosleep(32);
+        __threadfence_block();
+        item = *reinterpret_cast<volatile int*>(&slot_item[sl]);
       }
     }
-    if (p_it - addr_base >= 32) {  // next window of 32 block addresses
-      addr_base += 32;
-      const int j = addr_base + lane;
-      my_addr = j < p_n ? p.block_base[p_tbl[kWarps * j]] + p_off : 0;
-    }
-    const uint64_t a = __shfl_sync(0xffffffffu, my_addr, p_it - addr_base);
-    ++p_it;
-    __syncwarp();
-    if (lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&bars[warp][stage], 2 * TILE);
-      bulk_g2s(ring + stage * 2 * TILE, reinterpret_cast<const void*>(a), 2 * TILE, &bars[warp][stage]);
+    return __shfl_sync(0xffffffffu, item, 0);
+  };
+
+  // ---- producer: walks this warp's tile stream (blocks warp, warp+W, ... of each
+  // of the CTA's items; tile t goes to stage t % NS) up to NS tiles ahead of the
+  // consumer, across item boundaries, so the ring never drains between items.
+  // It never claims an item more than QB-1 items ahead of its own consumer: by
+  // then every warp has passed the merge of the item that last used the slot.
+  int pk = -1, p_it = 0, p_n = 0, addr_base = 0;
+  bool p_done = false;
+  uint32_t pt = 0, rc = 0;  // tiles issued / consumed by this warp
+  const uint64_t* p_tbl = nullptr;
+  uint64_t p_off = 0, my_addr = 0;
+  auto pump = [&](int ck) {
+    while (pt < rc + NS && !p_done) {
+      if (p_it >= p_n) {
+        if (pk + 1 > ck + QB - 1) return;  // slot window
+        const int pf = get_item(++pk);
+        if (pf >= n_flat) {
+          p_done = true;
+          return;
+        }
+        const AttnUnit u = p.units[pf / p.H_kv];
+        const int first = u.b0 + warp;
+        p_n = first < u.b1 ? (u.b1 - first + kWarps - 1) / kWarps : 0;
+        p_it = 0;
+        p_tbl = p.addrs + u.addr_off + first;
+        p_off = p.layer_off + (uint64_t)(pf % p.H_kv) * (2 * TILE);
+        addr_base = 0;
+        my_addr = lane < p_n ? p_tbl[kWarps * lane] + p_off : 0;
+        continue;
+      }
+      if (p_it - addr_base >= 32) {  // next window of 32 block addresses
+        addr_base += 32;
+        const int j = addr_base + lane;
+        my_addr = j < p_n ? p_tbl[kWarps * j] + p_off : 0;
+      }
+      const uint64_t a = __shfl_sync(0xffffffffu, my_addr, p_it - addr_base);
+      const int stage = pt % NS;
+      ++p_it;
+      ++pt;
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bars[warp][stage], 2 * TILE);
+        bulk_g2s(ring + stage * 2 * TILE, reinterpret_cast<const void*>(a), 2 * TILE, &bars[warp][stage]);
+      }
     }
   };
-#pragma unroll
-  for (int i = 0; i < NS; ++i) produce(i);
+  pump(0);
 
   // ldmatrix row addresses (byte offsets within a tile, before the swizzle)
   const int k_row = (lane & 7) + ((lane >> 3) & 1) * 8, k_cadd = lane >> 4;
   const int v_row = (lane & 7) + (lane >> 4) * 8, v_cadd = (lane >> 3) & 1;
-  uint32_t rc = 0;  // consumer ring counter
-  uint32_t cq = 0;  // consumer item counter (indexes the q ring)
 
-  for (int f = blockIdx.x; f < n_flat; f += gridDim.x) {
+  for (int ck = 0;; ++ck) {
+    pump(ck);  // the producer has now visited item ck (or the stream has ended there)
+    const int f =
+        __shfl_sync(0xffffffffu, lane == 0 ? *reinterpret_cast<volatile int*>(&slot_item[ck % QB]) : 0, 0);
+    if (f >= n_flat) break;
     const AttnUnit u = p.units[f / p.H_kv];
     const int hk = f % p.H_kv;
     const int s = u.seq;
-    const int L = p.ctx_len[s];
-    const int b0 = u.split * p.split_blocks;
-    const int b1 = min(b0 + p.split_blocks, (L + 15) >> 4);
-    const int first = b0 + warp;
-    const int n_it = first < b1 ? (b1 - first + kWarps - 1) / kWarps : 0;
+    const int L = u.len;
+    const int first = u.b0 + warp;
+    const int n_it = first < u.b1 ? (u.b1 - first + kWarps - 1) / kWarps : 0;
 
     // B fragments of the query columns: column n = gq (+8 nt): head nt*4 + gq/2, part gq&1
     uint32_t qb[NT][KS][2];
-    const float* qs = &qbuf[cq % QB][0];
-    if (n_it > 0) mbar_wait(&qbars[cq % QB], (cq / QB) & 1);
-    ++cq;
+    const float* qs = &qbuf[ck % QB][0];
+    if (n_it > 0) mbar_wait(&qbars[ck % QB], (ck / QB) & 1);
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int hh = nt * 4 + (gq >> 1);
@@ -253,7 +283,7 @@ paged_attention_kernel(const AttnParams p) {
         for (int j = 0; j < 4; ++j) o[nt][ks][j] = 0.f;
     }
 
-    for (int it = 0; it < n_it; ++it, ++rc) {
+    for (int it = 0; it < n_it; ++it) {
       const int st = rc % NS;
       const uint32_t phase = (rc / NS) & 1;
       const int blk = first + kWarps * it;
@@ -328,7 +358,8 @@ paged_attention_kernel(const AttnParams p) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) mma_bf16(o[nt][ks], a, pb[nt]);
       }
-      produce(st);  // refill this stage with the tile NS ahead in the stream
+      ++rc;
+      pump(ck);  // refill the freed stage with the tile NS ahead in the stream
     }
     // l: sum the lane partials over the 8 token groups
 #pragma unroll
@@ -441,6 +472,15 @@ paged_attention_kernel(const AttnParams p) {
       const size_t oi = ((size_t)s * p.H + hk * G + g) * D + d;
       if (p.out_fp32) reinterpret_cast<float*>(p.out)[oi] = r;
       else reinterpret_cast<__nv_bfloat16*>(p.out)[oi] = __float2bfloat16_rn(r);
+    }
+  }
+  // the last CTA to finish resets the work counter for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
+      atomicExch(p.sched, 0);
+      atomicExch(p.sched + 1, 0);
     }
   }
 }

@@ -6,28 +6,29 @@
 
 namespace mirage {
 
-// One attention work unit: a (sequence, split) pair; blockIdx.y is the KV head.
+// One attention work unit: a (sequence, split) pair; the kernel expands it over
+// the kv heads. 32 bytes, everything the kernel needs without dependent loads.
 struct AttnUnit {
-  int32_t seq;     // row in the step's batch
-  int32_t split;   // split index within the sequence
-  int32_t nsplit;  // number of splits of this sequence
-  int32_t pbase;   // first partial record of this sequence (valid if nsplit > 1)
+  int32_t seq;       // row in the step's batch
+  int32_t split;     // split index within the sequence
+  int32_t nsplit;    // number of splits of this sequence
+  int32_t pbase;     // first partial record of this sequence (valid if nsplit > 1)
+  int32_t len;       // tokens attended by the sequence
+  int32_t b0, b1;    // this split's block range [b0, b1)
+  int32_t addr_off;  // index of the sequence's block 0 in AttnParams::addrs
 };
 
 struct AttnParams {
   const float* q;              // [B][H][D] fp32 (unscaled)
-  const int32_t* tables;       // [B][tbl_pitch] block ids
-  int32_t tbl_pitch;
-  const int32_t* ctx_len;      // [B] tokens attended (incl. the new one)
-  const uint64_t* block_base;  // [ids] device address of each physical block
+  const uint64_t* addrs;       // per-step block base addresses (host-resolved table -> block_base)
   uint64_t layer_off;          // layer * H_kv * 2 * 16 * D * 2 bytes
-  const AttnUnit* units;       // [n_units]
+  const AttnUnit* units;       // [n_units], longest first
   int32_t n_units;
-  int32_t split_blocks;        // 16-token blocks per split
   int32_t H, H_kv, D;
   float scale_log2;            // log2(e) / sqrt(D)
   float* partial;              // [(pbase + split) * H + h][D + 2]
   int32_t* tickets;            // [B * H_kv], zero between launches
+  int32_t* sched;              // [2] dynamic item counter + finished CTAs, zero between launches
   void* out;                   // [B][H][D] fp32 or bf16
   int32_t out_fp32;
 };
@@ -51,11 +52,11 @@ cudaError_t launch_residual_norm(int family, int B, int d, const float* y, int l
                                  const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
                                  cudaStream_t s);
 // qkv [B][(H+2Hk)D] fp32 (+bias, +RoPE) -> q fp32 [B][H][D]; K/V bf16 appended to
-// the paged cache at positions[b].
+// the paged cache at positions[b] (block address addrs[seq_off[b] + pos / 16]).
 cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float* qkv,
                             const __nv_bfloat16* bias, const int32_t* positions,
-                            const int32_t* tables, int tbl_pitch, const uint64_t* block_base,
-                            uint64_t layer_off, float rope_theta, float* q, cudaStream_t s);
+                            const int32_t* seq_off, const uint64_t* addrs, uint64_t layer_off,
+                            float rope_theta, float* q, cudaStream_t s);
 // OPT: f = bf16(relu(y + b)); Llama: f = bf16(silu(y[:, :f]) * y[:, f:]).
 cudaError_t launch_act(int family, int B, int f, const float* y, const __nv_bfloat16* bias,
                        __nv_bfloat16* out, cudaStream_t s);

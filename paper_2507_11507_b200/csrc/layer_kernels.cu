@@ -154,8 +154,8 @@ residual_norm_kernel(int family, int d, const float* y, int ldy, const __nv_bflo
 // chunks: (head, chunk pair c, c + D/16) for q/k, (kv head, chunk) for v.
 __global__ void __launch_bounds__(256)
 qkv_post_kernel(int family, int H, int Hk, int D, const float* qkv, const __nv_bfloat16* bias,
-                const int32_t* positions, const int32_t* tables, int tbl_pitch,
-                const uint64_t* block_base, uint64_t layer_off, float rope_theta, float* q) {
+                const int32_t* positions, const int32_t* seq_off, const uint64_t* addrs,
+                uint64_t layer_off, float rope_theta, float* q) {
   extern __shared__ float cs[];  // [D/2] cos, [D/2] sin
   const int b = blockIdx.x;
   const int pos = positions[b];
@@ -172,8 +172,7 @@ qkv_post_kernel(int family, int H, int Hk, int D, const float* qkv, const __nv_b
     }
     __syncthreads();
   }
-  const int32_t blk = tables[(size_t)b * tbl_pitch + (pos >> 4)];
-  char* kvbase = reinterpret_cast<char*>(block_base[blk] + layer_off);
+  char* kvbase = reinterpret_cast<char*>(addrs[seq_off[b] + (pos >> 4)] + layer_off);
   const int r = pos & 15;
   const int n_qk = (H + Hk) * hc, n_v = Hk * (D / 8);
   for (int e = threadIdx.x; e < n_qk + n_v; e += blockDim.x) {
@@ -393,11 +392,10 @@ cudaError_t launch_residual_norm(int family, int B, int d, const float* y, int l
 
 cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float* qkv,
                             const __nv_bfloat16* bias, const int32_t* positions,
-                            const int32_t* tables, int tbl_pitch, const uint64_t* block_base,
-                            uint64_t layer_off, float rope_theta, float* q, cudaStream_t s) {
-  qkv_post_kernel<<<B, 256, D * sizeof(float), s>>>(family, H, Hk, D, qkv, bias, positions, tables,
-                                                    tbl_pitch, block_base, layer_off, rope_theta,
-                                                    q);
+                            const int32_t* seq_off, const uint64_t* addrs, uint64_t layer_off,
+                            float rope_theta, float* q, cudaStream_t s) {
+  qkv_post_kernel<<<B, 256, D * sizeof(float), s>>>(family, H, Hk, D, qkv, bias, positions, seq_off,
+                                                    addrs, layer_off, rope_theta, q);
   return cudaGetLastError();
 }
 

@@ -317,7 +317,7 @@ WsPlan ws_plan(const Shape& s, int Bm, int max_units) {
   w.q = (uint64_t)Bm * s.H * s.D * 4;
   w.f = (uint64_t)Bm * s.f * 2;
   w.partial = (uint64_t)max_units * s.H * (s.D + 2) * 4;
-  w.tickets = (uint64_t)Bm * s.Hk * 4;
+  w.tickets = (uint64_t)Bm * s.Hk * 4 + 8;  // split tickets + the attention work counter
   w.argmax = (uint64_t)Bm * 4;
   return w;
 }
@@ -347,9 +347,17 @@ Model* get_model(mirage_ctx* c, int32_t id) {
 }
 
 // ---- step metadata packing ---------------------------------------------------
+// One pinned staging buffer per step, uploaded with one H2D:
+//   tokens | positions | lengths | seq_off | attention units | block addresses
+// The block addresses are the step's table rows resolved through block_base on
+// the host (addrs[seq_off[i] + j] = block_base[table[i][j]]), so the kernels
+// need no dependent table lookups. The KV hooks reuse the address region for a
+// plain int32 table row.
 struct MetaView {
-  int32_t *tokens, *pos, *len, *tables;
+  int32_t *tokens, *pos, *len, *seq_off;
   mirage::AttnUnit* units;
+  uint64_t* addrs;
+  int32_t* tables;  // aliases addrs (fill/write hooks only)
 };
 
 MetaView meta_view(mirage_ctx* c, char* base) {
@@ -359,15 +367,17 @@ MetaView meta_view(mirage_ctx* c, char* base) {
   v.tokens = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
   v.pos = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
   v.len = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
-  v.units = reinterpret_cast<mirage::AttnUnit*>(p); p += align_up((uint64_t)c->max_units * 16, 16);
+  v.seq_off = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
+  v.units = reinterpret_cast<mirage::AttnUnit*>(p); p += align_up((uint64_t)c->max_units * sizeof(mirage::AttnUnit), 16);
+  v.addrs = reinterpret_cast<uint64_t*>(p);
   v.tables = reinterpret_cast<int32_t*>(p);
   return v;
 }
 
 size_t meta_size(mirage_ctx* c) {
   const int Bm = c->cfg.max_batch;
-  return 3 * align_up((uint64_t)Bm * 4, 16) + align_up((uint64_t)c->max_units * 16, 16) +
-         (uint64_t)Bm * c->max_blk * 4;
+  return 4 * align_up((uint64_t)Bm * 4, 16) + align_up((uint64_t)c->max_units * sizeof(mirage::AttnUnit), 16) +
+         (uint64_t)Bm * c->max_blk * 8;
 }
 
 int32_t acquire_stage(mirage_ctx* c, char** host) {
@@ -380,77 +390,53 @@ int32_t acquire_stage(mirage_ctx* c, char** host) {
 // Build attention units for lens[] (logical lengths only -> placement
 // independent splits). Returns the unit count and split size in blocks.
 // Split-K planning for the persistent attention kernel (a9). Work items are
-// (sequence, split, kv head); `grid` CTAs take items round-robin in longest-first
-// order, each spreading an item's blocks over `warps` warps. The split size P
-// (blocks) is chosen from logical lengths only -- never from block placement --
-// by minimising the estimated makespan of CTA 0 (it receives the largest item of
-// every round): sum over rounds of ceil(size / warps) + 1 tile times, plus the
-// last CTA's combine read of the largest split count.
-int choose_split(const int32_t* lens, int B, int Hk, int G, int grid, int warps, int* max_nb_out) {
+// (sequence, split, kv head), claimed dynamically by `grid` resident CTAs in
+// longest-first order (greedy LPT). Splitting adds per-item overhead and a
+// combine, so the split size P (blocks) is the LARGEST one that still gives
+// every resident CTA about one item to start with: items(P) >= f * grid, with
+// f = 0.8 (f = 1.0 for G = 8, whose tiles are compute-heavier), and at most
+// kMaxSplits splits per sequence. Calibrated on B200 (tools/attn_bench.py
+// --split sweeps). P depends on logical lengths only, never on
+// block placement.
+int choose_split(const int32_t* lens, int B, int Hk, int G, int grid, int warps) {
+  (void)warps;
   int max_nb = 0;
-  int64_t work = 0;
   std::vector<int> nbs(B);
   for (int b = 0; b < B; ++b) {
     nbs[b] = (lens[b] + kBlockTokens - 1) / kBlockTokens;
     max_nb = std::max(max_nb, nbs[b]);
-    work += (int64_t)nbs[b] * Hk;
   }
-  *max_nb_out = max_nb;
   const int p_lo = std::max(1, (max_nb + kMaxSplits - 1) / kMaxSplits);
-  if (grid <= 0 || (int64_t)B * Hk >= 16LL * grid) return std::max(p_lo, max_nb);  // many items: no split
-  std::vector<int64_t> cnt;
-  int best_p = max_nb;
-  double best = 1e300;
-  for (int P = max_nb; P >= p_lo;) {
-    // item sizes histogram (per kv head multiplicity Hk)
-    cnt.assign(P + 1, 0);
-    int max_ns = 1;
-    for (int b = 0; b < B; ++b) {
-      const int full = nbs[b] / P, rem = nbs[b] % P;
-      cnt[P] += (int64_t)full * Hk;
-      if (rem) cnt[rem] += Hk;
-      max_ns = std::max(max_ns, full + (rem ? 1 : 0));
-    }
-    // CTA 0 takes sorted items 0, grid, 2*grid, ...
-    double t = 0;
-    int64_t pos = 0;  // index of the first item of the current size bucket
-    for (int sz = P; sz >= 1; --sz) {
-      if (!cnt[sz]) continue;
-      const int64_t first_k = (pos + grid - 1) / grid;           // first k with k*grid >= pos
-      const int64_t last_k = (pos + cnt[sz] - 1) / grid;          // last k with k*grid < pos+cnt
-      if (last_k >= first_k) t += (double)(last_k - first_k + 1) * ((sz + warps - 1) / warps + 1);
-      pos += cnt[sz];
-    }
-    if (max_ns > 1) t += (double)max_ns * G / 16.0;
-    if (t < best - 1e-9) {
-      best = t;
-      best_p = P;
-    }
-    const int next = (int)(P * 0.9);
-    P = next < P ? next : P - 1;
+  const double need = (G >= 8 ? 1.0 : 0.8) * std::max(grid, 1);
+  auto items = [&](int P) {
+    int64_t n = 0;
+    for (int b = 0; b < B; ++b) n += (nbs[b] + P - 1) / P;
+    return (double)n * Hk;
+  };
+  int P = std::max(p_lo, max_nb);
+  while (P > p_lo && items(P) < need) {
+    const int next = std::max(p_lo, std::min(P - 1, (int)(P * 0.97)));
+    P = next;
   }
-  (void)work;
-  return best_p;
+  return P;
 }
 
-int build_units(const int32_t* lens, int B, int Hk, int G, int grid, int warps, int override_blocks,
-                mirage::AttnUnit* units, int max_units, int* split_blocks) {
-  int max_nb = 0;
-  int P = choose_split(lens, B, Hk, G, grid, warps, &max_nb);
+int build_units(const int32_t* lens, const int32_t* seq_off, int B, int Hk, int G, int grid, int warps,
+                int override_blocks, mirage::AttnUnit* units, int max_units, int* split_blocks) {
+  int P = choose_split(lens, B, Hk, G, grid, warps);
   if (override_blocks > 0) P = override_blocks;
   int n = 0, pbase = 0;
   for (int b = 0; b < B; ++b) {
     const int nb = (lens[b] + kBlockTokens - 1) / kBlockTokens;
     const int ns = std::max(1, (nb + P - 1) / P);
     if (n + ns > max_units || ns > kMaxSplits) return -1;
-    for (int i = 0; i < ns; ++i) units[n++] = mirage::AttnUnit{b, i, ns, ns > 1 ? pbase : 0};
+    for (int i = 0; i < ns; ++i)
+      units[n++] = mirage::AttnUnit{b, i, ns, ns > 1 ? pbase : 0, lens[b], i * P, std::min(nb, (i + 1) * P),
+                                    seq_off[b]};
     if (ns > 1) pbase += ns;
   }
   // longest-first order for the persistent kernel's round-robin item assignment
-  auto size_of = [&](const mirage::AttnUnit& u) {
-    const int nb = (lens[u.seq] + kBlockTokens - 1) / kBlockTokens;
-    return std::min(P, nb - u.split * P);
-  };
+  auto size_of = [&](const mirage::AttnUnit& u) { return u.b1 - u.b0; };
   std::stable_sort(units, units + n, [&](const mirage::AttnUnit& a, const mirage::AttnUnit& b) {
     return size_of(a) > size_of(b);
   });
@@ -938,7 +924,6 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
       return fail(c, MIRAGE_ERR_STATE, "step: model %d has reclaimed layers and no cycle", model);
   // ---- validate (before any enqueue) ----
   std::vector<const std::vector<int32_t>*> rows(B);
-  int pitch = 1;
   for (int i = 0; i < B; ++i) {
     auto it = M->tables.find(seq_ids[i]);
     const int32_t len = M->lens.count(seq_ids[i]) ? M->lens[seq_ids[i]] : 0;
@@ -952,7 +937,6 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     if (it == M->tables.end() || (int)it->second.size() < need)
       return fail(c, MIRAGE_ERR_NO_BLOCKS, "step: seq %lld needs %d blocks", (long long)seq_ids[i], need);
     rows[i] = &it->second;
-    pitch = std::max(pitch, need);
   }
   for (int i = 0; i < B; ++i)
     for (int j = 0; j < i; ++j)
@@ -963,19 +947,23 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   char* host;
   if (int32_t e = acquire_stage(c, &host)) return e;
   MetaView hv = meta_view(c, host), dv = meta_view(c, c->meta_dev);
+  int n_addr = 0;
   for (int i = 0; i < B; ++i) {
     hv.tokens[i] = tokens[i];
     hv.pos[i] = positions[i];
     hv.len[i] = positions[i] + 1;
-    std::copy(rows[i]->begin(), rows[i]->begin() + std::min<size_t>(rows[i]->size(), pitch),
-              hv.tables + (size_t)i * pitch);
+    hv.seq_off[i] = n_addr;
+    const int need = (positions[i] + 1 + kBlockTokens - 1) / kBlockTokens;
+    for (int j = 0; j < need; ++j) hv.addrs[n_addr + j] = M->bbase_host[(*rows[i])[j]];
+    n_addr += need;
   }
   int split_blocks = 1;
-  const int n_units = build_units(hv.len, B, s.Hk, s.H / s.Hk, mirage::attention_grid_ctas(s.H, s.Hk, s.D),
-                                  mirage::attention_cta_warps(s.Hk), 0, hv.units, c->max_units, &split_blocks);
+  const int n_units = build_units(hv.len, hv.seq_off, B, s.Hk, s.H / s.Hk,
+                                  mirage::attention_grid_ctas(s.H, s.Hk, s.D), mirage::attention_cta_warps(s.Hk),
+                                  0, hv.units, c->max_units, &split_blocks);
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "step: too many attention units");
-  const size_t tbl_bytes = (size_t)B * pitch * 4;
-  const size_t head = reinterpret_cast<char*>(hv.tables) - host;
+  const size_t tbl_bytes = (size_t)n_addr * 8;
+  const size_t head = reinterpret_cast<char*>(hv.addrs) - host;
   cudaStream_t cs = c->cs;
   const bool timed = !M->step_timed;
   if (timed) CK(c, cudaEventRecord(M->st0, cs));
@@ -1044,19 +1032,16 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   }
   mirage::AttnParams ap{};
   ap.q = M->q;
-  ap.tables = dv.tables;
-  ap.tbl_pitch = pitch;
-  ap.ctx_len = dv.len;
-  ap.block_base = M->bbase_dev;
+  ap.addrs = dv.addrs;
   ap.units = dv.units;
   ap.n_units = n_units;
-  ap.split_blocks = split_blocks;
   ap.H = H;
   ap.H_kv = Hk;
   ap.D = D;
   ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
   ap.partial = M->partial;
   ap.tickets = M->tickets;
+  ap.sched = M->tickets + (size_t)c->cfg.max_batch * Hk;
   ap.out = M->x;  // bf16 [B][H*D]: the O-projection input
   ap.out_fp32 = 0;
   const bool time_attn = c->cfg.flags & MIRAGE_FLAG_TIME_ATTN;
@@ -1068,7 +1053,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     const uint64_t layer_off = (uint64_t)l * Hk * 2 * kBlockTokens * D * 2;
     if (int32_t e = gemm_lt(c, B, qkvN, d, w.w_qkv, M->x, M->y, 0, nullptr, 0)) return e;
     KL(c, mirage::launch_qkv_post(s.family, B, H, Hk, D, M->y, opt ? w.b_qkv : nullptr, dv.pos,
-                                 dv.tables, pitch, M->bbase_dev, layer_off, s.theta, M->q, cs));
+                                 dv.seq_off, dv.addrs, layer_off, s.theta, M->q, cs));
     ap.layer_off = layer_off;
     if (time_attn) {
       Model::AttnTiming at{pool_event(M), pool_event(M), attn_bytes};
@@ -1143,50 +1128,46 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
   if (!M || layer < 0 || layer >= M->shp.n || B <= 0 || B > c->cfg.max_batch || !seq_ids || !q_dev ||
       !out_dev || split_tokens_override < 0 || split_tokens_override % kBlockTokens)
     return fail(c, MIRAGE_ERR_RANGE, "attn_only: arguments");
-  std::vector<const std::vector<int32_t>*> rows(B);
-  int pitch = 1;
   char* host;
   if (int32_t e = acquire_stage(c, &host)) return e;
   MetaView hv = meta_view(c, host), dv = meta_view(c, c->meta_dev);
+  int n_addr = 0;
   for (int i = 0; i < B; ++i) {
     auto it = M->tables.find(seq_ids[i]);
     const int32_t len = M->lens.count(seq_ids[i]) ? M->lens[seq_ids[i]] : 0;
     if (it == M->tables.end() || len <= 0)
       return fail(c, MIRAGE_ERR_STATE, "attn_only: seq %lld has no tokens", (long long)seq_ids[i]);
-    rows[i] = &it->second;
     hv.len[i] = len;
-    pitch = std::max(pitch, (len + kBlockTokens - 1) / kBlockTokens);
-  }
-  for (int i = 0; i < B; ++i) {
-    const size_t nb = (hv.len[i] + kBlockTokens - 1) / kBlockTokens;
-    std::copy(rows[i]->begin(), rows[i]->begin() + nb, hv.tables + (size_t)i * pitch);
+    hv.seq_off[i] = n_addr;
+    const int nb = (len + kBlockTokens - 1) / kBlockTokens;
+    for (int j = 0; j < nb; ++j) hv.addrs[n_addr + j] = M->bbase_host[it->second[j]];
+    n_addr += nb;
   }
   int split_blocks = 1;
-  const int n_units = build_units(hv.len, B, M->shp.Hk, M->shp.H / M->shp.Hk,
+  const int n_units = build_units(hv.len, hv.seq_off, B, M->shp.Hk, M->shp.H / M->shp.Hk,
                                   mirage::attention_grid_ctas(M->shp.H, M->shp.Hk, M->shp.D),
                                   mirage::attention_cta_warps(M->shp.Hk), split_tokens_override / kBlockTokens,
                                   hv.units, c->max_units, &split_blocks);
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "attn_only: too many units for the split override");
-  const size_t head = reinterpret_cast<char*>(hv.tables) - host;
-  CK(c, cudaMemcpyAsync(c->meta_dev, host, head + (size_t)B * pitch * 4, cudaMemcpyHostToDevice, c->cs));
+  const size_t head = reinterpret_cast<char*>(hv.addrs) - host;
+  CK(c, cudaMemcpyAsync(c->meta_dev, host, head + (size_t)n_addr * 8, cudaMemcpyHostToDevice, c->cs));
   CK(c, cudaEventRecord(c->stage_ev[c->stage_i], c->cs));
+  M->last_units = n_units;
+  M->last_split = split_blocks;
   const Shape& s = M->shp;
   mirage::AttnParams ap{};
   ap.q = q_dev;
-  ap.tables = dv.tables;
-  ap.tbl_pitch = pitch;
-  ap.ctx_len = dv.len;
-  ap.block_base = M->bbase_dev;
+  ap.addrs = dv.addrs;
   ap.layer_off = (uint64_t)layer * s.Hk * 2 * kBlockTokens * s.D * 2;
   ap.units = dv.units;
   ap.n_units = n_units;
-  ap.split_blocks = split_blocks;
   ap.H = s.H;
   ap.H_kv = s.Hk;
   ap.D = s.D;
   ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)s.D));
   ap.partial = M->partial;
   ap.tickets = M->tickets;
+  ap.sched = M->tickets + (size_t)c->cfg.max_batch * s.Hk;
   ap.out = out_dev;
   ap.out_fp32 = out_fp32;
   KL(c, mirage::launch_paged_attention(ap, c->cs));

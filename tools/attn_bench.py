@@ -35,7 +35,7 @@ CASES = {
 }
 
 
-def run(name, reps, seed=0):
+def run(name, reps, seed=0, split=0):
     L, H, Hk, D, B, ctx = CASES[name]
     shape = models.ModelShape(f"attn-{name}", models.LLAMA, L, 128, H, Hk, D, 128, 128, 65536)
     lens = ([int(c) for c in workload.mid_generation_contexts(B, seed=seed)] if ctx == "sharegpt" else [ctx] * B)
@@ -52,12 +52,12 @@ def run(name, reps, seed=0):
     ctx_.sync()
     layers = list(range(L))
     for w in range(3):
-        ctx_.attn_only(mid, layers[w % L], list(range(B)), q, out)
+        ctx_.attn_only(mid, layers[w % L], list(range(B)), q, out, split_tokens=split)
     ctx_.sync()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
     ev[0].record(ctx_.stream)
     for r in range(reps):
-        ctx_.attn_only(mid, layers[r % L], list(range(B)), q, out)
+        ctx_.attn_only(mid, layers[r % L], list(range(B)), q, out, split_tokens=split)
         ev[r + 1].record(ctx_.stream)
     ctx_.sync()
     ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(reps)]
@@ -66,7 +66,7 @@ def run(name, reps, seed=0):
     nbytes = sum(lens) * 2 * Hk * D * 2
     st = ctx_.query(mid)
     ctx_.close()
-    return {"case": name, "batch": B, "ctx_sum": sum(lens), "bytes": nbytes, "median_ms": med, "best_ms": ms[0],
+    return {"case": name, "split_blocks": st["last_split_blocks"], "units": st["last_attn_units"], "batch": B, "ctx_sum": sum(lens), "bytes": nbytes, "median_ms": med, "best_ms": ms[0],
             "gbs_median": nbytes / med / 1e6, "gbs_best": nbytes / ms[0] / 1e6}
 
 
@@ -74,6 +74,13 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", nargs="*", default=list(CASES))
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--split", type=int, nargs="*", default=[0], help="split sizes in tokens (0 = planner)")
     a = ap.parse_args()
     for c in a.case:
-        print(json.dumps(run(c, a.reps)), flush=True)
+        for sp in a.split:
+            try:
+                r = run(c, a.reps, split=sp)
+            except Exception as e:  # e.g. too many splits for the override
+                print(json.dumps({"case": c, "split": sp, "error": str(e)[:120]}), flush=True)
+                continue
+            print(json.dumps({k: (round(v, 1) if isinstance(v, float) else v) for k, v in r.items()}), flush=True)
