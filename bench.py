@@ -36,9 +36,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mirage", choices=["mirage", "reference"])
-    ap.add_argument("--batch", type=int, default=400)
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"],
+                    help="BASELINE.json configs[1..3]; c2 is the headline")
+    ap.add_argument("--batch", type=int, default=0, help="0 = config default (c2: 400, c4: 32)")
+    ap.add_argument("--ctx", type=int, default=0, help="c4 context length (default 32768)")
     ap.add_argument("--alpha", type=int, default=1)
-    ap.add_argument("--beta", type=int, default=1)
+    ap.add_argument("--beta", type=int, default=0, help="0 = config default (c2: 1, c4: 2)")
     ap.add_argument("--placement", default="uniform", choices=["uniform", "last"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-resident-arm", action="store_true")
@@ -93,25 +96,25 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ cpu oracle ----
-def oracle_leg(n_seqs=2, seed=0, steps=1, batch=400):
-    """Time the CPU oracle (oracle/, as it stands) on a bounded sample of the C2
-    workload: one OPT-13B-shaped layer + the LM head for `n_seqs` sequences of the
-    same ShareGPT-shaped context mix, KV from the counter-based generator.
-    Scaled to tok/s of the full 40-layer model:
-      t_token = 40 * (t_layer_step - t_head) / n + t_head / n."""
+def oracle_leg(shape, ctxs, n_seqs=2, seed=0, steps=1):
+    """Time the CPU oracle (oracle/, as it stands) on a bounded sample of the
+    workload: one layer of `shape` + the LM head for `n_seqs` sequences of the
+    batch's context mix (capped at 4096 tokens), KV from the counter-based
+    generator. Scaled to tok/s of the full model:
+      t_token = (n_layers * (t_layer_step - t_head) + t_head) / n."""
     import numpy as np
     import torch
     from oracle import kvgen
     from oracle.decode import Decoder
-    from synth import models, weights, workload
-    shape = models.OPT_13B
+    from synth import weights, workload
     one = shape.with_layers(1)
-    ctxs = workload.mid_generation_contexts(batch, seed=seed)[:n_seqs]
+    sample = [min(int(c), 4096) for c in list(ctxs)[:n_seqs]]
     t0 = time.perf_counter()
     dec = Decoder(one, [weights.layer_tensors(one, 0, seed)], weights.global_tensors(one, seed))
-    for i, L in enumerate(ctxs):
-        K = np.stack([kvgen.kv_values(seed, i, shape.n_layers, 40, 128, 0, h, 0, range(L)) for h in range(40)])
-        V = np.stack([kvgen.kv_values(seed, i, shape.n_layers, 40, 128, 0, h, 1, range(L)) for h in range(40)])
+    Hk, D = shape.n_kv_heads, shape.head_dim
+    for i, L in enumerate(sample):
+        K = np.stack([kvgen.kv_values(seed, i, shape.n_layers, Hk, D, 0, h, 0, range(L)) for h in range(Hk)])
+        V = np.stack([kvgen.kv_values(seed, i, shape.n_layers, Hk, D, 0, h, 1, range(L)) for h in range(Hk)])
         dec.set_kv(i, [(K, V)])
     setup = time.perf_counter() - t0
     threads = torch.get_num_threads()
@@ -122,35 +125,36 @@ def oracle_leg(n_seqs=2, seed=0, steps=1, batch=400):
         pass
     per_step = []
     for s in range(steps):
-        pos = [int(L) + s for L in ctxs]
+        pos = [L + s for L in sample]
         toks = [workload.teacher_tokens(i, p, shape.vocab) for i, p in enumerate(pos)]
         t1 = time.perf_counter()
-        dec.step(list(range(n_seqs)), toks, pos)
+        dec.step(list(range(len(sample))), toks, pos)
         t_step = time.perf_counter() - t1
         x = np.ones(shape.d_model)
+        head = dec.G["embed"] if "lm_head" not in dec.G else dec.G["lm_head"]
         t2 = time.perf_counter()
-        for _ in range(n_seqs):
-            dec.G["embed"] @ x
+        for _ in range(len(sample)):
+            head @ x
         t_head = time.perf_counter() - t2
-        t_tok = (shape.n_layers * (t_step - t_head) + t_head) / n_seqs
-        per_step.append(t_tok)
+        per_step.append((shape.n_layers * (t_step - t_head) + t_head) / len(sample))
     return {"tok_s": 1.0 / statistics.median(per_step), "t_token_s": statistics.median(per_step),
             "cores": threads, "setup_s": setup, "per_step_token_s": per_step,
-            "sample": (f"oracle c4 decode of {n_seqs} seqs (ctx {list(map(int, ctxs))}) through 1 OPT-13B "
-                       f"layer + LM head, fp64 numpy, scaled x{shape.n_layers} layers to tok/s")}
+            "sample": (f"oracle c4 decode of {len(sample)} seqs (ctx {sample}) through 1 {shape.name} layer + "
+                       f"LM head, fp64 numpy, scaled x{shape.n_layers} layers to tok/s")}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    res = oracle_leg(n_seqs=2, seed=args.seed, steps=args.warmup + args.steps, batch=args.batch)
+    wl, _ = build_workload(args, rank, args.warmup + args.steps + args.e2e_steps + 1)
+    res = oracle_leg(wl.tenants[0][0], wl.ctxs, n_seqs=2, seed=args.seed, steps=args.warmup + args.steps)
     times = res["per_step_token_s"][args.warmup:]
     tok_s = 1.0 / statistics.median(times)
     line = {"impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tok/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded random-init weights, counter-based KV, ShareGPT-shaped lengths)",
-            "config": {"workload": "C2 OPT-13B-shaped decode, ShareGPT-shaped contexts (bounded oracle sample)"},
+            "config": {"workload": wl.desc + " (bounded oracle sample)"},
             "cpu_baseline": {"value": tok_s, "unit": "tok/s", "cores": res["cores"], "kind": "oracle",
                              "sample": res["sample"]},
             "e2e": {"value": tok_s, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -175,49 +179,126 @@ def measure_h2d_peak(torch, dev, nbytes=1 << 30):
     return nbytes / best / 1e6
 
 
+class Workload:
+    """What one bench run decodes. tenants[0] is the active (decoding) model."""
+
+    def __init__(self, name, desc, tenants, remaps, ctxs, max_ctx, kernel, compare):
+        self.name, self.desc, self.tenants, self.remaps = name, desc, tenants, remaps
+        self.ctxs, self.max_ctx, self.kernel, self.compare = ctxs, max_ctx, kernel, compare
+
+
+def blocks_of(lengths):
+    return sum((c + 15) // 16 for c in lengths)
+
+
+def reclaimed_blocks(S_donor, BB_recipient, R):
+    runs, cur = [], None
+    for l in sorted(R):
+        if cur and cur[-1] == l - 1:
+            cur.append(l)
+        else:
+            cur = [l]
+            runs.append(cur)
+    return sum(len(r) * S_donor // BB_recipient for r in runs)
+
+
+def plan_cycle(shape, alpha, beta, placement):
+    from paper_2507_11507_b200 import _lib
+    if alpha == 0:
+        return [], 0
+    if placement == "uniform":   # PAPER.md §5.4 uniform-interval placement
+        cycle, m, b = _lib.plan(shape.n_layers, alpha, beta, 0, 1)
+        return cycle, b
+    m = alpha + beta             # last alpha layers reclaimed, the beta before them are slots
+    return list(range(shape.n_layers - m, shape.n_layers)), beta
+
+
 def build_workload(args, rank, total_steps):
     from paper_2507_11507_b200 import _lib
     from synth import models, workload
-    shape = models.OPT_13B
-    S, G, BB = _lib.model_sizes(shape)
-    max_ctx = shape.max_pos
-    ctxs = workload.mid_generation_contexts(args.batch, seed=args.seed + 1000 * rank, max_ctx=max_ctx)
-    ctxs = [int(min(c, max_ctx - total_steps - 1)) for c in ctxs]
-    need = sum((c + total_steps + 15) // 16 for c in ctxs)
-    if args.alpha:
-        if args.placement == "uniform":
-            cycle, m, beta = _lib.plan(shape.n_layers, args.alpha, args.beta, 0, 1)
-        else:   # last alpha layers reclaimed, the beta layers just before them are the slots
-            m, beta = args.alpha + args.beta, args.beta
-            cycle = list(range(shape.n_layers - m, shape.n_layers))
-        R = cycle[beta:]
-        runs, cur = [], None
-        for l in R:
-            if cur and cur[-1] == l - 1:
-                cur.append(l)
-            else:
-                cur = [l]
-                runs.append(cur)
-        reclaimed = sum(len(r) * S // BB for r in runs)
-    else:
-        cycle, beta, reclaimed = [], 0, 0
-    return shape, ctxs, need, cycle, beta, reclaimed, (S, G, BB)
+    cfg = args.config
+    if cfg in ("c2", "c4"):
+        if cfg == "c2":
+            shape = models.OPT_13B
+            B = args.batch or 400
+            ctxs = workload.mid_generation_contexts(B, seed=args.seed + 1000 * rank, max_ctx=shape.max_pos)
+            ctxs = [int(min(c, shape.max_pos - total_steps - 1)) for c in ctxs]
+            beta_pol = args.beta or 1
+            desc = ("C2: OPT-13B-shaped decode, ShareGPT-shaped contexts, {a} layer(s) remapped to KV "
+                    "({p} placement, beta={b}); native pool sized so the batch fits only with the reclaimed blocks")
+            kernel = "paged_attention_kernel<128,1>"
+        else:
+            shape = models.LLAMA3_8B
+            B = args.batch or 32
+            L = min(args.ctx or 32768, shape.max_pos) - total_steps - 1
+            ctxs = [L] * B
+            beta_pol = args.beta or 2
+            desc = ("C4: Llama-3-8B-shaped GQA decode, %d x %d-token contexts, split-K paged attention; "
+                    "{a} layer(s) remapped ({p} placement, beta={b}); native pool sized so the batch fits only "
+                    "with the reclaimed blocks" % (B, L))
+            kernel = "paged_attention_kernel<128,4>"
+        S, G, BB = _lib.model_sizes(shape)
+        cycle, beta = plan_cycle(shape, args.alpha, beta_pol, args.placement)
+        reclaimed = reclaimed_blocks(S, BB, cycle[beta:])
+        need = sum((c + total_steps + 15) // 16 for c in ctxs)
+        tenants = [(shape, args.seed, need - reclaimed)]
+        remaps = [(0, 0, cycle, beta)] if cycle else []
+        compare = {"kind": "all_resident", "tenants": [(shape, args.seed, need)], "remaps": [], "ctxs": ctxs}
+        return Workload(cfg, desc.format(a=args.alpha, p=args.placement, b=beta), tenants, remaps, ctxs,
+                        shape.max_pos, kernel, compare), {"cycle": cycle, "beta": beta, "reclaimed_blocks": reclaimed,
+                                                          "native_blocks": need - reclaimed, "block_bytes": BB,
+                                                          "layer_bytes": S}
+    if cfg == "c3":
+        act, don = models.OPT_13B, models.LLAMA2_7B
+        Sa, Ga, BBa = _lib.model_sizes(act)
+        Sd, _, _ = _lib.model_sizes(don)
+        # Table 1 reservation (PAPER.md:599) on GH200's 96 GB (:635): 35% minus the active params
+        native = int((0.35 * 96e9 - (act.n_layers * Sa + Ga)) // BBa)
+        gained = reclaimed_blocks(Sd, BBa, range(don.n_layers))
+        trace = workload.mid_generation_contexts(4096, seed=args.seed + 1000 * rank, max_ctx=act.max_pos)
+        trace = [int(min(c, act.max_pos - total_steps - 1)) for c in trace]
+
+        def admit(pool):
+            out, used = [], 0
+            for c in trace:
+                nb = (c + total_steps + 15) // 16
+                if used + nb > pool:
+                    break
+                out.append(c)
+                used += nb
+            return out
+        ctxs, base = admit(native + gained), admit(native)
+        desc = ("C3: OPT-13B-shaped active tenant + inactive Llama-2-7B-shaped tenant whose params are fully "
+                "remapped to KV (beta=0); ShareGPT-shaped trace admitted in order until the pool is full "
+                "(native pool = 35%% x 96 GB - params = %d blocks)" % native)
+        tenants = [(act, args.seed, native), (don, args.seed + 1, 0)]
+        remaps = [("inactive", 1), (1, 0, list(range(don.n_layers)), 0)]
+        compare = {"kind": "no_reclaim", "tenants": [(act, args.seed, native)], "remaps": [], "ctxs": base}
+        return Workload(cfg, desc, tenants, remaps, ctxs, act.max_pos, "paged_attention_kernel<128,1>", compare), \
+            {"native_blocks": native, "reclaimed_blocks": gained, "batch_without_reclaim": len(base),
+             "block_bytes": BBa, "layer_bytes": Sa}
+    raise SystemExit(f"unknown config {cfg}")
 
 
-def run_arm(args, torch, dev, shape, blob, ctxs, n_native, cycle, beta, steps, warmup, e2e_steps,
-            clock=None, record=True):
-    """One context: fill KV, warm up, time `steps` decode steps on the device,
-    then `e2e_steps` end-to-end steps (host sync + argmax read-back each step)."""
+def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warmup, e2e_steps, clock=None):
+    """One context: add the tenants, apply the remaps, fill the batch's prompt KV,
+    warm up, time `steps` decode steps of tenant 0 on the device, then
+    `e2e_steps` end-to-end steps (host sync + argmax read-back each step)."""
     import ctypes as C
     import harness
     from paper_2507_11507_b200 import _lib
+    from synth import workload
     B = len(ctxs)
-    max_ctx = shape.max_pos
-    arena = harness.arena_for([(shape, n_native)], B, max_ctx)
+    arena = harness.arena_for([(sh, nat) for sh, _, nat in tenants], B, max_ctx)
     ctx = _lib.Context(arena, B, max_ctx, device=dev.index, flags=_lib.FLAG_TIME_ATTN)
-    mid = ctx.add_model(shape, blob, n_native)
-    if cycle:
-        ctx.remap_layers(mid, mid, cycle, beta)
+    mids = [ctx.add_model(sh, blobs[(sh.name, seed)], nat) for sh, seed, nat in tenants]
+    for r in remaps:
+        if r[0] == "inactive":
+            ctx.set_active(mids[r[1]], False)
+        else:
+            ctx.remap_layers(mids[r[0]], mids[r[1]], r[2], r[3])
+    mid = mids[0]
+    shape = tenants[0][0]
     for i, L in enumerate(ctxs):
         ctx.alloc_blocks(mid, i, harness.blocks_for(L))
         ctx.fill_kv(mid, i, L, seed=args.seed * 7919 + i)
@@ -227,7 +308,6 @@ def run_arm(args, torch, dev, shape, blob, ctxs, n_native, cycle, beta, steps, w
     tok_c = (C.c_int32 * B)()
     pos_c = (C.c_int32 * B)()
     am_c = (C.c_int32 * B)()
-    from synth import workload
 
     def step(read_back):
         for i in range(B):
@@ -264,7 +344,6 @@ def run_arm(args, torch, dev, shape, blob, ctxs, n_native, cycle, beta, steps, w
     total_ms = evs[0].elapsed_time(evs[steps])
     launches = ctx.kernel_launches() - l0
     st1 = ctx.query(mid)
-    # end-to-end: host arrays in, argmax read back to host every step
     e2e_ms = []
     for _ in range(e2e_steps):
         t0 = time.perf_counter()
@@ -291,9 +370,7 @@ def run_mirage(args, rank, world):
     dev = torch.device("cuda", lr)
     torch.cuda.set_device(dev)
     total = args.warmup + args.steps + args.e2e_steps + 1
-    shape, ctxs, need, cycle, beta, reclaimed, (S, G, BB) = build_workload(args, rank, total)
-    n_native = need - reclaimed
-    assert n_native > 0
+    wl, info = build_workload(args, rank, total)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -302,19 +379,23 @@ def run_mirage(args, rank, world):
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     h2d_peak = measure_h2d_peak(torch, dev)
     t0 = time.time()
-    blob = harness.make_blob(shape, seed=args.seed, model_idx=rank, gen_device=dev)
+    blobs = {}
+    for sh, seed, _ in wl.tenants:
+        blobs[(sh.name, seed)] = harness.make_blob(sh, seed=seed, model_idx=rank, gen_device=dev)
     setup_blob_s = time.time() - t0
     clock = ClockSampler(lr)
-    res = run_arm(args, torch, dev, shape, blob, ctxs, n_native, cycle, beta, args.steps, args.warmup,
+    res = run_arm(args, torch, dev, wl.tenants, wl.remaps, wl.ctxs, wl.max_ctx, blobs, args.steps, args.warmup,
                   args.e2e_steps, clock)
-    resident, r2 = None, None
-    if not args.no_resident_arm and cycle and world == 1:
-        # the same batch with every layer resident (pool grown by the reclaimed blocks)
-        # same warm-up and step count, so both arms time the same context lengths
-        r2 = run_arm(args, torch, dev, shape, blob, ctxs, n_native + reclaimed, [], 0,
-                     args.steps, args.warmup, 0)
-        resident = statistics.median(r2["step_ms"])
-    B = len(ctxs)
+    cmp = None
+    if not args.no_resident_arm and wl.compare and world == 1 and (wl.remaps or wl.compare["kind"] != "all_resident"):
+        c = wl.compare
+        r2 = run_arm(args, torch, dev, c["tenants"], c["remaps"], c["ctxs"], wl.max_ctx, blobs, args.steps,
+                     args.warmup, 0)
+        med = statistics.median(r2["step_ms"])
+        cmp = {"kind": c["kind"], "batch": len(c["ctxs"]), "step_ms": med,
+               "tok_s": len(c["ctxs"]) / (sum(r2["step_ms"]) / len(r2["step_ms"]) / 1e3),
+               "steps_ms": [round(x, 3) for x in r2["step_ms"]]}
+    B = len(wl.ctxs)
     t_local = res["total_ms"]
     t_all = t_local
     if world > 1:
@@ -330,7 +411,7 @@ def run_mirage(args, rank, world):
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "attention_traffic.json")))
-        traffic = tr.get("dram_bytes_per_launch")
+        traffic = tr.get(wl.name, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
     if rank != 0:
@@ -338,25 +419,24 @@ def run_mirage(args, rank, world):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            o = oracle_leg(n_seqs=2, seed=args.seed, steps=1, batch=args.batch)
+            o = oracle_leg(wl.tenants[0][0], wl.ctxs, n_seqs=2, seed=args.seed, steps=1)
             cpu = {"value": o["tok_s"], "unit": "tok/s", "cores": o["cores"], "kind": "oracle", "sample": o["sample"]}
         except Exception as e:  # the CPU leg must not hide the GPU number
             cpu = {"value": None, "unit": "tok/s", "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {e}"}
     step_med = statistics.median(res["step_ms"])
     h2d_gbs = res["h2d_bytes"] / (res["h2d_ms"] * 1e-3) / 1e9 if res["h2d_ms"] else None
+    config = {"workload": wl.desc, "batch_per_gpu": B, "ctx_mean": sum(wl.ctxs) / B, "ctx_max": max(wl.ctxs),
+              "split_blocks": res["split_blocks"], "attention_units": res["units"],
+              "l2": "inputs larger than L2 (weights + KV read every step)", "parallelism": f"tenant-replica x{world}"}
+    config.update(info)
     line = {
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_all / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: seeded random-init bf16 weights (torch CUDA generator), counter-based KV, ShareGPT-shaped lengths",
-        "config": {"workload": "C2: OPT-13B-shaped decode, 1xB200 per rank, ShareGPT-shaped contexts, "
-                               f"{args.alpha} layer(s) remapped to KV ({args.placement} placement, beta={beta}), "
-                               "native pool sized so the batch fits only with the reclaimed blocks",
-                   "batch_per_gpu": B, "ctx_mean": sum(ctxs) / B, "ctx_max": max(ctxs), "cycle": cycle, "beta": beta,
-                   "native_blocks": n_native, "reclaimed_blocks": reclaimed, "block_bytes": BB, "layer_bytes": S,
-                   "l2": "inputs larger than L2 (weights 26.7 GB + KV per step)", "parallelism": f"tenant-replica x{world}"},
+        "config": config,
         "p99_tbt_ms": nearest_rank(res["step_ms"], 99), "p50_tbt_ms": nearest_rank(res["step_ms"], 50),
-        "roofline": {"kernel": "paged_attention_kernel<128,1>", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": wl.kernel, "bound": "hbm", "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": attn_bytes_launch, "avg_launch_ms": attn_avg_ms,
                      "launches": res["attn_launches"], "share_of_step": res["attn_ms"] / t_local,
@@ -364,10 +444,8 @@ def run_mirage(args, rank, world):
         "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": h2d_peak, "frac": (h2d_gbs / h2d_peak) if h2d_gbs else None,
                 "bytes_per_step": res["h2d_bytes"] / args.steps, "copies": res["h2d_copies"],
                 "peak_source": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this run"},
-        "remap": {"step_ms_remapped": step_med, "step_ms_all_resident": resident,
-                  "ratio": (step_med / resident) if resident else None,
-                  "steps_ms_remapped": [round(x, 3) for x in res["step_ms"]],
-                  "steps_ms_resident": [round(x, 3) for x in r2["step_ms"]] if resident else None},
+        "compare": cmp, "step_ms_median": step_med,
+        "steps_ms": [round(x, 3) for x in res["step_ms"]],
         "cpu_baseline": cpu, "clocks": res["clocks"],
         "e2e": {"value": B / (e2e_med / 1e3) * world if e2e_med else None, "unit": "tok/s",
                 "h2d_bytes_per_step": res["meta_bytes"], "d2h_bytes_per_step": 4 * B,

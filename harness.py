@@ -34,3 +34,37 @@ def arena_for(shapes_and_pools, max_batch, max_ctx, slack=64 << 20):
 
 def blocks_for(tokens):
     return (tokens + _lib.BLOCK_TOKENS - 1) // _lib.BLOCK_TOKENS
+
+
+def shard_shape(shape, tp):
+    """This rank's model shape under head-sharded tensor parallelism."""
+    from dataclasses import replace
+    return replace(shape, n_heads=shape.n_heads // tp, n_kv_heads=shape.n_kv_heads // tp,
+                   ffn_dim=shape.ffn_dim // tp, name=f"{shape.name}-tp{tp}")
+
+
+def shard_layer(shape, t, rank, tp):
+    """Slice one Llama layer's full tensors into rank `rank`'s shard (include/mirage.h)."""
+    H, Hk, D, f = shape.n_heads, shape.n_kv_heads, shape.head_dim, shape.ffn_dim
+    h, hk, fs = H // tp, Hk // tp, f // tp
+    q = t["w_qkv"][rank * h * D:(rank + 1) * h * D]
+    k = t["w_qkv"][H * D + rank * hk * D:H * D + (rank + 1) * hk * D]
+    v = t["w_qkv"][(H + Hk) * D + rank * hk * D:(H + Hk) * D + (rank + 1) * hk * D]
+    return {
+        "w_qkv": torch.cat([q, k, v]), "w_o": t["w_o"][:, rank * h * D:(rank + 1) * h * D],
+        "w_gateup": torch.cat([t["w_gateup"][rank * fs:(rank + 1) * fs], t["w_gateup"][f + rank * fs:f + (rank + 1) * fs]]),
+        "w_down": t["w_down"][:, rank * fs:(rank + 1) * fs], "rms1_g": t["rms1_g"], "rms2_g": t["rms2_g"],
+    }
+
+
+def make_shard_blob(shape, rank, tp, seed=0, model_idx=0):
+    """Pinned blob of rank `rank`'s shard of the full seeded model (CPU generation)."""
+    sh = shard_shape(shape, tp)
+    S, G, _ = _lib.model_sizes(sh)
+    blob = torch.empty(shape.n_layers * S + G, dtype=torch.uint8, pin_memory=True)
+    order = [n for n, _, _ in weights.layer_spec(sh)]
+    for l in range(shape.n_layers):
+        t = shard_layer(shape, weights.layer_tensors(shape, l, seed, model_idx), rank, tp)
+        blob[l * S:(l + 1) * S].copy_(_lib.tensors_to_bytes({k: v.contiguous() for k, v in t.items()}, order))
+    blob[shape.n_layers * S:].copy_(global_bytes_tensor(shape, seed, model_idx))
+    return blob

@@ -82,8 +82,13 @@ typedef struct mirage_init_cfg {
   int32_t max_batch;        /* max sequences per decode step                        */
   int32_t max_ctx;          /* max tokens per sequence                              */
   uint32_t flags;           /* MIRAGE_FLAG_* bits                                   */
-  int32_t tp_rank, tp_size; /* tensor parallel rank/size; this version: 0 / 1        */
-  void* nccl_comm;          /* reserved, NULL                                       */
+  int32_t tp_rank, tp_size; /* head-sharded tensor parallelism (a10): rank / size     */
+  const void* nccl_id;      /* tp_size > 1: 128-byte ncclUniqueId from
+                             * mirage_nccl_unique_id() on rank 0, broadcast by the
+                             * caller; the library creates and owns the communicator.
+                             * NULL: no communicator (tp_size must be 1). With
+                             * tp_size == 1 and an id, the all-reduce path runs on
+                             * a one-rank communicator (identity; for testing).   */
 } mirage_init_cfg;
 
 typedef struct mirage_model_cfg {
@@ -130,9 +135,14 @@ int32_t mirage_model_sizes(const mirage_model_cfg* m, uint64_t* layer_bytes,
 int32_t mirage_model_arena_bytes(const mirage_model_cfg* m, int64_t native_kv_blocks,
                                  int32_t max_batch, int32_t max_ctx, uint64_t* bytes);
 
-/* Bind device and streams; create events, the cuBLAS handle and staging.
- * Errors: CONFIG (block_tokens != 16, tp_size != 1, null arena/stream), CUDA. */
+/* Bind device and streams; create events, the cuBLAS handle, staging and, for
+ * tp_size > 1, the NCCL communicator (collective over the tp_size ranks).
+ * Errors: CONFIG (block_tokens != 16, bad tp rank/size, null arena/stream),
+ * CUDA, NCCL. */
 int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out);
+
+/* Fill out[128] with a fresh ncclUniqueId (call on TP rank 0 only). */
+int32_t mirage_nccl_unique_id(void* out);
 
 /* Synchronise the compute and copy streams, release everything the library
  * owns. Borrowed pointers are not freed. Safe on NULL. */
@@ -142,7 +152,14 @@ void mirage_destroy(mirage_ctx* ctx);
 const char* mirage_last_error(const mirage_ctx* ctx);
 
 /* Add a tenant model. host_blob (pinned, caller-owned, must outlive ctx) holds
- * the layout above and is copied once H2D into the arena; it stays the
+ * the layout above and is copied once H2D into the arena. Under tensor
+ * parallelism (tp_size > 1, Llama family only; SURVEY.md §8(e) head sharding)
+ * m describes the FULL model and the blob holds this rank's shard in the same
+ * layout with H/tp q heads, H_kv/tp kv heads and ffn/tp: w_qkv = [the rank's q
+ * heads | its k heads | its v heads] rows, w_o = columns of the rank's heads,
+ * w_gateup = [the rank's gate rows | its up rows], w_down = the rank's columns;
+ * norms, embeddings and the LM head are replicated. The decode step then sums
+ * the O-projection and down-projection partials with ncclAllReduce (a10); it stays the
  * authoritative copy re-streamed for cycled layers (PAPER.md:555 footnote: the
  * serving framework keeps a complete host copy of the parameters). The native
  * KV pool gets ids [0, native_kv_blocks). Model ids are 0,1,2,... in call order.

@@ -39,7 +39,7 @@ class InitCfg(C.Structure):
     _fields_ = [("device", C.c_int32), ("dev_arena", C.c_void_p), ("dev_arena_bytes", C.c_uint64),
                 ("block_tokens", C.c_int32), ("compute_stream", C.c_void_p), ("copy_stream", C.c_void_p),
                 ("max_batch", C.c_int32), ("max_ctx", C.c_int32), ("flags", C.c_uint32),
-                ("tp_rank", C.c_int32), ("tp_size", C.c_int32), ("nccl_comm", C.c_void_p)]
+                ("tp_rank", C.c_int32), ("tp_size", C.c_int32), ("nccl_id", C.c_void_p)]
 
 
 class ModelCfg(C.Structure):
@@ -95,6 +95,7 @@ def _load():
         "mirage_fill_kv": (I32, [P, I32, I64, I32, U64]),
         "mirage_write_kv": (I32, [P, I32, I64, I32, P]),
         "mirage_kernel_launches": (I64, [P]),
+        "mirage_nccl_unique_id": (I32, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -109,7 +110,7 @@ EXPORTED = [
     "mirage_add_model", "mirage_plan", "mirage_remap_layers", "mirage_set_active", "mirage_alloc_blocks",
     "mirage_free_blocks", "mirage_get_block_table", "mirage_block_location", "mirage_seq_len",
     "mirage_decode_step", "mirage_query", "mirage_slot_log", "mirage_sync", "mirage_attn_only",
-    "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches"]
+    "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches", "mirage_nccl_unique_id"]
 
 
 def model_cfg(shape):
@@ -145,6 +146,15 @@ def plan(n_layers, alpha, beta_policy, t_transfer_ns, t_compute_layer_ns, anchor
     if rc:
         raise MirageError(rc, "plan")
     return list(cyc[: m.value]), m.value, beta.value
+
+
+def nccl_unique_id():
+    """128-byte ncclUniqueId (TP rank 0), to broadcast to the other ranks."""
+    buf = C.create_string_buffer(128)
+    rc = LIB.mirage_nccl_unique_id(buf)
+    if rc:
+        raise MirageError(rc, "nccl_unique_id")
+    return buf.raw
 
 
 def _i32(seq):
@@ -204,15 +214,18 @@ class Context:
         self._check(rc, "add_model")
         return mid.value
 
-    def __init__(self, arena_bytes, max_batch, max_ctx, device=0, stream=None, flags=0):
+    def __init__(self, arena_bytes, max_batch, max_ctx, device=0, stream=None, flags=0, tp_rank=0, tp_size=1,
+                 nccl_id=None):
         self.device = torch.device("cuda", device)
         self.arena = torch.empty(int(arena_bytes) + 256, dtype=torch.uint8, device=self.device)
         base = self.arena.data_ptr()
         self._arena_ptr = (base + 255) // 256 * 256
         self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
         self._blobs = []
+        self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         cfg = InitCfg(device, self._arena_ptr, int(arena_bytes), BLOCK_TOKENS, self.stream.cuda_stream,
-                      None, max_batch, max_ctx, flags, 0, 1, None)
+                      None, max_batch, max_ctx, flags, tp_rank, tp_size,
+                      C.addressof(self._nccl_id) if self._nccl_id is not None else None)
         self._ctx = C.c_void_p()
         rc = LIB.mirage_init(C.byref(cfg), C.byref(self._ctx))
         if rc:

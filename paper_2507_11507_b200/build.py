@@ -10,8 +10,13 @@ OUT = os.path.join(HERE, "libmirage.so")
 BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+try:  # NCCL ships with torch (nvidia-nccl wheel); headers + libnccl.so.2
+    import nvidia.nccl as _nccl
+    NCCL_DIR = list(_nccl.__path__)[0]
+except Exception:  # pragma: no cover
+    NCCL_DIR = "/usr"
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
-         "--expt-relaxed-constexpr"]
+         "--expt-relaxed-constexpr", "-I" + os.path.join(NCCL_DIR, "include")]
 SOURCES = ["attention.cu", "layer_kernels.cu", "runtime.cpp", "planner.cpp"]
 
 
@@ -40,7 +45,9 @@ def build(verbose=False):
             sys.stderr.write(log)
     if not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC] + ARCH + ["-shared", "-o", OUT] + objs + [
-            "-L/usr/local/cuda/lib64", "-lcublas", "-lcublasLt", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+            "-L/usr/local/cuda/lib64", "-lcublas", "-lcublasLt", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
+            "-L" + os.path.join(NCCL_DIR, "lib"), "-l:libnccl.so.2",
+            "-Xlinker", "-rpath," + os.path.join(NCCL_DIR, "lib")]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -6,6 +6,7 @@
 #include <cublas_v2.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -225,6 +226,8 @@ struct mirage_ctx {
   int32_t sticky = MIRAGE_OK;
   int64_t launches = 0;
   bool host_only = false;  // MIRAGE_FLAG_HOST_ONLY: allocator/planner state only, no device
+  ncclComm_t nccl = nullptr;  // tensor-parallel communicator (tp_size > 1)
+  int tp = 1, tp_rank = 0;
 };
 
 namespace {
@@ -262,6 +265,14 @@ int32_t fail(mirage_ctx* c, int32_t code, const char* fmt, ...) {
   do {                     \
     ++(ctx)->launches;     \
     CK(ctx, (expr));       \
+  } while (0)
+
+#define CKN(ctx, expr)                                                                             \
+  do {                                                                                             \
+    ncclResult_t e_ = (expr);                                                                      \
+    if (e_ != ncclSuccess)                                                                         \
+      return fail(ctx, MIRAGE_ERR_NCCL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                                       \
   } while (0)
 
 #define GUARD(ctx)                                                      \
@@ -547,6 +558,14 @@ int32_t gemm_lt(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf16* x
 // ============================================================================
 extern "C" {
 
+int32_t mirage_nccl_unique_id(void* out) {
+  if (!out) return MIRAGE_ERR_RANGE;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return MIRAGE_ERR_NCCL;
+  std::memcpy(out, &id, sizeof id);
+  return MIRAGE_OK;
+}
+
 int32_t mirage_model_sizes(const mirage_model_cfg* m, uint64_t* layer_bytes, uint64_t* global_bytes,
                            uint64_t* block_bytes) {
   if (!m) return MIRAGE_ERR_CONFIG;
@@ -572,7 +591,8 @@ int32_t mirage_model_arena_bytes(const mirage_model_cfg* m, int64_t native_kv_bl
 int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
   if (!cfg || !out) return MIRAGE_ERR_CONFIG;
   *out = nullptr;
-  if (cfg->block_tokens != kBlockTokens || cfg->tp_size != 1 || cfg->tp_rank != 0 ||
+  if (cfg->block_tokens != kBlockTokens || cfg->tp_size < 1 || cfg->tp_rank < 0 ||
+      cfg->tp_rank >= cfg->tp_size || (cfg->tp_size > 1 && !cfg->nccl_id) ||
       !cfg->dev_arena || (!cfg->compute_stream && !(cfg->flags & MIRAGE_FLAG_HOST_ONLY)) ||
       cfg->max_batch <= 0 || cfg->max_ctx <= 0 ||
       (reinterpret_cast<uintptr_t>(cfg->dev_arena) % kAlign))
@@ -616,6 +636,13 @@ int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
   }
   if (cudaMalloc(reinterpret_cast<void**>(&c->meta_dev), c->meta_bytes) != cudaSuccess)
     return bail(MIRAGE_ERR_CUDA);
+  c->tp = cfg->tp_size;
+  c->tp_rank = cfg->tp_rank;
+  if (cfg->nccl_id) {  // tp_size == 1 with an id runs the same all-reduce path on one rank
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_id, sizeof id);
+    if (ncclCommInitRank(&c->nccl, c->tp, id, c->tp_rank) != ncclSuccess) return bail(MIRAGE_ERR_NCCL);
+  }
   *out = c;
   return MIRAGE_OK;
 }
@@ -661,6 +688,7 @@ void mirage_destroy(mirage_ctx* c) {
   if (c->lt) cublasLtDestroy(c->lt);
   if (c->blas_ws) cudaFree(c->blas_ws);
   if (c->own_xs && c->xs) cudaStreamDestroy(c->xs);
+  if (c->nccl) ncclCommDestroy(c->nccl);
   (void)cudaGetLastError();
   delete c;
 }
@@ -674,8 +702,15 @@ int32_t mirage_add_model(mirage_ctx* c, const mirage_model_cfg* mc, const void* 
   GUARD(c);
   if (!mc || !host_blob || !model_id || native_kv_blocks < 0)
     return fail(c, MIRAGE_ERR_CONFIG, "add_model: null argument or negative pool");
-  const Shape s = shape_of(mc);
+  Shape s = shape_of(mc);
   if (const char* why = check_shape(s)) return fail(c, MIRAGE_ERR_CONFIG, "add_model: bad %s", why);
+  if (c->tp > 1) {  // this rank's head shard (include/mirage.h)
+    if (s.family != MIRAGE_FAMILY_LLAMA || s.H % c->tp || s.Hk % c->tp || s.f % (128 * c->tp))
+      return fail(c, MIRAGE_ERR_CONFIG, "add_model: tensor parallelism needs a Llama shape divisible by tp");
+    s.H /= c->tp;
+    s.Hk /= c->tp;
+    s.f /= c->tp;
+  }
   const Sizes z = sizes_of(s);
   if (host_bytes != (uint64_t)s.n * z.S + z.G)
     return fail(c, MIRAGE_ERR_CONFIG, "add_model: host_bytes %llu != n*S+G %llu",
@@ -1065,6 +1100,8 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
       KL(c, mirage::launch_paged_attention(ap, cs));
     }
     if (int32_t e = gemm_lt(c, B, d, H * D, w.w_o, M->x, M->y, 0, nullptr, 0)) return e;
+    if (c->nccl)  // a10: sum the heads' partial O-projections over the TP ranks
+      CKN(c, ncclAllReduce(M->y, M->y, (size_t)B * d, ncclFloat32, ncclSum, c->nccl, cs));
     KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_o : nullptr, w.n2_g,
                                       opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs));
     if (opt) {
@@ -1075,6 +1112,8 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
       KL(c, mirage::launch_act(s.family, B, s.f, M->y, nullptr, M->f, cs));
     }
     if (int32_t e = gemm_lt(c, B, d, s.f, w.w_2, M->f, M->y, 0, nullptr, 0)) return e;
+    if (c->nccl)  // a10: sum the FFN shards' partial down-projections
+      CKN(c, ncclAllReduce(M->y, M->y, (size_t)B * d, ncclFloat32, ncclSum, c->nccl, cs));
     // residual, then the next layer's first norm (or the final norm)
     const bool last = l + 1 == s.n;
     const bf16* ng = last ? gw.nf_g : nullptr;
