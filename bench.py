@@ -367,7 +367,7 @@ def run_mirage(args, rank, world):
     import torch
     import harness
     lr = int(os.environ.get("LOCAL_RANK", "0"))
-    dev = torch.device("cuda", lr)
+    dev = torch.device("cuda", int(os.environ.get("MIRAGE_BENCH_DEVICE", lr)))
     torch.cuda.set_device(dev)
     total = args.warmup + args.steps + args.e2e_steps + 1
     wl, info = build_workload(args, rank, total)
@@ -381,7 +381,11 @@ def run_mirage(args, rank, world):
     t0 = time.time()
     blobs = {}
     for sh, seed, _ in wl.tenants:
-        blobs[(sh.name, seed)] = harness.make_blob(sh, seed=seed, model_idx=rank, gen_device=dev)
+        if world == 1:
+            blobs[(sh.name, seed)] = harness.make_blob(sh, seed=seed, model_idx=0, gen_device=dev)
+        else:  # replicas of one model share one page-locked host copy (PAPER.md:555 fn.)
+            blobs[(sh.name, seed)] = harness.shared_blob(sh, seed, 0, "bench", lr == 0,
+                                                         torch.distributed.barrier, gen_device=dev)
     setup_blob_s = time.time() - t0
     clock = ClockSampler(lr)
     res = run_arm(args, torch, dev, wl.tenants, wl.remaps, wl.ctxs, wl.max_ctx, blobs, args.steps, args.warmup,
@@ -398,8 +402,8 @@ def run_mirage(args, rank, world):
     B = len(wl.ctxs)
     t_local = res["total_ms"]
     t_all = t_local
-    if world > 1:
-        t = torch.tensor([t_local], device=dev, dtype=torch.float64)
+    if world > 1:  # max over ranks of the device-timed region
+        t = torch.tensor([t_local], dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_all = float(t.item())
     tokens = B * args.steps * world
@@ -461,13 +465,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:
-        import torch
+        # replicas share nothing on the data path; the bench's own barrier and
+        # max-over-ranks reduction are tiny host-side collectives (gloo)
         import torch.distributed as dist
-        if args.impl == "mirage":
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-            dist.init_process_group("nccl")
-        else:
-            dist.init_process_group("gloo")
+        dist.init_process_group("gloo")
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

@@ -68,3 +68,31 @@ def make_shard_blob(shape, rank, tp, seed=0, model_idx=0):
         blob[l * S:(l + 1) * S].copy_(_lib.tensors_to_bytes({k: v.contiguous() for k, v in t.items()}, order))
     blob[shape.n_layers * S:].copy_(global_bytes_tensor(shape, seed, model_idx))
     return blob
+
+
+def shared_blob(shape, seed, model_idx, tag, creator, barrier, gen_device="cpu"):
+    """A weight blob in a file mapping shared by all replicas on the node (the
+    paper's single host copy of the parameters, PAPER.md:555 fn.), page-locked in
+    every process. `creator` (local rank 0) generates it; `barrier()` syncs."""
+    import os
+    S, G, _ = _lib.model_sizes(shape)
+    n = shape.n_layers * S + G
+    shm = "/dev/shm"
+    try:
+        st = os.statvfs(shm)
+        base = shm if st.f_bavail * st.f_frsize > n + (1 << 30) else "/tmp"
+    except OSError:
+        base = "/tmp"
+    path = os.path.join(base, f"mirage_blob_{tag}_{shape.name}_{seed}_{model_idx}.bin")
+    if creator:
+        with open(path, "wb") as f:
+            f.truncate(n)
+        t = torch.from_file(path, shared=True, size=n, dtype=torch.uint8)
+        for l in range(shape.n_layers):
+            t[l * S:(l + 1) * S].copy_(layer_bytes_tensor(shape, l, seed, model_idx, gen_device))
+        t[shape.n_layers * S:].copy_(global_bytes_tensor(shape, seed, model_idx, gen_device))
+        del t
+    barrier()
+    t = torch.from_file(path, shared=True, size=n, dtype=torch.uint8)
+    _lib.host_register(t)
+    return t

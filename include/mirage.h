@@ -293,6 +293,12 @@ int32_t mirage_fill_kv(mirage_ctx* ctx, int32_t model, int64_t seq_id, int32_t n
 int32_t mirage_write_kv(mirage_ctx* ctx, int32_t model, int64_t seq_id, int32_t n_tokens,
                         const void* host_kv);
 
+/* Page-lock (cudaHostRegister, portable) / release caller host memory, e.g. a
+ * weight blob in a file mapping shared by the replicas on one node, so it can
+ * serve as a pinned host blob. Errors: RANGE (null/zero), CUDA. */
+int32_t mirage_host_register(void* ptr, uint64_t bytes);
+int32_t mirage_host_unregister(void* ptr);
+
 /* Number of kernels this ctx has launched (its own kernels, not cuBLAS). */
 int64_t mirage_kernel_launches(const mirage_ctx* ctx);
 

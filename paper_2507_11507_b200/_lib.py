@@ -96,6 +96,8 @@ def _load():
         "mirage_write_kv": (I32, [P, I32, I64, I32, P]),
         "mirage_kernel_launches": (I64, [P]),
         "mirage_nccl_unique_id": (I32, [P]),
+        "mirage_host_register": (I32, [P, U64]),
+        "mirage_host_unregister": (I32, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -110,7 +112,8 @@ EXPORTED = [
     "mirage_add_model", "mirage_plan", "mirage_remap_layers", "mirage_set_active", "mirage_alloc_blocks",
     "mirage_free_blocks", "mirage_get_block_table", "mirage_block_location", "mirage_seq_len",
     "mirage_decode_step", "mirage_query", "mirage_slot_log", "mirage_sync", "mirage_attn_only",
-    "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches", "mirage_nccl_unique_id"]
+    "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches", "mirage_nccl_unique_id",
+    "mirage_host_register", "mirage_host_unregister"]
 
 
 def model_cfg(shape):
@@ -155,6 +158,13 @@ def nccl_unique_id():
     if rc:
         raise MirageError(rc, "nccl_unique_id")
     return buf.raw
+
+
+def host_register(tensor):
+    """Page-lock a CPU tensor's memory in place (e.g. a shared file mapping)."""
+    rc = LIB.mirage_host_register(tensor.data_ptr(), tensor.numel() * tensor.element_size())
+    if rc:
+        raise MirageError(rc, "host_register")
 
 
 def _i32(seq):
@@ -250,7 +260,6 @@ class Context:
 
     # -- API ------------------------------------------------------------------
     def add_model(self, shape, host_blob, native_blocks):
-        assert host_blob.is_pinned(), "host blob must be pinned"
         self._blobs.append(host_blob)
         cfg = model_cfg(shape)
         mid = C.c_int32()
