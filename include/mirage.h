@@ -195,6 +195,31 @@ int32_t mirage_remap_layers(mirage_ctx* ctx, int32_t donor, int32_t recipient,
                             const int32_t* cycle, int32_t m, int32_t beta,
                             int64_t* blocks_gained, uint64_t* reclaimed_bytes);
 
+/* One reclaimed region of a recipient: a maximal run of consecutive donor
+ * layers carved by one mirage_remap_layers call. */
+typedef struct mirage_region {
+  int32_t donor, first_layer, n_layers; /* donor model and its layers [first, first+n)     */
+  int32_t first_id, n_blocks;           /* recipient block ids [first_id, first_id+n)      */
+  int32_t n_free;                       /* of those, currently free                        */
+  int32_t cycle;                        /* 1: part of a streaming self-remap (beta > 0)    */
+  int32_t retired;                      /* 1: reverted by mirage_unremap                   */
+} mirage_region;
+
+int32_t mirage_region_count(mirage_ctx* ctx, int32_t model, int32_t* n);
+int32_t mirage_region_info(mirage_ctx* ctx, int32_t model, int32_t idx, mirage_region* out);
+
+/* Dynamic Reversion (§5.1 "the reclaimed memory is then
+ * restored for parameter usage", :830-839 §7.6.1): give region `region` of
+ * `recipient` back to its donor's parameters. Every block of the region must be
+ * free; the ids are retired (never handed out again, reading #13); the layers'
+ * weights are reloaded from the host copy on the compute stream (ordered after
+ * every kernel that used the bytes as KV), and the layers become resident. A
+ * region of a streaming self-remap reverts the donor's whole cycle (all its
+ * regions, slot holders reloaded, streaming stops at the next step).
+ * Errors: RANGE; STATE (already reverted); PRESSURE (blocks still hold KV);
+ * CUDA. */
+int32_t mirage_unremap(mirage_ctx* ctx, int32_t recipient, int32_t region);
+
 /* Mark a tenant active (1) or inactive (0) (temporal sharing).
  * Errors: RANGE; STATE (activating a model with reclaimed layers: needs
  * unremap, not in this version). */

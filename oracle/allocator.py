@@ -16,6 +16,9 @@ readings #1, #11-#15 (listed in DESIGN.md):
 * alloc(r, seq, n): the n lowest free ids, ascending, all-or-nothing;
 * free(r, seq): return all of seq's blocks; unknown seq -> DoubleFree.
 
+* unremap(r, region) (NEXT-1, Dynamic Reversion): all of the region's ids free
+  -> retired (never reused), donor layers resident again; PRESSURE otherwise.
+
 Pins: worked examples (toy layer -> 48 blocks; SPEC 2 GB / 16 MB -> 128),
 invariants I1-I4 and an exhaustive comparison against an independent set-based
 model in tests/test_oracle_allocator.py.
@@ -42,6 +45,12 @@ class DoubleFree(RuntimeError):
     pass
 
 
+class Pressure(RuntimeError):
+    def __init__(self, used):
+        super().__init__(f"{used} blocks still hold KV")
+        self.used = used
+
+
 class Model:
     def __init__(self, n_layers, layer_bytes, block_bytes, n_native):
         self.n_layers = n_layers
@@ -57,7 +66,7 @@ class Model:
         self.reclaimed_bytes = 0          # bytes of R carved into this model's pool
         self.donated_bytes = 0            # bytes of this model's layers reclaimed
         self.block_loc = {i: ("native", i * block_bytes) for i in range(n_native)}
-        self.regions = []                 # (donor, first_layer, n_layers, first_id, n_blocks)
+        self.regions = []                 # dicts: donor, first_layer, n_layers, first_id, n_blocks, cycle, retired
         self.active = True
 
 
@@ -108,7 +117,8 @@ class Allocator:
                 r.next_id += 1
                 r.free.add(bid)
                 r.block_loc[bid] = (donor, off + i * r.BB)
-            r.regions.append((donor, run[0], len(run), first, k))
+            r.regions.append(dict(donor=donor, first_layer=run[0], n_layers=len(run), first_id=first,
+                                  n_blocks=k, cycle=beta > 0, retired=False))
             gained += k
         r.reclaimed_bytes += len(R) * d.S
         d.donated_bytes += len(R) * d.S
@@ -120,6 +130,39 @@ class Allocator:
             d.cycle = list(C)
             d.beta = beta
         return gained
+
+    def unremap(self, recipient, region):
+        """Dynamic Reversion: the region's blocks must
+        all be free; its ids are retired (never handed out again); the donor's
+        layers become resident. A streaming cycle's region reverts the whole cycle
+        (all its regions; slot holders become plain resident layers)."""
+        r = self.models[recipient]
+        if not (0 <= region < len(r.regions)):
+            raise RangeError("region")
+        reg = r.regions[region]
+        if reg["retired"]:
+            raise StateError("already reverted")
+        d = self.models[reg["donor"]]
+        if reg["cycle"]:
+            which = [g for g in r.regions if g["cycle"] and g["donor"] == reg["donor"] and not g["retired"]]
+        else:
+            which = [reg]
+        ids = [i for g in which for i in range(g["first_id"], g["first_id"] + g["n_blocks"])]
+        busy = [i for i in ids if i not in r.free]
+        if busy:
+            raise Pressure(len(busy))
+        for i in ids:
+            r.free.discard(i)
+        for g in which:
+            g["retired"] = True
+            r.reclaimed_bytes -= g["n_layers"] * d.S
+            d.donated_bytes -= g["n_layers"] * d.S
+            for l in range(g["first_layer"], g["first_layer"] + g["n_layers"]):
+                d.layer_state[l] = RESIDENT
+        if reg["cycle"]:
+            for l in d.cycle[: d.beta]:
+                d.layer_state[l] = RESIDENT
+            d.cycle, d.beta = [], 0
 
     def alloc(self, model, seq, n):
         r = self.models[model]

@@ -49,6 +49,15 @@ class ModelCfg(C.Structure):
                 ("norm_eps", C.c_float), ("rope_theta", C.c_float)]
 
 
+class Region(C.Structure):
+    _fields_ = [("donor", C.c_int32), ("first_layer", C.c_int32), ("n_layers", C.c_int32),
+                ("first_id", C.c_int32), ("n_blocks", C.c_int32), ("n_free", C.c_int32),
+                ("cycle", C.c_int32), ("retired", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class Stats(C.Structure):
     _fields_ = [("native_blocks", C.c_int64), ("total_blocks", C.c_int64), ("free_blocks", C.c_int64),
                 ("layer_bytes", C.c_uint64), ("block_bytes", C.c_uint64),
@@ -97,6 +106,9 @@ def _load():
         "mirage_kernel_launches": (I64, [P]),
         "mirage_nccl_unique_id": (I32, [P]),
         "mirage_host_register": (I32, [P, U64]),
+        "mirage_region_count": (I32, [P, I32, pI32]),
+        "mirage_region_info": (I32, [P, I32, I32, C.POINTER(Region)]),
+        "mirage_unremap": (I32, [P, I32, I32]),
         "mirage_host_unregister": (I32, [P]),
     }
     for name, (res, args) in sig.items():
@@ -113,7 +125,8 @@ EXPORTED = [
     "mirage_free_blocks", "mirage_get_block_table", "mirage_block_location", "mirage_seq_len",
     "mirage_decode_step", "mirage_query", "mirage_slot_log", "mirage_sync", "mirage_attn_only",
     "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches", "mirage_nccl_unique_id",
-    "mirage_host_register", "mirage_host_unregister"]
+    "mirage_host_register", "mirage_host_unregister", "mirage_region_count", "mirage_region_info",
+    "mirage_unremap"]
 
 
 def model_cfg(shape):
@@ -274,6 +287,19 @@ class Context:
                                      C.byref(gained), C.byref(rb))
         self._check(rc, "remap_layers")
         return gained.value, rb.value
+
+    def regions(self, model):
+        n = C.c_int32()
+        self._check(LIB.mirage_region_count(self._ctx, model, C.byref(n)), "region_count")
+        out = []
+        for i in range(n.value):
+            r = Region()
+            self._check(LIB.mirage_region_info(self._ctx, model, i, C.byref(r)), "region_info")
+            out.append(r.as_dict())
+        return out
+
+    def unremap(self, recipient, region):
+        self._check(LIB.mirage_unremap(self._ctx, recipient, region), "unremap")
 
     def set_active(self, model, active):
         self._check(LIB.mirage_set_active(self._ctx, model, int(active)), "set_active")

@@ -1,0 +1,129 @@
+"""Remapping Controller (§5, Algorithm 1; SURVEY.md
+NEXT-1) driving libmirage through the C-ABI.
+
+Host-side policy, as in the paper (a Python component of the serving system):
+
+* when the active model runs out of KV blocks, ``remapping()`` reclaims one more
+  layer of the lowest-priority inactive model (Alg. 1 lines 14-23; P:373-388
+  "prioritizes remapping parameters from inactive models with the lowest
+  priority"; without priorities, round robin with Most-Recently-Used first,
+  P:380-383), up to a per-model cap of the model's layers (P:387 threshold;
+  Alg. 1 P:530 removes a model at remapped == layers, reading #8);
+* when KV usage subsides, Dynamic Reversion gives empty reclaimed regions back
+  to parameters, newest first (Alg. 1 lines 7-12), keeping
+  ``headroom`` free blocks;
+* activating an inactive model first reverts the regions it donated (its
+  parameters must be resident to run).
+
+Layer choice for an inactive donor (unstated by the paper, reading in
+DESIGN.md): highest remaining layer index first, ``layers_per_call`` at a time.
+Active-model self-remap (streaming) is delegated to an optional callback.
+"""
+from . import _lib
+
+
+class RemappingController:
+    def __init__(self, ctx, models, active, cap=1.0, layers_per_call=1, self_remap=None):
+        """models: {model_id: (n_layers, priority or None)}; active: model id."""
+        self.ctx = ctx
+        self.info = {m: {"layers": n, "prio": p, "remapped": [], "act": 0} for m, (n, p) in models.items()}
+        self.cap, self.per_call, self.self_remap = cap, layers_per_call, self_remap
+        self.clock = 0
+        self.log = []
+        self.active = None
+        self.activate(active)
+
+    # ---- Metadata Store views ---------------------------------------------------
+    def enable_remap(self):
+        return any(not r["retired"] for r in self.ctx.regions(self.active))
+
+    def _candidates(self):
+        out = []
+        for m, i in self.info.items():
+            if m == self.active:
+                continue
+            if len(i["remapped"]) >= int(self.cap * i["layers"] + 1e-9):
+                continue
+            prio = i["prio"] if i["prio"] is not None else 0
+            out.append((prio, -i["act"], m))      # lowest priority, then most recently activated
+        return [m for _, _, m in sorted(out)]
+
+    # ---- Alg. 1 remapping() -----------------------------------------------------
+    def remapping(self):
+        cands = self._candidates()
+        if not cands:
+            if self.self_remap is not None:
+                act = self.self_remap(self)
+                if act:
+                    self.log.append(("self_remap",) + tuple(act))
+                return act
+            return None
+        m = cands[0]
+        i = self.info[m]
+        left = [l for l in range(i["layers"]) if l not in i["remapped"]]
+        limit = int(self.cap * i["layers"] + 1e-9) - len(i["remapped"])
+        take = sorted(left, reverse=True)[: min(self.per_call, limit)]
+        layers = sorted(take)
+        gained, _ = self.ctx.remap_layers(m, self.active, layers, 0)
+        i["remapped"].extend(layers)
+        act = ("remap", m, tuple(layers), gained)
+        self.log.append(act)
+        return act
+
+    def alloc(self, seq, n):
+        """alloc_blocks on the active model, remapping on shortfall (Alg. 1 line 3)."""
+        while True:
+            try:
+                return self.ctx.alloc_blocks(self.active, seq, n)
+            except _lib.MirageError as e:
+                if e.code != _lib.ERR_NO_BLOCKS:
+                    raise
+                if self.remapping() is None:
+                    raise
+
+    def free(self, seq):
+        self.ctx.free_blocks(self.active, seq)
+
+    # ---- Dynamic Reversion ----------------------------------------------------------
+    def revert(self, headroom):
+        """Revert empty regions newest-first while free blocks stay >= headroom."""
+        done = []
+        regs = self.ctx.regions(self.active)
+        for idx in range(len(regs) - 1, -1, -1):
+            r = self.ctx.regions(self.active)[idx]
+            if r["retired"] or r["n_free"] != r["n_blocks"]:
+                continue
+            free = self.ctx.query(self.active)["free_blocks"]
+            if free - r["n_blocks"] < headroom:
+                continue
+            self.ctx.unremap(self.active, idx)
+            lay = set(range(r["first_layer"], r["first_layer"] + r["n_layers"]))
+            if r["donor"] in self.info:
+                i = self.info[r["donor"]]
+                i["remapped"] = [l for l in i["remapped"] if l not in lay]
+            act = ("revert", idx, r["donor"], r["n_layers"])
+            self.log.append(act)
+            done.append(act)
+        return done
+
+    # ---- temporal sharing -------------------------------------------------------------
+    def activate(self, model):
+        """Make `model` the active model; its donated regions are reverted first."""
+        self.clock += 1
+        if self.active is not None and self.active != model:
+            # the model's parameters must be resident before it runs
+            for owner in sorted(self.info):
+                regs = self.ctx.regions(owner)
+                for idx, r in enumerate(regs):
+                    if r["donor"] == model and not r["retired"] and owner != model:
+                        self.ctx.unremap(owner, idx)
+                        self.log.append(("revert", idx, model, r["n_layers"]))
+            self.info[model]["remapped"] = []
+            self.ctx.set_active(self.active, False)
+        for m in self.info:
+            if m != model:
+                self.ctx.set_active(m, False)
+        self.ctx.set_active(model, True)
+        self.info[model]["act"] = self.clock
+        self.active = model
+        self.log.append(("activate", model))

@@ -129,6 +129,14 @@ GlobalW global_ptrs(const Shape& m, const char* base) {
   return g;
 }
 
+// One reclaimed region: a maximal run of consecutive donor layers carved in one
+// remap call into blocks [first_id, first_id + n_blocks) of the recipient.
+struct Region {
+  int32_t donor, first_layer, n_layers, first_id, n_blocks;
+  bool cycle;    // part of a streaming self-remap (reverted only with the whole cycle)
+  bool retired;  // reverted: ids retired, bytes back to parameters
+};
+
 struct CopyTiming {
   cudaEvent_t t0, t1;
   uint64_t bytes;
@@ -155,6 +163,7 @@ struct Model {
   int64_t bbase_cap = 0;
   uint64_t reclaimed_bytes = 0, donated_bytes = 0;
   std::vector<int> layer_state;
+  std::vector<Region> regions;  // as recipient, in creation order
   // ---- prefetcher (a4, a5) ----
   std::vector<int32_t> cycle;
   int32_t beta = 0;
@@ -878,6 +887,7 @@ int32_t mirage_remap_layers(mirage_ctx* c, int32_t donor, int32_t recipient, con
     const uint64_t off = (uint64_t)r.first * D->sz.S;
     const uint64_t len = (uint64_t)r.second * D->sz.S;
     const int64_t k = (int64_t)(len / R->sz.BB);
+    R->regions.push_back(Region{donor, r.first, r.second, R->next_id, (int32_t)k, beta > 0, false});
     for (int64_t i = 0; i < k; ++i) {
       const int32_t id = R->next_id++;
       R->free_ids.insert(id);
@@ -912,6 +922,97 @@ int32_t mirage_remap_layers(mirage_ctx* c, int32_t donor, int32_t recipient, con
   if (gained && !c->host_only) CK(c, cudaStreamSynchronize(c->cs));  // the host staging above is a pageable vector
   if (blocks_gained) *blocks_gained = gained;
   if (reclaimed_bytes) *reclaimed_bytes = (uint64_t)Rl.size() * D->sz.S;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_region_count(mirage_ctx* c, int32_t model, int32_t* n) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || !n) return fail(c, MIRAGE_ERR_RANGE, "region_count: model %d", model);
+  *n = (int32_t)M->regions.size();
+  return MIRAGE_OK;
+}
+
+int32_t mirage_region_info(mirage_ctx* c, int32_t model, int32_t idx, mirage_region* out) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || !out || idx < 0 || idx >= (int32_t)M->regions.size())
+    return fail(c, MIRAGE_ERR_RANGE, "region_info: model %d region %d", model, idx);
+  const Region& r = M->regions[idx];
+  out->donor = r.donor;
+  out->first_layer = r.first_layer;
+  out->n_layers = r.n_layers;
+  out->first_id = r.first_id;
+  out->n_blocks = r.n_blocks;
+  out->n_free = 0;
+  for (int32_t i = r.first_id; i < r.first_id + r.n_blocks; ++i) out->n_free += M->free_ids.count(i);
+  out->cycle = r.cycle;
+  out->retired = r.retired;
+  return MIRAGE_OK;
+}
+
+// Dynamic Reversion.
+int32_t mirage_unremap(mirage_ctx* c, int32_t recipient, int32_t region) {
+  GUARD(c);
+  Model* R = get_model(c, recipient);
+  if (!R || region < 0 || region >= (int32_t)R->regions.size())
+    return fail(c, MIRAGE_ERR_RANGE, "unremap: model %d region %d", recipient, region);
+  if (R->regions[region].retired) return fail(c, MIRAGE_ERR_STATE, "unremap: region %d already reverted", region);
+  const int32_t donor = R->regions[region].donor;
+  Model* D = get_model(c, donor);
+  // a streaming cycle is reverted as a whole (all of its regions); otherwise one region
+  std::vector<int32_t> which;
+  if (R->regions[region].cycle) {
+    for (int32_t i = 0; i < (int32_t)R->regions.size(); ++i)
+      if (R->regions[i].cycle && R->regions[i].donor == donor && !R->regions[i].retired) which.push_back(i);
+  } else {
+    which.push_back(region);
+  }
+  int64_t used = 0;
+  for (int32_t i : which) {
+    const Region& r = R->regions[i];
+    for (int32_t b = r.first_id; b < r.first_id + r.n_blocks; ++b) used += !R->free_ids.count(b);
+  }
+  if (used) return fail(c, MIRAGE_ERR_PRESSURE, "unremap: %lld blocks of the region still hold KV", (long long)used);
+  // retire the ids: never handed out again
+  std::vector<int32_t> layers;
+  for (int32_t i : which) {
+    Region& r = R->regions[i];
+    for (int32_t b = r.first_id; b < r.first_id + r.n_blocks; ++b) R->free_ids.erase(b);
+    r.retired = true;
+    for (int32_t l = r.first_layer; l < r.first_layer + r.n_layers; ++l) layers.push_back(l);
+    R->reclaimed_bytes -= (uint64_t)r.n_layers * D->sz.S;
+    D->donated_bytes -= (uint64_t)r.n_layers * D->sz.S;
+  }
+  const bool was_cycle = R->regions[region].cycle;
+  if (was_cycle)  // the slot holders' storage may hold another cycled layer's weights
+    for (int i = 0; i < D->beta; ++i) layers.push_back(D->cycle[i]);
+  if (!c->host_only) {
+    if (was_cycle) {  // finish in-flight prefetch copies before reloading the slots
+      cudaEvent_t e;
+      CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(c, cudaEventRecord(e, c->xs));
+      CK(c, cudaStreamWaitEvent(c->cs, e, 0));
+      cudaEventDestroy(e);
+    }
+    // stream-ordered after every kernel that used these bytes as KV
+    for (int32_t l : layers)
+      CK(c, cudaMemcpyAsync(D->w_dev + (uint64_t)l * D->sz.S, D->host + (uint64_t)l * D->sz.S, D->sz.S,
+                            cudaMemcpyHostToDevice, c->cs));
+  }
+  for (int32_t l : layers) D->layer_state[l] = RESIDENT;
+  if (was_cycle) {
+    for (int32_t l : D->cycle) D->cyc_index[l] = -1;
+    D->cycle.clear();
+    D->beta = 0;
+    if (!c->host_only) {
+      CK(c, cudaStreamSynchronize(c->xs));
+      for (auto e : D->ready_ev) cudaEventDestroy(e);
+      for (auto e : D->free_ev) cudaEventDestroy(e);
+    }
+    D->ready_ev.clear();
+    D->free_ev.clear();
+  }
   return MIRAGE_OK;
 }
 

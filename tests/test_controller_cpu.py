@@ -1,0 +1,137 @@
+"""NEXT-1 Remapping Controller (Alg. 1) and Dynamic Reversion. Directional pins
+of the oracle controller against the paper's worked example and rules, and
+bit-exact parity of the product controller (libmirage host-only context) with
+the oracle on seeded traces. CPU only."""
+import random
+
+import pytest
+
+from oracle import allocator as OA
+from oracle.controller import Controller as OracleController
+from synth import models, weights
+
+TOY = models.TOY                       # 2 layers
+DONOR = models.TOY.with_layers(8)      # 8-layer toy donors
+
+
+def bb(m):
+    return m.n_layers * m.n_kv_heads * 2 * 16 * m.head_dim * 2
+
+
+def oracle_setup(prios, native=4):
+    al = OA.Allocator()
+    a = al.add_model(TOY.n_layers, weights.layer_bytes(TOY), bb(TOY), native)
+    spec = {a: (TOY.n_layers, None)}
+    for p in prios:
+        d = al.add_model(DONOR.n_layers, weights.layer_bytes(DONOR), bb(DONOR), 0)
+        spec[d] = (DONOR.n_layers, p)
+    return al, spec
+
+
+def test_paper_example_lowest_priority_first_then_next():
+    # Model-A active; B, C inactive, C lowest priority -> C first; after
+    # C reaches its limit, continue with B; active A only after all inactive ones.
+    al, spec = oracle_setup([2, 1])            # model 1 = "B" (prio 2), model 2 = "C" (prio 1)
+    ctl = OracleController(al, spec, active=0, cap=0.5)
+    victims = []
+    for _ in range(8):
+        e = ctl.remapping()
+        victims.append(e[1] if e else None)
+    assert victims == [2, 2, 2, 2, 1, 1, 1, 1]
+    assert ctl.remapping() is None            # both at cap; active self-remap not enabled
+    assert ctl.log[1][2] == (7,)               # highest remaining layer first
+
+
+def test_mru_without_priorities():
+    # no priorities -> remap the most recently activated model first
+    al, spec = oracle_setup([None, None, None])
+    ctl = OracleController(al, spec, active=1)
+    for _ in range(3):                         # drain model 1's use as active: switch to 2, then 0
+        pass
+    ctl.activate(2)
+    ctl.activate(0)
+    e = ctl.remapping()
+    assert e[1] == 2                           # 2 was activated after 1 (and 3 never)
+
+
+def test_alloc_remaps_on_shortfall_and_reverts_lifo():
+    al, spec = oracle_setup([1])
+    ctl = OracleController(al, spec, active=0)
+    per_layer = weights.layer_bytes(DONOR) // bb(TOY)
+    ids = ctl.alloc(0, 4 + 2 * per_layer)      # native 4 blocks + two donor layers
+    assert [e[0] for e in ctl.log] == ["activate", "remap", "remap"]
+    assert len(ids) == 4 + 2 * per_layer
+    ctl.free(0)
+    assert ctl.revert(headroom=4 + per_layer) == [("revert", 1, 1, 1)]   # newest first, keep headroom
+    assert ctl.revert(headroom=0) == [("revert", 0, 1, 1)]
+    assert al.models[1].layer_state == [OA.RESIDENT] * 8
+    ctl.alloc(1, 4)                            # native blocks only; retired ids never return
+    assert sorted(al.models[0].free) == []
+
+
+def test_revert_refused_while_blocks_hold_kv():
+    al, spec = oracle_setup([1])
+    ctl = OracleController(al, spec, active=0)
+    ctl.alloc(0, 10)
+    assert ctl.revert(headroom=0) == []
+    with pytest.raises(OA.Pressure):
+        al.unremap(0, 0)
+
+
+def make_trace(seed, n=250):
+    rng = random.Random(seed)
+    ev, live, nxt = [], [], 0
+    for t in range(n):
+        r = rng.random()
+        if r < 0.35 or not live:
+            ev.append(("alloc", nxt, rng.randint(1, 30)))
+            live.append(nxt)
+            nxt += 1
+        elif r < 0.7:
+            ev.append(("alloc", rng.choice(live), 1))
+        elif r < 0.9:
+            s = rng.choice(live)
+            live.remove(s)
+            ev.append(("free", s))
+        else:
+            ev.append(("revert", rng.choice([0, 8, 40])))
+        if t % 83 == 82 and not live:
+            ev.append(("activate", rng.choice([0, 1])))
+    ev += [("free", s) for s in live] + [("revert", 0)]   # off-peak: everything reverts
+    return ev
+
+
+def replay(ctl, ev, errors):
+    for e in ev:
+        try:
+            if e[0] == "alloc":
+                ctl.alloc(e[1], e[2])
+            elif e[0] == "free":
+                ctl.free(e[1])
+            elif e[0] == "revert":
+                ctl.revert(e[1])
+            else:
+                ctl.activate(e[1])
+        except errors:
+            ctl.log.append(("fail",) + tuple(e))
+
+
+@pytest.mark.parametrize("seed,prios", [(1, [3, 1, 2]), (2, [None, None, None]), (3, [1, 1, 5])])
+def test_product_controller_matches_oracle(seed, prios):
+    from paper_2507_11507_b200 import _lib
+    from paper_2507_11507_b200.controller import RemappingController
+    ev = make_trace(seed)
+    al, spec = oracle_setup(prios, native=6)
+    octl = OracleController(al, spec, active=0, cap=0.75)
+    replay(octl, ev, (OA.NoBlocks, OA.DoubleFree, OA.Pressure))
+    ctx = _lib.Context.host_only(1 << 38, 64, 4096)
+    ids = [ctx.add_model_host_only(TOY, 6)] + [ctx.add_model_host_only(DONOR, 0) for _ in prios]
+    pspec = {i: spec[i] for i in ids}
+    pctl = RemappingController(ctx, pspec, active=0, cap=0.75)
+    replay(pctl, ev, (_lib.MirageError,))
+    assert pctl.log == octl.log
+    assert any(e[0] == "remap" for e in octl.log) and any(e[0] == "revert" for e in octl.log)
+    for m in ids:
+        for s, t in al.models[m].tables.items():
+            assert ctx.block_table(m, s) == t
+        assert ctx.query(m)["free_blocks"] == len(al.models[m].free)

@@ -1,0 +1,58 @@
+"""Dynamic Reversion on the device (NEXT-1): after mirage_unremap the donor's
+parameters are reloaded from the host copy and every model decodes exactly as
+the oracle says; a reverted streaming cycle stops re-streaming. GPU only."""
+import numpy as np
+import pytest
+import torch
+
+import harness
+from oracle.decode import Decoder
+from synth import models, weights, workload
+
+pytestmark = pytest.mark.gpu
+
+
+def decode_and_check(ctx, mid, shape, seed, seqs, steps, t0=0):
+    dec = Decoder(shape, [weights.layer_tensors(shape, l, seed) for l in range(shape.n_layers)],
+                  weights.global_tensors(shape, seed))
+    hid = torch.empty((len(seqs), shape.d_model), dtype=torch.bfloat16, device="cuda")
+    for t in range(steps):
+        if t % 16 == 0:
+            for s in seqs:
+                ctx.alloc_blocks(mid, s, 1)
+        toks = [workload.teacher_tokens(s, t, shape.vocab) for s in seqs]
+        ctx.decode_step(mid, seqs, toks, [t] * len(seqs), hidden_out=hid)
+        ref, _, _ = dec.step(seqs, toks, [t] * len(seqs))
+        ctx.sync()
+        got = hid.float().cpu().numpy()
+        rel = np.sqrt(((got - ref) ** 2).mean() / (ref ** 2).mean())
+        assert rel < 1e-2, (t, rel)
+
+
+def test_cycle_and_inactive_donor_reversion():
+    from paper_2507_11507_b200 import Context
+    a, d = models.TOY, models.TOY_LLAMA
+    ctx = Context(harness.arena_for([(a, 8), (d, 8)], 8, 128), 8, 128)
+    ma = ctx.add_model(a, harness.make_blob(a, seed=7), 8)
+    md = ctx.add_model(d, harness.make_blob(d, seed=8), 8)
+    # self-remap cycle on A and a full reclaim of the inactive donor D into A
+    ctx.remap_layers(ma, ma, [0, 1], 1)
+    ctx.set_active(md, False)
+    ctx.remap_layers(md, ma, [0, 1], 0)
+    decode_and_check(ctx, ma, a, 7, list(range(8)), 40)      # 24 blocks: native + reclaimed
+    for s in range(8):
+        ctx.free_blocks(ma, s)
+    regs = ctx.regions(ma)
+    assert [r["cycle"] for r in regs] == [1, 0]
+    ctx.unremap(ma, 1)                                       # D's weights back
+    ctx.unremap(ma, 0)                                       # A's cycle reverted
+    assert all(r["retired"] for r in ctx.regions(ma))
+    st = ctx.query(ma)
+    assert st["m"] == 0 and st["total_blocks"] - st["free_blocks"] == st["total_blocks"] - 8
+    copies = st["h2d_copies"]
+    decode_and_check(ctx, ma, a, 7, [100, 101], 20)
+    ctx.sync()
+    assert ctx.query(ma)["h2d_copies"] == copies             # streaming stopped
+    ctx.set_active(ma, False)
+    ctx.set_active(md, True)                                  # donor runs on its restored weights
+    decode_and_check(ctx, md, d, 8, [0, 1, 2], 20)
