@@ -530,13 +530,10 @@ int variant() {
 
 template <int D, int G>
 cudaError_t launch_dg(const AttnParams& p, cudaStream_t s, bool query, int* grid_out) {
+  // the 4 warps of a CTA split the blocks of one work item, for any H_kv
   constexpr int NS = D == 128 ? 2 : 4;
-  if (p.H_kv % 4 == 0) {
-    if (D == 128 && variant() == 1) return launch_v<D, G, 4, 3>(p, s, query, grid_out);
-    return launch_v<D, G, 4, NS>(p, s, query, grid_out);
-  }
-  if (p.H_kv % 2 == 0) return launch_v<D, G, 2, NS>(p, s, query, grid_out);
-  return launch_v<D, G, 1, NS>(p, s, query, grid_out);
+  if (D == 128 && variant() == 1) return launch_v<D, G, 4, 3>(p, s, query, grid_out);
+  return launch_v<D, G, 4, NS>(p, s, query, grid_out);
 }
 
 template <int D>
@@ -570,6 +567,6 @@ int attention_grid_ctas(int H, int H_kv, int D) {
   return g;
 }
 
-int attention_cta_warps(int H_kv) { return H_kv % 4 == 0 ? 4 : H_kv % 2 == 0 ? 2 : 1; }
+int attention_cta_warps(int) { return 4; }
 
 }  // namespace mirage

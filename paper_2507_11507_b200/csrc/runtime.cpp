@@ -414,7 +414,8 @@ int32_t acquire_stage(mirage_ctx* c, char** host) {
 // longest-first order (greedy LPT). Splitting adds per-item overhead and a
 // combine, so the split size P (blocks) is the LARGEST one that still gives
 // every resident CTA about one item to start with: items(P) >= f * grid, with
-// f = 0.8 (f = 1.0 for G = 8, whose tiles are compute-heavier), and at most
+// f = 0.8 (f = 0.6 for G = 8), equalised so the longest sequence has no runt
+// last split, and at most
 // kMaxSplits splits per sequence. Calibrated on B200 (tools/attn_bench.py
 // --split sweeps). P depends on logical lengths only, never on
 // block placement.
@@ -427,7 +428,7 @@ int choose_split(const int32_t* lens, int B, int Hk, int G, int grid, int warps)
     max_nb = std::max(max_nb, nbs[b]);
   }
   const int p_lo = std::max(1, (max_nb + kMaxSplits - 1) / kMaxSplits);
-  const double need = (G >= 8 ? 1.0 : 0.8) * std::max(grid, 1);
+  const double need = (G >= 8 ? 0.6 : 0.8) * std::max(grid, 1);
   auto items = [&](int P) {
     int64_t n = 0;
     for (int b = 0; b < B; ++b) n += (nbs[b] + P - 1) / P;
@@ -438,7 +439,9 @@ int choose_split(const int32_t* lens, int B, int Hk, int G, int grid, int warps)
     const int next = std::max(p_lo, std::min(P - 1, (int)(P * 0.97)));
     P = next;
   }
-  return P;
+  // equalise the longest sequence's splits (no runt last split)
+  const int ns = (max_nb + P - 1) / P;
+  return std::max(1, (max_nb + ns - 1) / ns);
 }
 
 int build_units(const int32_t* lens, const int32_t* seq_off, int B, int Hk, int G, int grid, int warps,
