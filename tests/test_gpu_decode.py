@@ -120,3 +120,34 @@ def test_error_paths():
         ctx.remap_layers(mid, mid, [0, 1], 0)             # active donor, beta 0
     assert e.value.code == _lib.ERR_STATE
     ctx.sync()
+
+
+def test_long_prompt_decode_uses_split_k_and_matches_oracle():
+    """A 3000-token prompt (uploaded through mirage_write_kv) makes the planner split
+    the attention of the decode step; the result still matches oracle c4."""
+    from paper_2507_11507_b200 import Context
+    shape = models.TOY_LLAMA
+    B, P = 2, 3000
+    ctx = Context(harness.arena_for([(shape, 400)], B, 4096), B, 4096)
+    mid = ctx.add_model(shape, harness.make_blob(shape, seed=6), 400)
+    layers = [weights.layer_tensors(shape, l, 6) for l in range(shape.n_layers)]
+    dec = Decoder(shape, layers, weights.global_tensors(shape, 6))
+    for i in range(B):
+        kv = workload.logical_kv(shape.n_layers, shape.n_kv_heads, shape.head_dim, P - i * 700, seed=2, seq=i)
+        ctx.alloc_blocks(mid, i, harness.blocks_for(P + 8))
+        ctx.write_kv(mid, i, kv)
+        kvf = kv.float().double().numpy()
+        dec.set_kv(i, [(kvf[l, :, 0], kvf[l, :, 1]) for l in range(shape.n_layers)])
+    hid = torch.empty((B, shape.d_model), dtype=torch.bfloat16, device="cuda")
+    pos = [P - i * 700 for i in range(B)]
+    for t in range(4):
+        toks = [workload.teacher_tokens(i, pos[i], shape.vocab) for i in range(B)]
+        ctx.decode_step(mid, list(range(B)), toks, pos, hidden_out=hid)
+        ref, _, _ = dec.step(list(range(B)), toks, pos)
+        ctx.sync()
+        got = hid.float().cpu().numpy()
+        rel = np.sqrt(((got - ref) ** 2).mean() / (ref ** 2).mean())
+        assert rel <= REL_RMS and np.abs(got - ref).max() <= MAX_ABS, (t, rel)
+        pos = [p + 1 for p in pos]
+    st = ctx.query(mid)
+    assert st["last_split_blocks"] < (P + 15) // 16 and st["last_attn_units"] > B   # split-K active
