@@ -1,0 +1,200 @@
+"""Trace-driven serving loop on one B200 exercising the Remapping Controller
+(Alg. 1) and Dynamic Reversion, directionally against the
+paper's claims (§7.2, §7.6.1). Decode steps run through libmirage;
+prompt KV is written by mirage_fill_kv (prefill is out of the path's scope);
+TBT = decode step time (every running sequence emits one token per step).
+
+E1 temporal sharing: active OPT-13B + inactive Llama-2-7B-shaped tenant.
+   MIRAGE (controller reclaims donor layers on shortfall) vs no-remap (queue).
+E2 dynamic reversion: single OPT-13B that self-remaps alpha=1 (C={0,20}) under
+   peak load; off-peak, with reversion the cycle is reverted when its blocks
+   drain, without it the layers keep streaming.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import harness  # noqa: E402
+from paper_2507_11507_b200 import _lib  # noqa: E402
+from paper_2507_11507_b200.controller import RemappingController  # noqa: E402
+from synth import models, workload  # noqa: E402
+
+
+def pct(xs, p):
+    s = sorted(xs)
+    return s[max(0, int(np.ceil(p / 100 * len(s))) - 1)] if s else None
+
+
+def serve(ctx, ctl, mid, shape, arrivals, prompts, outs, max_batch, revert_every=None, headroom=0, tag=""):
+    """Closed decode loop. arrivals[t] = number of new requests at step t."""
+    queue, running, pos, left = [], [], {}, {}
+    nxt, step_ms, waits, t0s = 0, [], [], {}
+    preempted = [0]
+    held = {}
+    C = __import__("ctypes")
+    evs = []
+    t = 0
+    total_steps = len(arrivals)
+    tokens = 0
+    while t < total_steps or running or queue:
+        if t < total_steps:
+            for _ in range(arrivals[t]):
+                queue.append((nxt, t))
+                nxt += 1
+        # admit in FIFO order while blocks allow (controller may remap on shortfall)
+        while queue and len(running) < max_batch:
+            sid, ta = queue[0]
+            P = int(prompts[sid % len(prompts)])
+            try:
+                ctl.alloc(sid, harness.blocks_for(P + 1)) if ctl else ctx.alloc_blocks(mid, sid, harness.blocks_for(P + 1))
+            except _lib.MirageError as e:
+                if e.code != _lib.ERR_NO_BLOCKS:
+                    raise
+                break
+            ctx.fill_kv(mid, sid, P, seed=sid)
+            held[sid] = harness.blocks_for(P + 1)
+            queue.pop(0)
+            running.append(sid)
+            pos[sid], left[sid] = P, int(outs[sid % len(outs)])
+            waits.append(t - ta)
+        if not running:
+            t += 1
+            continue
+        # grow blocks for sequences crossing a block boundary; on exhaustion preempt
+        # the newest running sequence (vLLM-style evict, re-queued for recompute)
+        for sid in list(running):
+            if sid not in running or harness.blocks_for(pos[sid] + 1) <= held[sid]:
+                continue
+            while True:
+                try:
+                    ctl.alloc(sid, 1) if ctl else ctx.alloc_blocks(mid, sid, 1)
+                    held[sid] += 1
+                    break
+                except _lib.MirageError as e:
+                    if e.code != _lib.ERR_NO_BLOCKS:
+                        raise
+                    victim = running[-1]
+                    running.remove(victim)
+                    (ctl.free(victim) if ctl else ctx.free_blocks(mid, victim))
+                    queue.insert(0, (victim, t))
+                    preempted[0] += 1
+                    if victim == sid:
+                        break
+        batch = list(running)
+        if not batch:
+            t += 1
+            continue
+        toks = [workload.teacher_tokens(s, pos[s], shape.vocab) for s in batch]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream)
+        ctx.decode_step(mid, batch, toks, [pos[s] for s in batch], argmax=False)
+        e1.record(ctx.stream)
+        evs.append((e0, e1, t))
+        tokens += len(batch)
+        for s in batch:
+            pos[s] += 1
+            left[s] -= 1
+        for s in [s for s in batch if left[s] <= 0]:
+            running.remove(s)
+            (ctl.free(s) if ctl else ctx.free_blocks(mid, s))
+        if ctl and revert_every and t % revert_every == 0:
+            for a in ctl.revert(headroom):
+                ctl.timeline = getattr(ctl, "timeline", []) + [(t, a)]
+        t += 1
+    ctx.sync()
+    step_ms = [(a.elapsed_time(b), tt) for a, b, tt in evs]
+    serve.preempted = preempted[0]
+    return step_ms, waits, tokens
+
+
+def e1(args):
+    act, don = models.OPT_13B, models.LLAMA2_7B
+    Sa, Ga, BBa = _lib.model_sizes(act)
+    native = int((0.35 * 96e9 - (act.n_layers * Sa + Ga)) // BBa)
+    prompts, outs = workload.sharegpt_trace(2000, seed=5)
+    rng = np.random.default_rng(1)
+    # bursty arrivals: alternating high / low phases (Azure-trace-like burstiness)
+    arr = [rng.poisson(3.0 if (t // 60) % 2 == 0 else 0.3) for t in range(args.steps)]
+    blobs = {0: harness.make_blob(act, 0, 0, gen_device="cuda"), 1: harness.make_blob(don, 1, 1, gen_device="cuda")}
+    res = {}
+    for mode in ("mirage", "no_remap"):
+        ctx = _lib.Context(harness.arena_for([(act, native), (don, 0)], 256, 2048), 256, 2048)
+        ma = ctx.add_model(act, blobs[0], native)
+        md = ctx.add_model(don, blobs[1], 0)
+        ctl = RemappingController(ctx, {ma: (act.n_layers, None), md: (don.n_layers, 0)}, active=ma,
+                                  layers_per_call=4) if mode == "mirage" else None
+        if not ctl:
+            ctx.set_active(md, False)
+        t0 = time.time()
+        st, waits, tokens = serve(ctx, ctl, ma, act, arr, prompts, outs, 256, revert_every=10, headroom=64)
+        ms = [x for x, _ in st]
+        res[mode] = {"tok_s": tokens / (sum(ms) / 1e3), "p50_tbt_ms": pct(ms, 50), "p99_tbt_ms": pct(ms, 99),
+                     "mean_wait_steps": statistics.mean(waits) if waits else 0, "preemptions": serve.preempted,
+                     "p99_wait_steps": pct(waits, 99), "steps": len(ms), "wall_s": time.time() - t0,
+                     "actions": (ctl.log[:6] + [f"... {len(ctl.log)} actions"]) if ctl else None,
+                     "remaps": sum(1 for a in ctl.log if a[0] == "remap") if ctl else 0,
+                     "reverts": sum(1 for a in ctl.log if a[0] == "revert") if ctl else 0}
+        ctx.close()
+        del ctx
+        torch.cuda.empty_cache()
+    return res
+
+
+def e2(args):
+    shape = models.OPT_13B
+    S, G, BB = _lib.model_sizes(shape)
+    native = 300      # the burst overflows the native pool
+    prompts, outs = workload.sharegpt_trace(2000, seed=6)
+    rng = np.random.default_rng(2)
+    # a burst, then a long off-peak phase with a trickle of arrivals
+    arr = [rng.poisson(0.6 if t < 100 else 0.01) for t in range(args.steps * 5)]
+    blob = harness.make_blob(shape, 0, 0, gen_device="cuda")
+
+    def self_remap(ctl):
+        if ctl.ctx.query(ctl.active)["m"]:
+            return None
+        cycle, m, beta = _lib.plan(shape.n_layers, 1, _lib.BETA_1, 0, 1)
+        gained, _ = ctl.ctx.remap_layers(ctl.active, ctl.active, cycle, beta)
+        return ("cycle", tuple(cycle), gained)
+
+    res = {}
+    for mode in ("reversion", "no_reversion"):
+        ctx = _lib.Context(harness.arena_for([(shape, native)], 256, 2048), 256, 2048)
+        mid = ctx.add_model(shape, blob, native)
+        ctl = RemappingController(ctx, {mid: (shape.n_layers, None)}, active=mid, self_remap=self_remap)
+        st, waits, tokens = serve(ctx, ctl, mid, shape, arr, prompts, outs, 256,
+                                  revert_every=10 if mode == "reversion" else None, headroom=0)
+        horizon = len(arr)
+        off = [x for x, t in st if horizon * 2 // 3 <= t < horizon]   # last third of the off-peak phase
+        rv = next((t for t, a in ctl.timeline if a[0] == "revert"), None) if hasattr(ctl, "timeline") else None
+        res[mode] = {"tok_s": tokens / (sum(x for x, _ in st) / 1e3), "offpeak_p50_tbt_ms": pct(off, 50),
+                     "peak_p50_tbt_ms": pct([x for x, t in st if t < 100], 50), "revert_at_step": rv,
+                     "offpeak_p99_tbt_ms": pct(off, 99), "offpeak_steps": len(off),
+                     "revert_step": next((i for i, a in enumerate(ctl.log) if a[0] == "revert"), None),
+                     "actions": [a for a in ctl.log if a[0] != "activate"][:6]}
+        ctx.close()
+        del ctx
+        torch.cuda.empty_cache()
+    return res
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=600)
+    ap.add_argument("--exp", nargs="*", default=["e1", "e2"])
+    a = ap.parse_args()
+    out = {}
+    if "e1" in a.exp:
+        out["e1_temporal_sharing"] = e1(a)
+    if "e2" in a.exp:
+        out["e2_dynamic_reversion"] = e2(a)
+    print(json.dumps(out, indent=1, default=str))
