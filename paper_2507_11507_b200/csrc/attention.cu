@@ -129,7 +129,8 @@ paged_attention_kernel(const AttnParams p) {
   float(*sm_acc)[G][D] = reinterpret_cast<float(*)[G][D]>(sm_accf);
   __shared__ int am_last;
   // dynamic item queue: CTA item k (in claim order) lives in slot k % QB
-  __shared__ int slot_item[QB], slot_gen[QB], slot_claim[QB];
+  __shared__ int slot_claim[QB];
+  __shared__ unsigned long long slot_word[QB];  // ((k + 1) << 32) | item, published atomically
   __shared__ float sLam[G];
   // split-combine scratch aliases sm_acc (free once the partials are written)
   float(*sw)[G] = reinterpret_cast<float(*)[G]>(sm_accf);
@@ -151,7 +152,7 @@ paged_attention_kernel(const AttnParams p) {
 #pragma unroll
       for (int i = 0; i < QB; ++i) {
         mbar_init(&qbars[i], 1);
-        slot_gen[i] = -1;
+        slot_word[i] = 0ull;
         slot_claim[i] = i - QB;
       }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -175,13 +176,11 @@ paged_attention_kernel(const AttnParams p) {
           mbar_expect_tx(&qbars[sl], G * D * 4);
           bulk_g2s(&qbuf[sl][0], src, G * D * 4, &qbars[sl]);
         }
-        *reinterpret_cast<volatile int*>(&slot_item[sl]) = item;
-        __threadfence_block();
-        atomicExch(&slot_gen[sl], k);
+        atomicExch(&slot_word[sl], ((unsigned long long)(k + 1) << 32) | (unsigned int)item);
       } else {
-        while (*reinterpret_cast<volatile int*>(&slot_gen[sl]) != k) __nanosleep(32);
-        __threadfence_block();
-        item = *reinterpret_cast<volatile int*>(&slot_item[sl]);
+        unsigned long long w;
+        while (((w = atomicAdd(&slot_word[sl], 0ull)) >> 32) != (unsigned long long)(k + 1)) __nanosleep(32);
+        item = (int)(unsigned int)(w & 0xffffffffull);
       }
     }
     return __shfl_sync(0xffffffffu, item, 0);
@@ -241,8 +240,8 @@ paged_attention_kernel(const AttnParams p) {
 
   for (int ck = 0;; ++ck) {
     pump(ck);  // the producer has now visited item ck (or the stream has ended there)
-    const int f =
-        __shfl_sync(0xffffffffu, lane == 0 ? *reinterpret_cast<volatile int*>(&slot_item[ck % QB]) : 0, 0);
+    const int f = __shfl_sync(
+        0xffffffffu, lane == 0 ? (int)(unsigned int)(atomicAdd(&slot_word[ck % QB], 0ull) & 0xffffffffull) : 0, 0);
     if (f >= n_flat) break;
     const AttnUnit u = p.units[f / p.H_kv];
     const int hk = f % p.H_kv;

@@ -125,8 +125,9 @@ def test_error_paths():
 def test_long_prompt_decode_uses_split_k_and_matches_oracle():
     """A 3000-token prompt (uploaded through mirage_write_kv) makes the planner split
     the attention of the decode step; the result still matches oracle c4."""
+    from dataclasses import replace
     from paper_2507_11507_b200 import Context
-    shape = models.TOY_LLAMA
+    shape = replace(models.TOY_LLAMA, max_pos=8192)
     B, P = 2, 3000
     ctx = Context(harness.arena_for([(shape, 400)], B, 4096), B, 4096)
     mid = ctx.add_model(shape, harness.make_blob(shape, seed=6), 400)
