@@ -105,3 +105,15 @@ def test_kvgen_distribution_and_bf16():
         b = x.astype(np.float32).view(np.uint32)
         assert np.all(b & 0xFFFF == 0)
     assert not np.array_equal(k, kvgen.kv_values(2, 3, 2, 4, 128, 1, 2, 0, range(512)))
+
+
+def test_bf16_rounding_matches_torch():
+    """oracle.bf16.round_bf16 (round-half-even on 8 significant bits) vs torch's
+    fp32 -> bfloat16 conversion (library routine), including exact ties."""
+    from oracle.bf16 import round_bf16
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.standard_normal(20000) * 10 ** rng.uniform(-3, 3, 20000),
+                        np.array([1 + 2 ** -8, 1 + 3 * 2 ** -8, -(1 + 2 ** -8), 2 ** -7 * 1.5, 0.0])])
+    x32 = x.astype(np.float32)
+    ref = torch.from_numpy(x32).to(torch.bfloat16).double().numpy()
+    np.testing.assert_array_equal(round_bf16(x32.astype(np.float64)), ref)
