@@ -61,6 +61,11 @@ extern "C" {
 #define MIRAGE_BETA_DYNAMIC 3 /* smallest m with zero predicted stall (reading #6) */
 
 #define MIRAGE_FLAG_TIME_ATTN 1u /* init flag: time every attention launch with events */
+#define MIRAGE_FLAG_SLOT_TAGS 4u /* init flag: race detector for re-streaming. Behind every
+                                  * layer DMA the copy stream writes a 4-byte tag
+                                  * {0xA5, model, layer} into the slot's tag word; before
+                                  * the first kernel of a cycled layer a check kernel
+                                  * compares it (mirage_stats.slot_tag_errors).      */
 #define MIRAGE_FLAG_HOST_ONLY 2u /* init flag: no device; allocator/remap/table/query
                                   * calls only (the arena pointer is used for address
                                   * arithmetic, never dereferenced); device calls
@@ -284,6 +289,8 @@ typedef struct mirage_stats {
   uint64_t last_meta_h2d_bytes; /* step metadata uploaded by the last decode step    */
   int32_t last_attn_units;      /* attention work units of the last decode step      */
   int32_t last_split_blocks;    /* blocks per split-K partition of the last step     */
+  int64_t slot_tag_errors;      /* MIRAGE_FLAG_SLOT_TAGS: cycled layers that started
+                                 * before their weights had landed (must stay 0)     */
 } mirage_stats;
 
 int32_t mirage_query(mirage_ctx* ctx, int32_t model, mirage_stats* out);

@@ -21,6 +21,7 @@ BETA_1, BETA_2, BETA_DYNAMIC = 1, 2, 3
 BLOCK_TOKENS = 16
 FLAG_TIME_ATTN = 1
 FLAG_HOST_ONLY = 2
+FLAG_SLOT_TAGS = 4
 MAX_CYCLE = 256
 
 _NAMES = {ERR_CONFIG: "CONFIG", ERR_CAPACITY: "CAPACITY", ERR_RANGE: "RANGE", ERR_STATE: "STATE",
@@ -67,7 +68,8 @@ class Stats(C.Structure):
                 ("h2d_bytes", C.c_uint64), ("h2d_ms", C.c_double), ("last_step_ms", C.c_double),
                 ("steps", C.c_int64), ("attn_launches", C.c_int64), ("attn_ms", C.c_double),
                 ("attn_bytes", C.c_uint64), ("last_meta_h2d_bytes", C.c_uint64),
-                ("last_attn_units", C.c_int32), ("last_split_blocks", C.c_int32)]
+                ("last_attn_units", C.c_int32), ("last_split_blocks", C.c_int32),
+                ("slot_tag_errors", C.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "cycle"}

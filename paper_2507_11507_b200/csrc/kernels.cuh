@@ -63,6 +63,12 @@ cudaError_t launch_act(int family, int B, int f, const float* y, const __nv_bflo
 // argmax over each row of logits [B][V] (lowest index on ties).
 cudaError_t launch_argmax(int B, int V, const float* logits, int32_t* out, cudaStream_t s);
 
+// ---- slot tags (MIRAGE_FLAG_SLOT_TAGS): race detector for the copy engine ----
+// errors[0] += 1 and errors[1] = got if *tag != expected.
+cudaError_t launch_tag_check(const uint32_t* tag, uint32_t expected, uint32_t* errors, cudaStream_t s);
+// debug only: occupy the stream for ~ns nanoseconds (forces copy/compute races in tests)
+cudaError_t launch_spin(uint64_t ns, cudaStream_t s);
+
 // ---- KV hooks ----------------------------------------------------------------
 cudaError_t launch_fill_kv(uint64_t seed, int64_t seq_id, int L, int Hk, int D, int p0, int n,
                            const int32_t* table, const uint64_t* block_base, cudaStream_t s);

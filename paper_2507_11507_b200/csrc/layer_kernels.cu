@@ -362,6 +362,24 @@ __global__ void write_kv_kernel(int L, int Hk, int D, int p0, int n, const __nv_
   }
 }
 
+__global__ void tag_check_kernel(const uint32_t* tag, uint32_t expected, uint32_t* errors) {
+  const uint32_t got = *reinterpret_cast<const volatile uint32_t*>(tag);
+  if (got != expected) {
+    atomicAdd(errors, 1u);
+    errors[1] = got;
+  }
+}
+
+__global__ void spin_kernel(uint64_t ns) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 >= ns) break;
+  }
+}
+
 int grid_for(size_t n, int threads) {
   size_t g = (n + threads - 1) / threads;
   if (g > 148 * 16) g = 148 * 16;
@@ -408,6 +426,16 @@ cudaError_t launch_act(int family, int B, int f, const float* y, const __nv_bflo
 
 cudaError_t launch_argmax(int B, int V, const float* logits, int32_t* out, cudaStream_t s) {
   argmax_kernel<<<B, 1024, 0, s>>>(V, logits, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tag_check(const uint32_t* tag, uint32_t expected, uint32_t* errors, cudaStream_t s) {
+  tag_check_kernel<<<1, 1, 0, s>>>(tag, expected, errors);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spin(uint64_t ns, cudaStream_t s) {
+  spin_kernel<<<1, 1, 0, s>>>(ns);
   return cudaGetLastError();
 }
 

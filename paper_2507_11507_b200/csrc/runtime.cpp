@@ -172,6 +172,9 @@ struct Model {
   int64_t cyc_steps = 0;
   std::vector<int64_t> slot_log;  // rows of 5
   std::vector<cudaEvent_t> ready_ev, free_ev;
+  uint32_t* slot_tag = nullptr;   // device [MAX_CYCLE] tag of the layer each slot holds (SLOT_TAGS)
+  uint32_t* tag_err = nullptr;    // device [2] mismatch count, last bad tag
+  uint32_t* host_tags = nullptr;  // pinned [n_layers] tag values copied behind each layer DMA
   std::deque<CopyTiming> pending;
   uint64_t h2d_copies = 0, h2d_bytes = 0;
   double h2d_ms = 0;
@@ -476,8 +479,8 @@ void harvest_copy_times(Model* M) {
     M->h2d_ms += ms;
     M->h2d_bytes += t.bytes;
     M->h2d_copies += 1;
-    cudaEventDestroy(t.t0);
-    cudaEventDestroy(t.t1);
+    M->ev_pool.push_back(t.t0);  // recycled (no event create/destroy on the step path)
+    M->ev_pool.push_back(t.t1);
     M->pending.pop_front();
   }
   (void)cudaGetLastError();
@@ -723,6 +726,9 @@ void mirage_destroy(mirage_ctx* c) {
     if (M->st0) cudaEventDestroy(M->st0);
     if (M->st1) cudaEventDestroy(M->st1);
     if (M->bbase_dev) cudaFree(M->bbase_dev);
+    if (M->slot_tag) cudaFree(M->slot_tag);
+    if (M->tag_err) cudaFree(M->tag_err);
+    if (M->host_tags) cudaFreeHost(M->host_tags);
     for (auto& t : M->attn_pending) {
       cudaEventDestroy(t.t0);
       cudaEventDestroy(t.t1);
@@ -825,6 +831,14 @@ int32_t mirage_add_model(mirage_ctx* c, const mirage_model_cfg* mc, const void* 
     *model_id = M->id;
     return MIRAGE_OK;
   }
+  if (c->cfg.flags & MIRAGE_FLAG_SLOT_TAGS) {
+    CK(c, cudaMalloc(reinterpret_cast<void**>(&M->slot_tag), MIRAGE_MAX_CYCLE * 4));
+    CK(c, cudaMalloc(reinterpret_cast<void**>(&M->tag_err), 8));
+    CK(c, cudaMemsetAsync(M->tag_err, 0, 8, c->cs));
+    CK(c, cudaHostAlloc(reinterpret_cast<void**>(&M->host_tags), (size_t)s.n * 4, cudaHostAllocDefault));
+    for (int l = 0; l < s.n; ++l)
+      M->host_tags[l] = 0xA5000000u | ((uint32_t)(c->models.size() & 0xff) << 16) | (uint32_t)l;
+  }
   CK(c, cudaMemcpyAsync(M->w_dev, host_blob, host_bytes, cudaMemcpyHostToDevice, c->cs));
   if (native_kv_blocks)
     CK(c, cudaMemcpyAsync(M->bbase_dev, M->bbase_host.data(), native_kv_blocks * 8,
@@ -914,6 +928,9 @@ int32_t mirage_remap_layers(mirage_ctx* c, int32_t donor, int32_t recipient, con
     D->uses = 0;
     D->cyc_steps = 0;
     D->slot_log.clear();
+    if (D->slot_tag && !c->host_only)
+      for (int j = 0; j < beta; ++j)
+        CK(c, cudaMemcpyAsync(D->slot_tag + j, D->host_tags + cycle[j], 4, cudaMemcpyHostToDevice, c->cs));
     for (int j = 0; j < beta && !c->host_only; ++j) {
       cudaEvent_t a, b;
       CK(c, cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
@@ -1176,10 +1193,12 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
       wptr[l] = M->w_dev + (uint64_t)l * M->sz.S;
     }
   }
-  static const int dbg_nowait = getenv("MIRAGE_PREFETCH_DEBUG") && atoi(getenv("MIRAGE_PREFETCH_DEBUG")) == 2;
+  static const int dbg_nowait = getenv("MIRAGE_PREFETCH_DEBUG") && atoi(getenv("MIRAGE_PREFETCH_DEBUG")) >= 2;
   auto gate = [&](int l) -> int32_t {  // wait until layer l's weights are in its slot
     if (!dbg_nowait && l < s.n && use_of[l] >= beta && use_of[l] >= 0)
       CK(c, cudaStreamWaitEvent(cs, M->ready_ev[use_of[l] % beta], 0));
+    if (M->slot_tag && l < s.n && use_of[l] >= 0)  // SLOT_TAGS: the slot must hold layer l now
+      KL(c, mirage::launch_tag_check(M->slot_tag + use_of[l] % beta, M->host_tags[l], M->tag_err, cs));
     return MIRAGE_OK;
   };
   auto release = [&](int l) -> int32_t {  // layer l done reading its slot; prefetch use+beta
@@ -1192,15 +1211,16 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     const uint64_t nu = u + beta;
     const int nl = M->cycle[nu % m];
     CK(c, cudaStreamWaitEvent(c->xs, M->free_ev[slot], 0));
-    CopyTiming t{};
-    CK(c, cudaEventCreate(&t.t0));
-    CK(c, cudaEventCreate(&t.t1));
-    t.bytes = M->sz.S;
+    CopyTiming t{pool_event(M), pool_event(M), M->sz.S};
+    if (!t.t0 || !t.t1) return fail(c, MIRAGE_ERR_CUDA, "release: event pool");
     CK(c, cudaEventRecord(t.t0, c->xs));
     static const int dbg_mode = getenv("MIRAGE_PREFETCH_DEBUG") ? atoi(getenv("MIRAGE_PREFETCH_DEBUG")) : 0;
+    if (dbg_mode == 3) KL(c, mirage::launch_spin(20000000ull, c->xs));  // test hook: a slow link
     if (dbg_mode != 1)  // experiment hook: 1 = events only, no DMA
       CK(c, cudaMemcpyAsync(M->w_dev + (uint64_t)M->cycle[slot] * M->sz.S,
                             M->host + (uint64_t)nl * M->sz.S, M->sz.S, cudaMemcpyHostToDevice, c->xs));
+    if (M->slot_tag)  // same stream, after the weights: a correct tag proves they landed
+      CK(c, cudaMemcpyAsync(M->slot_tag + slot, M->host_tags + nl, 4, cudaMemcpyHostToDevice, c->xs));
     CK(c, cudaEventRecord(t.t1, c->xs));
     CK(c, cudaEventRecord(M->ready_ev[slot], c->xs));
     M->pending.push_back(t);
@@ -1452,6 +1472,11 @@ int32_t mirage_query(mirage_ctx* c, int32_t model, mirage_stats* o) {
   o->attn_ms = M->attn_ms;
   o->attn_bytes = M->attn_bytes;
   o->last_meta_h2d_bytes = M->last_meta;
+  if (M->tag_err) {
+    uint32_t e[2] = {0, 0};
+    CK(c, cudaMemcpy(e, M->tag_err, 8, cudaMemcpyDeviceToHost));
+    o->slot_tag_errors = e[0];
+  }
   o->last_attn_units = M->last_units;
   o->last_split_blocks = M->last_split;
   return MIRAGE_OK;
