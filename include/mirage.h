@@ -240,6 +240,14 @@ int32_t mirage_alloc_blocks(mirage_ctx* ctx, int32_t model, int64_t seq_id, int3
  * Errors: RANGE; DOUBLE_FREE for an unknown or already freed sequence. */
 int32_t mirage_free_blocks(mirage_ctx* ctx, int32_t model, int64_t seq_id);
 
+/* KV swapping baseline (Pie-style):
+ * swap_out copies seq_id's KV blocks (all layers, ceil(len/16) * BB bytes, in
+ * table order) to host_dst (pinned, >= that size) on the compute stream and
+ * frees the blocks; swap_in allocates blocks again and copies them back. The
+ * cached length is kept while swapped out. Errors: RANGE, STATE, NO_BLOCKS, CUDA. */
+int32_t mirage_swap_out(mirage_ctx* ctx, int32_t model, int64_t seq_id, void* host_dst, uint64_t bytes);
+int32_t mirage_swap_in(mirage_ctx* ctx, int32_t model, int64_t seq_id, const void* host_src);
+
 /* Copy of the host block table of seq_id. Errors: RANGE (unknown seq, cap too
  * small; *n_out still receives the length). */
 int32_t mirage_get_block_table(mirage_ctx* ctx, int32_t model, int64_t seq_id, int32_t* out,

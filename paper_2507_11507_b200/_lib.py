@@ -111,6 +111,8 @@ def _load():
         "mirage_region_count": (I32, [P, I32, pI32]),
         "mirage_region_info": (I32, [P, I32, I32, C.POINTER(Region)]),
         "mirage_unremap": (I32, [P, I32, I32]),
+        "mirage_swap_out": (I32, [P, I32, I64, P, U64]),
+        "mirage_swap_in": (I32, [P, I32, I64, P]),
         "mirage_host_unregister": (I32, [P]),
     }
     for name, (res, args) in sig.items():
@@ -128,7 +130,7 @@ EXPORTED = [
     "mirage_decode_step", "mirage_query", "mirage_slot_log", "mirage_sync", "mirage_attn_only",
     "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches", "mirage_nccl_unique_id",
     "mirage_host_register", "mirage_host_unregister", "mirage_region_count", "mirage_region_info",
-    "mirage_unremap"]
+    "mirage_unremap", "mirage_swap_out", "mirage_swap_in"]
 
 
 def model_cfg(shape):
@@ -299,6 +301,14 @@ class Context:
             self._check(LIB.mirage_region_info(self._ctx, model, i, C.byref(r)), "region_info")
             out.append(r.as_dict())
         return out
+
+    def swap_out(self, model, seq_id, host_buf):
+        """host_buf: pinned uint8 CPU tensor with room for the sequence's blocks."""
+        self._check(LIB.mirage_swap_out(self._ctx, model, int(seq_id), host_buf.data_ptr(), host_buf.numel()),
+                    "swap_out")
+
+    def swap_in(self, model, seq_id, host_buf):
+        self._check(LIB.mirage_swap_in(self._ctx, model, int(seq_id), host_buf.data_ptr()), "swap_in")
 
     def unremap(self, recipient, region):
         self._check(LIB.mirage_unremap(self._ctx, recipient, region), "unremap")

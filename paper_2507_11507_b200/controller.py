@@ -17,14 +17,22 @@ Host-side policy, as in the paper (a Python component of the serving system):
 
 Layer choice for an inactive donor (unstated by the paper, reading in
 DESIGN.md): highest remaining layer index first, ``layers_per_call`` at a time.
-Active-model self-remap (streaming) is delegated to an optional callback.
+
+Active-model self-remap (streaming), when no inactive model is left: with
+``self_remap="auto"`` the controller applies §5.3: with T_T the
+profiled per-layer transfer time (layer bytes / ``host_link_gbs``) and T_Compute
+the measured decode time per token, it remaps alpha = 1 more layer only if
+T_T * N <= T_Compute admits N >= 1 and the §5.4 planner finds a zero-stall
+cycle (mirage_plan, BETA_DYNAMIC); otherwise it declines (logged). A callable
+may be passed instead.
 """
 from . import _lib
 
 
 class RemappingController:
-    def __init__(self, ctx, models, active, cap=1.0, layers_per_call=1, self_remap=None):
+    def __init__(self, ctx, models, active, cap=1.0, layers_per_call=1, self_remap=None, host_link_gbs=None):
         """models: {model_id: (n_layers, priority or None)}; active: model id."""
+        self.link_gbs = host_link_gbs
         self.ctx = ctx
         self.info = {m: {"layers": n, "prio": p, "remapped": [], "act": 0} for m, (n, p) in models.items()}
         self.cap, self.per_call, self.self_remap = cap, layers_per_call, self_remap
@@ -52,6 +60,8 @@ class RemappingController:
     def remapping(self):
         cands = self._candidates()
         if not cands:
+            if self.self_remap == "auto":
+                return self._auto_self_remap()
             if self.self_remap is not None:
                 act = self.self_remap(self)
                 if act:
@@ -67,6 +77,26 @@ class RemappingController:
         gained, _ = self.ctx.remap_layers(m, self.active, layers, 0)
         i["remapped"].extend(layers)
         act = ("remap", m, tuple(layers), gained)
+        self.log.append(act)
+        return act
+
+    def _auto_self_remap(self):
+        st = self.ctx.query(self.active)
+        if st["m"] or not self.link_gbs or st["last_step_ms"] <= 0:
+            return None
+        n = self.info[self.active]["layers"]
+        tt = int(st["layer_bytes"] / (self.link_gbs * 1e9) * 1e9)      # T_T, ns
+        tcomp = int(st["last_step_ms"] * 1e6)                           # T_Compute per token, ns
+        if tcomp // max(tt, 1) < 1:                                      # §5.3: T_T * N <= T_Compute
+            self.log.append(("self_remap_declined", tt, tcomp))
+            return None
+        try:
+            cycle, m, beta = _lib.plan(n, 1, _lib.BETA_DYNAMIC, tt, max(1, tcomp // n))
+        except _lib.MirageError:
+            self.log.append(("self_remap_declined", tt, tcomp))
+            return None
+        gained, _ = self.ctx.remap_layers(self.active, self.active, cycle, beta)
+        act = ("self_remap", tuple(cycle), beta, gained)
         self.log.append(act)
         return act
 

@@ -156,6 +156,7 @@ struct Model {
   std::set<int32_t> free_ids;
   std::unordered_map<int64_t, std::vector<int32_t>> tables;
   std::unordered_map<int64_t, int32_t> lens;
+  std::unordered_map<int64_t, int32_t> swapped;  // seq -> cached length while swapped out
   std::vector<int32_t> loc_donor;  // -1 native
   std::vector<uint64_t> loc_off;
   std::vector<uint64_t> bbase_host;
@@ -1068,6 +1069,52 @@ int32_t mirage_free_blocks(mirage_ctx* c, int32_t model, int64_t seq_id) {
   for (int32_t id : it->second) M->free_ids.insert(id);
   M->tables.erase(it);
   M->lens.erase(seq_id);
+  return MIRAGE_OK;
+}
+
+// KV swapping (the Pie-style baseline MIRAGE is compared against, PAPER.md:82-86,
+// :212-221, :778-790): bidirectional KV movement over the host link.
+int32_t mirage_swap_out(mirage_ctx* c, int32_t model, int64_t seq_id, void* host_dst, uint64_t bytes) {
+  GUARD(c);
+  if (c->host_only) return fail(c, MIRAGE_ERR_STATE, "host-only context has no device");
+  Model* M = get_model(c, model);
+  if (!M || !host_dst) return fail(c, MIRAGE_ERR_RANGE, "swap_out: arguments");
+  auto it = M->tables.find(seq_id);
+  if (it == M->tables.end()) return fail(c, MIRAGE_ERR_RANGE, "swap_out: unknown seq %lld", (long long)seq_id);
+  const int32_t len = M->lens.count(seq_id) ? M->lens[seq_id] : 0;
+  const int nb = (len + kBlockTokens - 1) / kBlockTokens;
+  if ((uint64_t)nb * M->sz.BB > bytes) return fail(c, MIRAGE_ERR_RANGE, "swap_out: host buffer too small");
+  char* dst = reinterpret_cast<char*>(host_dst);
+  for (int j = 0; j < nb; ++j)  // ordered after every kernel that wrote the KV
+    CK(c, cudaMemcpyAsync(dst + (uint64_t)j * M->sz.BB, reinterpret_cast<const void*>(M->bbase_host[it->second[j]]),
+                          M->sz.BB, cudaMemcpyDeviceToHost, c->cs));
+  // the blocks are free for later work on the same stream (ordered after the copies)
+  for (int32_t id : it->second) M->free_ids.insert(id);
+  M->tables.erase(it);
+  M->lens.erase(seq_id);
+  M->swapped[seq_id] = len;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_swap_in(mirage_ctx* c, int32_t model, int64_t seq_id, const void* host_src) {
+  GUARD(c);
+  if (c->host_only) return fail(c, MIRAGE_ERR_STATE, "host-only context has no device");
+  Model* M = get_model(c, model);
+  if (!M || !host_src) return fail(c, MIRAGE_ERR_RANGE, "swap_in: arguments");
+  auto sw = M->swapped.find(seq_id);
+  if (sw == M->swapped.end() || M->tables.count(seq_id))
+    return fail(c, MIRAGE_ERR_STATE, "swap_in: seq %lld is not swapped out", (long long)seq_id);
+  const int32_t len = sw->second;
+  const int nb = (len + kBlockTokens - 1) / kBlockTokens;
+  int32_t short_n = 0;
+  if (int32_t e = mirage_alloc_blocks(c, model, seq_id, nb, nullptr, &short_n)) return e;
+  const auto& t = M->tables[seq_id];
+  const char* src = reinterpret_cast<const char*>(host_src);
+  for (int j = 0; j < nb; ++j)
+    CK(c, cudaMemcpyAsync(reinterpret_cast<void*>(M->bbase_host[t[j]]), src + (uint64_t)j * M->sz.BB, M->sz.BB,
+                          cudaMemcpyHostToDevice, c->cs));
+  M->lens[seq_id] = len;
+  M->swapped.erase(sw);
   return MIRAGE_OK;
 }
 

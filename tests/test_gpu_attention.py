@@ -153,3 +153,28 @@ def test_deterministic_repeat():
     ctx.attn_only(r, 0, list(range(6)), q, b)
     ctx.sync()
     assert torch.equal(a, b)
+
+
+def test_kv_swap_round_trip_bit_exact():
+    """mirage_swap_out / swap_in (Pie-style baseline, NEXT-3): after a round trip
+    through host memory into different blocks, attention is bit-identical."""
+    shape = small_shape(8, 2, 128)
+    ctx, r, _, _ = setup_ctx(shape, 200, donor_layers=0)
+    lens = [77, 300]
+    for i, L in enumerate(lens):
+        ctx.alloc_blocks(r, i, harness.blocks_for(L))
+        ctx.fill_kv(r, i, L, seed=i)
+    q = workload.queries(2, 8, 128, seed=5).cuda()
+    a = torch.empty((2, 8, 128), device="cuda")
+    b = torch.empty_like(a)
+    ctx.attn_only(r, 1, [0, 1], q, a)
+    bb = shape.n_layers * shape.n_kv_heads * 2 * 16 * shape.head_dim * 2
+    buf = torch.empty(harness.blocks_for(300) * bb, dtype=torch.uint8, pin_memory=True)
+    before = ctx.block_table(r, 1)
+    ctx.swap_out(r, 1, buf)
+    ctx.alloc_blocks(r, 7, 5)                 # take some of the freed blocks: new placement
+    ctx.swap_in(r, 1, buf)
+    assert ctx.block_table(r, 1) != before and ctx.seq_len(r, 1) == 300
+    ctx.attn_only(r, 1, [0, 1], q, b)
+    ctx.sync()
+    assert torch.equal(a, b)

@@ -34,8 +34,39 @@ def pct(xs, p):
     return s[max(0, int(np.ceil(p / 100 * len(s))) - 1)] if s else None
 
 
-def serve(ctx, ctl, mid, shape, arrivals, prompts, outs, max_batch, revert_every=None, headroom=0, tag=""):
-    """Closed decode loop. arrivals[t] = number of new requests at step t."""
+class HostPool:
+    """First-fit extents of one pinned host buffer (KV swap space)."""
+
+    def __init__(self, nbytes):
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        self.free = [(0, nbytes)]
+
+    def get(self, n):
+        for i, (o, sz) in enumerate(self.free):
+            if sz >= n:
+                self.free[i] = (o + n, sz - n)
+                return o
+        return None
+
+    def put(self, o, n):
+        self.free.append((o, n))
+        self.free.sort()
+        merged = []
+        for a, b in self.free:
+            if merged and merged[-1][0] + merged[-1][1] == a:
+                merged[-1] = (merged[-1][0], merged[-1][1] + b)
+            elif b:
+                merged.append((a, b))
+        self.free = merged
+
+
+def serve(ctx, ctl, mid, shape, arrivals, prompts, outs, max_batch, revert_every=None, headroom=0, tag="",
+          on_exhaust="recompute", pool=None):
+    """Closed decode loop. arrivals[t] = number of new requests at step t.
+    on_exhaust: 'recompute' preempts the newest sequence (re-queued, vLLM-style);
+    'swap' moves its KV to host memory and back when blocks free up (Pie-style)."""
+    _, _, BB = _lib.model_sizes(shape)
+    swapped = []   # (sid, offset, nbytes)
     queue, running, pos, left = [], [], {}, {}
     nxt, step_ms, waits, t0s = 0, [], [], {}
     preempted = [0]
@@ -45,13 +76,27 @@ def serve(ctx, ctl, mid, shape, arrivals, prompts, outs, max_batch, revert_every
     t = 0
     total_steps = len(arrivals)
     tokens = 0
-    while t < total_steps or running or queue:
+    while t < total_steps or running or queue or swapped:
         if t < total_steps:
             for _ in range(arrivals[t]):
                 queue.append((nxt, t))
                 nxt += 1
+        # swapped-out sequences come back first (Pie-style), then new admissions
+        while swapped and len(running) < max_batch:
+            sid, off, nb = swapped[0]
+            try:
+                ctx.swap_in(mid, sid, pool.buf[off:off + nb])
+            except _lib.MirageError as e:
+                if e.code != _lib.ERR_NO_BLOCKS:
+                    raise
+                break
+            ctx.sync()
+            pool.put(off, nb)
+            swapped.pop(0)
+            running.append(sid)
+            held[sid] = harness.blocks_for(pos[sid])
         # admit in FIFO order while blocks allow (controller may remap on shortfall)
-        while queue and len(running) < max_batch:
+        while queue and len(running) < max_batch and not swapped:
             sid, ta = queue[0]
             P = int(prompts[sid % len(prompts)])
             try:
@@ -84,9 +129,15 @@ def serve(ctx, ctl, mid, shape, arrivals, prompts, outs, max_batch, revert_every
                         raise
                     victim = running[-1]
                     running.remove(victim)
-                    (ctl.free(victim) if ctl else ctx.free_blocks(mid, victim))
-                    queue.insert(0, (victim, t))
                     preempted[0] += 1
+                    nbytes = harness.blocks_for(pos[victim]) * BB
+                    off = pool.get(nbytes) if (on_exhaust == "swap" and pool) else None
+                    if off is not None:
+                        ctx.swap_out(mid, victim, pool.buf[off:off + nbytes])
+                        swapped.append((victim, off, nbytes))
+                    else:
+                        (ctl.free(victim) if ctl else ctx.free_blocks(mid, victim))
+                        queue.insert(0, (victim, t))
                     if victim == sid:
                         break
         batch = list(running)
@@ -187,6 +238,62 @@ def e2(args):
     return res
 
 
+def h2d_gbs(n=1 << 30):
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    best = 1e9
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d.copy_(h, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return n / best / 1e6
+
+
+def e3(args):
+    """MIRAGE self-remap vs Pie-style KV swapping vs vLLM-style recompute on one
+    OPT-13B (P:771-790 compares against Pie on a single model)."""
+    shape = models.OPT_13B
+    native = 300
+    prompts, outs = workload.sharegpt_trace(2000, seed=6)
+    rng = np.random.default_rng(3)
+    arr = [rng.poisson(0.6 if t < 100 else 0.01) for t in range(args.steps * 5)]
+    blob = harness.make_blob(shape, 0, 0, gen_device="cuda")
+    pool = HostPool(48 << 30)
+
+    def self_remap(ctl):
+        if ctl.ctx.query(ctl.active)["m"]:
+            return None
+        cycle, m, beta = _lib.plan(shape.n_layers, 1, _lib.BETA_1, 0, 1)
+        gained, _ = ctl.ctx.remap_layers(ctl.active, ctl.active, cycle, beta)
+        return ("cycle", tuple(cycle), gained)
+
+    link = h2d_gbs()
+    res = {"host_link_gbs": link}
+    for mode in ("mirage_s53", "mirage_forced", "kvswap", "recompute"):
+        ctx = _lib.Context(harness.arena_for([(shape, native)], 256, 2048), 256, 2048)
+        mid = ctx.add_model(shape, blob, native)
+        ctl = None
+        if mode == "mirage_s53":     # §5.3-gated self-remap (declines when T_T > T_Compute)
+            ctl = RemappingController(ctx, {mid: (shape.n_layers, None)}, active=mid, self_remap="auto",
+                                      host_link_gbs=link)
+        elif mode == "mirage_forced":  # alpha = 1 regardless of §5.3
+            ctl = RemappingController(ctx, {mid: (shape.n_layers, None)}, active=mid, self_remap=self_remap)
+        st, waits, tokens = serve(ctx, ctl, mid, shape, arr, prompts, outs, 256,
+                                  revert_every=10 if ctl else None, headroom=0,
+                                  on_exhaust="swap" if mode == "kvswap" else "recompute", pool=pool)
+        ms = [x for x, _ in st]
+        res[mode] = {"tok_s": tokens / (sum(ms) / 1e3), "p50_tbt_ms": pct(ms, 50), "p99_tbt_ms": pct(ms, 99),
+                     "mean_wait_steps": statistics.mean(waits) if waits else 0, "preempt_or_swap": serve.preempted,
+                     "steps": len(ms), "controller": sorted({a[0] for a in ctl.log}) if ctl else None}
+        ctx.close()
+        del ctx
+        torch.cuda.empty_cache()
+    return res
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=600)
@@ -197,4 +304,6 @@ if __name__ == "__main__":
         out["e1_temporal_sharing"] = e1(a)
     if "e2" in a.exp:
         out["e2_dynamic_reversion"] = e2(a)
+    if "e3" in a.exp:
+        out["e3_vs_kv_swap"] = e3(a)
     print(json.dumps(out, indent=1, default=str))
