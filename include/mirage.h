@@ -66,6 +66,10 @@ extern "C" {
                                   * {0xA5, model, layer} into the slot's tag word; before
                                   * the first kernel of a cycled layer a check kernel
                                   * compares it (mirage_stats.slot_tag_errors).      */
+#define MIRAGE_FLAG_CUDA_GRAPHS 8u /* init flag: capture the decode-step body (embed .. argmax)
+                                    * into one CUDA graph per batch size for models without
+                                    * a streaming cycle (captured on the second step of a
+                                    * size; ignored with MIRAGE_FLAG_TIME_ATTN)          */
 #define MIRAGE_FLAG_HOST_ONLY 2u /* init flag: no device; allocator/remap/table/query
                                   * calls only (the arena pointer is used for address
                                   * arithmetic, never dereferenced); device calls

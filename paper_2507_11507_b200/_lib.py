@@ -22,6 +22,7 @@ BLOCK_TOKENS = 16
 FLAG_TIME_ATTN = 1
 FLAG_HOST_ONLY = 2
 FLAG_SLOT_TAGS = 4
+FLAG_CUDA_GRAPHS = 8
 MAX_CYCLE = 256
 
 _NAMES = {ERR_CONFIG: "CONFIG", ERR_CAPACITY: "CAPACITY", ERR_RANGE: "RANGE", ERR_STATE: "STATE",

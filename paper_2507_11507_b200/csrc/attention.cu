@@ -140,7 +140,7 @@ paged_attention_kernel(const AttnParams p) {
   const int warp = threadIdx.x >> 5;
   const int gq = lane >> 2;  // mma group id (row / column index)
   const int tq = lane & 3;   // thread in group
-  const int n_flat = p.n_units * p.H_kv;  // work item f = unit * H_kv + kv head
+  const int n_flat = (p.n_units_dev ? *p.n_units_dev : p.n_units) * p.H_kv;  // item f = unit * H_kv + kv head
   uint8_t* ring = smem + (size_t)warp * NS * 2 * TILE;
   // q staging (dynamic smem after the rings): [QB][G*D] fp32, one copy per CTA item
   float(*qbuf)[G * D] = reinterpret_cast<float(*)[G * D]>(smem + (size_t)kWarps * NS * 2 * TILE);

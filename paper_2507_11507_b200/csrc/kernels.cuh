@@ -23,7 +23,8 @@ struct AttnParams {
   const uint64_t* addrs;       // per-step block base addresses (host-resolved table -> block_base)
   uint64_t layer_off;          // layer * H_kv * 2 * 16 * D * 2 bytes
   const AttnUnit* units;       // [n_units], longest first
-  int32_t n_units;
+  int32_t n_units;             // host count (sizes the grid)
+  const int32_t* n_units_dev;  // if set, the count is read here (CUDA-graph replays)
   int32_t H, H_kv, D;
   float scale_log2;            // log2(e) / sqrt(D)
   float* partial;              // [(pbase + split) * H + h][D + 2]

@@ -201,6 +201,13 @@ struct Model {
   uint64_t attn_bytes = 0;
   uint64_t last_meta = 0;
   int32_t last_units = 0, last_split = 0;
+  // ---- CUDA graphs of the decode step (MIRAGE_FLAG_CUDA_GRAPHS, models without a cycle) ----
+  struct Graph {
+    cudaGraphExec_t exec;
+    int64_t kernels;
+  };
+  std::map<int, Graph> graphs;  // by batch size
+  std::set<int> graph_seen;     // batch sizes run once eagerly (plans/autotune done)
   // ---- step timing ----
   cudaEvent_t st0 = nullptr, st1 = nullptr;
   bool step_timed = false;
@@ -378,6 +385,7 @@ Model* get_model(mirage_ctx* c, int32_t id) {
 // need no dependent table lookups. The KV hooks reuse the address region for a
 // plain int32 table row.
 struct MetaView {
+  int32_t* hdr;  // [4]: n_units, ...
   int32_t *tokens, *pos, *len, *seq_off;
   mirage::AttnUnit* units;
   uint64_t* addrs;
@@ -388,6 +396,7 @@ MetaView meta_view(mirage_ctx* c, char* base) {
   MetaView v;
   const int Bm = c->cfg.max_batch;
   char* p = base;
+  v.hdr = reinterpret_cast<int32_t*>(p); p += 16;
   v.tokens = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
   v.pos = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
   v.len = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
@@ -400,7 +409,7 @@ MetaView meta_view(mirage_ctx* c, char* base) {
 
 size_t meta_size(mirage_ctx* c) {
   const int Bm = c->cfg.max_batch;
-  return 4 * align_up((uint64_t)Bm * 4, 16) + align_up((uint64_t)c->max_units * sizeof(mirage::AttnUnit), 16) +
+  return 16 + 4 * align_up((uint64_t)Bm * 4, 16) + align_up((uint64_t)c->max_units * sizeof(mirage::AttnUnit), 16) +
          (uint64_t)Bm * c->max_blk * 8;
 }
 
@@ -735,6 +744,7 @@ void mirage_destroy(mirage_ctx* c) {
       cudaEventDestroy(t.t1);
     }
     for (auto e : M->ev_pool) cudaEventDestroy(e);
+    for (auto& g : M->graphs) cudaGraphExecDestroy(g.second.exec);
     delete M;
   }
   for (int i = 0; i < 2; ++i) {
@@ -1210,6 +1220,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
                                   mirage::attention_grid_ctas(s.H, s.Hk, s.D), mirage::attention_cta_warps(s.Hk),
                                   0, hv.units, c->max_units, &split_blocks);
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "step: too many attention units");
+  hv.hdr[0] = n_units;
   const size_t tbl_bytes = (size_t)n_addr * 8;
   const size_t head = reinterpret_cast<char*>(hv.addrs) - host;
   cudaStream_t cs = c->cs;
@@ -1274,6 +1285,28 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     return MIRAGE_OK;
   };
 
+  // CUDA graph of the step body (embed ... argmax): models without a streaming
+  // cycle, one graph per batch size, captured on the second step of that size
+  // (the first runs eagerly so cuBLASLt plans/autotuning happen outside capture)
+  const bool graphable = (c->cfg.flags & MIRAGE_FLAG_CUDA_GRAPHS) && m == 0 &&
+                         !(c->cfg.flags & MIRAGE_FLAG_TIME_ATTN);
+  bool body_done = false, capturing = false;
+  int64_t l0 = 0;
+  if (graphable) {
+    auto g = M->graphs.find(B);
+    if (g != M->graphs.end()) {
+      CK(c, cudaGraphLaunch(g->second.exec, cs));
+      c->launches += g->second.kernels;
+      body_done = true;
+    } else if (M->graph_seen.count(B)) {
+      CK(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      capturing = true;
+      l0 = c->launches;
+    } else {
+      M->graph_seen.insert(B);
+    }
+  }
+  if (!body_done) {
   // embedding + layer 0's first norm
   if (int32_t e = gate(0)) return e;
   {
@@ -1286,6 +1319,11 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   ap.addrs = dv.addrs;
   ap.units = dv.units;
   ap.n_units = n_units;
+  ap.n_units_dev = nullptr;
+  if (capturing) {  // replays keep the full persistent grid; the unit count comes from the metadata
+    ap.n_units = c->max_units;
+    ap.n_units_dev = dv.hdr;
+  }
   ap.H = H;
   ap.H_kv = Hk;
   ap.D = D;
@@ -1359,6 +1397,16 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   // LM head + argmax
   if (int32_t e = gemm_lt(c, B, s.V, d, gw.lm_head, M->x, M->y, 0, nullptr, 0)) return e;
   KL(c, mirage::launch_argmax(B, s.V, M->y, M->argmax, cs));
+  if (capturing) {
+    cudaGraph_t graph;
+    CK(c, cudaStreamEndCapture(cs, &graph));
+    cudaGraphExec_t exec;
+    CK(c, cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    M->graphs[B] = Model::Graph{exec, c->launches - l0};
+    CK(c, cudaGraphLaunch(exec, cs));
+  }
+  }  // !body_done
   if (hidden_out)
     CK(c, cudaMemcpyAsync(hidden_out, M->x, (size_t)B * d * 2, cudaMemcpyDeviceToDevice, cs));
   if (argmax_out) CK(c, cudaMemcpyAsync(argmax_out, M->argmax, (size_t)B * 4, cudaMemcpyDeviceToHost, cs));
