@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--alpha", type=int, default=1)
     ap.add_argument("--beta", type=int, default=0, help="0 = config default (c2: 1, c4: 2)")
     ap.add_argument("--placement", default="uniform", choices=["uniform", "last"])
+    ap.add_argument("--weight-source", default="host", choices=["host", "device"],
+                    help="re-streaming tier: pinned host copy (paper) or a device-resident copy "
+                         "(NEXT-2: a peer B200's HBM in deployment; this GPU here)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-resident-arm", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -292,6 +295,9 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
     arena = harness.arena_for([(sh, nat) for sh, _, nat in tenants], B, max_ctx)
     ctx = _lib.Context(arena, B, max_ctx, device=dev.index, flags=_lib.FLAG_TIME_ATTN)
     mids = [ctx.add_model(sh, blobs[(sh.name, seed)], nat) for sh, seed, nat in tenants]
+    if args.weight_source == "device" and remaps:
+        dev_copy = blobs[(tenants[0][0].name, tenants[0][1])].to(dev)
+        ctx.set_weight_source(mids[0], dev_copy)
     for r in remaps:
         if r[0] == "inactive":
             ctx.set_active(mids[r[1]], False)

@@ -177,6 +177,15 @@ const char* mirage_last_error(const mirage_ctx* ctx);
 int32_t mirage_add_model(mirage_ctx* ctx, const mirage_model_cfg* m, const void* host_blob,
                          uint64_t host_bytes, int64_t native_kv_blocks, int32_t* model_id);
 
+/* Re-streaming source tier: point the model's authoritative
+ * weight copy -- used for cycled-layer re-streaming and reversion reloads -- at
+ * `src` (same layout as the blob): pinned host memory (the default
+ * fn.), or device memory, e.g. a peer B200's HBM reached over NVLink 5 (peer
+ * access is enabled here), which restores the GH200-like T_T/T_c regime
+ * (P:60, :883-890). Caller-owned, must outlive the ctx. Errors: RANGE, CONFIG
+ * (size mismatch, pageable memory, no peer access), CUDA. */
+int32_t mirage_set_weight_source(mirage_ctx* ctx, int32_t model, const void* src, uint64_t bytes);
+
 /* Pure planner (§5.3-5.4, Eqs. 1-5). Writes the
  * cycle C (ascending, m entries; cycle_out capacity >= n_layers), m and beta.
  * Slot holders are C[0..beta), reclaimed layers R = C[beta..m).

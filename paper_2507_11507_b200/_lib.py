@@ -114,6 +114,7 @@ def _load():
         "mirage_unremap": (I32, [P, I32, I32]),
         "mirage_swap_out": (I32, [P, I32, I64, P, U64]),
         "mirage_swap_in": (I32, [P, I32, I64, P]),
+        "mirage_set_weight_source": (I32, [P, I32, P, U64]),
         "mirage_host_unregister": (I32, [P]),
     }
     for name, (res, args) in sig.items():
@@ -131,7 +132,7 @@ EXPORTED = [
     "mirage_decode_step", "mirage_query", "mirage_slot_log", "mirage_sync", "mirage_attn_only",
     "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches", "mirage_nccl_unique_id",
     "mirage_host_register", "mirage_host_unregister", "mirage_region_count", "mirage_region_info",
-    "mirage_unremap", "mirage_swap_out", "mirage_swap_in"]
+    "mirage_unremap", "mirage_swap_out", "mirage_swap_in", "mirage_set_weight_source"]
 
 
 def model_cfg(shape):
@@ -302,6 +303,11 @@ class Context:
             self._check(LIB.mirage_region_info(self._ctx, model, i, C.byref(r)), "region_info")
             out.append(r.as_dict())
         return out
+
+    def set_weight_source(self, model, src):
+        """src: a uint8 tensor (pinned CPU or CUDA, this or a peer GPU) holding the blob."""
+        self._blobs.append(src)
+        self._check(LIB.mirage_set_weight_source(self._ctx, model, src.data_ptr(), src.numel()), "set_weight_source")
 
     def swap_out(self, model, seq_id, host_buf):
         """host_buf: pinned uint8 CPU tensor with room for the sequence's blocks."""

@@ -864,6 +864,34 @@ int32_t mirage_add_model(mirage_ctx* c, const mirage_model_cfg* mc, const void* 
   return MIRAGE_OK;
 }
 
+int32_t mirage_set_weight_source(mirage_ctx* c, int32_t model, const void* src, uint64_t bytes) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || !src) return fail(c, MIRAGE_ERR_RANGE, "weight_source: arguments");
+  if (bytes != (uint64_t)M->shp.n * M->sz.S + M->sz.G)
+    return fail(c, MIRAGE_ERR_CONFIG, "weight_source: %llu bytes, blob is %llu", (unsigned long long)bytes,
+                (unsigned long long)((uint64_t)M->shp.n * M->sz.S + M->sz.G));
+  if (!c->host_only) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, src) != cudaSuccess ||
+        (a.type != cudaMemoryTypeHost && a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)) {
+      (void)cudaGetLastError();
+      return fail(c, MIRAGE_ERR_CONFIG, "weight_source: must be pinned host or device memory");
+    }
+    if (a.type == cudaMemoryTypeDevice && a.device != c->cfg.device) {  // a peer GPU's HBM over NVLink
+      cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        (void)cudaGetLastError();
+        return fail(c, MIRAGE_ERR_CONFIG, "weight_source: no peer access to device %d", a.device);
+      }
+      (void)cudaGetLastError();
+    }
+    CK(c, cudaStreamSynchronize(c->xs));  // no copy from the old source is in flight
+  }
+  M->host = reinterpret_cast<const char*>(src);
+  return MIRAGE_OK;
+}
+
 int32_t mirage_set_active(mirage_ctx* c, int32_t model, int32_t active) {
   GUARD(c);
   Model* M = get_model(c, model);
@@ -1029,7 +1057,7 @@ int32_t mirage_unremap(mirage_ctx* c, int32_t recipient, int32_t region) {
     // stream-ordered after every kernel that used these bytes as KV
     for (int32_t l : layers)
       CK(c, cudaMemcpyAsync(D->w_dev + (uint64_t)l * D->sz.S, D->host + (uint64_t)l * D->sz.S, D->sz.S,
-                            cudaMemcpyHostToDevice, c->cs));
+                            cudaMemcpyDefault, c->cs));
   }
   for (int32_t l : layers) D->layer_state[l] = RESIDENT;
   if (was_cycle) {
@@ -1276,7 +1304,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     if (dbg_mode == 3) KL(c, mirage::launch_spin(20000000ull, c->xs));  // test hook: a slow link
     if (dbg_mode != 1)  // experiment hook: 1 = events only, no DMA
       CK(c, cudaMemcpyAsync(M->w_dev + (uint64_t)M->cycle[slot] * M->sz.S,
-                            M->host + (uint64_t)nl * M->sz.S, M->sz.S, cudaMemcpyHostToDevice, c->xs));
+                            M->host + (uint64_t)nl * M->sz.S, M->sz.S, cudaMemcpyDefault, c->xs));
     if (M->slot_tag)  // same stream, after the weights: a correct tag proves they landed
       CK(c, cudaMemcpyAsync(M->slot_tag + slot, M->host_tags + nl, 4, cudaMemcpyHostToDevice, c->xs));
     CK(c, cudaEventRecord(t.t1, c->xs));

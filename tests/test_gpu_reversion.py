@@ -56,3 +56,32 @@ def test_cycle_and_inactive_donor_reversion():
     ctx.set_active(ma, False)
     ctx.set_active(md, True)                                  # donor runs on its restored weights
     decode_and_check(ctx, md, d, 8, [0, 1, 2], 20)
+
+
+def test_device_weight_source_tier_is_bit_identical():
+    """NEXT-2 mechanism: re-streaming from a device-resident master copy (a peer
+    B200's HBM in deployment; the same GPU here) gives bit-identical steps."""
+    from paper_2507_11507_b200 import Context
+    shape = models.TOY
+    outs = []
+    for src in ("host", "device"):
+        ctx = Context(harness.arena_for([(shape, 16)], 4, 128), 4, 128)
+        blob = harness.make_blob(shape, seed=9)
+        mid = ctx.add_model(shape, blob, 16)
+        if src == "device":
+            ctx.set_weight_source(mid, blob.cuda())
+        ctx.remap_layers(mid, mid, [0, 1], 1)
+        hid = torch.empty((4, shape.d_model), dtype=torch.bfloat16, device="cuda")
+        o = []
+        for t in range(20):
+            if t % 16 == 0:
+                for s in range(4):
+                    ctx.alloc_blocks(mid, s, 1)
+            ctx.decode_step(mid, [0, 1, 2, 3], [workload.teacher_tokens(s, t, shape.vocab) for s in range(4)],
+                            [t] * 4, hidden_out=hid)
+            ctx.sync()
+            o.append(hid.float().cpu().numpy().copy())
+        outs.append(o)
+        assert ctx.query(mid)["h2d_copies"] >= 30
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
