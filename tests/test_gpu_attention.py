@@ -178,3 +178,34 @@ def test_kv_swap_round_trip_bit_exact():
     ctx.attn_only(r, 1, [0, 1], q, b)
     ctx.sync()
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("H,Hk,D", [(4, 4, 64), (16, 2, 128)])
+def test_edges_block_boundaries_max_batch_max_ctx(H, Hk, D):
+    """Block-boundary lengths (16, 32, 33), a full batch (max_batch), a sequence at
+    max_ctx, forced splits of 1 block and ragged tails, vs oracle c3."""
+    from paper_2507_11507_b200 import Context
+    shape = small_shape(H, Hk, D, L=1)
+    max_ctx, B = 1024, 12
+    lens = [16, 32, 33, 1, 2, 1024, 17, 48, 49, 160, 511, 512]
+    need = sum(harness.blocks_for(x) for x in lens)
+    ctx = Context(harness.arena_for([(shape, need)], B, max_ctx), B, max_ctx)
+    r = ctx.add_model(shape, harness.make_blob(shape, seed=2), need)
+    for i, L in enumerate(lens):
+        ctx.alloc_blocks(r, i, harness.blocks_for(L))
+        ctx.fill_kv(r, i, L, seed=40 + i)
+    q = workload.queries(B, H, D, seed=12)
+    for split in (0, 16, 64):
+        out = torch.empty((B, H, D), dtype=torch.float32, device="cuda")
+        ctx.attn_only(r, 0, list(range(B)), q.cuda(), out, split_tokens=split)
+        ctx.sync()
+        o = out.cpu().double().numpy()
+        for i, L in enumerate(lens):
+            for h in range(0, H, max(1, H // 4)):
+                K = kvgen.kv_values(40 + i, i, 1, Hk, D, 0, h // (H // Hk), 0, range(L))
+                V = kvgen.kv_values(40 + i, i, 1, Hk, D, 0, h // (H // Hk), 1, range(L))
+                ref = OAT.attend(q[i, h].double().numpy(), K, V)
+                assert np.abs(o[i, h] - ref).max() <= TOL, (split, i, h)
+    from paper_2507_11507_b200 import MirageError
+    with pytest.raises(MirageError):
+        ctx.alloc_blocks(r, 5, 1)            # seq 5 already holds max_ctx tokens of blocks
