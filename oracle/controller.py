@@ -23,13 +23,14 @@ from .allocator import NoBlocks
 
 
 class Controller:
-    def __init__(self, alloc, models, active, cap=1.0, layers_per_call=1):
+    def __init__(self, alloc, models, active, cap=1.0, layers_per_call=1, order="mru"):
         self.al = alloc
         self.n = {m: v[0] for m, v in models.items()}
         self.prio = {m: (v[1] if v[1] is not None else 0) for m, v in models.items()}
         self.taken = {m: set() for m in models}
         self.last_act = {m: 0 for m in models}
         self.cap, self.k = cap, layers_per_call
+        self.sign = -1 if order == "mru" else 1   # MRU: most recently activated first
         self.t = 0
         self.log = []
         self.active = None
@@ -43,7 +44,7 @@ class Controller:
         for m in sorted(self.n):
             if m == self.active or len(self.taken[m]) >= self.limit(m):
                 continue
-            key = (self.prio[m], -self.last_act[m], m)
+            key = (self.prio[m], self.sign * self.last_act[m], m)
             if best is None or key < best[0]:
                 best = (key, m)
         if best is None:

@@ -30,9 +30,12 @@ from . import _lib
 
 
 class RemappingController:
-    def __init__(self, ctx, models, active, cap=1.0, layers_per_call=1, self_remap=None, host_link_gbs=None):
-        """models: {model_id: (n_layers, priority or None)}; active: model id."""
+    def __init__(self, ctx, models, active, cap=1.0, layers_per_call=1, self_remap=None, host_link_gbs=None,
+                 order="mru"):
+        """models: {model_id: (n_layers, priority or None)}; active: model id;
+        order: "mru" (the paper's default) or "lru" (the ablation)."""
         self.link_gbs = host_link_gbs
+        self.order = order
         self.ctx = ctx
         self.info = {m: {"layers": n, "prio": p, "remapped": [], "act": 0} for m, (n, p) in models.items()}
         self.cap, self.per_call, self.self_remap = cap, layers_per_call, self_remap
@@ -53,7 +56,8 @@ class RemappingController:
             if len(i["remapped"]) >= int(self.cap * i["layers"] + 1e-9):
                 continue
             prio = i["prio"] if i["prio"] is not None else 0
-            out.append((prio, -i["act"], m))      # lowest priority, then most recently activated
+            rec = -i["act"] if self.order == "mru" else i["act"]
+            out.append((prio, rec, m))            # lowest priority, then most (MRU) / least (LRU) recent
         return [m for _, _, m in sorted(out)]
 
     # ---- Alg. 1 remapping() -----------------------------------------------------

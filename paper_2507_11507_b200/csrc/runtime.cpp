@@ -936,8 +936,21 @@ int32_t mirage_remap_layers(mirage_ctx* c, int32_t donor, int32_t recipient, con
   }
   int64_t total_new = 0;
   for (auto& r : runs) total_new += (int64_t)((uint64_t)r.second * D->sz.S / R->sz.BB);
-  if ((int64_t)R->next_id + total_new > R->bbase_cap)
-    return fail(c, MIRAGE_ERR_CAPACITY, "remap: block table capacity %lld exceeded", (long long)R->bbase_cap);
+  if ((int64_t)R->next_id + total_new > R->bbase_cap) {  // grow the device block_base mirror
+    if (c->host_only) {
+      R->bbase_cap = std::max<int64_t>(2 * R->bbase_cap, R->next_id + total_new);
+    } else {
+      const int64_t cap = std::max<int64_t>(2 * R->bbase_cap, R->next_id + total_new + 16);
+      uint64_t* nb = nullptr;
+      CK(c, cudaStreamSynchronize(c->cs));
+      CK(c, cudaMalloc(reinterpret_cast<void**>(&nb), cap * 8));
+      if (R->next_id)
+        CK(c, cudaMemcpy(nb, R->bbase_host.data(), (size_t)R->next_id * 8, cudaMemcpyHostToDevice));
+      cudaFree(R->bbase_dev);
+      R->bbase_dev = nb;
+      R->bbase_cap = cap;
+    }
+  }
   const int32_t first_new = R->next_id;
   for (auto& r : runs) {
     const uint64_t off = (uint64_t)r.first * D->sz.S;

@@ -34,4 +34,11 @@ LLAMA2_7B = ModelShape("llama-2-7b", LLAMA, 32, 4096, 32, 32, 128, 11008, 32000,
 LLAMA3_8B = ModelShape("llama-3-8b", LLAMA, 32, 4096, 32, 8, 128, 14336, 128256, 32768, 1e-5, 500000.0)
 LLAMA_70B = ModelShape("llama-70b", LLAMA, 80, 8192, 64, 8, 128, 28672, 128256, 8192, 1e-5, 500000.0)
 
-PRESETS = {m.name: m for m in (TOY, TOY_LLAMA, OPT_13B, LLAMA2_7B, LLAMA3_8B, LLAMA_70B)}
+# PAPER.md Table 1 combinations: C1 = OPT-13b, Llama-2-13b, Llama-3-8b;
+# C2 = OPT-30b, OPT-6.7b (public configs)
+LLAMA2_13B = ModelShape("llama-2-13b", LLAMA, 40, 5120, 40, 40, 128, 13824, 32000, 4096, 1e-5, 10000.0)
+OPT_30B = ModelShape("opt-30b", OPT, 48, 7168, 56, 56, 128, 28672, 50272, 2048)
+OPT_6_7B = ModelShape("opt-6.7b", OPT, 32, 4096, 32, 32, 128, 16384, 50272, 2048)
+
+PRESETS = {m.name: m for m in (TOY, TOY_LLAMA, OPT_13B, LLAMA2_7B, LLAMA3_8B, LLAMA_70B, LLAMA2_13B, OPT_30B,
+                               OPT_6_7B)}

@@ -116,18 +116,27 @@ def replay(ctl, ev, errors):
             ctl.log.append(("fail",) + tuple(e))
 
 
-@pytest.mark.parametrize("seed,prios", [(1, [3, 1, 2]), (2, [None, None, None]), (3, [1, 1, 5])])
-def test_product_controller_matches_oracle(seed, prios):
+def test_lru_is_the_reverse_order():
+    al, spec = oracle_setup([None, None, None])
+    ctl = OracleController(al, spec, active=1, order="lru")
+    ctl.activate(2)
+    ctl.activate(0)
+    assert ctl.remapping()[1] == 3            # never activated = least recently
+
+
+@pytest.mark.parametrize("seed,prios,order", [(1, [3, 1, 2], "mru"), (2, [None, None, None], "mru"),
+                                              (3, [1, 1, 5], "mru"), (4, [None, None, None], "lru")])
+def test_product_controller_matches_oracle(seed, prios, order):
     from paper_2507_11507_b200 import _lib
     from paper_2507_11507_b200.controller import RemappingController
     ev = make_trace(seed)
     al, spec = oracle_setup(prios, native=6)
-    octl = OracleController(al, spec, active=0, cap=0.75)
+    octl = OracleController(al, spec, active=0, cap=0.75, order=order)
     replay(octl, ev, (OA.NoBlocks, OA.DoubleFree, OA.Pressure))
     ctx = _lib.Context.host_only(1 << 38, 64, 4096)
     ids = [ctx.add_model_host_only(TOY, 6)] + [ctx.add_model_host_only(DONOR, 0) for _ in prios]
     pspec = {i: spec[i] for i in ids}
-    pctl = RemappingController(ctx, pspec, active=0, cap=0.75)
+    pctl = RemappingController(ctx, pspec, active=0, cap=0.75, order=order)
     replay(pctl, ev, (_lib.MirageError,))
     assert pctl.log == octl.log
     assert any(e[0] == "remap" for e in octl.log) and any(e[0] == "revert" for e in octl.log)

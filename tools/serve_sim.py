@@ -294,10 +294,125 @@ def e3(args):
     return res
 
 
+def e4(args):
+    """Table 1 C1 under round-robin temporal sharing: OPT-13b, Llama-2-13b
+    and Llama-3-8b with the paper's GH200 reservations (35%/35%/20% of 96 GB).
+    Each phase one model is active; at the phase end its running requests are
+    preempted and the next model activates (its donated layers are reloaded).
+    Controller with MRU (the paper's default) vs LRU vs no remap."""
+    shapes = [models.OPT_13B, models.LLAMA2_13B, models.LLAMA3_8B]
+    resv = [0.35, 0.35, 0.20]
+    natives = []
+    for sh, r in zip(shapes, resv):
+        S, G, BB = _lib.model_sizes(sh)
+        natives.append(int((r * 96e9 - (sh.n_layers * S + G)) // BB))
+    blobs = [harness.make_blob(sh, i, i, gen_device="cuda") for i, sh in enumerate(shapes)]
+    prompts, outs = workload.sharegpt_trace(4000, seed=8)
+    phase, n_phases = args.phase, args.phases
+    rng = np.random.default_rng(4)
+    arrivals = [[rng.poisson(1.5 if (t // 20) % 2 == 0 else 0.2) for t in range(phase * n_phases)] for _ in shapes]
+    res = {"natives": natives}
+    for mode in ("mru", "lru", "no_remap"):
+        ctx = _lib.Context(harness.arena_for(list(zip(shapes, natives)), 256, 4096), 256, 4096)
+        mids = [ctx.add_model(sh, b, n) for sh, b, n in zip(shapes, blobs, natives)]
+        ctl = None
+        if mode != "no_remap":
+            ctl = RemappingController(ctx, {m: (sh.n_layers, None) for m, sh in zip(mids, shapes)}, active=mids[0],
+                                      layers_per_call=4, order=mode)
+        else:
+            for m in mids[1:]:
+                ctx.set_active(m, False)
+        queues = [[] for _ in shapes]
+        nxt = 0
+        step_ms, switch_ms, waits, tokens = [], [], [], 0
+        sid_model = {}
+        for ph in range(n_phases):
+            a = ph % len(shapes)
+            mid, sh = mids[a], shapes[a]
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ctx.stream)
+            if ctl:
+                ctl.activate(mid)
+            else:
+                for m in mids:
+                    ctx.set_active(m, m == mid)
+            e1.record(ctx.stream)
+            ctx.sync()
+            switch_ms.append(e0.elapsed_time(e1))
+            running, pos, left, held = [], {}, {}, {}
+            for t in range(ph * phase, (ph + 1) * phase):
+                for m in range(len(shapes)):
+                    for _ in range(arrivals[m][t]):
+                        queues[m].append((nxt, t))
+                        nxt += 1
+                q = queues[a]
+                while q and len(running) < 256:
+                    sid, ta = q[0]
+                    P = int(prompts[sid % len(prompts)])
+                    try:
+                        (ctl.alloc(sid, harness.blocks_for(P + 1)) if ctl else
+                         ctx.alloc_blocks(mid, sid, harness.blocks_for(P + 1)))
+                    except _lib.MirageError as e:
+                        if e.code != _lib.ERR_NO_BLOCKS:
+                            raise
+                        break
+                    ctx.fill_kv(mid, sid, P, seed=sid)
+                    q.pop(0)
+                    running.append(sid)
+                    pos[sid], left[sid], held[sid] = P, int(outs[sid % len(outs)]), harness.blocks_for(P + 1)
+                    waits.append(t - ta)
+                for sid in list(running):
+                    if sid not in running or harness.blocks_for(pos[sid] + 1) <= held[sid]:
+                        continue
+                    while True:
+                        try:
+                            ctl.alloc(sid, 1) if ctl else ctx.alloc_blocks(mid, sid, 1)
+                            held[sid] += 1
+                            break
+                        except _lib.MirageError:
+                            v = running.pop()
+                            (ctl.free(v) if ctl else ctx.free_blocks(mid, v))
+                            q.insert(0, (v, t))
+                            if v == sid:
+                                break
+                if not running:
+                    continue
+                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                f0.record(ctx.stream)
+                ctx.decode_step(mid, running, [workload.teacher_tokens(x, pos[x], sh.vocab) for x in running],
+                                [pos[x] for x in running], argmax=False)
+                f1.record(ctx.stream)
+                step_ms.append((f0, f1))
+                tokens += len(running)
+                for x in list(running):
+                    pos[x] += 1
+                    left[x] -= 1
+                    if left[x] <= 0:
+                        running.remove(x)
+                        (ctl.free(x) if ctl else ctx.free_blocks(mid, x))
+            for x in running:   # phase end: the model's requests are preempted (re-queued)
+                (ctl.free(x) if ctl else ctx.free_blocks(mid, x))
+                queues[a].insert(0, (x, (ph + 1) * phase))
+        ctx.sync()
+        ms = [a_.elapsed_time(b_) for a_, b_ in step_ms]
+        total = sum(ms) + sum(switch_ms)
+        res[mode] = {"tok_s": tokens / (total / 1e3), "p50_tbt_ms": pct(ms, 50), "p99_tbt_ms": pct(ms, 99),
+                     "switch_ms_total": sum(switch_ms), "switch_ms": [round(x, 1) for x in switch_ms], "mean_wait_steps": statistics.mean(waits) if waits else 0,
+                     "p99_wait_steps": pct(waits, 99), "served_tokens": tokens,
+                     "remaps": sum(1 for x in ctl.log if x[0] == "remap") if ctl else 0,
+                     "reverts": sum(1 for x in ctl.log if x[0] == "revert") if ctl else 0}
+        ctx.close()
+        del ctx
+        torch.cuda.empty_cache()
+    return res
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=600)
     ap.add_argument("--exp", nargs="*", default=["e1", "e2"])
+    ap.add_argument("--phase", type=int, default=150)
+    ap.add_argument("--phases", type=int, default=9)
     a = ap.parse_args()
     out = {}
     if "e1" in a.exp:
@@ -306,4 +421,6 @@ if __name__ == "__main__":
         out["e2_dynamic_reversion"] = e2(a)
     if "e3" in a.exp:
         out["e3_vs_kv_swap"] = e3(a)
+    if "e4" in a.exp:
+        out["e4_table1_c1_round_robin"] = e4(a)
     print(json.dumps(out, indent=1, default=str))
