@@ -70,6 +70,12 @@ extern "C" {
                                     * into one CUDA graph per batch size for models without
                                     * a streaming cycle (captured on the second step of a
                                     * size; ignored with MIRAGE_FLAG_TIME_ATTN)          */
+#define MIRAGE_FLAG_TP_IPC 16u /* init flag: tensor parallelism without NCCL: after
+                                * mirage_tp_export/import, each partial O-/down-projection
+                                * is summed by one kernel that reads the peers' partials
+                                * over peer memory (NVLink) and applies the residual and
+                                * next norm (a one-shot all-reduce fused into its
+                                * consumer; fixed rank order, bit-identical on all ranks) */
 #define MIRAGE_FLAG_HOST_ONLY 2u /* init flag: no device; allocator/remap/table/query
                                   * calls only (the arena pointer is used for address
                                   * arithmetic, never dereferenced); device calls
@@ -176,6 +182,13 @@ const char* mirage_last_error(const mirage_ctx* ctx);
  * CAPACITY (arena exhausted), CUDA. */
 int32_t mirage_add_model(mirage_ctx* ctx, const mirage_model_cfg* m, const void* host_blob,
                          uint64_t host_bytes, int64_t native_kv_blocks, int32_t* model_id);
+
+/* MIRAGE_FLAG_TP_IPC setup: tp_export writes this rank's 64-byte CUDA IPC handle
+ * of its partial-sum exchange buffer ([flag][2 x max_batch x d fp32]); the caller
+ * all-gathers the tp handles (rank order) and passes them to tp_import, which
+ * maps the peers' buffers. Errors: CONFIG, STATE, RANGE, CUDA. */
+int32_t mirage_tp_export(mirage_ctx* ctx, int32_t model, void* handle_out);
+int32_t mirage_tp_import(mirage_ctx* ctx, int32_t model, const void* handles);
 
 /* Re-streaming source tier: point the model's authoritative
  * weight copy -- used for cycled-layer re-streaming and reversion reloads -- at
@@ -312,6 +325,8 @@ typedef struct mirage_stats {
   int32_t last_split_blocks;    /* blocks per split-K partition of the last step     */
   int64_t slot_tag_errors;      /* MIRAGE_FLAG_SLOT_TAGS: cycled layers that started
                                  * before their weights had landed (must stay 0)     */
+  int64_t tp_peer_timeouts;     /* MIRAGE_FLAG_TP_IPC: all-reduce waits that gave up
+                                 * on a peer (must stay 0)                            */
 } mirage_stats;
 
 int32_t mirage_query(mirage_ctx* ctx, int32_t model, mirage_stats* out);

@@ -23,6 +23,7 @@ FLAG_TIME_ATTN = 1
 FLAG_HOST_ONLY = 2
 FLAG_SLOT_TAGS = 4
 FLAG_CUDA_GRAPHS = 8
+FLAG_TP_IPC = 16
 MAX_CYCLE = 256
 
 _NAMES = {ERR_CONFIG: "CONFIG", ERR_CAPACITY: "CAPACITY", ERR_RANGE: "RANGE", ERR_STATE: "STATE",
@@ -70,7 +71,7 @@ class Stats(C.Structure):
                 ("steps", C.c_int64), ("attn_launches", C.c_int64), ("attn_ms", C.c_double),
                 ("attn_bytes", C.c_uint64), ("last_meta_h2d_bytes", C.c_uint64),
                 ("last_attn_units", C.c_int32), ("last_split_blocks", C.c_int32),
-                ("slot_tag_errors", C.c_int64)]
+                ("slot_tag_errors", C.c_int64), ("tp_peer_timeouts", C.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "cycle"}
@@ -115,6 +116,8 @@ def _load():
         "mirage_swap_out": (I32, [P, I32, I64, P, U64]),
         "mirage_swap_in": (I32, [P, I32, I64, P]),
         "mirage_set_weight_source": (I32, [P, I32, P, U64]),
+        "mirage_tp_export": (I32, [P, I32, P]),
+        "mirage_tp_import": (I32, [P, I32, P]),
         "mirage_host_unregister": (I32, [P]),
     }
     for name, (res, args) in sig.items():
@@ -132,7 +135,8 @@ EXPORTED = [
     "mirage_decode_step", "mirage_query", "mirage_slot_log", "mirage_sync", "mirage_attn_only",
     "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches", "mirage_nccl_unique_id",
     "mirage_host_register", "mirage_host_unregister", "mirage_region_count", "mirage_region_info",
-    "mirage_unremap", "mirage_swap_out", "mirage_swap_in", "mirage_set_weight_source"]
+    "mirage_unremap", "mirage_swap_out", "mirage_swap_in", "mirage_set_weight_source", "mirage_tp_export",
+    "mirage_tp_import"]
 
 
 def model_cfg(shape):
@@ -303,6 +307,16 @@ class Context:
             self._check(LIB.mirage_region_info(self._ctx, model, i, C.byref(r)), "region_info")
             out.append(r.as_dict())
         return out
+
+    def tp_export(self, model):
+        buf = C.create_string_buffer(64)
+        self._check(LIB.mirage_tp_export(self._ctx, model, buf), "tp_export")
+        return buf.raw
+
+    def tp_import(self, model, handles):
+        """handles: list of the tp ranks' 64-byte handles, in rank order."""
+        blob = C.create_string_buffer(b"".join(handles), 64 * len(handles))
+        self._check(LIB.mirage_tp_import(self._ctx, model, blob), "tp_import")
 
     def set_weight_source(self, model, src):
         """src: a uint8 tensor (pinned CPU or CUDA, this or a peer GPU) holding the blob."""

@@ -64,6 +64,18 @@ cudaError_t launch_act(int family, int B, int f, const float* y, const __nv_bflo
 // argmax over each row of logits [B][V] (lowest index on ties).
 cudaError_t launch_argmax(int B, int V, const float* logits, int32_t* out, cudaStream_t s);
 
+// ---- tensor parallelism over peer memory (MIRAGE_FLAG_TP_IPC, a10 fused) ----
+// One-shot all-reduce fused with the residual (+bias) and the next norm: rank r
+// publishes `epoch` in its flag after its partial GEMM output is complete,
+// waits for every peer's flag, sums the tp partial rows in fixed rank order
+// (bit-identical on all ranks), then h += sum (+ bias); x = norm(h) if g.
+// parts[r] / flags[r]: rank r's partial buffer / flag (peer pointers via IPC).
+cudaError_t launch_tp_residual_norm(int family, int B, int d, const float* const* parts, int tp, int rank,
+                                    unsigned long long* const* flags, unsigned long long epoch,
+                                    unsigned int* err, const __nv_bfloat16* bias, const __nv_bfloat16* g,
+                                    const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
+                                    cudaStream_t s);
+
 // ---- slot tags (MIRAGE_FLAG_SLOT_TAGS): race detector for the copy engine ----
 // errors[0] += 1 and errors[1] = got if *tag != expected.
 cudaError_t launch_tag_check(const uint32_t* tag, uint32_t expected, uint32_t* errors, cudaStream_t s);

@@ -148,6 +148,62 @@ residual_norm_kernel(int family, int d, const float* y, int ldy, const __nv_bflo
   if (g) norm_row8(family, d, own, v, g, bta, eps, x + (size_t)b * d, red);
 }
 
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(1024)
+tp_residual_norm_kernel(int family, int d, const float* const* parts, int tp, int rank,
+                        unsigned long long* const* flags, unsigned long long epoch, unsigned int* err,
+                        const __nv_bfloat16* bias, const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps,
+                        float* h, __nv_bfloat16* x) {
+  __shared__ float red[32];
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    if (b == 0) {  // my partial (written by the preceding GEMM) is complete: publish
+      __threadfence_system();
+      st_release_sys(flags[rank], epoch);
+    }
+    for (int r = 0; r < tp; ++r) {  // bounded spin: a lost peer raises err instead of hanging
+      if (r == rank) continue;
+      long long n = 0;
+      while (ld_acquire_sys(flags[r]) < epoch) {
+        if (++n > (1ll << 26)) {
+          atomicAdd(err, 1u);
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+  }
+  __syncthreads();
+  const int e0 = threadIdx.x * 8;
+  const bool own = e0 < d;
+  float v[8];
+  if (own) {
+    load8(h + (size_t)b * d + e0, v);
+    for (int r = 0; r < tp; ++r) {  // fixed order: every rank computes the same sum
+      float pv[8];
+      load8(parts[r] + (size_t)b * d + e0, pv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] += pv[k];
+    }
+    if (bias) {
+      float bv[8];
+      load8bf(bias + e0, bv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] += bv[k];
+    }
+    store8(h + (size_t)b * d + e0, v);
+  }
+  if (g) norm_row8(family, d, own, v, g, bta, eps, x + (size_t)b * d, red);
+}
+
 // One CTA per sequence. Adds the bias, applies rotate-half RoPE (Llama) with the
 // angle pos * theta^(-2i/D) evaluated in fp64, writes q (fp32) and appends k, v
 // (bf16) into the paged cache row of position pos. Work items are 8-element
@@ -426,6 +482,17 @@ cudaError_t launch_act(int family, int B, int f, const float* y, const __nv_bflo
 
 cudaError_t launch_argmax(int B, int V, const float* logits, int32_t* out, cudaStream_t s) {
   argmax_kernel<<<B, 1024, 0, s>>>(V, logits, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tp_residual_norm(int family, int B, int d, const float* const* parts, int tp, int rank,
+                                    unsigned long long* const* flags, unsigned long long epoch,
+                                    unsigned int* err, const __nv_bfloat16* bias, const __nv_bfloat16* g,
+                                    const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
+                                    cudaStream_t s) {
+  if (d % 8 || d > 8192) return cudaErrorInvalidValue;
+  tp_residual_norm_kernel<<<B, ((d / 8 + 31) / 32) * 32, 0, s>>>(family, d, parts, tp, rank, flags, epoch, err,
+                                                                 bias, g, bta, eps, h, x);
   return cudaGetLastError();
 }
 

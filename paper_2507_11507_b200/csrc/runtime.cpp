@@ -208,6 +208,15 @@ struct Model {
   };
   std::map<int, Graph> graphs;  // by batch size
   std::set<int> graph_seen;     // batch sizes run once eagerly (plans/autotune done)
+  // ---- tensor parallelism over peer memory (MIRAGE_FLAG_TP_IPC) ----
+  char* xfer = nullptr;               // [flag u64 | pad][partial par 0][partial par 1]
+  size_t xfer_part = 0;               // bytes of one partial buffer (max_batch * d * 4)
+  std::vector<char*> peer_base;       // rank -> base of its xfer (own or IPC-opened)
+  float** parts_dev = nullptr;        // device [2][tp]
+  unsigned long long** flags_dev = nullptr;  // device [tp]
+  unsigned int* tp_err = nullptr;     // device counter of lost-peer timeouts
+  unsigned long long tp_epoch = 0;
+  bool tp_ready = false;
   // ---- step timing ----
   cudaEvent_t st0 = nullptr, st1 = nullptr;
   bool step_timed = false;
@@ -662,7 +671,8 @@ int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
   if (!cfg || !out) return MIRAGE_ERR_CONFIG;
   *out = nullptr;
   if (cfg->block_tokens != kBlockTokens || cfg->tp_size < 1 || cfg->tp_rank < 0 ||
-      cfg->tp_rank >= cfg->tp_size || (cfg->tp_size > 1 && !cfg->nccl_id) ||
+      cfg->tp_rank >= cfg->tp_size ||
+      (cfg->tp_size > 1 && !cfg->nccl_id && !(cfg->flags & MIRAGE_FLAG_TP_IPC)) ||
       !cfg->dev_arena || (!cfg->compute_stream && !(cfg->flags & MIRAGE_FLAG_HOST_ONLY)) ||
       cfg->max_batch <= 0 || cfg->max_ctx <= 0 ||
       (reinterpret_cast<uintptr_t>(cfg->dev_arena) % kAlign))
@@ -745,6 +755,12 @@ void mirage_destroy(mirage_ctx* c) {
     }
     for (auto e : M->ev_pool) cudaEventDestroy(e);
     for (auto& g : M->graphs) cudaGraphExecDestroy(g.second.exec);
+    for (size_t r = 0; r < M->peer_base.size(); ++r)
+      if (M->peer_base[r] && M->peer_base[r] != M->xfer) cudaIpcCloseMemHandle(M->peer_base[r]);
+    if (M->xfer) cudaFree(M->xfer);
+    if (M->parts_dev) cudaFree(M->parts_dev);
+    if (M->flags_dev) cudaFree(M->flags_dev);
+    if (M->tp_err) cudaFree(M->tp_err);
     delete M;
   }
   for (int i = 0; i < 2; ++i) {
@@ -861,6 +877,57 @@ int32_t mirage_add_model(mirage_ctx* c, const mirage_model_cfg* mc, const void* 
   M->id = (int32_t)c->models.size();
   c->models.push_back(M);
   *model_id = M->id;
+  return MIRAGE_OK;
+}
+
+int32_t mirage_tp_export(mirage_ctx* c, int32_t model, void* handle_out) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || !handle_out) return fail(c, MIRAGE_ERR_RANGE, "tp_export: arguments");
+  if (!(c->cfg.flags & MIRAGE_FLAG_TP_IPC) || c->host_only)
+    return fail(c, MIRAGE_ERR_CONFIG, "tp_export: needs MIRAGE_FLAG_TP_IPC");
+  if (!M->xfer) {
+    M->xfer_part = align_up((uint64_t)c->cfg.max_batch * M->shp.d * 4, kAlign);
+    CK(c, cudaMalloc(reinterpret_cast<void**>(&M->xfer), kAlign + 2 * M->xfer_part));
+    CK(c, cudaMemset(M->xfer, 0, kAlign + 2 * M->xfer_part));
+  }
+  cudaIpcMemHandle_t h;
+  CK(c, cudaIpcGetMemHandle(&h, M->xfer));
+  std::memcpy(handle_out, &h, sizeof h);
+  return MIRAGE_OK;
+}
+
+int32_t mirage_tp_import(mirage_ctx* c, int32_t model, const void* handles) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || !handles || !M->xfer) return fail(c, MIRAGE_ERR_STATE, "tp_import: export first");
+  const int tp = c->tp;
+  M->peer_base.assign(tp, nullptr);
+  for (int r = 0; r < tp; ++r) {
+    if (r == c->tp_rank) {
+      M->peer_base[r] = M->xfer;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, reinterpret_cast<const char*>(handles) + (size_t)r * sizeof h, sizeof h);
+    void* p = nullptr;
+    CK(c, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    M->peer_base[r] = reinterpret_cast<char*>(p);
+  }
+  std::vector<float*> parts(2 * tp);
+  std::vector<unsigned long long*> flags(tp);
+  for (int r = 0; r < tp; ++r) {
+    flags[r] = reinterpret_cast<unsigned long long*>(M->peer_base[r]);
+    for (int par = 0; par < 2; ++par)
+      parts[par * tp + r] = reinterpret_cast<float*>(M->peer_base[r] + kAlign + par * M->xfer_part);
+  }
+  CK(c, cudaMalloc(reinterpret_cast<void**>(&M->parts_dev), parts.size() * sizeof(float*)));
+  CK(c, cudaMalloc(reinterpret_cast<void**>(&M->flags_dev), flags.size() * sizeof(void*)));
+  CK(c, cudaMalloc(reinterpret_cast<void**>(&M->tp_err), 4));
+  CK(c, cudaMemcpy(M->parts_dev, parts.data(), parts.size() * sizeof(float*), cudaMemcpyHostToDevice));
+  CK(c, cudaMemcpy(M->flags_dev, flags.data(), flags.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  CK(c, cudaMemset(M->tp_err, 0, 4));
+  M->tp_ready = true;
   return MIRAGE_OK;
 }
 
@@ -1330,7 +1397,9 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   // cycle, one graph per batch size, captured on the second step of that size
   // (the first runs eagerly so cuBLASLt plans/autotuning happen outside capture)
   const bool graphable = (c->cfg.flags & MIRAGE_FLAG_CUDA_GRAPHS) && m == 0 &&
-                         !(c->cfg.flags & MIRAGE_FLAG_TIME_ATTN);
+                         !(c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) && !M->tp_ready;
+  if (c->tp > 1 && !c->nccl && !M->tp_ready)
+    return fail(c, MIRAGE_ERR_STATE, "step: tensor parallel model without a collective (tp_import first)");
   bool body_done = false, capturing = false;
   int64_t l0 = 0;
   if (graphable) {
@@ -1394,11 +1463,20 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     } else {
       KL(c, mirage::launch_paged_attention(ap, cs));
     }
-    if (int32_t e = gemm_lt(c, B, d, H * D, w.w_o, M->x, M->y, 0, nullptr, 0)) return e;
-    if (c->nccl)  // a10: sum the heads' partial O-projections over the TP ranks
-      CKN(c, ncclAllReduce(M->y, M->y, (size_t)B * d, ncclFloat32, ncclSum, c->nccl, cs));
-    KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_o : nullptr, w.n2_g,
-                                      opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs));
+    if (M->tp_ready) {  // a10 over peer memory: partial O-proj -> fused all-reduce + residual + norm
+      const uint64_t ep = ++M->tp_epoch;
+      float* part = reinterpret_cast<float*>(M->xfer + kAlign + (ep & 1) * M->xfer_part);
+      if (int32_t e = gemm_lt(c, B, d, H * D, w.w_o, M->x, part, 0, nullptr, 0)) return e;
+      KL(c, mirage::launch_tp_residual_norm(s.family, B, d, M->parts_dev + (ep & 1) * c->tp, c->tp, c->tp_rank,
+                                           M->flags_dev, ep, M->tp_err, opt ? w.b_o : nullptr, w.n2_g,
+                                           opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs));
+    } else {
+      if (int32_t e = gemm_lt(c, B, d, H * D, w.w_o, M->x, M->y, 0, nullptr, 0)) return e;
+      if (c->nccl)  // a10: sum the heads' partial O-projections over the TP ranks
+        CKN(c, ncclAllReduce(M->y, M->y, (size_t)B * d, ncclFloat32, ncclSum, c->nccl, cs));
+      KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_o : nullptr, w.n2_g,
+                                        opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs));
+    }
     if (opt) {
       // FC1 + bias + ReLU fused in the GEMM epilogue, bf16 out (one rounding, as before)
       if (int32_t e = gemm_lt(c, B, s.f, d, w.w_1, M->x, M->f, 1, w.b_1, 2)) return e;
@@ -1406,9 +1484,26 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
       if (int32_t e = gemm_lt(c, B, 2 * s.f, d, w.w_1, M->x, M->y, 0, nullptr, 0)) return e;
       KL(c, mirage::launch_act(s.family, B, s.f, M->y, nullptr, M->f, cs));
     }
-    if (int32_t e = gemm_lt(c, B, d, s.f, w.w_2, M->f, M->y, 0, nullptr, 0)) return e;
+    uint64_t ep2 = 0;
+    if (M->tp_ready) {
+      ep2 = ++M->tp_epoch;
+      float* part = reinterpret_cast<float*>(M->xfer + kAlign + (ep2 & 1) * M->xfer_part);
+      if (int32_t e = gemm_lt(c, B, d, s.f, w.w_2, M->f, part, 0, nullptr, 0)) return e;
+    } else {
+      if (int32_t e = gemm_lt(c, B, d, s.f, w.w_2, M->f, M->y, 0, nullptr, 0)) return e;
+    }
     if (c->nccl)  // a10: sum the FFN shards' partial down-projections
       CKN(c, ncclAllReduce(M->y, M->y, (size_t)B * d, ncclFloat32, ncclSum, c->nccl, cs));
+    // residual of layer l (+ the next norm): plain, or fused with the peer all-reduce
+    auto residual = [&](const bf16* bias2, const bf16* g2, const bf16* b2) -> int32_t {
+      if (M->tp_ready) {
+        KL(c, mirage::launch_tp_residual_norm(s.family, B, d, M->parts_dev + (ep2 & 1) * c->tp, c->tp, c->tp_rank,
+                                             M->flags_dev, ep2, M->tp_err, bias2, g2, b2, s.eps, M->h, M->x, cs));
+      } else {
+        KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, bias2, g2, b2, s.eps, M->h, M->x, cs));
+      }
+      return MIRAGE_OK;
+    };
     // residual, then the next layer's first norm (or the final norm)
     const bool last = l + 1 == s.n;
     const bf16* ng = last ? gw.nf_g : nullptr;
@@ -1416,8 +1511,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     const bool split_gate = !last && use_of[l] >= 0 && use_of[l + 1] >= 0 && beta == 1;
     if (split_gate) {
       // l and l+1 share the single slot: finish l, hand the slot over, then norm
-      KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_2 : nullptr, nullptr,
-                                        nullptr, s.eps, M->h, M->x, cs));
+      if (int32_t e = residual(opt ? w.b_2 : nullptr, nullptr, nullptr)) return e;
       if (int32_t e = release(l)) return e;
       if (int32_t e = gate(l + 1)) return e;
       const LayerW wn = layer_ptrs(s, wptr[l + 1]);
@@ -1430,8 +1524,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
         ng = wn.n1_g;
         nb = opt ? wn.n1_b : nullptr;
       }
-      KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_2 : nullptr, ng,
-                                        opt ? nb : nullptr, s.eps, M->h, M->x, cs));
+      if (int32_t e = residual(opt ? w.b_2 : nullptr, ng, opt ? nb : nullptr)) return e;
       if (int32_t e = release(l)) return e;
     }
   }
@@ -1608,6 +1701,11 @@ int32_t mirage_query(mirage_ctx* c, int32_t model, mirage_stats* o) {
   o->attn_ms = M->attn_ms;
   o->attn_bytes = M->attn_bytes;
   o->last_meta_h2d_bytes = M->last_meta;
+  if (M->tp_err) {
+    uint32_t e = 0;
+    CK(c, cudaMemcpy(&e, M->tp_err, 4, cudaMemcpyDeviceToHost));
+    o->tp_peer_timeouts = e;
+  }
   if (M->tag_err) {
     uint32_t e[2] = {0, 0};
     CK(c, cudaMemcpy(e, M->tag_err, 8, cudaMemcpyDeviceToHost));

@@ -1,0 +1,85 @@
+"""Tensor parallelism over peer memory (a10, MIRAGE_FLAG_TP_IPC) with TWO ranks:
+two processes share the one GPU of the test box through CUDA IPC (on a multi-GPU
+box the same code reads the peers' HBM over NVLink). Each rank holds its head /
+FFN shard; the fused kernel sums the partial O- and down-projections in fixed
+rank order. Both ranks must equal oracle c4 on the FULL model and be
+bit-identical to each other. GPU only."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, tp, port, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=tp)
+    import harness
+    from paper_2507_11507_b200 import Context, _lib
+    from synth import models, workload
+    shape = models.ModelShape("tp-llama", models.LLAMA, 2, 256, 8, 4, 64, 512, 1024, 256)
+    sh = harness.shard_shape(shape, tp)
+    ctx = Context(harness.arena_for([(sh, 16)], 4, 128), 4, 128, flags=_lib.FLAG_TP_IPC, tp_rank=rank, tp_size=tp)
+    mid = ctx.add_model(shape, harness.make_shard_blob(shape, rank, tp, seed=13), 16)
+    handles = [None] * tp
+    dist.all_gather_object(handles, ctx.tp_export(mid))
+    ctx.tp_import(mid, handles)
+    dist.barrier()
+    hid = torch.empty((4, shape.d_model), dtype=torch.bfloat16, device="cuda")
+    outs = []
+    for t in range(12):
+        if t % 16 == 0:
+            for s in range(4):
+                ctx.alloc_blocks(mid, s, 1)
+        ctx.decode_step(mid, [0, 1, 2, 3], [workload.teacher_tokens(s, t, shape.vocab) for s in range(4)], [t] * 4,
+                        hidden_out=hid)
+        ctx.sync()
+        outs.append(hid.float().cpu().numpy().copy())
+    q.put((rank, np.stack(outs), ctx.query(mid)["tp_peer_timeouts"]))
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_two_rank_tp_over_peer_memory_matches_oracle():
+    from oracle.decode import Decoder
+    from synth import models, weights, workload
+    tp = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank, args=(r, tp, port, q)) for r in range(tp)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(tp):
+        r, o, to = q.get(timeout=600)
+        res[r] = (o, to)
+    for p in ps:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in ps)
+    assert res[0][1] == 0 and res[1][1] == 0                   # no lost-peer timeouts
+    assert np.array_equal(res[0][0], res[1][0])                 # fixed-order sum: identical ranks
+    shape = models.ModelShape("tp-llama", models.LLAMA, 2, 256, 8, 4, 64, 512, 1024, 256)
+    dec = Decoder(shape, [weights.layer_tensors(shape, l, 13) for l in range(2)], weights.global_tensors(shape, 13))
+    for t in range(12):
+        ref, _, _ = dec.step([0, 1, 2, 3], [workload.teacher_tokens(s, t, shape.vocab) for s in range(4)], [t] * 4)
+        got = res[0][0][t]
+        rel = np.sqrt(((got - ref) ** 2).mean() / (ref ** 2).mean())
+        assert rel < 1e-2, (t, rel)

@@ -311,14 +311,14 @@ def e4(args):
     phase, n_phases = args.phase, args.phases
     rng = np.random.default_rng(4)
     arrivals = [[rng.poisson(1.5 if (t // 20) % 2 == 0 else 0.2) for t in range(phase * n_phases)] for _ in shapes]
-    res = {"natives": natives}
+    res = {"natives": natives, "cap": args.cap}
     for mode in ("mru", "lru", "no_remap"):
         ctx = _lib.Context(harness.arena_for(list(zip(shapes, natives)), 256, 4096), 256, 4096)
         mids = [ctx.add_model(sh, b, n) for sh, b, n in zip(shapes, blobs, natives)]
         ctl = None
         if mode != "no_remap":
             ctl = RemappingController(ctx, {m: (sh.n_layers, None) for m, sh in zip(mids, shapes)}, active=mids[0],
-                                      layers_per_call=4, order=mode)
+                                      layers_per_call=4, order=mode, cap=args.cap)
         else:
             for m in mids[1:]:
                 ctx.set_active(m, False)
@@ -413,6 +413,7 @@ if __name__ == "__main__":
     ap.add_argument("--exp", nargs="*", default=["e1", "e2"])
     ap.add_argument("--phase", type=int, default=150)
     ap.add_argument("--phases", type=int, default=9)
+    ap.add_argument("--cap", type=float, default=1.0, help="max remapped fraction of an inactive model (P:387)")
     a = ap.parse_args()
     out = {}
     if "e1" in a.exp:
