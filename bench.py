@@ -383,6 +383,8 @@ def run_mirage(args, rank, world):
     except Exception:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = ("MEASURED_PEAKS.json hbm_gbs (copy, of measured)" if "hbm_gbs" in peaks
+                else "B200_PROFILING.md fallback 6.65 TB/s (of fallback; MEASURED_PEAKS.json absent)")
     h2d_peak = measure_h2d_peak(torch, dev)
     t0 = time.time()
     blobs = {}
@@ -450,7 +452,7 @@ def run_mirage(args, rank, world):
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": attn_bytes_launch, "avg_launch_ms": attn_avg_ms,
                      "launches": res["attn_launches"], "share_of_step": res["attn_ms"] / t_local,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, of measured)"},
+                     "peak_source": peak_src},
         "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": h2d_peak, "frac": (h2d_gbs / h2d_peak) if h2d_gbs else None,
                 "bytes_per_step": res["h2d_bytes"] / args.steps, "copies": res["h2d_copies"],
                 "peak_source": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this run"},

@@ -1607,6 +1607,17 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
   ap.sched = M->tickets + (size_t)c->cfg.max_batch * s.Hk;
   ap.out = out_dev;
   ap.out_fp32 = out_fp32;
+  if (c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) {  // kernel-only time, excluding the metadata upload
+    harvest_attn_times(M);
+    uint64_t nbytes = 0;
+    for (int i = 0; i < B; ++i) nbytes += (uint64_t)hv.len[i] * 2 * s.Hk * s.D * 2;
+    Model::AttnTiming at{pool_event(M), pool_event(M), nbytes};
+    CK(c, cudaEventRecord(at.t0, c->cs));
+    KL(c, mirage::launch_paged_attention(ap, c->cs));
+    CK(c, cudaEventRecord(at.t1, c->cs));
+    M->attn_pending.push_back(at);
+    return MIRAGE_OK;
+  }
   KL(c, mirage::launch_paged_attention(ap, c->cs));
   return MIRAGE_OK;
 }

@@ -42,7 +42,7 @@ def run(name, reps, seed=0, split=0):
     need = sum(harness.blocks_for(x) for x in lens)
     max_ctx = max(lens) + 16
     arena = harness.arena_for([(shape, need)], B, max_ctx)
-    ctx_ = _lib.Context(arena, B, max_ctx)
+    ctx_ = _lib.Context(arena, B, max_ctx, flags=_lib.FLAG_TIME_ATTN)
     mid = ctx_.add_model(shape, harness.make_blob(shape), need)
     for i, x in enumerate(lens):
         ctx_.alloc_blocks(mid, i, harness.blocks_for(x))
@@ -54,6 +54,7 @@ def run(name, reps, seed=0, split=0):
     for w in range(3):
         ctx_.attn_only(mid, layers[w % L], list(range(B)), q, out, split_tokens=split)
     ctx_.sync()
+    q0 = ctx_.query(mid)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
     ev[0].record(ctx_.stream)
     for r in range(reps):
@@ -65,9 +66,11 @@ def run(name, reps, seed=0, split=0):
     med = ms[len(ms) // 2]
     nbytes = sum(lens) * 2 * Hk * D * 2
     st = ctx_.query(mid)
+    k_ms = (st["attn_ms"] - q0["attn_ms"]) / max(1, st["attn_launches"] - q0["attn_launches"])
     ctx_.close()
     return {"case": name, "split_blocks": st["last_split_blocks"], "units": st["last_attn_units"], "batch": B, "ctx_sum": sum(lens), "bytes": nbytes, "median_ms": med, "best_ms": ms[0],
-            "gbs_median": nbytes / med / 1e6, "gbs_best": nbytes / ms[0] / 1e6}
+            "gbs_median": nbytes / med / 1e6, "gbs_best": nbytes / ms[0] / 1e6,
+            "kernel_ms": k_ms, "gbs_kernel": nbytes / k_ms / 1e6}
 
 
 if __name__ == "__main__":
@@ -83,4 +86,4 @@ if __name__ == "__main__":
             except Exception as e:  # e.g. too many splits for the override
                 print(json.dumps({"case": c, "split": sp, "error": str(e)[:120]}), flush=True)
                 continue
-            print(json.dumps({k: (round(v, 1) if isinstance(v, float) else v) for k, v in r.items()}), flush=True)
+            print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}), flush=True)
