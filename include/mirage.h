@@ -243,8 +243,12 @@ int32_t mirage_region_info(mirage_ctx* ctx, int32_t model, int32_t idx, mirage_r
  * restored for parameter usage", :830-839 §7.6.1): give region `region` of
  * `recipient` back to its donor's parameters. Every block of the region must be
  * free; the ids are retired (never handed out again, reading #13); the layers'
- * weights are reloaded from the host copy on the compute stream (ordered after
- * every kernel that used the bytes as KV), and the layers become resident. A
+ * weights are reloaded from the host copy on the COPY stream, ordered after
+ * every kernel already enqueued on the compute stream (the last readers of the
+ * bytes as KV), one event per layer. The call returns without waiting: the first
+ * kernel of a later decode step / prefill that reads layer l waits for layer l's
+ * event only, so a cold start's prefill overlaps the reload layer by layer
+ * ("T_T * N <= T_Compute" with T_Compute = prefill). A
  * region of a streaming self-remap reverts the donor's whole cycle (all its
  * regions, slot holders reloaded, streaming stops at the next step).
  * Errors: RANGE; STATE (already reverted); PRESSURE (blocks still hold KV);
@@ -252,8 +256,8 @@ int32_t mirage_region_info(mirage_ctx* ctx, int32_t model, int32_t idx, mirage_r
 int32_t mirage_unremap(mirage_ctx* ctx, int32_t recipient, int32_t region);
 
 /* Mark a tenant active (1) or inactive (0) (temporal sharing).
- * Errors: RANGE; STATE (activating a model with reclaimed layers: needs
- * unremap, not in this version). */
+ * Errors: RANGE; STATE (activating a model with reclaimed layers: unremap its
+ * regions first; the reload then overlaps the next prefill). */
 int32_t mirage_set_active(mirage_ctx* ctx, int32_t model, int32_t active);
 
 /* Allocate n blocks for seq_id: the n lowest free ids, ascending, appended to
@@ -288,11 +292,15 @@ int32_t mirage_block_location(mirage_ctx* ctx, int32_t model, int32_t block_id, 
 /* Tokens cached for seq_id (0 if unknown). */
 int32_t mirage_seq_len(mirage_ctx* ctx, int32_t model, int64_t seq_id, int32_t* len_out);
 
-/* One decode step for `batch` sequences (Alg. 1 line 13
- * "GPU LLM Kernel(enable_remap, remapped_layer_list)"). positions[i] must equal
- * the tokens already cached for seq_ids[i]; the step appends the new token's
- * K/V at that position and attends over positions[i]+1 tokens, so seq i needs
- * >= ceil((positions[i]+1)/16) blocks. tokens are teacher-forced by the caller.
+/* One decode step for `batch` rows (Alg. 1 line 13
+ * "GPU LLM Kernel(enable_remap, remapped_layer_list)"). A row is one token of
+ * seq_ids[i] at positions[i]; the step appends the row's K/V at that position
+ * and attends over positions[i]+1 tokens (causal), so the sequence needs
+ * >= ceil((positions[i]+1)/16) blocks. Normally every row is a different
+ * sequence and positions[i] equals its cached length. Several rows may name one
+ * sequence (a prefill / extend chunk): in row order they must take consecutive
+ * positions starting at its cached length; all rows' K/V are appended before any
+ * row attends. tokens are teacher-forced by the caller.
  * hidden_out: device bf16 [batch, d] (final normalised hidden) or NULL.
  * argmax_out: host int32 [batch] (greedy token, lowest index on ties) or NULL;
  * valid after the compute stream is synchronised.
@@ -302,6 +310,19 @@ int32_t mirage_seq_len(mirage_ctx* ctx, int32_t model, int64_t seq_id, int32_t* 
 int32_t mirage_decode_step(mirage_ctx* ctx, int32_t model, int32_t batch, const int64_t* seq_ids,
                            const int32_t* tokens, const int32_t* positions, void* hidden_out,
                            int32_t* argmax_out);
+
+/* Prefill (§2.1: the prompt is processed in parallel and its
+ * KV cached; the cold-start phase of :395-397). n_seqs prompts; prompt i has
+ * prompt_lens[i] > 0 tokens, concatenated in `tokens` (host int32, sum of
+ * lengths). Each prompt is appended at its sequence's cached length (0 for a
+ * new sequence: prefill; > 0: extend). The rows run as mirage_decode_step
+ * chunks of at most max_batch rows, each one layer-major pass, so a pending
+ * asynchronous reload gates each layer separately. last_argmax_out: host int32
+ * [n_seqs], the greedy next token after each prompt (the call then synchronises
+ * the compute stream), or NULL (asynchronous). Blocks must be allocated.
+ * Errors: RANGE (lengths, duplicate seq), NO_BLOCKS, STATE, CUDA. */
+int32_t mirage_prefill(mirage_ctx* ctx, int32_t model, int32_t n_seqs, const int64_t* seq_ids,
+                       const int32_t* prompt_lens, const int32_t* tokens, int32_t* last_argmax_out);
 
 typedef struct mirage_stats {
   int64_t native_blocks, total_blocks, free_blocks;

@@ -101,6 +101,7 @@ def _load():
         "mirage_block_location": (I32, [P, I32, I32, pI32, pU64]),
         "mirage_seq_len": (I32, [P, I32, I64, pI32]),
         "mirage_decode_step": (I32, [P, I32, I32, pI64, pI32, pI32, P, pI32]),
+        "mirage_prefill": (I32, [P, I32, I32, pI64, pI32, pI32, pI32]),
         "mirage_query": (I32, [P, I32, C.POINTER(Stats)]),
         "mirage_slot_log": (I32, [P, I32, pI64, I32, pI32]),
         "mirage_sync": (I32, [P]),
@@ -136,7 +137,7 @@ EXPORTED = [
     "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches", "mirage_nccl_unique_id",
     "mirage_host_register", "mirage_host_unregister", "mirage_region_count", "mirage_region_info",
     "mirage_unremap", "mirage_swap_out", "mirage_swap_in", "mirage_set_weight_source", "mirage_tp_export",
-    "mirage_tp_import"]
+    "mirage_tp_import", "mirage_prefill"]
 
 
 def model_cfg(shape):
@@ -374,6 +375,17 @@ class Context:
                                     hp, am)
         self._check(rc, "decode_step")
         return am
+
+    def prefill(self, model, seq_ids, prompts, argmax=True):
+        """prompts: list of token lists, one per seq (appended at the cached length).
+        Returns the greedy next token per seq (synchronises) or None."""
+        n = len(seq_ids)
+        lens = [len(p) for p in prompts]
+        flat = [int(t) for p in prompts for t in p]
+        am = (C.c_int32 * n)() if argmax else None
+        rc = LIB.mirage_prefill(self._ctx, model, n, _i64(seq_ids), _i32(lens), _i32(flat), am)
+        self._check(rc, "prefill")
+        return list(am) if argmax else None
 
     def decode_step_raw(self, model, B, seq_ids_c, tokens_c, positions_c, hidden_ptr, argmax_c):
         """Pre-marshalled variant (ctypes arrays) for timed loops."""

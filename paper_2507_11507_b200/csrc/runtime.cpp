@@ -173,6 +173,10 @@ struct Model {
   int64_t cyc_steps = 0;
   std::vector<int64_t> slot_log;  // rows of 5
   std::vector<cudaEvent_t> ready_ev, free_ev;
+  // asynchronous reloads (mirage_unremap): layer l's weights land on the copy
+  // stream; the first kernel that reads layer l waits for reload_ev[l]
+  std::vector<cudaEvent_t> reload_ev;  // per layer, created on first use
+  std::vector<char> reload_pending;
   uint32_t* slot_tag = nullptr;   // device [MAX_CYCLE] tag of the layer each slot holds (SLOT_TAGS)
   uint32_t* tag_err = nullptr;    // device [2] mismatch count, last bad tag
   uint32_t* host_tags = nullptr;  // pinned [n_layers] tag values copied behind each layer DMA
@@ -521,6 +525,11 @@ void harvest_attn_times(Model* M) {
   (void)cudaGetLastError();
 }
 
+int prefetch_debug() {
+  static const int v = getenv("MIRAGE_PREFETCH_DEBUG") ? atoi(getenv("MIRAGE_PREFETCH_DEBUG")) : 0;
+  return v;
+}
+
 cudaEvent_t pool_event(Model* M) {
   if (!M->ev_pool.empty()) {
     cudaEvent_t e = M->ev_pool.back();
@@ -739,6 +748,8 @@ void mirage_destroy(mirage_ctx* c) {
   for (Model* M : c->models) {
     for (auto e : M->ready_ev) cudaEventDestroy(e);
     for (auto e : M->free_ev) cudaEventDestroy(e);
+    for (auto e : M->reload_ev)
+      if (e) cudaEventDestroy(e);
     for (auto& t : M->pending) {
       cudaEventDestroy(t.t0);
       cudaEventDestroy(t.t1);
@@ -959,6 +970,17 @@ int32_t mirage_set_weight_source(mirage_ctx* c, int32_t model, const void* src, 
   return MIRAGE_OK;
 }
 
+// Order the compute stream after every pending asynchronous reload of M (before
+// M's weight bytes are handed out again, swapped or re-streamed).
+static int32_t settle_reloads(mirage_ctx* c, Model* M) {
+  for (size_t l = 0; l < M->reload_pending.size(); ++l)
+    if (M->reload_pending[l]) {
+      CK(c, cudaStreamWaitEvent(c->cs, M->reload_ev[l], 0));
+      M->reload_pending[l] = 0;
+    }
+  return MIRAGE_OK;
+}
+
 int32_t mirage_set_active(mirage_ctx* c, int32_t model, int32_t active) {
   GUARD(c);
   Model* M = get_model(c, model);
@@ -993,6 +1015,8 @@ int32_t mirage_remap_layers(mirage_ctx* c, int32_t donor, int32_t recipient, con
   if (beta > 0 && donor != recipient)
     return fail(c, MIRAGE_ERR_STATE, "remap: streaming remap must be a self-remap");
   if (beta > 0 && !D->cycle.empty()) return fail(c, MIRAGE_ERR_STATE, "remap: donor already has a cycle");
+  if (!c->host_only)  // bytes still being reloaded must land before they become KV or slots again
+    if (int32_t e = settle_reloads(c, D)) return e;
   // carve R = cycle[beta:] into runs of consecutive layers
   std::vector<int32_t> Rl(cycle + beta, cycle + m);
   int64_t gained = 0;
@@ -1127,17 +1151,37 @@ int32_t mirage_unremap(mirage_ctx* c, int32_t recipient, int32_t region) {
   if (was_cycle)  // the slot holders' storage may hold another cycled layer's weights
     for (int i = 0; i < D->beta; ++i) layers.push_back(D->cycle[i]);
   if (!c->host_only) {
-    if (was_cycle) {  // finish in-flight prefetch copies before reloading the slots
-      cudaEvent_t e;
-      CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      CK(c, cudaEventRecord(e, c->xs));
-      CK(c, cudaStreamWaitEvent(c->cs, e, 0));
-      cudaEventDestroy(e);
+    // The reload runs on the copy stream, ordered after every kernel enqueued so
+    // far on the compute stream (the last readers of these bytes as KV, or of
+    // the slots) and, by stream order, after in-flight prefetches. Layer l's
+    // event gates the first kernel that reads it (mirage_decode_step /
+    // mirage_prefill), so a cold start's prefill overlaps the reload layer by
+    // layer (T_T * N <= T_Compute of the prefill).
+    cudaEvent_t e;
+    CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(c, cudaEventRecord(e, c->cs));
+    CK(c, cudaStreamWaitEvent(c->xs, e, 0));
+    cudaEventDestroy(e);
+    if (D->reload_ev.empty()) {
+      D->reload_ev.assign(D->shp.n, nullptr);
+      D->reload_pending.assign(D->shp.n, 0);
     }
-    // stream-ordered after every kernel that used these bytes as KV
-    for (int32_t l : layers)
+    std::sort(layers.begin(), layers.end());
+    layers.erase(std::unique(layers.begin(), layers.end()), layers.end());
+    for (int32_t l : layers) {
+      if (!D->reload_ev[l]) CK(c, cudaEventCreateWithFlags(&D->reload_ev[l], cudaEventDisableTiming));
+      CopyTiming t{pool_event(D), pool_event(D), D->sz.S};
+      if (!t.t0 || !t.t1) return fail(c, MIRAGE_ERR_CUDA, "unremap: event pool");
+      CK(c, cudaEventRecord(t.t0, c->xs));
+      if (prefetch_debug() == 3 || prefetch_debug() == 4)  // test hook: a slow link
+        KL(c, mirage::launch_spin(20000000ull, c->xs));
       CK(c, cudaMemcpyAsync(D->w_dev + (uint64_t)l * D->sz.S, D->host + (uint64_t)l * D->sz.S, D->sz.S,
-                            cudaMemcpyDefault, c->cs));
+                            cudaMemcpyDefault, c->xs));
+      CK(c, cudaEventRecord(t.t1, c->xs));
+      CK(c, cudaEventRecord(D->reload_ev[l], c->xs));
+      D->pending.push_back(t);
+      D->reload_pending[l] = 1;
+    }
   }
   for (int32_t l : layers) D->layer_state[l] = RESIDENT;
   if (was_cycle) {
@@ -1289,13 +1333,24 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     if (st == RECLAIMED && M->cycle.empty())
       return fail(c, MIRAGE_ERR_STATE, "step: model %d has reclaimed layers and no cycle", model);
   // ---- validate (before any enqueue) ----
+  // A row is one token. Several rows may belong to one sequence (a prefill or
+  // extend chunk): in row order they must take consecutive positions starting at
+  // the sequence's cached length. Each row attends causally over positions
+  // 0..positions[i] (prefill = the prompt's tokens in parallel).
   std::vector<const std::vector<int32_t>*> rows(B);
+  std::unordered_map<int64_t, int32_t> next_pos;  // seq -> expected position of its next row
+  std::vector<int32_t> first_row(B);               // row whose address list this row shares
+  std::unordered_map<int64_t, int32_t> first_of;
   for (int i = 0; i < B; ++i) {
     auto it = M->tables.find(seq_ids[i]);
-    const int32_t len = M->lens.count(seq_ids[i]) ? M->lens[seq_ids[i]] : 0;
+    auto np = next_pos.find(seq_ids[i]);
+    const int32_t len = np != next_pos.end() ? np->second
+                                             : (M->lens.count(seq_ids[i]) ? M->lens[seq_ids[i]] : 0);
     if (positions[i] != len)
-      return fail(c, MIRAGE_ERR_STATE, "step: seq %lld position %d != cached %d",
+      return fail(c, MIRAGE_ERR_STATE, "step: seq %lld position %d != expected %d",
                   (long long)seq_ids[i], positions[i], len);
+    next_pos[seq_ids[i]] = len + 1;
+    first_row[i] = first_of.emplace(seq_ids[i], i).first->second;
     if (positions[i] + 1 > c->cfg.max_ctx || positions[i] + 1 > s.max_pos)
       return fail(c, MIRAGE_ERR_RANGE, "step: seq %lld exceeds max_ctx", (long long)seq_ids[i]);
     if (tokens[i] < 0 || tokens[i] >= s.V) return fail(c, MIRAGE_ERR_RANGE, "step: token %d", tokens[i]);
@@ -1304,22 +1359,24 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
       return fail(c, MIRAGE_ERR_NO_BLOCKS, "step: seq %lld needs %d blocks", (long long)seq_ids[i], need);
     rows[i] = &it->second;
   }
-  for (int i = 0; i < B; ++i)
-    for (int j = 0; j < i; ++j)
-      if (seq_ids[i] == seq_ids[j]) return fail(c, MIRAGE_ERR_RANGE, "step: duplicate seq");
   harvest_copy_times(M);
   harvest_step_time(M);
   // ---- pack metadata ----
   char* host;
   if (int32_t e = acquire_stage(c, &host)) return e;
   MetaView hv = meta_view(c, host), dv = meta_view(c, c->meta_dev);
+  // one resolved address list per sequence, long enough for its last row
   int n_addr = 0;
   for (int i = 0; i < B; ++i) {
     hv.tokens[i] = tokens[i];
     hv.pos[i] = positions[i];
     hv.len[i] = positions[i] + 1;
+    if (first_row[i] != i) {
+      hv.seq_off[i] = hv.seq_off[first_row[i]];
+      continue;
+    }
     hv.seq_off[i] = n_addr;
-    const int need = (positions[i] + 1 + kBlockTokens - 1) / kBlockTokens;
+    const int need = (next_pos[seq_ids[i]] + kBlockTokens - 1) / kBlockTokens;
     for (int j = 0; j < need; ++j) hv.addrs[n_addr + j] = M->bbase_host[(*rows[i])[j]];
     n_addr += need;
   }
@@ -1359,8 +1416,16 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
       wptr[l] = M->w_dev + (uint64_t)l * M->sz.S;
     }
   }
-  static const int dbg_nowait = getenv("MIRAGE_PREFETCH_DEBUG") && atoi(getenv("MIRAGE_PREFETCH_DEBUG")) >= 2;
+  // test/experiment hooks (MIRAGE_PREFETCH_DEBUG): 1 = events only, no DMA; 2 = no waits;
+  // 3 = no waits + a 20 ms stall before each copy (slow link); 4 = slow link, waits kept
+  static const int dbg_nowait = prefetch_debug() == 2 || prefetch_debug() == 3;
+  bool reloading = false;
+  for (char r : M->reload_pending) reloading |= r != 0;
   auto gate = [&](int l) -> int32_t {  // wait until layer l's weights are in its slot
+    if (reloading && l < s.n && M->reload_pending[l]) {  // an asynchronous reload (mirage_unremap)
+      if (!dbg_nowait) CK(c, cudaStreamWaitEvent(cs, M->reload_ev[l], 0));
+      M->reload_pending[l] = 0;
+    }
     if (!dbg_nowait && l < s.n && use_of[l] >= beta && use_of[l] >= 0)
       CK(c, cudaStreamWaitEvent(cs, M->ready_ev[use_of[l] % beta], 0));
     if (M->slot_tag && l < s.n && use_of[l] >= 0)  // SLOT_TAGS: the slot must hold layer l now
@@ -1380,8 +1445,8 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     CopyTiming t{pool_event(M), pool_event(M), M->sz.S};
     if (!t.t0 || !t.t1) return fail(c, MIRAGE_ERR_CUDA, "release: event pool");
     CK(c, cudaEventRecord(t.t0, c->xs));
-    static const int dbg_mode = getenv("MIRAGE_PREFETCH_DEBUG") ? atoi(getenv("MIRAGE_PREFETCH_DEBUG")) : 0;
-    if (dbg_mode == 3) KL(c, mirage::launch_spin(20000000ull, c->xs));  // test hook: a slow link
+    const int dbg_mode = prefetch_debug();
+    if (dbg_mode == 3 || dbg_mode == 4) KL(c, mirage::launch_spin(20000000ull, c->xs));  // a slow link
     if (dbg_mode != 1)  // experiment hook: 1 = events only, no DMA
       CK(c, cudaMemcpyAsync(M->w_dev + (uint64_t)M->cycle[slot] * M->sz.S,
                             M->host + (uint64_t)nl * M->sz.S, M->sz.S, cudaMemcpyDefault, c->xs));
@@ -1396,7 +1461,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   // CUDA graph of the step body (embed ... argmax): models without a streaming
   // cycle, one graph per batch size, captured on the second step of that size
   // (the first runs eagerly so cuBLASLt plans/autotuning happen outside capture)
-  const bool graphable = (c->cfg.flags & MIRAGE_FLAG_CUDA_GRAPHS) && m == 0 &&
+  const bool graphable = (c->cfg.flags & MIRAGE_FLAG_CUDA_GRAPHS) && m == 0 && !reloading &&
                          !(c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) && !M->tp_ready;
   if (c->tp > 1 && !c->nccl && !M->tp_ready)
     return fail(c, MIRAGE_ERR_STATE, "step: tensor parallel model without a collective (tp_import first)");
@@ -1553,6 +1618,54 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   if (m) M->cyc_steps++;
   M->steps++;
   for (int i = 0; i < B; ++i) M->lens[seq_ids[i]] = positions[i] + 1;
+  return MIRAGE_OK;
+}
+
+// Prefill / extend (§2.1; the cold-start prefill of P:395-397).
+// The prompts' tokens are laid out as rows of decode steps (one row per token,
+// rows of one sequence at consecutive positions) and run in chunks of at most
+// max_batch rows. Each chunk is one layer-major pass, so a chunk's layer l waits
+// only for layer l's weights (an asynchronous reload, mirage_unremap, overlaps
+// with the chunk's earlier layers).
+int32_t mirage_prefill(mirage_ctx* c, int32_t model, int32_t n_seqs, const int64_t* seq_ids,
+                       const int32_t* prompt_lens, const int32_t* tokens, int32_t* last_argmax_out) {
+  GUARD(c);
+  Model* M = get_model(c, model);
+  if (!M || n_seqs <= 0 || !seq_ids || !prompt_lens || !tokens)
+    return fail(c, MIRAGE_ERR_RANGE, "prefill: arguments");
+  std::vector<int64_t> rs;
+  std::vector<int32_t> rt, rp, last_row(n_seqs);
+  int64_t tok = 0;
+  for (int i = 0; i < n_seqs; ++i) {
+    if (prompt_lens[i] <= 0) return fail(c, MIRAGE_ERR_RANGE, "prefill: prompt %d has length %d", i, prompt_lens[i]);
+    for (int j = 0; j < i; ++j)
+      if (seq_ids[j] == seq_ids[i]) return fail(c, MIRAGE_ERR_RANGE, "prefill: duplicate seq");
+    const int32_t p0 = M->lens.count(seq_ids[i]) ? M->lens[seq_ids[i]] : 0;
+    auto it = M->tables.find(seq_ids[i]);  // all blocks checked before the first chunk runs
+    const int need = (p0 + prompt_lens[i] + kBlockTokens - 1) / kBlockTokens;
+    if (it == M->tables.end() || (int)it->second.size() < need)
+      return fail(c, MIRAGE_ERR_NO_BLOCKS, "prefill: seq %lld needs %d blocks", (long long)seq_ids[i], need);
+    if (p0 + prompt_lens[i] > c->cfg.max_ctx || p0 + prompt_lens[i] > M->shp.max_pos)
+      return fail(c, MIRAGE_ERR_RANGE, "prefill: seq %lld exceeds max_ctx", (long long)seq_ids[i]);
+    for (int32_t t = 0; t < prompt_lens[i]; ++t) {
+      rs.push_back(seq_ids[i]);
+      rt.push_back(tokens[tok++]);
+      rp.push_back(p0 + t);
+    }
+    last_row[i] = (int32_t)rs.size() - 1;
+  }
+  const int64_t R = (int64_t)rs.size();
+  std::vector<int32_t> am(last_argmax_out ? R : 0);
+  for (int64_t r0 = 0; r0 < R; r0 += c->cfg.max_batch) {
+    const int32_t n = (int32_t)std::min<int64_t>(c->cfg.max_batch, R - r0);
+    if (int32_t e = mirage_decode_step(c, model, n, rs.data() + r0, rt.data() + r0, rp.data() + r0, nullptr,
+                                       last_argmax_out ? am.data() + r0 : nullptr))
+      return e;
+  }
+  if (last_argmax_out) {
+    CK(c, cudaStreamSynchronize(c->cs));
+    for (int i = 0; i < n_seqs; ++i) last_argmax_out[i] = am[last_row[i]];
+  }
   return MIRAGE_OK;
 }
 

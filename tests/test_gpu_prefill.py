@@ -1,0 +1,196 @@
+"""Prefill / extend through the C-ABI (rows of one sequence at consecutive
+positions in one step; mirage_prefill chunks them by max_batch) against oracle
+c4, which defines prefill as the causal forward, token by token (PAPER.md:131-138
+§2.1; pinned to HF's one-shot causal forward in tests/test_oracle_decode.py).
+Cold start: an inactive donor's
+reclaimed layers are reloaded asynchronously by mirage_unremap and its prefill
+waits per layer; the result is bit-identical to a donor that was never
+reclaimed, and wrong when the per-layer waits are removed on a slow link.
+GPU only."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import harness
+from oracle.decode import Decoder
+from synth import models, weights, workload
+
+pytestmark = pytest.mark.gpu
+
+REL_RMS, MAX_ABS = 1e-2, 5e-2     # DESIGN.md reading #19 (end-to-end bf16 decode)
+LENS = [1, 7, 16, 17, 40, 3]      # ragged: single token, block boundary, one past it, 3 blocks
+
+
+def prompt(seq, n, vocab):
+    return [workload.teacher_tokens(seq, t, vocab) for t in range(n)]
+
+
+def oracle_for(shape, seed):
+    return Decoder(shape, [weights.layer_tensors(shape, l, seed) for l in range(shape.n_layers)],
+                   weights.global_tensors(shape, seed), round_points=True)
+
+
+def check(got, ref, what):
+    rel = np.sqrt(((got - ref) ** 2).mean() / (ref ** 2).mean())
+    assert rel <= REL_RMS and np.abs(got - ref).max() <= MAX_ABS, (what, rel, np.abs(got - ref).max())
+
+
+def new_ctx(shape, seed, rows, n_native=64, max_ctx=128):
+    from paper_2507_11507_b200 import Context
+    ctx = Context(harness.arena_for([(shape, n_native)], rows, max_ctx), rows, max_ctx)
+    mid = ctx.add_model(shape, harness.make_blob(shape, seed=seed), n_native)
+    return ctx, mid
+
+
+@pytest.mark.parametrize("shape", [models.TOY, models.TOY_LLAMA])
+def test_multirow_step_matches_oracle_row_by_row(shape):
+    """All prompt tokens of all sequences as rows of ONE step: every row's final
+    hidden equals the oracle's causal forward at that position."""
+    seed, seqs = 11, list(range(len(LENS)))
+    rows = sum(LENS)
+    ctx, mid = new_ctx(shape, seed, rows)
+    for s, n in zip(seqs, LENS):
+        ctx.alloc_blocks(mid, s, harness.blocks_for(n + 4))
+    rs = [s for s, n in zip(seqs, LENS) for _ in range(n)]
+    rt = [t for s, n in zip(seqs, LENS) for t in prompt(s, n, shape.vocab)]
+    rp = [p for n in LENS for p in range(n)]
+    hid = torch.empty((rows, shape.d_model), dtype=torch.bfloat16, device="cuda")
+    am = ctx.decode_step(mid, rs, rt, rp, hidden_out=hid)
+    ctx.sync()
+    got = hid.float().cpu().numpy()
+    dec = oracle_for(shape, seed)
+    for i, (s, t, p) in enumerate(zip(rs, rt, rp)):
+        x, lg = dec.step_one(s, t, p)
+        check(got[i], x, (s, p))
+        srt = np.sort(lg)
+        if srt[-1] - srt[-2] > 0.5:
+            assert am[i] == int(np.argmax(lg)), (s, p)
+    for s, n in zip(seqs, LENS):
+        assert ctx.seq_len(mid, s) == n
+    # then ordinary decode steps continue from the cached prompts
+    for k in range(4):
+        toks = [workload.teacher_tokens(s, n + k, shape.vocab) for s, n in zip(seqs, LENS)]
+        pos = [n + k for n in LENS]
+        h2 = torch.empty((len(seqs), shape.d_model), dtype=torch.bfloat16, device="cuda")
+        ctx.decode_step(mid, seqs, toks, pos, hidden_out=h2)
+        ctx.sync()
+        ref, _, _ = dec.step(seqs, toks, pos)
+        check(h2.float().cpu().numpy(), ref, ("decode", k))
+
+
+@pytest.mark.parametrize("shape", [models.TOY, models.TOY_LLAMA])
+def test_prefill_chunks_match_oracle(shape):
+    """mirage_prefill with max_batch = 16 rows: chunks split sequences mid-prompt;
+    the next-token argmax and the following decode step match the oracle."""
+    seed, seqs = 12, [5, 9, 2, 30, 31, 7]
+    ctx, mid = new_ctx(shape, seed, 16)
+    for s, n in zip(seqs, LENS):
+        ctx.alloc_blocks(mid, s, harness.blocks_for(n + 1))
+    prompts = [prompt(s, n, shape.vocab) for s, n in zip(seqs, LENS)]
+    am = ctx.prefill(mid, seqs, prompts)
+    dec = oracle_for(shape, seed)
+    for s, p, a in zip(seqs, prompts, am):
+        for t, tok in enumerate(p):
+            _, lg = dec.step_one(s, tok, t)
+        srt = np.sort(lg)
+        if srt[-1] - srt[-2] > 0.5:
+            assert a == int(np.argmax(lg)), s
+    # extend: a second prefill call appends at the cached length
+    more = [[workload.teacher_tokens(s, 1000 + j, shape.vocab) for j in range(3)] for s in seqs[:2]]
+    for s in seqs[:2]:
+        ctx.alloc_blocks(mid, s, 1)
+    ctx.prefill(mid, seqs[:2], more, argmax=False)
+    for s, p in zip(seqs[:2], more):
+        for j, tok in enumerate(p):
+            dec.step_one(s, tok, dec.cache_len(s))
+    cur = [ctx.seq_len(mid, s) for s in seqs]
+    assert cur == [n + 3 if i < 2 else n for i, n in enumerate(LENS)]
+    toks = [workload.teacher_tokens(s, 77, shape.vocab) for s in seqs]
+    hid = torch.empty((len(seqs), shape.d_model), dtype=torch.bfloat16, device="cuda")
+    ctx.decode_step(mid, seqs, toks, cur, hidden_out=hid)
+    ctx.sync()
+    ref, _, _ = dec.step(seqs, toks, cur)
+    check(hid.float().cpu().numpy(), ref, "after prefill")
+
+
+def test_multirow_errors():
+    from paper_2507_11507_b200 import MirageError
+    shape = models.TOY
+    ctx, mid = new_ctx(shape, 1, 8)
+    ctx.alloc_blocks(mid, 0, 1)
+    with pytest.raises(MirageError):      # rows of one seq must be consecutive from the cached length
+        ctx.decode_step(mid, [0, 0], [1, 2], [0, 2])
+    with pytest.raises(MirageError):
+        ctx.decode_step(mid, [0, 0], [1, 2], [1, 2])
+    with pytest.raises(MirageError):      # 17 tokens need 2 blocks
+        ctx.prefill(mid, [0], [list(range(17))])
+    assert ctx.seq_len(mid, 0) == 0       # nothing committed on error
+    ctx.prefill(mid, [0], [list(range(16))])
+    assert ctx.seq_len(mid, 0) == 16
+
+
+COLD = r"""
+import sys, torch, numpy as np
+sys.path.insert(0, %(root)r)
+import harness
+from paper_2507_11507_b200 import Context
+from synth import models, workload
+a, d = models.TOY, models.TOY_LLAMA
+LENS = [5, 17, 32, 9]
+prompts = [[workload.teacher_tokens(s, t, d.vocab) for t in range(n)] for s, n in enumerate(LENS)]
+
+def donor_run(ctx, md):
+    for s, n in enumerate(LENS):
+        ctx.alloc_blocks(md, s, harness.blocks_for(n + 1))
+    am = ctx.prefill(md, list(range(len(LENS))), prompts, argmax=False)
+    hid = torch.empty((len(LENS), d.d_model), dtype=torch.bfloat16, device="cuda")
+    ctx.decode_step(md, list(range(len(LENS))), [7] * len(LENS), LENS, hidden_out=hid)
+    ctx.sync()
+    return hid.float().cpu().numpy()
+
+# reference: the donor was never reclaimed
+ref_ctx = Context(harness.arena_for([(d, 16)], 64, 128), 64, 128)
+ref = donor_run(ref_ctx, ref_ctx.add_model(d, harness.make_blob(d, seed=8), 16))
+ref_ctx.close()
+
+ctx = Context(harness.arena_for([(a, 8), (d, 16)], 64, 128), 64, 128)
+ma = ctx.add_model(a, harness.make_blob(a, seed=7), 8)
+md = ctx.add_model(d, harness.make_blob(d, seed=8), 16)
+ctx.set_active(md, False)
+ctx.remap_layers(md, ma, [0, 1], 0)                   # the inactive donor is reclaimed whole
+for s in range(8):                                    # A's KV overwrites D's parameter bytes
+    ctx.alloc_blocks(ma, s, 3)
+for t in range(40):
+    ctx.decode_step(ma, list(range(8)), [workload.teacher_tokens(s, t, a.vocab) for s in range(8)], [t] * 8)
+for s in range(8):
+    ctx.free_blocks(ma, s)
+for r in range(len(ctx.regions(ma))):
+    ctx.unremap(ma, r)                                # asynchronous reload on the copy stream
+ctx.set_active(ma, False)
+ctx.set_active(md, True)
+got = donor_run(ctx, md)                              # enqueued at once: gated per layer
+print("MATCH", int(np.array_equal(got, ref)), "H2D", ctx.query(md)["h2d_copies"])
+"""
+
+
+def run_cold(mode):
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("MIRAGE_PREFETCH_DEBUG", None)
+    if mode is not None:
+        env["MIRAGE_PREFETCH_DEBUG"] = str(mode)
+    r = subprocess.run([sys.executable, "-c", COLD % {"root": root}], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("MATCH")][-1].split()
+    return int(line[1]), int(line[3])
+
+
+def test_cold_start_reload_gated_per_layer():
+    assert run_cold(None) == (1, 2)     # both donor layers reloaded, prefill bit-identical
+    assert run_cold(4)[0] == 1          # slow link (20 ms per layer), waits kept: still exact
+    assert run_cold(3)[0] == 0          # slow link, waits removed: the prefill reads KV bytes
