@@ -243,12 +243,16 @@ int32_t mirage_region_info(mirage_ctx* ctx, int32_t model, int32_t idx, mirage_r
  * restored for parameter usage", :830-839 §7.6.1): give region `region` of
  * `recipient` back to its donor's parameters. Every block of the region must be
  * free; the ids are retired (never handed out again, reading #13); the layers'
- * weights are reloaded from the host copy on the COPY stream, ordered after
- * every kernel already enqueued on the compute stream (the last readers of the
- * bytes as KV), one event per layer. The call returns without waiting: the first
- * kernel of a later decode step / prefill that reads layer l waits for layer l's
- * event only, so a cold start's prefill overlaps the reload layer by layer
- * ("T_T * N <= T_Compute" with T_Compute = prefill). A
+ * weights are reloaded from the host copy on the COPY stream, one event per
+ * layer. The call returns without waiting and enqueues nothing: the donor's next
+ * decode step / prefill issues the copies right after its own metadata upload
+ * (the host-to-device copy engine is FIFO across streams, so copies queued
+ * earlier would hold that upload back), ordered after every kernel enqueued
+ * before it on the compute stream (the last readers of the bytes as KV); its
+ * first kernel that reads layer l waits for layer l's event only, so a cold
+ * start's prefill overlaps the reload layer by layer (PAPER.md:387, :395-397
+ * "T_T * N <= T_Compute" with T_Compute = prefill). mirage_sync also issues
+ * requested reloads. A
  * region of a streaming self-remap reverts the donor's whole cycle (all its
  * regions, slot holders reloaded, streaming stops at the next step).
  * Errors: RANGE; STATE (already reverted); PRESSURE (blocks still hold KV);

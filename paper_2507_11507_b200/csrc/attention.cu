@@ -142,8 +142,8 @@ paged_attention_kernel(const AttnParams p) {
   const int tq = lane & 3;   // thread in group
   const int n_flat = (p.n_units_dev ? *p.n_units_dev : p.n_units) * p.H_kv;  // item f = unit * H_kv + kv head
   uint8_t* ring = smem + (size_t)warp * NS * 2 * TILE;
-  // q staging (dynamic smem after the rings): [QB][G*D] fp32, one copy per CTA item
-  float(*qbuf)[G * D] = reinterpret_cast<float(*)[G * D]>(smem + (size_t)kWarps * NS * 2 * TILE);
+  // q staging (dynamic smem after the rings): [QB][G][2][D/2] packed bf16 hi|lo words, one copy per CTA item
+  uint32_t(*qbuf)[G * D] = reinterpret_cast<uint32_t(*)[G * D]>(smem + (size_t)kWarps * NS * 2 * TILE);
 
   if (lane == 0) {
 #pragma unroll
@@ -171,7 +171,7 @@ paged_attention_kernel(const AttnParams p) {
         item = atomicAdd(p.sched, 1);
         if (item < n_flat) {
           const AttnUnit u = p.units[item / p.H_kv];
-          const float* src = p.q + ((size_t)u.seq * p.H + (item % p.H_kv) * G) * D;
+          const uint32_t* src = p.q + ((size_t)u.seq * p.H + (item % p.H_kv) * G) * D;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           mbar_expect_tx(&qbars[sl], G * D * 4);
           bulk_g2s(&qbuf[sl][0], src, G * D * 4, &qbars[sl]);
@@ -250,21 +250,21 @@ paged_attention_kernel(const AttnParams p) {
     const int first = u.b0 + warp;
     const int n_it = first < u.b1 ? (u.b1 - first + kWarps - 1) / kWarps : 0;
 
-    // B fragments of the query columns: column n = gq (+8 nt): head nt*4 + gq/2, part gq&1
+    // B fragments of the query columns: column n = gq (+8 nt): head nt*4 + gq/2, part gq&1.
+    // q arrives pre-scaled and pre-split (qkv_post): word i of (head, part) packs
+    // elements 2i, 2i+1, so a fragment is two shared-memory words.
     uint32_t qb[NT][KS][2];
-    const float* qs = &qbuf[ck % QB][0];
+    const uint32_t* qs = &qbuf[ck % QB][0];
     if (n_it > 0) mbar_wait(&qbars[ck % QB], (ck / QB) & 1);
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int hh = nt * 4 + (gq >> 1);
-      const int part = gq & 1;
+      const uint32_t* qw = qs + hh * D + (gq & 1) * (D / 2) + tq;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         if (hh < G && n_it > 0) {
-          const float* qp = qs + hh * D + ks * 16 + 2 * tq;
-          const float sc = p.scale_log2;
-          qb[nt][ks][0] = pack_bf16(bf16_part(qp[0] * sc, part), bf16_part(qp[1] * sc, part));
-          qb[nt][ks][1] = pack_bf16(bf16_part(qp[8] * sc, part), bf16_part(qp[9] * sc, part));
+          qb[nt][ks][0] = qw[ks * 8];
+          qb[nt][ks][1] = qw[ks * 8 + 4];
         } else {
           qb[nt][ks][0] = qb[nt][ks][1] = 0u;
         }
@@ -296,20 +296,24 @@ paged_attention_kernel(const AttnParams p) {
         }
         __syncwarp();
       }
-      // ---- S = K Qc ----
-      float sacc[NT][4];
+      // ---- S = K Qc (two independent accumulation chains: even / odd k-slices) ----
+      float sacc[NT][4], sacc2[NT][4];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) sacc[nt][j] = 0.f;
+        for (int j = 0; j < 4; ++j) sacc[nt][j] = sacc2[nt][j] = 0.f;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         uint32_t a[4];
         const int c = 2 * ks + k_cadd;
         ldsm_x4(a, tile + k_row * ROW + ((c ^ (k_row & 7)) << 4));
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) mma_bf16(sacc[nt], a, qb[nt][ks]);
+        for (int nt = 0; nt < NT; ++nt) mma_bf16((ks & 1) ? sacc2[nt] : sacc[nt], a, qb[nt][ks]);
       }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sacc[nt][j] += sacc2[nt][j];
       // ---- online softmax (base 2) per head nt*4+tq; rows gq and gq+8 ----
       float pA[NT], pB[NT];
 #pragma unroll
@@ -321,15 +325,20 @@ paged_attention_kernel(const AttnParams p) {
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
         const float m_new = fmaxf(m[nt], bm);
-        const float alpha = exp2f(m[nt] - m_new);
         pA[nt] = exp2f(s0 - m_new);
         pB[nt] = exp2f(s1 - m_new);
-        l[nt] = l[nt] * alpha + pA[nt] + pB[nt];
+        // rescale only when some head's running max moved (alpha == 1 otherwise:
+        // skipping the multiply by exactly 1 leaves every bit unchanged)
+        if (__any_sync(0xffffffffu, m_new != m[nt])) {
+          const float alpha = exp2f(m[nt] - m_new);
+          l[nt] *= alpha;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[nt][ks][j] *= alpha;
+        }
+        l[nt] = l[nt] + pA[nt] + pB[nt];
         m[nt] = m_new;
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) o[nt][ks][j] *= alpha;
       }
       // ---- P as B fragments: lane needs P[2tq, 2tq+1, 2tq+8, 2tq+9][column gq] ----
       uint32_t pb[NT][2];

@@ -19,14 +19,15 @@ struct AttnUnit {
 };
 
 struct AttnParams {
-  const float* q;              // [B][H][D] fp32 (unscaled)
+  const uint32_t* q;           // [B][H][2][D/2]: q * scale_log2 split into bf16 hi (part 0) and
+                               // lo = bf16(x - hi) (part 1); word i packs elements 2i (low half), 2i+1
   const uint64_t* addrs;       // per-step block base addresses (host-resolved table -> block_base)
   uint64_t layer_off;          // layer * H_kv * 2 * 16 * D * 2 bytes
   const AttnUnit* units;       // [n_units], longest first
   int32_t n_units;             // host count (sizes the grid)
   const int32_t* n_units_dev;  // if set, the count is read here (CUDA-graph replays)
   int32_t H, H_kv, D;
-  float scale_log2;            // log2(e) / sqrt(D)
+  float scale_log2;            // log2(e) / sqrt(D) (already applied to q)
   float* partial;              // [(pbase + split) * H + h][D + 2]
   int32_t* tickets;            // [B * H_kv], zero between launches
   int32_t* sched;              // [2] dynamic item counter + finished CTAs, zero between launches
@@ -52,12 +53,25 @@ cudaError_t launch_residual_norm(int family, int B, int d, const float* y, int l
                                  const __nv_bfloat16* bias, const __nv_bfloat16* g,
                                  const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
                                  cudaStream_t s);
-// qkv [B][(H+2Hk)D] fp32 (+bias, +RoPE) -> q fp32 [B][H][D]; K/V bf16 appended to
-// the paged cache at positions[b] (block address addrs[seq_off[b] + pos / 16]).
+// qkv [B][(H+2Hk)D] fp32 (+bias, +RoPE) -> q in the attention kernel's split
+// format (AttnParams::q, scaled by q_scale); K/V bf16 appended to the paged cache
+// at positions[b] (block address addrs[seq_off[b] + pos / 16]).
 cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float* qkv,
                             const __nv_bfloat16* bias, const int32_t* positions,
                             const int32_t* seq_off, const uint64_t* addrs, uint64_t layer_off,
-                            float rope_theta, float* q, cudaStream_t s);
+                            float rope_theta, float q_scale, uint32_t* q, cudaStream_t s);
+// Step metadata upload without the copy engine: the kernel reads the pinned
+// (UVA-mapped) staging buffer over the host link with SM loads and writes the
+// device copy. A DMA would queue behind large H2D weight copies already in the
+// copy engine (re-streaming, reloads); this keeps the compute stream
+// independent of them. Segments are 16-byte aligned, byte counts rounded up to 16.
+struct PullSegs {
+  uint32_t off[8], bytes[8];
+  int n;
+};
+cudaError_t launch_meta_pull(char* dst, const char* src_host, const PullSegs& segs, cudaStream_t s);
+// fp32 q [n_rows * D] (unscaled) -> the split format of AttnParams::q (test hook path)
+cudaError_t launch_q_split(int64_t n, int D, const float* q, float q_scale, uint32_t* out, cudaStream_t s);
 // OPT: f = bf16(relu(y + b)); Llama: f = bf16(silu(y[:, :f]) * y[:, f:]).
 cudaError_t launch_act(int family, int B, int f, const float* y, const __nv_bfloat16* bias,
                        __nv_bfloat16* out, cudaStream_t s);

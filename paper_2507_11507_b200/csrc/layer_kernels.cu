@@ -6,6 +6,8 @@
 // library's own kernels between cuBLAS GEMMs.
 #include <math_constants.h>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace mirage {
@@ -20,6 +22,35 @@ __device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
   const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
+// 8 consecutive q elements (scaled) -> 4 words of part 0 (bf16 hi) at p and 4
+// words of part 1 (lo = bf16(x - hi)) at p + D/2; word k packs elements 2k, 2k+1.
+__device__ __forceinline__ void store_q_split(uint32_t* p, const float (&v)[8], float sc, int D) {
+  uint32_t hi[4], lo[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float a = v[2 * k] * sc, b = v[2 * k + 1] * sc;
+    const __nv_bfloat16 ah = __float2bfloat16_rn(a), bh = __float2bfloat16_rn(b);
+    const __nv_bfloat16 al = __float2bfloat16_rn(a - __bfloat162float(ah));
+    const __nv_bfloat16 bl = __float2bfloat16_rn(b - __bfloat162float(bh));
+    hi[k] = (uint32_t)__bfloat16_as_ushort(ah) | ((uint32_t)__bfloat16_as_ushort(bh) << 16);
+    lo[k] = (uint32_t)__bfloat16_as_ushort(al) | ((uint32_t)__bfloat16_as_ushort(bl) << 16);
+  }
+  *reinterpret_cast<uint4*>(p) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  *reinterpret_cast<uint4*>(p + D / 2) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+}
+
+__global__ void q_split_kernel(int64_t n8, int D, const float* q, float sc, uint32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 8, row = e / D;
+    const int col = (int)(e % D);
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = q[e + k];
+    uint32_t* dst = out + row * D + col / 2;  // word i of a part packs dims 2i, 2i+1
+    store_q_split(dst, v, sc, D);
+  }
+}
+
 __device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
   *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
   *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
@@ -211,7 +242,7 @@ tp_residual_norm_kernel(int family, int d, const float* const* parts, int tp, in
 __global__ void __launch_bounds__(256)
 qkv_post_kernel(int family, int H, int Hk, int D, const float* qkv, const __nv_bfloat16* bias,
                 const int32_t* positions, const int32_t* seq_off, const uint64_t* addrs,
-                uint64_t layer_off, float rope_theta, float* q) {
+                uint64_t layer_off, float rope_theta, float q_scale, uint32_t* q) {
   extern __shared__ float cs[];  // [D/2] cos, [D/2] sin
   const int b = blockIdx.x;
   const int pos = positions[b];
@@ -257,10 +288,10 @@ qkv_post_kernel(int family, int H, int Hk, int D, const float* qkv, const __nv_b
           x1[k] = y1;
         }
       }
-      if (hh < H) {
-        float* qd = q + ((size_t)b * H + hh) * D + c * 8;
-        store8(qd, x0);
-        store8(qd + half, x1);
+      if (hh < H) {  // q * scale, split into bf16 hi | lo word pairs (AttnParams::q)
+        uint32_t* qd = q + ((size_t)b * H + hh) * D + c * 4;
+        store_q_split(qd, x0, q_scale, D);
+        store_q_split(qd + half / 2, x1, q_scale, D);
       } else {
         char* dst = kvbase + ((size_t)((hh - H) * 2 + 0) * 16 + r) * D * 2;
         *reinterpret_cast<uint4*>(dst + ((c ^ (r & 7)) << 4)) = pack8bf(x0);
@@ -467,9 +498,41 @@ cudaError_t launch_residual_norm(int family, int B, int d, const float* y, int l
 cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float* qkv,
                             const __nv_bfloat16* bias, const int32_t* positions,
                             const int32_t* seq_off, const uint64_t* addrs, uint64_t layer_off,
-                            float rope_theta, float* q, cudaStream_t s) {
+                            float rope_theta, float q_scale, uint32_t* q, cudaStream_t s) {
   qkv_post_kernel<<<B, 256, D * sizeof(float), s>>>(family, H, Hk, D, qkv, bias, positions, seq_off,
-                                                    addrs, layer_off, rope_theta, q);
+                                                    addrs, layer_off, rope_theta, q_scale, q);
+  return cudaGetLastError();
+}
+
+__global__ void meta_pull_kernel(char* dst, const char* src, PullSegs g) {
+  uint32_t total = 0;
+  for (int k = 0; k < g.n; ++k) total += g.bytes[k] / 16;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t j = i;
+    int k = 0;
+    while (j >= g.bytes[k] / 16) j -= g.bytes[k++] / 16;
+    const size_t o = g.off[k] + (size_t)j * 16;
+    *reinterpret_cast<uint4*>(dst + o) = __ldcv(reinterpret_cast<const uint4*>(src + o));  // no stale cache
+  }
+}
+
+cudaError_t launch_meta_pull(char* dst, const char* src_host, const PullSegs& segs, cudaStream_t s) {
+  uint32_t total = 0;
+  for (int k = 0; k < segs.n; ++k) {
+    if (segs.off[k] % 16 || segs.bytes[k] % 16) return cudaErrorInvalidValue;
+    total += segs.bytes[k] / 16;
+  }
+  if (!total) return cudaSuccess;
+  const int threads = 256;
+  const int blocks = (int)std::min<uint32_t>((total + threads - 1) / threads, 296);
+  meta_pull_kernel<<<blocks, threads, 0, s>>>(dst, src_host, segs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_q_split(int64_t n, int D, const float* q, float q_scale, uint32_t* out, cudaStream_t s) {
+  if (n % 8 || D % 16) return cudaErrorInvalidValue;
+  const int64_t n8 = n / 8;
+  q_split_kernel<<<(int)std::min<int64_t>((n8 + 255) / 256, 4096), 256, 0, s>>>(n8, D, q, q_scale, out);
   return cudaGetLastError();
 }
 

@@ -177,6 +177,11 @@ struct Model {
   // stream; the first kernel that reads layer l waits for reload_ev[l]
   std::vector<cudaEvent_t> reload_ev;  // per layer, created on first use
   std::vector<char> reload_pending;
+  // layers whose reload is requested but not yet enqueued: the copies are issued
+  // by the model's next step right after its metadata upload (the host->device
+  // copy engine is FIFO across streams, so copies queued earlier would hold the
+  // step's own upload back until all of them finished)
+  std::vector<int32_t> reload_queue;
   uint32_t* slot_tag = nullptr;   // device [MAX_CYCLE] tag of the layer each slot holds (SLOT_TAGS)
   uint32_t* tag_err = nullptr;    // device [2] mismatch count, last bad tag
   uint32_t* host_tags = nullptr;  // pinned [n_layers] tag values copied behind each layer DMA
@@ -187,7 +192,7 @@ struct Model {
   float* h = nullptr;
   bf16* x = nullptr;
   float* y = nullptr;
-  float* q = nullptr;
+  uint32_t* q = nullptr;  // [B][H][2][D/2] split-format q (AttnParams::q)
   bf16* f = nullptr;
   float* partial = nullptr;
   int32_t* tickets = nullptr;
@@ -424,6 +429,33 @@ size_t meta_size(mirage_ctx* c) {
   const int Bm = c->cfg.max_batch;
   return 16 + 4 * align_up((uint64_t)Bm * 4, 16) + align_up((uint64_t)c->max_units * sizeof(mirage::AttnUnit), 16) +
          (uint64_t)Bm * c->max_blk * 8;
+}
+
+uint32_t up16(size_t x) { return (uint32_t)((x + 15) & ~(size_t)15); }
+
+// Upload the used parts of a packed step (header, B-row arrays, n_units units,
+// n_addr addresses) from staging buffer `host` with the pull kernel.
+int32_t upload_meta(mirage_ctx* c, char* host, int B, int n_units, int n_addr, size_t* bytes_out = nullptr) {
+  MetaView hv = meta_view(c, host);
+  mirage::PullSegs g{};
+  auto seg = [&](const void* p, size_t bytes) {
+    g.off[g.n] = (uint32_t)(reinterpret_cast<const char*>(p) - host);
+    g.bytes[g.n] = up16(bytes);
+    ++g.n;
+  };
+  seg(hv.hdr, 16);
+  seg(hv.tokens, (size_t)B * 4);
+  seg(hv.pos, (size_t)B * 4);
+  seg(hv.len, (size_t)B * 4);
+  seg(hv.seq_off, (size_t)B * 4);
+  seg(hv.units, (size_t)n_units * sizeof(mirage::AttnUnit));
+  seg(hv.addrs, (size_t)n_addr * 8);
+  KL(c, mirage::launch_meta_pull(c->meta_dev, host, g, c->cs));
+  if (bytes_out) {
+    *bytes_out = 0;
+    for (int k = 0; k < g.n; ++k) *bytes_out += g.bytes[k];
+  }
+  return MIRAGE_OK;
 }
 
 int32_t acquire_stage(mirage_ctx* c, char** host) {
@@ -716,7 +748,7 @@ int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
   if (cublasSetWorkspace(c->blas, c->blas_ws, kCublasWs) != CUBLAS_STATUS_SUCCESS ||
       cublasSetStream(c->blas, c->cs) != CUBLAS_STATUS_SUCCESS)
     return bail(MIRAGE_ERR_CUDA);
-  c->meta_bytes = meta_size(c);
+  c->meta_bytes = meta_size(c) + 16;  // segments are rounded up to 16 bytes
   for (int i = 0; i < 2; ++i) {
     if (cudaHostAlloc(reinterpret_cast<void**>(&c->stage[i]), c->meta_bytes, cudaHostAllocDefault) !=
             cudaSuccess ||
@@ -835,7 +867,7 @@ int32_t mirage_add_model(mirage_ctx* c, const mirage_model_cfg* mc, const void* 
   M->h = reinterpret_cast<float*>(C(w.h));
   M->x = reinterpret_cast<bf16*>(C(w.x));
   M->y = reinterpret_cast<float*>(C(w.y));
-  M->q = reinterpret_cast<float*>(C(w.q));
+  M->q = reinterpret_cast<uint32_t*>(C(w.q));
   M->f = reinterpret_cast<bf16*>(C(w.f));
   M->partial = reinterpret_cast<float*>(C(w.partial));
   M->tickets = reinterpret_cast<int32_t*>(C(w.tickets));
@@ -970,9 +1002,45 @@ int32_t mirage_set_weight_source(mirage_ctx* c, int32_t model, const void* src, 
   return MIRAGE_OK;
 }
 
+// Enqueue M's requested reloads on the copy stream, ordered after everything
+// enqueued so far on the compute stream (the last readers of the bytes as KV,
+// and the caller's metadata upload), one event per layer (reload_ev).
+static int32_t flush_reloads(mirage_ctx* c, Model* D) {
+  if (D->reload_queue.empty() || c->host_only) return MIRAGE_OK;
+  std::vector<int32_t> layers;
+  layers.swap(D->reload_queue);
+  std::sort(layers.begin(), layers.end());
+  layers.erase(std::unique(layers.begin(), layers.end()), layers.end());
+  cudaEvent_t e;
+  CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(c, cudaEventRecord(e, c->cs));
+  CK(c, cudaStreamWaitEvent(c->xs, e, 0));
+  cudaEventDestroy(e);
+  if (D->reload_ev.empty()) {
+    D->reload_ev.assign(D->shp.n, nullptr);
+    D->reload_pending.assign(D->shp.n, 0);
+  }
+  for (int32_t l : layers) {
+    if (!D->reload_ev[l]) CK(c, cudaEventCreateWithFlags(&D->reload_ev[l], cudaEventDisableTiming));
+    CopyTiming t{pool_event(D), pool_event(D), D->sz.S};
+    if (!t.t0 || !t.t1) return fail(c, MIRAGE_ERR_CUDA, "reload: event pool");
+    CK(c, cudaEventRecord(t.t0, c->xs));
+    if (prefetch_debug() == 3 || prefetch_debug() == 4)  // test hook: a slow link
+      KL(c, mirage::launch_spin(20000000ull, c->xs));
+    CK(c, cudaMemcpyAsync(D->w_dev + (uint64_t)l * D->sz.S, D->host + (uint64_t)l * D->sz.S, D->sz.S,
+                          cudaMemcpyDefault, c->xs));
+    CK(c, cudaEventRecord(t.t1, c->xs));
+    CK(c, cudaEventRecord(D->reload_ev[l], c->xs));
+    D->pending.push_back(t);
+    D->reload_pending[l] = 1;
+  }
+  return MIRAGE_OK;
+}
+
 // Order the compute stream after every pending asynchronous reload of M (before
 // M's weight bytes are handed out again, swapped or re-streamed).
 static int32_t settle_reloads(mirage_ctx* c, Model* M) {
+  if (int32_t e = flush_reloads(c, M)) return e;
   for (size_t l = 0; l < M->reload_pending.size(); ++l)
     if (M->reload_pending[l]) {
       CK(c, cudaStreamWaitEvent(c->cs, M->reload_ev[l], 0));
@@ -1157,31 +1225,9 @@ int32_t mirage_unremap(mirage_ctx* c, int32_t recipient, int32_t region) {
     // event gates the first kernel that reads it (mirage_decode_step /
     // mirage_prefill), so a cold start's prefill overlaps the reload layer by
     // layer (T_T * N <= T_Compute of the prefill).
-    cudaEvent_t e;
-    CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CK(c, cudaEventRecord(e, c->cs));
-    CK(c, cudaStreamWaitEvent(c->xs, e, 0));
-    cudaEventDestroy(e);
-    if (D->reload_ev.empty()) {
-      D->reload_ev.assign(D->shp.n, nullptr);
-      D->reload_pending.assign(D->shp.n, 0);
-    }
-    std::sort(layers.begin(), layers.end());
-    layers.erase(std::unique(layers.begin(), layers.end()), layers.end());
-    for (int32_t l : layers) {
-      if (!D->reload_ev[l]) CK(c, cudaEventCreateWithFlags(&D->reload_ev[l], cudaEventDisableTiming));
-      CopyTiming t{pool_event(D), pool_event(D), D->sz.S};
-      if (!t.t0 || !t.t1) return fail(c, MIRAGE_ERR_CUDA, "unremap: event pool");
-      CK(c, cudaEventRecord(t.t0, c->xs));
-      if (prefetch_debug() == 3 || prefetch_debug() == 4)  // test hook: a slow link
-        KL(c, mirage::launch_spin(20000000ull, c->xs));
-      CK(c, cudaMemcpyAsync(D->w_dev + (uint64_t)l * D->sz.S, D->host + (uint64_t)l * D->sz.S, D->sz.S,
-                            cudaMemcpyDefault, c->xs));
-      CK(c, cudaEventRecord(t.t1, c->xs));
-      CK(c, cudaEventRecord(D->reload_ev[l], c->xs));
-      D->pending.push_back(t);
-      D->reload_pending[l] = 1;
-    }
+    D->reload_queue.insert(D->reload_queue.end(), layers.begin(), layers.end());
+    if (was_cycle)  // the slots are needed now: no deferral
+      if (int32_t e = flush_reloads(c, D)) return e;
   }
   for (int32_t l : layers) D->layer_state[l] = RESIDENT;
   if (was_cycle) {
@@ -1386,14 +1432,14 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
                                   0, hv.units, c->max_units, &split_blocks);
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "step: too many attention units");
   hv.hdr[0] = n_units;
-  const size_t tbl_bytes = (size_t)n_addr * 8;
-  const size_t head = reinterpret_cast<char*>(hv.addrs) - host;
   cudaStream_t cs = c->cs;
   const bool timed = !M->step_timed;
   if (timed) CK(c, cudaEventRecord(M->st0, cs));
-  CK(c, cudaMemcpyAsync(c->meta_dev, host, head + tbl_bytes, cudaMemcpyHostToDevice, cs));
+  size_t meta_bytes = 0;
+  if (int32_t e = upload_meta(c, host, B, n_units, n_addr, &meta_bytes)) return e;
   CK(c, cudaEventRecord(c->stage_ev[c->stage_i], cs));
-  M->last_meta = head + tbl_bytes;
+  M->last_meta = meta_bytes;
+  if (int32_t e = flush_reloads(c, M)) return e;  // requested reloads start behind this step's upload
   M->last_units = n_units;
   M->last_split = split_blocks;
 
@@ -1517,7 +1563,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     const uint64_t layer_off = (uint64_t)l * Hk * 2 * kBlockTokens * D * 2;
     if (int32_t e = gemm_lt(c, B, qkvN, d, w.w_qkv, M->x, M->y, 0, nullptr, 0)) return e;
     KL(c, mirage::launch_qkv_post(s.family, B, H, Hk, D, M->y, opt ? w.b_qkv : nullptr, dv.pos,
-                                 dv.seq_off, dv.addrs, layer_off, s.theta, M->q, cs));
+                                 dv.seq_off, dv.addrs, layer_off, s.theta, ap.scale_log2, M->q, cs));
     ap.layer_off = layer_off;
     if (time_attn) {
       Model::AttnTiming at{pool_event(M), pool_event(M), attn_bytes};
@@ -1699,14 +1745,15 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
                                   mirage::attention_cta_warps(M->shp.Hk), split_tokens_override / kBlockTokens,
                                   hv.units, c->max_units, &split_blocks);
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "attn_only: too many units for the split override");
-  const size_t head = reinterpret_cast<char*>(hv.addrs) - host;
-  CK(c, cudaMemcpyAsync(c->meta_dev, host, head + (size_t)n_addr * 8, cudaMemcpyHostToDevice, c->cs));
+    if (int32_t e = upload_meta(c, host, B, n_units, n_addr)) return e;
   CK(c, cudaEventRecord(c->stage_ev[c->stage_i], c->cs));
   M->last_units = n_units;
   M->last_split = split_blocks;
   const Shape& s = M->shp;
   mirage::AttnParams ap{};
-  ap.q = q_dev;
+  ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)M->shp.D));
+  KL(c, mirage::launch_q_split((int64_t)B * M->shp.H * M->shp.D, M->shp.D, q_dev, ap.scale_log2, M->q, c->cs));
+  ap.q = M->q;
   ap.addrs = dv.addrs;
   ap.layer_off = (uint64_t)layer * s.Hk * 2 * kBlockTokens * s.D * 2;
   ap.units = dv.units;
@@ -1747,7 +1794,13 @@ static int32_t kv_hook_prepare(mirage_ctx* c, Model* M, int64_t seq_id, int32_t 
   MetaView hv = meta_view(c, host);
   std::copy(it->second.begin(), it->second.begin() + need, hv.tables);
   const size_t head = reinterpret_cast<char*>(hv.tables) - host;
-  CK(c, cudaMemcpyAsync(c->meta_dev + head, host + head, (size_t)need * 4, cudaMemcpyHostToDevice, c->cs));
+  {
+    mirage::PullSegs g{};
+    g.off[0] = (uint32_t)head;
+    g.bytes[0] = up16((size_t)need * 4);
+    g.n = 1;
+    KL(c, mirage::launch_meta_pull(c->meta_dev, host, g, c->cs));
+  }
   CK(c, cudaEventRecord(c->stage_ev[c->stage_i], c->cs));
   *p0 = len;
   return MIRAGE_OK;
@@ -1854,6 +1907,9 @@ int32_t mirage_slot_log(mirage_ctx* c, int32_t model, int64_t* out, int32_t cap,
 int32_t mirage_sync(mirage_ctx* c) {
   GUARD(c);
   if (c->host_only) return MIRAGE_OK;
+  for (Model* M : c->models)
+    if (M)
+      if (int32_t e = flush_reloads(c, M)) return e;
   CK(c, cudaStreamSynchronize(c->cs));
   CK(c, cudaStreamSynchronize(c->xs));
   CK(c, cudaGetLastError());

@@ -61,15 +61,20 @@ class HostPool:
 
 
 def serve(ctx, ctl, mid, shape, arrivals, prompts, outs, max_batch, revert_every=None, headroom=0, tag="",
-          on_exhaust="recompute", pool=None):
+          on_exhaust="recompute", pool=None, prefill="real"):
     """Closed decode loop. arrivals[t] = number of new requests at step t.
     on_exhaust: 'recompute' preempts the newest sequence (re-queued, vLLM-style);
-    'swap' moves its KV to host memory and back when blocks free up (Pie-style)."""
+    'swap' moves its KV to host memory and back when blocks free up (Pie-style).
+    prefill: 'real' runs the admitted prompts (and a recomputed sequence's prompt
+    + generated tokens) through mirage_prefill inside the step, so TBT includes
+    the prefill stall; 'fill' writes random prompt KV with mirage_fill_kv (no
+    prefill compute)."""
     _, _, BB = _lib.model_sizes(shape)
     swapped = []   # (sid, offset, nbytes)
     queue, running, pos, left = [], [], {}, {}
     nxt, step_ms, waits, t0s = 0, [], [], {}
     preempted = [0]
+    prefill_tokens = [0]
     held = {}
     C = __import__("ctypes")
     evs = []
@@ -96,21 +101,34 @@ def serve(ctx, ctl, mid, shape, arrivals, prompts, outs, max_batch, revert_every
             running.append(sid)
             held[sid] = harness.blocks_for(pos[sid])
         # admit in FIFO order while blocks allow (controller may remap on shortfall)
+        admitted = []
         while queue and len(running) < max_batch and not swapped:
             sid, ta = queue[0]
-            P = int(prompts[sid % len(prompts)])
+            resumed = sid in pos          # a preempted sequence: recompute prompt + generated tokens
+            P = pos[sid] if resumed else int(prompts[sid % len(prompts)])
             try:
                 ctl.alloc(sid, harness.blocks_for(P + 1)) if ctl else ctx.alloc_blocks(mid, sid, harness.blocks_for(P + 1))
             except _lib.MirageError as e:
                 if e.code != _lib.ERR_NO_BLOCKS:
                     raise
                 break
-            ctx.fill_kv(mid, sid, P, seed=sid)
+            if prefill == "fill":
+                ctx.fill_kv(mid, sid, P, seed=sid)
+            else:
+                admitted.append((sid, P))
             held[sid] = harness.blocks_for(P + 1)
             queue.pop(0)
             running.append(sid)
-            pos[sid], left[sid] = P, int(outs[sid % len(outs)])
+            if not resumed:
+                pos[sid], left[sid] = P, int(outs[sid % len(outs)])
             waits.append(t - ta)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream)
+        if admitted:
+            ctx.prefill(mid, [a for a, _ in admitted],
+                        [[workload.teacher_tokens(a, j, shape.vocab) for j in range(n)] for a, n in admitted],
+                        argmax=False)
+            prefill_tokens[0] += sum(n for _, n in admitted)
         if not running:
             t += 1
             continue
@@ -145,8 +163,7 @@ def serve(ctx, ctl, mid, shape, arrivals, prompts, outs, max_batch, revert_every
             t += 1
             continue
         toks = [workload.teacher_tokens(s, pos[s], shape.vocab) for s in batch]
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(ctx.stream)
+        e1 = torch.cuda.Event(enable_timing=True)
         ctx.decode_step(mid, batch, toks, [pos[s] for s in batch], argmax=False)
         e1.record(ctx.stream)
         evs.append((e0, e1, t))
@@ -164,6 +181,7 @@ def serve(ctx, ctl, mid, shape, arrivals, prompts, outs, max_batch, revert_every
     ctx.sync()
     step_ms = [(a.elapsed_time(b), tt) for a, b, tt in evs]
     serve.preempted = preempted[0]
+    serve.prefill_tokens = prefill_tokens[0]
     return step_ms, waits, tokens
 
 
