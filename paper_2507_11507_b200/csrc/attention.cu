@@ -98,8 +98,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
 
 constexpr int kMaxSplitsDev = 128;  // split-K partitions per (sequence, kv head); runtime agrees
 
-template <int D, int G, int W, int NS>
-constexpr int smem_bytes() { return W * NS * 2 * (16 * D * 2) + (NS + 1) * G * D * 4; }
+template <int D, int G, int QP, int W, int NS>
+constexpr int smem_bytes() { return W * NS * 2 * (16 * D * 2) + (NS + 1) * G * QP * D * 4; }
 
 // Tensor-core formulation per 16-token tile (one warp):
 //   S[16 tok x 8 col] = K[16 x D] * Qc[D x 8]      (D/16 mma.m16n8k16 per n-tile)
@@ -107,34 +107,38 @@ constexpr int smem_bytes() { return W * NS * 2 * (16 * D * 2) + (NS + 1) * G * D
 // where column n = 2*head + part holds the bf16 hi (part 0) or lo (part 1) half
 // of q (resp. p), so the fp32 accumulators see q and p to ~16 mantissa bits
 // while K and V stay exact bf16. G <= 4 heads fill one n8 tile, G = 8 two.
+// Prefill items (QP > 1) carry QP consecutive rows of one sequence: the columns
+// are GV = G * QP virtual heads (row pp = v / G, head g = v % G), each with its
+// own causal length len + pp, so one K|V tile serves QP query rows.
 // The KV tile is stored XOR-swizzled in 16-byte chunks (chunk ^ (row & 7), see
 // include/mirage.h), which makes every ldmatrix below bank-conflict free.
-template <int D, int G, int W, int NS>
+template <int D, int G, int QP, int W, int NS>
 __global__ void __launch_bounds__(W * 32)
 paged_attention_kernel(const AttnParams p) {
+  constexpr int GV = G * QP;          // query column groups (virtual heads) per item
   constexpr int kWarps = W;
   constexpr int TILE = 16 * D * 2;    // bytes of K (or V) of one block/layer/head
   constexpr int ROW = 2 * D;          // bytes per token row
   constexpr int KS = D / 16;          // k-slices (QK) == dim tiles (PV)
-  constexpr int NT = (2 * G + 7) / 8; // n8 tiles of (head, part) columns
+  constexpr int NT = (2 * GV + 7) / 8; // n8 tiles of (head, part) columns
 
   constexpr int QB = NS + 1;           // q staging buffers per CTA (warp 0's producer runs ahead)
 
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[kWarps][NS];
   __shared__ __align__(8) uint64_t qbars[QB];
-  __shared__ float sm_m[kWarps][G], sm_l[kWarps][G];
-  constexpr int ACC = (kWarps * D > 2 * kMaxSplitsDev ? kWarps * D : 2 * kMaxSplitsDev) * G;
+  __shared__ float sm_m[kWarps][GV], sm_l[kWarps][GV];
+  constexpr int ACC = (kWarps * D > 2 * kMaxSplitsDev ? kWarps * D : 2 * kMaxSplitsDev) * GV;
   __shared__ __align__(16) float sm_accf[ACC];
-  float(*sm_acc)[G][D] = reinterpret_cast<float(*)[G][D]>(sm_accf);
+  float(*sm_acc)[GV][D] = reinterpret_cast<float(*)[GV][D]>(sm_accf);
   __shared__ int am_last;
   // dynamic item queue: CTA item k (in claim order) lives in slot k % QB
   __shared__ int slot_claim[QB];
   __shared__ unsigned long long slot_word[QB];  // ((k + 1) << 32) | item, published atomically
-  __shared__ float sLam[G];
+  __shared__ float sLam[GV];
   // split-combine scratch aliases sm_acc (free once the partials are written)
-  float(*sw)[G] = reinterpret_cast<float(*)[G]>(sm_accf);
-  float(*sl)[G] = reinterpret_cast<float(*)[G]>(sm_accf + kMaxSplitsDev * G);
+  float(*sw)[GV] = reinterpret_cast<float(*)[GV]>(sm_accf);
+  float(*sl)[GV] = reinterpret_cast<float(*)[GV]>(sm_accf + kMaxSplitsDev * GV);
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -143,7 +147,7 @@ paged_attention_kernel(const AttnParams p) {
   const int n_flat = (p.n_units_dev ? *p.n_units_dev : p.n_units) * p.H_kv;  // item f = unit * H_kv + kv head
   uint8_t* ring = smem + (size_t)warp * NS * 2 * TILE;
   // q staging (dynamic smem after the rings): [QB][G][2][D/2] packed bf16 hi|lo words, one copy per CTA item
-  uint32_t(*qbuf)[G * D] = reinterpret_cast<uint32_t(*)[G * D]>(smem + (size_t)kWarps * NS * 2 * TILE);
+  uint32_t(*qbuf)[GV * D] = reinterpret_cast<uint32_t(*)[GV * D]>(smem + (size_t)kWarps * NS * 2 * TILE);
 
   if (lane == 0) {
 #pragma unroll
@@ -171,10 +175,12 @@ paged_attention_kernel(const AttnParams p) {
         item = atomicAdd(p.sched, 1);
         if (item < n_flat) {
           const AttnUnit u = p.units[item / p.H_kv];
-          const uint32_t* src = p.q + ((size_t)u.seq * p.H + (item % p.H_kv) * G) * D;
+          const int nq = QP == 1 ? 1 : u.nq;  // rows u.seq .. u.seq + nq - 1, G heads each
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_expect_tx(&qbars[sl], G * D * 4);
-          bulk_g2s(&qbuf[sl][0], src, G * D * 4, &qbars[sl]);
+          mbar_expect_tx(&qbars[sl], nq * G * D * 4);
+          for (int pp = 0; pp < nq; ++pp)
+            bulk_g2s(&qbuf[sl][pp * G * D], p.q + ((size_t)(u.seq + pp) * p.H + (item % p.H_kv) * G) * D,
+                     G * D * 4, &qbars[sl]);
         }
         atomicExch(&slot_word[sl], ((unsigned long long)(k + 1) << 32) | (unsigned int)item);
       } else {
@@ -247,6 +253,8 @@ paged_attention_kernel(const AttnParams p) {
     const int hk = f % p.H_kv;
     const int s = u.seq;
     const int L = u.len;
+    const int nq = QP == 1 ? 1 : u.nq;
+    const int Lmax = L + nq - 1;  // tokens attended by the item's last row
     const int first = u.b0 + warp;
     const int n_it = first < u.b1 ? (u.b1 - first + kWarps - 1) / kWarps : 0;
 
@@ -262,7 +270,7 @@ paged_attention_kernel(const AttnParams p) {
       const uint32_t* qw = qs + hh * D + (gq & 1) * (D / 2) + tq;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
-        if (hh < G && n_it > 0) {
+        if (hh < GV && hh / G < nq && n_it > 0) {
           qb[nt][ks][0] = qw[ks * 8];
           qb[nt][ks][1] = qw[ks * 8 + 4];
         } else {
@@ -272,6 +280,9 @@ paged_attention_kernel(const AttnParams p) {
     }
     // per lane: softmax state of head nt*4 + tq; O^T accumulators (dims ks*16+gq,+8)
     float m[NT], l[NT], o[NT][KS][4];
+    int Lv[NT];  // causal length of the lane's (virtual) head: row v / G of the item
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) Lv[nt] = L + min((nt * 4 + tq) / G, nq - 1);
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       m[nt] = -CUDART_INF_F;
@@ -288,7 +299,7 @@ paged_attention_kernel(const AttnParams p) {
       const int blk = first + kWarps * it;
       mbar_wait(&bars[warp][st], phase);
       uint8_t* tile = ring + st * 2 * TILE;
-      const int valid_rows = min(16, L - blk * 16);
+      const int valid_rows = min(16, Lmax - blk * 16);
       if (valid_rows < 16) {  // rows past the context may hold any bytes: zero V there
         for (int e = lane; e < (16 - valid_rows) * (ROW / 16); e += 32) {
           const int r = valid_rows + e / (ROW / 16), c = e % (ROW / 16);
@@ -318,8 +329,9 @@ paged_attention_kernel(const AttnParams p) {
       float pA[NT], pB[NT];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const float s0 = (gq < valid_rows) ? sacc[nt][0] + sacc[nt][1] : -CUDART_INF_F;
-        const float s1 = (gq + 8 < valid_rows) ? sacc[nt][2] + sacc[nt][3] : -CUDART_INF_F;
+        const int vr = QP == 1 ? valid_rows : Lv[nt] - blk * 16;  // rows of this tile the head sees
+        const float s0 = (gq < vr) ? sacc[nt][0] + sacc[nt][1] : -CUDART_INF_F;
+        const float s1 = (gq + 8 < vr) ? sacc[nt][2] + sacc[nt][3] : -CUDART_INF_F;
         float bm = fmaxf(s0, s1);
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 4));
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
@@ -327,10 +339,12 @@ paged_attention_kernel(const AttnParams p) {
         const float m_new = fmaxf(m[nt], bm);
         pA[nt] = exp2f(s0 - m_new);
         pB[nt] = exp2f(s1 - m_new);
+        if (QP > 1 && m_new == -CUDART_INF_F) pA[nt] = pB[nt] = 0.f;  // a row that sees none of this tile
         // rescale only when some head's running max moved (alpha == 1 otherwise:
         // skipping the multiply by exactly 1 leaves every bit unchanged)
         if (__any_sync(0xffffffffu, m_new != m[nt])) {
-          const float alpha = exp2f(m[nt] - m_new);
+          // (a prefill row that has seen no token yet keeps m = -inf: alpha = 1, not NaN)
+          const float alpha = (QP > 1 && m_new == -CUDART_INF_F) ? 1.f : exp2f(m[nt] - m_new);
           l[nt] *= alpha;
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks)
@@ -350,7 +364,7 @@ paged_attention_kernel(const AttnParams p) {
         const float c0 = __shfl_sync(0xffffffffu, pA[nt], src1);  // P[2tq+1]
         const float c8 = __shfl_sync(0xffffffffu, pB[nt], src1);  // P[2tq+9]
         const int part = gq & 1;
-        if (nt * 4 + (gq >> 1) < G) {
+        if (nt * 4 + (gq >> 1) < GV) {
           pb[nt][0] = pack_bf16(bf16_part(a0, part), bf16_part(c0, part));
           pb[nt][1] = pack_bf16(bf16_part(a8, part), bf16_part(c8, part));
         } else {
@@ -381,7 +395,7 @@ paged_attention_kernel(const AttnParams p) {
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int hh = nt * 4 + tq;
-      if (hh < G) {
+      if (hh < GV) {
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           sm_acc[warp][hh][ks * 16 + gq] = o[nt][ks][0] + o[nt][ks][1];
@@ -397,8 +411,9 @@ paged_attention_kernel(const AttnParams p) {
 
     // merge the warps in fixed order; thread t handles (g, d) pairs
     const bool split = u.nsplit > 1;
-    for (int e = threadIdx.x; e < G * D; e += kWarps * 32) {
+    for (int e = threadIdx.x; e < GV * D; e += kWarps * 32) {
       const int g = e / D, d = e % D;
+      if (QP > 1 && g / G >= nq) continue;
       float M = sm_m[0][g];
 #pragma unroll
       for (int w = 1; w < kWarps; ++w) M = fmaxf(M, sm_m[w][g]);
@@ -409,10 +424,10 @@ paged_attention_kernel(const AttnParams p) {
         Ls += fw * sm_l[w][g];
         ov += fw * sm_acc[w][g][d];
       }
-      const int h = hk * G + g;
+      const int h = hk * G + g % G;
       if (!split) {
         const float r = ov / Ls;
-        const size_t oi = ((size_t)s * p.H + h) * D + d;
+        const size_t oi = ((size_t)(s + g / G) * p.H + h) * D + d;
         if (p.out_fp32) reinterpret_cast<float*>(p.out)[oi] = r;
         else reinterpret_cast<__nv_bfloat16*>(p.out)[oi] = __float2bfloat16_rn(r);
       } else {
@@ -424,7 +439,7 @@ paged_attention_kernel(const AttnParams p) {
         }
       }
     }
-    if (!split) continue;
+    if (QP > 1 || !split) continue;  // prefill items are never split (host guarantees nsplit == 1)
 
     // ---- split-K combine by the last-arriving CTA of this (seq, kv head) ----
     __threadfence();
@@ -493,16 +508,16 @@ paged_attention_kernel(const AttnParams p) {
   }
 }
 
-template <int D, int G, int W, int NS>
+template <int D, int G, int QP, int W, int NS>
 int grid_ctas() {  // persistent grid: as many CTAs as fit on the GPU at once
-  constexpr int SMEM = smem_bytes<D, G, W, NS>();
+  constexpr int SMEM = smem_bytes<D, G, QP, W, NS>();
   static int ctas = 0;
   if (!ctas) {
-    if (cudaFuncSetAttribute(paged_attention_kernel<D, G, W, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(paged_attention_kernel<D, G, QP, W, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM) != cudaSuccess)
       return -1;
     int per_sm = 0, dev = 0, sms = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, paged_attention_kernel<D, G, W, NS>, W * 32,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, paged_attention_kernel<D, G, QP, W, NS>, W * 32,
                                                       SMEM) != cudaSuccess)
       return -1;
     cudaGetDevice(&dev);
@@ -512,9 +527,9 @@ int grid_ctas() {  // persistent grid: as many CTAs as fit on the GPU at once
   return ctas;
 }
 
-template <int D, int G, int W, int NS>
+template <int D, int G, int QP, int W, int NS>
 cudaError_t launch_v(const AttnParams& p, cudaStream_t s, bool query, int* grid_out) {
-  const int ctas = grid_ctas<D, G, W, NS>();
+  const int ctas = grid_ctas<D, G, QP, W, NS>();
   if (ctas < 0) return cudaErrorInvalidValue;
   if (query) {
     *grid_out = ctas;
@@ -522,7 +537,7 @@ cudaError_t launch_v(const AttnParams& p, cudaStream_t s, bool query, int* grid_
   }
   const long items = (long)p.n_units * p.H_kv;
   const int grid = (int)std::min<long>(items, ctas);
-  paged_attention_kernel<D, G, W, NS><<<grid, W * 32, smem_bytes<D, G, W, NS>(), s>>>(p);
+  paged_attention_kernel<D, G, QP, W, NS><<<grid, W * 32, smem_bytes<D, G, QP, W, NS>(), s>>>(p);
   return cudaGetLastError();
 }
 
@@ -540,8 +555,10 @@ template <int D, int G>
 cudaError_t launch_dg(const AttnParams& p, cudaStream_t s, bool query, int* grid_out) {
   // the 4 warps of a CTA split the blocks of one work item, for any H_kv
   constexpr int NS = D == 128 ? 2 : 4;
-  if (D == 128 && variant() == 1) return launch_v<D, G, 4, 3>(p, s, query, grid_out);
-  return launch_v<D, G, 4, NS>(p, s, query, grid_out);
+  constexpr int QP = G < 8 ? 8 / G : 1;  // prefill rows per item: 8 virtual heads per kv head
+  if (p.qp > 1 && QP > 1) return launch_v<D, G, QP, 4, NS>(p, s, query, grid_out);
+  if (D == 128 && variant() == 1) return launch_v<D, G, 1, 4, 3>(p, s, query, grid_out);
+  return launch_v<D, G, 1, 4, NS>(p, s, query, grid_out);
 }
 
 template <int D>
@@ -564,11 +581,12 @@ cudaError_t launch_paged_attention(const AttnParams& p, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
-int attention_grid_ctas(int H, int H_kv, int D) {
+int attention_grid_ctas(int H, int H_kv, int D, int qp) {
   AttnParams p{};
   p.H = H;
   p.H_kv = H_kv;
   p.D = D;
+  p.qp = qp;
   int g = -1;
   if (D == 128) launch_d<128>(p, nullptr, true, &g);
   if (D == 64) launch_d<64>(p, nullptr, true, &g);
@@ -576,5 +594,10 @@ int attention_grid_ctas(int H, int H_kv, int D) {
 }
 
 int attention_cta_warps(int) { return 4; }
+
+int attention_prefill_rows(int H, int H_kv) {
+  const int G = H / H_kv;
+  return G < 8 ? 8 / G : 1;
+}
 
 }  // namespace mirage

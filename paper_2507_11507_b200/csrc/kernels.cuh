@@ -6,17 +6,21 @@
 
 namespace mirage {
 
-// One attention work unit: a (sequence, split) pair; the kernel expands it over
-// the kv heads. 32 bytes, everything the kernel needs without dependent loads.
+// One attention work unit: a (sequence, split) pair -- or, in a prefill step,
+// nq consecutive rows of one sequence (positions len-1 .. len+nq-2); the kernel
+// expands it over the kv heads. 32 bytes, everything the kernel needs without
+// dependent loads.
 struct AttnUnit {
-  int32_t seq;       // row in the step's batch
-  int32_t split;     // split index within the sequence
-  int32_t nsplit;    // number of splits of this sequence
+  int32_t seq;       // (first) row in the step's batch
+  int16_t split;     // split index within the sequence
+  int16_t nsplit;    // number of splits of this sequence (1 when nq > 1)
   int32_t pbase;     // first partial record of this sequence (valid if nsplit > 1)
-  int32_t len;       // tokens attended by the sequence
-  int32_t b0, b1;    // this split's block range [b0, b1)
+  int32_t len;       // tokens attended by the first row; row seq + i attends len + i
+  int32_t b0, b1;    // this split's block range [b0, b1) (covers the last row)
   int32_t addr_off;  // index of the sequence's block 0 in AttnParams::addrs
+  int32_t nq;        // rows in this unit (1 for decode)
 };
+static_assert(sizeof(AttnUnit) == 32, "AttnUnit is one 32-byte record");
 
 struct AttnParams {
   const uint32_t* q;           // [B][H][2][D/2]: q * scale_log2 split into bf16 hi (part 0) and
@@ -33,12 +37,15 @@ struct AttnParams {
   int32_t* sched;              // [2] dynamic item counter + finished CTAs, zero between launches
   void* out;                   // [B][H][D] fp32 or bf16
   int32_t out_fp32;
+  int32_t qp;                  // rows per unit the launch was planned for (1, or 8 / G for prefill)
 };
 
 cudaError_t launch_paged_attention(const AttnParams& p, cudaStream_t s);
 // CTAs of the persistent attention grid on this device (for split planning), and
 // warps per CTA (blocks of one work item are spread over them).
-int attention_grid_ctas(int H, int H_kv, int D);
+int attention_grid_ctas(int H, int H_kv, int D, int qp = 1);
+// rows per unit of the prefill variant (8 / G, 1 for G = 8)
+int attention_prefill_rows(int H, int H_kv);
 int attention_cta_warps(int H_kv);
 
 // ---- dense-layer support kernels -------------------------------------------
@@ -60,16 +67,6 @@ cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float
                             const __nv_bfloat16* bias, const int32_t* positions,
                             const int32_t* seq_off, const uint64_t* addrs, uint64_t layer_off,
                             float rope_theta, float q_scale, uint32_t* q, cudaStream_t s);
-// Step metadata upload without the copy engine: the kernel reads the pinned
-// (UVA-mapped) staging buffer over the host link with SM loads and writes the
-// device copy. A DMA would queue behind large H2D weight copies already in the
-// copy engine (re-streaming, reloads); this keeps the compute stream
-// independent of them. Segments are 16-byte aligned, byte counts rounded up to 16.
-struct PullSegs {
-  uint32_t off[8], bytes[8];
-  int n;
-};
-cudaError_t launch_meta_pull(char* dst, const char* src_host, const PullSegs& segs, cudaStream_t s);
 // fp32 q [n_rows * D] (unscaled) -> the split format of AttnParams::q (test hook path)
 cudaError_t launch_q_split(int64_t n, int D, const float* q, float q_scale, uint32_t* out, cudaStream_t s);
 // OPT: f = bf16(relu(y + b)); Llama: f = bf16(silu(y[:, :f]) * y[:, f:]).

@@ -504,31 +504,6 @@ cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float
   return cudaGetLastError();
 }
 
-__global__ void meta_pull_kernel(char* dst, const char* src, PullSegs g) {
-  uint32_t total = 0;
-  for (int k = 0; k < g.n; ++k) total += g.bytes[k] / 16;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    uint32_t j = i;
-    int k = 0;
-    while (j >= g.bytes[k] / 16) j -= g.bytes[k++] / 16;
-    const size_t o = g.off[k] + (size_t)j * 16;
-    *reinterpret_cast<uint4*>(dst + o) = __ldcv(reinterpret_cast<const uint4*>(src + o));  // no stale cache
-  }
-}
-
-cudaError_t launch_meta_pull(char* dst, const char* src_host, const PullSegs& segs, cudaStream_t s) {
-  uint32_t total = 0;
-  for (int k = 0; k < segs.n; ++k) {
-    if (segs.off[k] % 16 || segs.bytes[k] % 16) return cudaErrorInvalidValue;
-    total += segs.bytes[k] / 16;
-  }
-  if (!total) return cudaSuccess;
-  const int threads = 256;
-  const int blocks = (int)std::min<uint32_t>((total + threads - 1) / threads, 296);
-  meta_pull_kernel<<<blocks, threads, 0, s>>>(dst, src_host, segs);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_q_split(int64_t n, int D, const float* q, float q_scale, uint32_t* out, cudaStream_t s) {
   if (n % 8 || D % 16) return cudaErrorInvalidValue;
   const int64_t n8 = n / 8;

@@ -431,30 +431,13 @@ size_t meta_size(mirage_ctx* c) {
          (uint64_t)Bm * c->max_blk * 8;
 }
 
-uint32_t up16(size_t x) { return (uint32_t)((x + 15) & ~(size_t)15); }
-
-// Upload the used parts of a packed step (header, B-row arrays, n_units units,
-// n_addr addresses) from staging buffer `host` with the pull kernel.
-int32_t upload_meta(mirage_ctx* c, char* host, int B, int n_units, int n_addr, size_t* bytes_out = nullptr) {
+// Upload a packed step (header and row arrays at capacity, n_addr addresses)
+// from staging buffer `host` to the device copy, on the compute stream.
+int32_t upload_meta(mirage_ctx* c, char* host, int n_addr, size_t* bytes_out = nullptr) {
   MetaView hv = meta_view(c, host);
-  mirage::PullSegs g{};
-  auto seg = [&](const void* p, size_t bytes) {
-    g.off[g.n] = (uint32_t)(reinterpret_cast<const char*>(p) - host);
-    g.bytes[g.n] = up16(bytes);
-    ++g.n;
-  };
-  seg(hv.hdr, 16);
-  seg(hv.tokens, (size_t)B * 4);
-  seg(hv.pos, (size_t)B * 4);
-  seg(hv.len, (size_t)B * 4);
-  seg(hv.seq_off, (size_t)B * 4);
-  seg(hv.units, (size_t)n_units * sizeof(mirage::AttnUnit));
-  seg(hv.addrs, (size_t)n_addr * 8);
-  KL(c, mirage::launch_meta_pull(c->meta_dev, host, g, c->cs));
-  if (bytes_out) {
-    *bytes_out = 0;
-    for (int k = 0; k < g.n; ++k) *bytes_out += g.bytes[k];
-  }
+  const size_t bytes = (size_t)(reinterpret_cast<char*>(hv.addrs) - host) + (size_t)n_addr * 8;
+  CK(c, cudaMemcpyAsync(c->meta_dev, host, bytes, cudaMemcpyHostToDevice, c->cs));
+  if (bytes_out) *bytes_out = bytes;
   return MIRAGE_OK;
 }
 
@@ -472,8 +455,9 @@ int32_t acquire_stage(mirage_ctx* c, char** host) {
 // longest-first order (greedy LPT). Splitting adds per-item overhead and a
 // combine, so the split size P (blocks) is the LARGEST one that still gives
 // every resident CTA about one item to start with: items(P) >= f * grid, with
-// f = 0.8 (f = 0.6 for G = 8), equalised so the longest sequence has no runt
-// last split, and at most
+// f = 0.8 (f = 0.6 for G = 8); when even the unsplit batch has fewer items than
+// the grid, the smallest P with items(P) <= grid (one item per CTA, equal SM
+// loads). Equalised so the longest sequence has no runt last split, and at most
 // kMaxSplits splits per sequence. Calibrated on B200 (tools/attn_bench.py
 // --split sweeps). P depends on logical lengths only, never on
 // block placement.
@@ -493,6 +477,19 @@ int choose_split(const int32_t* lens, int B, int Hk, int G, int grid, int warps)
     return (double)n * Hk;
   };
   int P = std::max(p_lo, max_nb);
+  if (items(P) < grid) {
+    // Fewer items than resident CTAs: split until the items just fill the grid
+    // (the smallest P with items(P) <= grid). Every CTA then holds one item, so
+    // the SMs carry equal loads (ncu on 1 x 32k: SMs with 2 CTAs ran ~1.6x
+    // longer than SMs with 1 under the "items >= f * grid" rule).
+    int lo = p_lo, hi = P;  // items(P) is non-increasing in P
+    while (lo < hi) {
+      const int mid = (lo + hi) / 2;
+      if (items(mid) <= grid) hi = mid;
+      else lo = mid + 1;
+    }
+    P = lo;
+  }
   while (P > p_lo && items(P) < need) {
     const int next = std::max(p_lo, std::min(P - 1, (int)(P * 0.97)));
     P = next;
@@ -512,8 +509,8 @@ int build_units(const int32_t* lens, const int32_t* seq_off, int B, int Hk, int 
     const int ns = std::max(1, (nb + P - 1) / P);
     if (n + ns > max_units || ns > kMaxSplits) return -1;
     for (int i = 0; i < ns; ++i)
-      units[n++] = mirage::AttnUnit{b, i, ns, ns > 1 ? pbase : 0, lens[b], i * P, std::min(nb, (i + 1) * P),
-                                    seq_off[b]};
+      units[n++] = mirage::AttnUnit{b, (int16_t)i, (int16_t)ns, ns > 1 ? pbase : 0, lens[b], i * P,
+                                    std::min(nb, (i + 1) * P), seq_off[b], 1};
     if (ns > 1) pbase += ns;
   }
   // longest-first order for the persistent kernel's round-robin item assignment
@@ -522,6 +519,26 @@ int build_units(const int32_t* lens, const int32_t* seq_off, int B, int Hk, int 
     return size_of(a) > size_of(b);
   });
   *split_blocks = P;
+  return n;
+}
+
+// Units of a step that holds prefill rows: runs of up to qp consecutive rows of
+// one sequence at consecutive positions become one unit (the kernel's QP
+// variant serves them from one pass over the K|V tiles); never split.
+int build_units_rows(const int32_t* lens, const int32_t* seq_off, const int64_t* seq_ids, int B, int qp,
+                     mirage::AttnUnit* units, int max_units) {
+  int n = 0;
+  for (int i = 0; i < B;) {
+    int j = i + 1;
+    while (j < B && j - i < qp && seq_ids[j] == seq_ids[i] && lens[j] == lens[j - 1] + 1) ++j;
+    if (n >= max_units) return -1;
+    const int nb = (lens[j - 1] + kBlockTokens - 1) / kBlockTokens;
+    units[n++] = mirage::AttnUnit{i, 0, 1, 0, lens[i], 0, nb, seq_off[i], j - i};
+    i = j;
+  }
+  std::stable_sort(units, units + n, [](const mirage::AttnUnit& a, const mirage::AttnUnit& b) {
+    return a.b1 - a.b0 > b.b1 - b.b0;
+  });
   return n;
 }
 
@@ -748,7 +765,7 @@ int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
   if (cublasSetWorkspace(c->blas, c->blas_ws, kCublasWs) != CUBLAS_STATUS_SUCCESS ||
       cublasSetStream(c->blas, c->cs) != CUBLAS_STATUS_SUCCESS)
     return bail(MIRAGE_ERR_CUDA);
-  c->meta_bytes = meta_size(c) + 16;  // segments are rounded up to 16 bytes
+  c->meta_bytes = meta_size(c);
   for (int i = 0; i < 2; ++i) {
     if (cudaHostAlloc(reinterpret_cast<void**>(&c->stage[i]), c->meta_bytes, cudaHostAllocDefault) !=
             cudaSuccess ||
@@ -1427,16 +1444,20 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     n_addr += need;
   }
   int split_blocks = 1;
-  const int n_units = build_units(hv.len, hv.seq_off, B, s.Hk, s.H / s.Hk,
-                                  mirage::attention_grid_ctas(s.H, s.Hk, s.D), mirage::attention_cta_warps(s.Hk),
-                                  0, hv.units, c->max_units, &split_blocks);
+  bool multi_row = false;  // a prefill / extend step: some sequence has several rows
+  for (int i = 0; i < B && !multi_row; ++i) multi_row = first_row[i] != i;
+  const int qp = multi_row ? mirage::attention_prefill_rows(s.H, s.Hk) : 1;
+  const int n_units =
+      qp > 1 ? build_units_rows(hv.len, hv.seq_off, seq_ids, B, qp, hv.units, c->max_units)
+             : build_units(hv.len, hv.seq_off, B, s.Hk, s.H / s.Hk, mirage::attention_grid_ctas(s.H, s.Hk, s.D),
+                           mirage::attention_cta_warps(s.Hk), 0, hv.units, c->max_units, &split_blocks);
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "step: too many attention units");
   hv.hdr[0] = n_units;
   cudaStream_t cs = c->cs;
   const bool timed = !M->step_timed;
   if (timed) CK(c, cudaEventRecord(M->st0, cs));
   size_t meta_bytes = 0;
-  if (int32_t e = upload_meta(c, host, B, n_units, n_addr, &meta_bytes)) return e;
+  if (int32_t e = upload_meta(c, host, n_addr, &meta_bytes)) return e;
   CK(c, cudaEventRecord(c->stage_ev[c->stage_i], cs));
   M->last_meta = meta_bytes;
   if (int32_t e = flush_reloads(c, M)) return e;  // requested reloads start behind this step's upload
@@ -1507,7 +1528,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   // CUDA graph of the step body (embed ... argmax): models without a streaming
   // cycle, one graph per batch size, captured on the second step of that size
   // (the first runs eagerly so cuBLASLt plans/autotuning happen outside capture)
-  const bool graphable = (c->cfg.flags & MIRAGE_FLAG_CUDA_GRAPHS) && m == 0 && !reloading &&
+  const bool graphable = (c->cfg.flags & MIRAGE_FLAG_CUDA_GRAPHS) && m == 0 && !reloading && qp == 1 &&
                          !(c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) && !M->tp_ready;
   if (c->tp > 1 && !c->nccl && !M->tp_ready)
     return fail(c, MIRAGE_ERR_STATE, "step: tensor parallel model without a collective (tp_import first)");
@@ -1554,6 +1575,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   ap.sched = M->tickets + (size_t)c->cfg.max_batch * Hk;
   ap.out = M->x;  // bf16 [B][H*D]: the O-projection input
   ap.out_fp32 = 0;
+  ap.qp = qp;
   const bool time_attn = c->cfg.flags & MIRAGE_FLAG_TIME_ATTN;
   uint64_t attn_bytes = 0;
   for (int i = 0; i < B; ++i) attn_bytes += (uint64_t)hv.len[i] * 2 * Hk * D * 2;
@@ -1745,7 +1767,7 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
                                   mirage::attention_cta_warps(M->shp.Hk), split_tokens_override / kBlockTokens,
                                   hv.units, c->max_units, &split_blocks);
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "attn_only: too many units for the split override");
-    if (int32_t e = upload_meta(c, host, B, n_units, n_addr)) return e;
+    if (int32_t e = upload_meta(c, host, n_addr)) return e;
   CK(c, cudaEventRecord(c->stage_ev[c->stage_i], c->cs));
   M->last_units = n_units;
   M->last_split = split_blocks;
@@ -1794,13 +1816,7 @@ static int32_t kv_hook_prepare(mirage_ctx* c, Model* M, int64_t seq_id, int32_t 
   MetaView hv = meta_view(c, host);
   std::copy(it->second.begin(), it->second.begin() + need, hv.tables);
   const size_t head = reinterpret_cast<char*>(hv.tables) - host;
-  {
-    mirage::PullSegs g{};
-    g.off[0] = (uint32_t)head;
-    g.bytes[0] = up16((size_t)need * 4);
-    g.n = 1;
-    KL(c, mirage::launch_meta_pull(c->meta_dev, host, g, c->cs));
-  }
+  CK(c, cudaMemcpyAsync(c->meta_dev + head, host + head, (size_t)need * 4, cudaMemcpyHostToDevice, c->cs));
   CK(c, cudaEventRecord(c->stage_ev[c->stage_i], c->cs));
   *p0 = len;
   return MIRAGE_OK;

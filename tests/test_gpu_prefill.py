@@ -80,6 +80,21 @@ def test_multirow_step_matches_oracle_row_by_row(shape):
         ctx.sync()
         ref, _, _ = dec.step(seqs, toks, pos)
         check(h2.float().cpu().numpy(), ref, ("decode", k))
+    # a mixed step: single decode rows next to a 9-row extend (crosses a prefill item of 8 rows)
+    ext = {1: 9, 3: 1, 0: 2}
+    rs = [q for q, n in ext.items() for _ in range(n)]
+    base = {q: ctx.seq_len(mid, q) for q in ext}
+    for q, n in ext.items():
+        ctx.alloc_blocks(mid, q, 1)
+    rp = [base[q] + j for q, n in ext.items() for j in range(n)]
+    rt = [workload.teacher_tokens(q, 500 + p_, shape.vocab) for q, p_ in zip(rs, rp)]
+    h3 = torch.empty((len(rs), shape.d_model), dtype=torch.bfloat16, device="cuda")
+    ctx.decode_step(mid, rs, rt, rp, hidden_out=h3)
+    ctx.sync()
+    got = h3.float().cpu().numpy()
+    for i, (q, t, p_) in enumerate(zip(rs, rt, rp)):
+        x, _ = dec.step_one(q, t, p_)
+        check(got[i], x, ("mixed", q, p_))
 
 
 @pytest.mark.parametrize("shape", [models.TOY, models.TOY_LLAMA])
