@@ -259,6 +259,18 @@ int32_t mirage_region_info(mirage_ctx* ctx, int32_t model, int32_t idx, mirage_r
  * CUDA. */
 int32_t mirage_unremap(mirage_ctx* ctx, int32_t recipient, int32_t region);
 
+/* Block migration before Dynamic Reversion (reading #29: the paper restores
+ * reclaimed memory "when KV cache space is sufficient", PAPER.md:352-354,
+ * :830-834, and is silent on blocks still live in it). The region's live block
+ * ids (a streaming cycle: all of its regions'), ascending, take the lowest free
+ * ids outside it, ascending, one for one; every block-table entry is renamed in
+ * place, the old ids become free, and each moved block's bytes (block_bytes, all
+ * layers) are copied on the compute stream after every kernel enqueued before.
+ * The region can then be reverted with mirage_unremap. *n_moved (may be NULL)
+ * receives the number of blocks moved. Errors: RANGE; STATE (already reverted);
+ * NO_BLOCKS (fewer free ids outside the region than live blocks; nothing changed). */
+int32_t mirage_migrate_region(mirage_ctx* ctx, int32_t model, int32_t region, int32_t* n_moved);
+
 /* Mark a tenant active (1) or inactive (0) (temporal sharing).
  * Errors: RANGE; STATE (activating a model with reclaimed layers: unremap its
  * regions first; the reload then overlaps the next prefill). */
@@ -338,7 +350,7 @@ typedef struct mirage_stats {
   uint64_t uses;            /* cycled-layer uses enqueued so far                 */
   uint64_t h2d_copies, h2d_bytes;
   double h2d_ms;            /* summed event time of completed H2D copies         */
-  double last_step_ms;      /* event time of the last completed decode step      */
+  double last_step_ms;      /* event time of the last completed decode step (steps with prefill rows excluded: T_Compute) */
   int64_t steps;
   /* with MIRAGE_FLAG_TIME_ATTN: completed attention launches, their summed event
    * time and algorithmic KV bytes (sum over sequences of ctx_len * 2 * H_kv * D * 2) */

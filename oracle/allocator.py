@@ -18,6 +18,13 @@ readings #1, #11-#15 (listed in DESIGN.md):
 
 * unremap(r, region) (NEXT-1, Dynamic Reversion): all of the region's ids free
   -> retired (never reused), donor layers resident again; PRESSURE otherwise.
+* migrate(r, region) (reading #29; the paper restores reclaimed memory "when KV
+  cache space is sufficient", and is silent on blocks still
+  live in it): the region's live ids (a streaming cycle: all its regions'),
+  ascending, take the lowest free ids outside it, ascending, one for one; every
+  table entry is renamed in place and the old ids become free. NoBlocks when
+  fewer free ids lie outside than are live. The product copies each moved
+  block's bytes; the oracle only renames.
 
 Pins: worked examples (toy layer -> 48 blocks; SPEC 2 GB / 16 MB -> 128),
 invariants I1-I4 and an exhaustive comparison against an independent set-based
@@ -163,6 +170,36 @@ class Allocator:
             for l in d.cycle[: d.beta]:
                 d.layer_state[l] = RESIDENT
             d.cycle, d.beta = [], 0
+
+    def _region_ids(self, r, region):
+        reg = r.regions[region]
+        if reg["cycle"]:
+            which = [g for g in r.regions if g["cycle"] and g["donor"] == reg["donor"] and not g["retired"]]
+        else:
+            which = [reg]
+        return {i for g in which for i in range(g["first_id"], g["first_id"] + g["n_blocks"])}
+
+    def migrate(self, recipient, region):
+        """Move the region's live blocks to free ids outside it (reading #29).
+        Returns the moves [(old, new)] in ascending old-id order."""
+        r = self.models[recipient]
+        if not (0 <= region < len(r.regions)):
+            raise RangeError("region")
+        if r.regions[region]["retired"]:
+            raise StateError("already reverted")
+        X = self._region_ids(r, region)
+        live = sorted(i for i in X if i not in r.free)
+        outside = sorted(i for i in r.free if i not in X)
+        if len(outside) < len(live):
+            raise NoBlocks(len(live) - len(outside))
+        moves = list(zip(live, outside[: len(live)]))
+        ren = dict(moves)
+        for seq in r.tables:
+            r.tables[seq] = [ren.get(i, i) for i in r.tables[seq]]
+        for old, new in moves:
+            r.free.remove(new)
+            r.free.add(old)
+        return moves
 
     def alloc(self, model, seq, n):
         r = self.models[model]

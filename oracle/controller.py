@@ -12,7 +12,8 @@ oracle allocator (c2), with the readings of DESIGN.md (NEXT-1):
       layers_per_call at a time, beta = 0, into the active model;
   Dynamic Reversion (lines 7-12): regions of the active
       model, newest first, whose blocks are all free are given back while at
-      least `headroom` blocks stay free;
+      least `headroom` blocks stay free; a region with at most migrate_max live
+      blocks is emptied first by moving them out (reading #29);
   activation: the newly active model's donated regions are reverted first.
 
 Pinned by the directional checks in tests/test_controller_cpu.py (victim order
@@ -69,7 +70,9 @@ class Controller:
     def free(self, seq):
         self.al.free_seq(self.active, seq)
 
-    def revert(self, headroom):
+    def revert(self, headroom, migrate_max=0):
+        """Dynamic Reversion, newest region first. A region still holding at most
+        migrate_max live blocks is first emptied by migrate (reading #29)."""
         out = []
         regs = self.al.models[self.active].regions
         for idx in reversed(range(len(regs))):
@@ -77,10 +80,15 @@ class Controller:
             if g["retired"]:
                 continue
             ids = range(g["first_id"], g["first_id"] + g["n_blocks"])
-            if any(i not in self.al.models[self.active].free for i in ids):
+            live = sum(1 for i in ids if i not in self.al.models[self.active].free)
+            if live > migrate_max:
                 continue
             if len(self.al.models[self.active].free) - g["n_blocks"] < headroom:
                 continue
+            if live:
+                moves = self.al.migrate(self.active, idx)
+                self.log.append(("migrate", idx, len(moves)))
+                out.append(self.log[-1])
             self.al.unremap(self.active, idx)
             self.taken[g["donor"]] -= set(range(g["first_layer"], g["first_layer"] + g["n_layers"]))
             entry = ("revert", idx, g["donor"], g["n_layers"])

@@ -114,6 +114,7 @@ def _load():
         "mirage_region_count": (I32, [P, I32, pI32]),
         "mirage_region_info": (I32, [P, I32, I32, C.POINTER(Region)]),
         "mirage_unremap": (I32, [P, I32, I32]),
+        "mirage_migrate_region": (I32, [P, I32, I32, pI32]),
         "mirage_swap_out": (I32, [P, I32, I64, P, U64]),
         "mirage_swap_in": (I32, [P, I32, I64, P]),
         "mirage_set_weight_source": (I32, [P, I32, P, U64]),
@@ -137,7 +138,7 @@ EXPORTED = [
     "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches", "mirage_nccl_unique_id",
     "mirage_host_register", "mirage_host_unregister", "mirage_region_count", "mirage_region_info",
     "mirage_unremap", "mirage_swap_out", "mirage_swap_in", "mirage_set_weight_source", "mirage_tp_export",
-    "mirage_tp_import", "mirage_prefill"]
+    "mirage_tp_import", "mirage_prefill", "mirage_migrate_region"]
 
 
 def model_cfg(shape):
@@ -334,6 +335,11 @@ class Context:
 
     def unremap(self, recipient, region):
         self._check(LIB.mirage_unremap(self._ctx, recipient, region), "unremap")
+
+    def migrate_region(self, model, region):
+        n = C.c_int32()
+        self._check(LIB.mirage_migrate_region(self._ctx, model, region, C.byref(n)), "migrate_region")
+        return n.value
 
     def set_active(self, model, active):
         self._check(LIB.mirage_set_active(self._ctx, model, int(active)), "set_active")

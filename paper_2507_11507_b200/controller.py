@@ -119,17 +119,24 @@ class RemappingController:
         self.ctx.free_blocks(self.active, seq)
 
     # ---- Dynamic Reversion ----------------------------------------------------------
-    def revert(self, headroom):
-        """Revert empty regions newest-first while free blocks stay >= headroom."""
+    def revert(self, headroom, migrate_max=0):
+        """Revert regions newest-first while free blocks stay >= headroom. A region
+        still holding at most migrate_max live blocks is emptied first by
+        mirage_migrate_region (reading #29)."""
         done = []
         regs = self.ctx.regions(self.active)
         for idx in range(len(regs) - 1, -1, -1):
             r = self.ctx.regions(self.active)[idx]
-            if r["retired"] or r["n_free"] != r["n_blocks"]:
+            live = r["n_blocks"] - r["n_free"]
+            if r["retired"] or live > migrate_max:
                 continue
             free = self.ctx.query(self.active)["free_blocks"]
             if free - r["n_blocks"] < headroom:
                 continue
+            if live:
+                moved = self.ctx.migrate_region(self.active, idx)
+                self.log.append(("migrate", idx, moved))
+                done.append(self.log[-1])
             self.ctx.unremap(self.active, idx)
             lay = set(range(r["first_layer"], r["first_layer"] + r["n_layers"]))
             if r["donor"] in self.info:

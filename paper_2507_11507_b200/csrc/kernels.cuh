@@ -67,6 +67,13 @@ cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float
                             const __nv_bfloat16* bias, const int32_t* positions,
                             const int32_t* seq_off, const uint64_t* addrs, uint64_t layer_off,
                             float rope_theta, float q_scale, uint32_t* q, cudaStream_t s);
+// Block migration (mirage_migrate_region): copy `bytes` from src[i] to dst[i]
+// for i < n (device addresses, 16-byte aligned, bytes % 16 == 0).
+struct BlockMoves {
+  uint64_t src[16], dst[16];
+  int n;
+};
+cudaError_t launch_block_copy(const BlockMoves& m, uint64_t bytes, cudaStream_t s);
 // fp32 q [n_rows * D] (unscaled) -> the split format of AttnParams::q (test hook path)
 cudaError_t launch_q_split(int64_t n, int D, const float* q, float q_scale, uint32_t* out, cudaStream_t s);
 // OPT: f = bf16(relu(y + b)); Llama: f = bf16(silu(y[:, :f]) * y[:, f:]).

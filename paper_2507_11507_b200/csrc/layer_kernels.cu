@@ -504,6 +504,22 @@ cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float
   return cudaGetLastError();
 }
 
+__global__ void block_copy_kernel(BlockMoves m, uint64_t n16) {
+  const uint4* src = reinterpret_cast<const uint4*>(m.src[blockIdx.y]);
+  uint4* dst = reinterpret_cast<uint4*>(m.dst[blockIdx.y]);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+cudaError_t launch_block_copy(const BlockMoves& m, uint64_t bytes, cudaStream_t s) {
+  if (m.n <= 0) return cudaSuccess;
+  if (bytes % 16 || m.n > 16) return cudaErrorInvalidValue;
+  const uint64_t n16 = bytes / 16;
+  const unsigned gx = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 148 * 4 / (unsigned)m.n + 1);
+  block_copy_kernel<<<dim3(gx, m.n), 256, 0, s>>>(m, n16);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_q_split(int64_t n, int D, const float* q, float q_scale, uint32_t* out, cudaStream_t s) {
   if (n % 8 || D % 16) return cudaErrorInvalidValue;
   const int64_t n8 = n / 8;

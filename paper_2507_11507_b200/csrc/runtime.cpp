@@ -1262,6 +1262,56 @@ int32_t mirage_unremap(mirage_ctx* c, int32_t recipient, int32_t region) {
   return MIRAGE_OK;
 }
 
+// Block migration before reversion (reading #29).
+int32_t mirage_migrate_region(mirage_ctx* c, int32_t model, int32_t region, int32_t* n_moved) {
+  GUARD(c);
+  Model* R = get_model(c, model);
+  if (n_moved) *n_moved = 0;
+  if (!R || region < 0 || region >= (int32_t)R->regions.size())
+    return fail(c, MIRAGE_ERR_RANGE, "migrate: model %d region %d", model, region);
+  const Region rg = R->regions[region];
+  if (rg.retired) return fail(c, MIRAGE_ERR_STATE, "migrate: region %d already reverted", region);
+  // the region's ids (a streaming cycle: all of its regions)
+  std::vector<char> in_x(R->next_id, 0);
+  for (int32_t i = 0; i < (int32_t)R->regions.size(); ++i) {
+    const Region& g = R->regions[i];
+    const bool take = rg.cycle ? (g.cycle && g.donor == rg.donor && !g.retired) : i == region;
+    if (take)
+      for (int32_t b = g.first_id; b < g.first_id + g.n_blocks; ++b) in_x[b] = 1;
+  }
+  std::vector<int32_t> live, outside;
+  for (int32_t b = 0; b < R->next_id; ++b)
+    if (in_x[b] && !R->free_ids.count(b)) live.push_back(b);
+  for (int32_t b : R->free_ids)  // ascending
+    if (!in_x[b] && outside.size() < live.size()) outside.push_back(b);
+  if (outside.size() < live.size())
+    return fail(c, MIRAGE_ERR_NO_BLOCKS, "migrate: %zu live blocks, %zu free outside", live.size(), outside.size());
+  std::unordered_map<int32_t, int32_t> ren;
+  for (size_t i = 0; i < live.size(); ++i) ren[live[i]] = outside[i];
+  if (!c->host_only) {  // stream-ordered after every kernel that wrote the old blocks
+    mirage::BlockMoves mv{};
+    for (size_t i = 0; i < live.size(); ++i) {
+      mv.src[mv.n] = R->bbase_host[live[i]];
+      mv.dst[mv.n] = R->bbase_host[outside[i]];
+      if (++mv.n == 16 || i + 1 == live.size()) {
+        KL(c, mirage::launch_block_copy(mv, R->sz.BB, c->cs));
+        mv.n = 0;
+      }
+    }
+  }
+  for (auto& kv : R->tables)
+    for (int32_t& b : kv.second) {
+      auto it = ren.find(b);
+      if (it != ren.end()) b = it->second;
+    }
+  for (size_t i = 0; i < live.size(); ++i) {
+    R->free_ids.erase(outside[i]);
+    R->free_ids.insert(live[i]);
+  }
+  if (n_moved) *n_moved = (int32_t)live.size();
+  return MIRAGE_OK;
+}
+
 int32_t mirage_alloc_blocks(mirage_ctx* c, int32_t model, int64_t seq_id, int32_t n, int32_t* ids_out,
                             int32_t* shortfall_out) {
   GUARD(c);
@@ -1454,7 +1504,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "step: too many attention units");
   hv.hdr[0] = n_units;
   cudaStream_t cs = c->cs;
-  const bool timed = !M->step_timed;
+  const bool timed = !M->step_timed && !multi_row;  // T_Compute = a decode step, not a prefill
   if (timed) CK(c, cudaEventRecord(M->st0, cs));
   size_t meta_bytes = 0;
   if (int32_t e = upload_meta(c, host, n_addr, &meta_bytes)) return e;

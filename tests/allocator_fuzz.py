@@ -28,6 +28,10 @@ def make_log(seed, n_ops=300, n_seqs=12):
         elif r < 0.07 and not self_cycle:
             self_cycle = True
             log.append(("remap", 0, 0, (0, 1), 1))
+        elif r < 0.09:   # Dynamic Reversion: move a region's live blocks out, then revert it
+            log.append(("migrate", 0, rng.randrange(4)))
+        elif r < 0.11:
+            log.append(("unremap", 0, rng.randrange(4)))
         elif r < 0.6:
             log.append(("alloc", 0, rng.randrange(n_seqs), rng.randint(0, 9)))
         else:
@@ -53,6 +57,11 @@ def replay_lib(log, shape=models.TOY):
                 out.append(("ok", tuple(ctx.alloc_blocks(op[1], op[2], op[3]))))
             elif op[0] == "free":
                 ctx.free_blocks(op[1], op[2])
+                out.append(("ok",))
+            elif op[0] == "migrate":
+                out.append(("ok", ctx.migrate_region(op[1], op[2])))
+            elif op[0] == "unremap":
+                ctx.unremap(op[1], op[2])
                 out.append(("ok",))
         except _lib.MirageError as e:
             out.append(("err", e.code, e.shortfall))
@@ -90,6 +99,14 @@ def replay_oracle(log, shape=models.TOY):
             elif op[0] == "free":
                 al.free_seq(op[1], op[2])
                 out.append(("ok",))
+            elif op[0] == "migrate":
+                try:
+                    out.append(("ok", len(al.migrate(op[1], op[2]))))
+                except OA.NoBlocks:          # the C-ABI reports no shortfall for migrate
+                    out.append(("err", _lib.ERR_NO_BLOCKS, 0))
+            elif op[0] == "unremap":
+                al.unremap(op[1], op[2])
+                out.append(("ok",))
         except OA.NoBlocks as e:
             out.append(("err", _lib.ERR_NO_BLOCKS, e.shortfall))
         except OA.DoubleFree:
@@ -98,6 +115,8 @@ def replay_oracle(log, shape=models.TOY):
             out.append(("err", _lib.ERR_STATE, 0))
         except OA.RangeError:
             out.append(("err", _lib.ERR_RANGE, 0))
+        except OA.Pressure:
+            out.append(("err", _lib.ERR_PRESSURE, 0))
     state = {}
     for m in (0, 1):
         M = al.models[m]

@@ -69,6 +69,22 @@ def test_alloc_remaps_on_shortfall_and_reverts_lifo():
     assert sorted(al.models[0].free) == []
 
 
+def test_revert_migrates_a_few_live_blocks():
+    """Reading #29: a region pinned by a few live blocks is emptied by moving them
+    to free ids outside it, then reverted; the sequence keeps its table length."""
+    al, spec = oracle_setup([1], native=8)
+    ctl = OracleController(al, spec, active=0)
+    ctl.alloc(0, 8 + 2)                        # 8 native + 2 blocks of the reclaimed layer
+    ctl.alloc(1, 3)
+    ctl.free(0)                                # native ids free again; seq 1 pins 3 region ids
+    assert ctl.revert(headroom=0) == []        # migrate_max = 0: region busy
+    assert ctl.revert(headroom=0, migrate_max=2) == []
+    out = ctl.revert(headroom=0, migrate_max=3)
+    assert out[0] == ("migrate", 0, 3) and out[1][0] == "revert"
+    assert al.models[0].tables[1] == [0, 1, 2]  # the lowest free native ids
+    assert al.models[1].layer_state == [OA.RESIDENT] * 8
+
+
 def test_revert_refused_while_blocks_hold_kv():
     al, spec = oracle_setup([1])
     ctl = OracleController(al, spec, active=0)
@@ -94,7 +110,7 @@ def make_trace(seed, n=250):
             live.remove(s)
             ev.append(("free", s))
         else:
-            ev.append(("revert", rng.choice([0, 8, 40])))
+            ev.append(("revert", rng.choice([0, 8, 40]), rng.choice([0, 0, 4, 64])))
         if t % 83 == 82 and not live:
             ev.append(("activate", rng.choice([0, 1])))
     ev += [("free", s) for s in live] + [("revert", 0)]   # off-peak: everything reverts
@@ -109,7 +125,7 @@ def replay(ctl, ev, errors):
             elif e[0] == "free":
                 ctl.free(e[1])
             elif e[0] == "revert":
-                ctl.revert(e[1])
+                ctl.revert(e[1], *e[2:])
             else:
                 ctl.activate(e[1])
         except errors:

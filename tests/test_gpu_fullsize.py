@@ -104,3 +104,35 @@ def test_opt13b_width_decode_vs_oracle():
         rel = np.sqrt(((got - ref) ** 2).mean() / (ref ** 2).mean())
         assert rel <= 1e-2 and np.abs(got - ref).max() <= 5e-2, (t, rel)
         pos = [p + 1 for p in pos]
+
+
+@pytest.mark.parametrize("base", [models.OPT_13B, models.LLAMA3_8B])
+def test_full_width_prefill_vs_oracle(base):
+    """Prefill at full width (D=128; OPT-13B G=1 -> 8-row items, Llama-3-8B G=4 ->
+    2-row items), two layers: the prompts go through mirage_prefill in one
+    layer-major step, then one decode step; both vs oracle c4 token by token."""
+    from paper_2507_11507_b200 import Context
+    shape = base.with_layers(2)
+    prompts_len = [20, 45, 9]
+    B = len(prompts_len)
+    ctx = Context(harness.arena_for([(shape, 16)], sum(prompts_len), 128), sum(prompts_len), 128)
+    mid = ctx.add_model(shape, harness.make_blob(shape, seed=5), 16)
+    dec = Decoder(shape, [weights.layer_tensors(shape, l, 5) for l in range(2)], weights.global_tensors(shape, 5))
+    prompts = [[workload.teacher_tokens(i, t, shape.vocab) for t in range(n)] for i, n in enumerate(prompts_len)]
+    for i, n in enumerate(prompts_len):
+        ctx.alloc_blocks(mid, i, harness.blocks_for(n + 1))
+    am = ctx.prefill(mid, list(range(B)), prompts)
+    for i, p in enumerate(prompts):
+        for t, tok in enumerate(p):
+            _, lg = dec.step_one(i, tok, t)
+        srt = np.sort(lg)
+        if srt[-1] - srt[-2] > 0.5:
+            assert am[i] == int(np.argmax(lg)), i
+    toks = [workload.teacher_tokens(i, 999, shape.vocab) for i in range(B)]
+    hid = torch.empty((B, shape.d_model), dtype=torch.bfloat16, device="cuda")
+    ctx.decode_step(mid, list(range(B)), toks, prompts_len, hidden_out=hid)
+    ctx.sync()
+    ref, _, _ = dec.step(list(range(B)), toks, prompts_len)
+    got = hid.float().cpu().numpy()
+    rel = np.sqrt(((got - ref) ** 2).mean() / (ref ** 2).mean())
+    assert rel <= 1e-2 and np.abs(got - ref).max() <= 5e-2, rel

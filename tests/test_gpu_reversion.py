@@ -85,3 +85,51 @@ def test_device_weight_source_tier_is_bit_identical():
         assert ctx.query(mid)["h2d_copies"] >= 30
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+def test_migrate_then_revert_keeps_outputs_bit_identical():
+    """Reading #29: live blocks of a reclaimed region are copied to free native
+    blocks (mirage_migrate_region), the region is reverted, and decoding goes on
+    bit-identically to a run whose KV never left the native pool; the donor's
+    layer is reloaded intact."""
+    from paper_2507_11507_b200 import Context
+    a, dn = models.TOY, models.TOY.with_layers(4)
+    seqs, steps = [0, 1, 2, 3], 40
+
+    def run(remap):
+        ctx = Context(harness.arena_for([(a, 64), (dn, 8)], 4, 128), 4, 128)
+        ma = ctx.add_model(a, harness.make_blob(a, seed=21), 8 if remap else 64)
+        md = ctx.add_model(dn, harness.make_blob(dn, seed=22), 8)
+        if remap:
+            ctx.set_active(md, False)
+            ctx.remap_layers(md, ma, [3], 0)
+        ctx.alloc_blocks(ma, 99, 6)                      # a filler holding native blocks
+        hid = torch.empty((4, a.d_model), dtype=torch.bfloat16, device="cuda")
+        outs, moved = [], None
+        for t in range(steps):
+            if t % 16 == 0:
+                for s in seqs:
+                    ctx.alloc_blocks(ma, s, 1)
+            if t == 20:
+                ctx.free_blocks(ma, 99)                  # native blocks free again
+                if remap:
+                    reg = ctx.regions(ma)[0]
+                    assert reg["n_free"] < reg["n_blocks"]   # the region still holds KV
+                    moved = ctx.migrate_region(ma, 0)
+                    ctx.unremap(ma, 0)
+            toks = [workload.teacher_tokens(s, t, a.vocab) for s in seqs]
+            ctx.decode_step(ma, seqs, toks, [t] * 4, hidden_out=hid)
+            ctx.sync()
+            outs.append(hid.float().cpu().numpy().copy())
+        if remap:                                        # the donor runs on its reloaded layer 3
+            ctx.set_active(ma, False)
+            ctx.set_active(md, True)
+            decode_and_check(ctx, md, dn, 22, [10, 11], 6)
+        ctx.close()
+        return outs, moved
+
+    got, moved = run(True)
+    ref, _ = run(False)
+    assert moved and moved > 0
+    for t in range(steps):
+        assert np.array_equal(got[t], ref[t]), t

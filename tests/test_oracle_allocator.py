@@ -210,3 +210,50 @@ def test_bytes_invariants():
             if donor != "native":
                 l0 = off // S
                 assert st[l0] == A.RECLAIMED and (off + BB - 1) // S in R
+
+
+def test_migrate_pins():
+    """migrate (reading #29): checked against a brute-force restatement (for each
+    live id of the region, ascending, the smallest free id outside the region not
+    yet taken), plus invariants: tables keep their lengths and order of the
+    unmoved entries, no table keeps a region id, the free count is unchanged, and
+    the region then reverts."""
+    rng = random.Random(5)
+    for trial in range(200):
+        al = A.Allocator()
+        S, BB, N0 = 300, 100, rng.randint(0, 8)
+        r = al.add_model(4, S, BB, N0)
+        d = al.add_model(6, S, BB, 0)
+        al.set_active(d, False)
+        al.remap(d, r, sorted(rng.sample(range(6), rng.randint(1, 4))), 0)
+        for _ in range(rng.randint(1, 12)):
+            seq = rng.randint(0, 5)
+            try:
+                al.alloc(r, seq, rng.randint(0, 5))
+            except A.NoBlocks:
+                pass
+            if rng.random() < 0.3 and al.models[r].tables:
+                al.free_seq(r, rng.choice(sorted(al.models[r].tables)))
+        M = al.models[r]
+        reg = rng.randrange(len(M.regions))
+        g = M.regions[reg]
+        X = set(range(g["first_id"], g["first_id"] + g["n_blocks"]))
+        before = {s: list(t) for s, t in M.tables.items()}
+        nfree = len(M.free)
+        live = [i for t in before.values() for i in t if i in X]
+        cand = [i for i in range(M.next_id) if i in M.free and i not in X]
+        if len(cand) < len(live):
+            with pytest.raises(A.NoBlocks):
+                al.migrate(r, reg)
+            assert {s: list(t) for s, t in M.tables.items()} == before
+            continue
+        moves = al.migrate(r, reg)
+        exp = dict(zip(sorted(live), cand))          # brute force
+        assert dict(moves) == exp
+        for s, t in before.items():
+            assert M.tables[s] == [exp.get(i, i) for i in t]
+            assert not (set(M.tables[s]) & X)
+        assert len(M.free) == nfree
+        check_invariants(al, r)
+        al.unremap(r, reg)                             # the region is empty now
+        assert M.regions[reg]["retired"]

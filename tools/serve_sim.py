@@ -61,7 +61,7 @@ class HostPool:
 
 
 def serve(ctx, ctl, mid, shape, arrivals, prompts, outs, max_batch, revert_every=None, headroom=0, tag="",
-          on_exhaust="recompute", pool=None, prefill="real"):
+          on_exhaust="recompute", pool=None, prefill="real", trace=None, migrate_max=0):
     """Closed decode loop. arrivals[t] = number of new requests at step t.
     on_exhaust: 'recompute' preempts the newest sequence (re-queued, vLLM-style);
     'swap' moves its KV to host memory and back when blocks free up (Pie-style).
@@ -174,8 +174,11 @@ def serve(ctx, ctl, mid, shape, arrivals, prompts, outs, max_batch, revert_every
         for s in [s for s in batch if left[s] <= 0]:
             running.remove(s)
             (ctl.free(s) if ctl else ctx.free_blocks(mid, s))
+        if trace is not None and t % 50 == 0:
+            regs = ctx.regions(mid)
+            trace.append((t, len(running), len(queue), [(r["n_blocks"] - r["n_free"]) for r in regs if not r["retired"]]))
         if ctl and revert_every and t % revert_every == 0:
-            for a in ctl.revert(headroom):
+            for a in ctl.revert(headroom, migrate_max):
                 ctl.timeline = getattr(ctl, "timeline", []) + [(t, a)]
         t += 1
     ctx.sync()
@@ -240,16 +243,21 @@ def e2(args):
         ctx = _lib.Context(harness.arena_for([(shape, native)], 256, 2048), 256, 2048)
         mid = ctx.add_model(shape, blob, native)
         ctl = RemappingController(ctx, {mid: (shape.n_layers, None)}, active=mid, self_remap=self_remap)
+        tr = []
+        # a region pinned by <= 12 live blocks (1/4 of the 48) is emptied by migration first (reading #29)
         st, waits, tokens = serve(ctx, ctl, mid, shape, arr, prompts, outs, 256,
-                                  revert_every=10 if mode == "reversion" else None, headroom=0)
+                                  revert_every=10 if mode == "reversion" else None, headroom=0, trace=tr,
+                                  migrate_max=12)
         horizon = len(arr)
         off = [x for x, t in st if horizon * 2 // 3 <= t < horizon]   # last third of the off-peak phase
         rv = next((t for t, a in ctl.timeline if a[0] == "revert"), None) if hasattr(ctl, "timeline") else None
+        mig = [(t, a) for t, a in getattr(ctl, "timeline", []) if a[0] == "migrate"]
         res[mode] = {"tok_s": tokens / (sum(x for x, _ in st) / 1e3), "offpeak_p50_tbt_ms": pct(off, 50),
                      "peak_p50_tbt_ms": pct([x for x, t in st if t < 100], 50), "revert_at_step": rv,
                      "offpeak_p99_tbt_ms": pct(off, 99), "offpeak_steps": len(off),
                      "revert_step": next((i for i, a in enumerate(ctl.log) if a[0] == "revert"), None),
-                     "actions": [a for a in ctl.log if a[0] != "activate"][:6]}
+                     "actions": [a for a in ctl.log if a[0] != "activate"][:6], "migrations": mig,
+                     "trace_running_queued_region_used": tr[::4]}
         ctx.close()
         del ctx
         torch.cuda.empty_cache()
