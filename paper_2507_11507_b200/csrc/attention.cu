@@ -97,6 +97,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
 }
 
 constexpr int kMaxSplitsDev = 128;  // split-K partitions per (sequence, kv head); runtime agrees
+// partial record: o[D], m, l, 2 pad floats (16-byte rows for float4 combine loads)
 
 template <int D, int G, int QP, int W, int NS>
 constexpr int smem_bytes() { return W * NS * 2 * (16 * D * 2) + (NS + 1) * G * QP * D * 4; }
@@ -431,7 +432,7 @@ paged_attention_kernel(const AttnParams p) {
         if (p.out_fp32) reinterpret_cast<float*>(p.out)[oi] = r;
         else reinterpret_cast<__nv_bfloat16*>(p.out)[oi] = __float2bfloat16_rn(r);
       } else {
-        float* rec = p.partial + ((size_t)(u.pbase + u.split) * p.H + h) * (D + 2);
+        float* rec = p.partial + ((size_t)(u.pbase + u.split) * p.H + h) * (D + 4);
         rec[d] = ov;
         if (d == 0) {
           rec[D] = M;
@@ -453,14 +454,14 @@ paged_attention_kernel(const AttnParams p) {
     __syncthreads();
     if (!am_last) continue;
     __threadfence();
-    const size_t rstride = (size_t)p.H * (D + 2);
-    const float* rec0 = p.partial + ((size_t)u.pbase * p.H + hk * G) * (D + 2);
+    const size_t rstride = (size_t)p.H * (D + 4);
+    const float* rec0 = p.partial + ((size_t)u.pbase * p.H + hk * G) * (D + 4);
     const int ns = u.nsplit;  // <= kMaxSplitsDev
     // (1) stage every split's (m, l) in shared memory
     for (int e = threadIdx.x; e < ns * G; e += kWarps * 32) {
       const int i = e / G, g = e % G;
-      sw[i][g] = __ldcg(rec0 + i * rstride + g * (D + 2) + D);
-      sl[i][g] = __ldcg(rec0 + i * rstride + g * (D + 2) + D + 1);
+      sw[i][g] = __ldcg(rec0 + i * rstride + g * (D + 4) + D);
+      sl[i][g] = __ldcg(rec0 + i * rstride + g * (D + 4) + D + 1);
     }
     __syncthreads();
     // (2) per head: M = max_i m_i, w_i = 2^(m_i - M), Lambda = sum_i w_i l_i (fixed order)
@@ -477,24 +478,42 @@ paged_attention_kernel(const AttnParams p) {
       sLam[g] = Ls;
     }
     __syncthreads();
-    // (3) o = sum_i w_i o_i / Lambda, 8 independent loads in flight per thread
-    for (int e = threadIdx.x; e < G * D; e += kWarps * 32) {
-      const int g = e / D, d = e % D;
-      const float* rg = rec0 + g * (D + 2) + d;
-      float acc = 0.f;
+    // (3) o = sum_i w_i o_i / Lambda: one float4 of dims per thread, 8 independent
+    // 16-byte loads in flight (same per-element order of operations as a scalar loop)
+    for (int e = threadIdx.x; e < G * D / 4; e += kWarps * 32) {
+      const int g = e / (D / 4), d = (e % (D / 4)) * 4;
+      const float* rg = rec0 + g * (D + 4) + d;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       int i = 0;
       for (; i + 8 <= ns; i += 8) {
-        float ov[8];
+        float4 ov[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) ov[k] = __ldcg(rg + (i + k) * rstride);
+        for (int k = 0; k < 8; ++k) ov[k] = __ldcg(reinterpret_cast<const float4*>(rg + (i + k) * rstride));
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc += sw[i + k][g] * ov[k];
+        for (int k = 0; k < 8; ++k) {
+          const float w = sw[i + k][g];
+          acc.x += w * ov[k].x;
+          acc.y += w * ov[k].y;
+          acc.z += w * ov[k].z;
+          acc.w += w * ov[k].w;
+        }
       }
-      for (; i < ns; ++i) acc += sw[i][g] * __ldcg(rg + i * rstride);
-      const float r = acc / sLam[g];
+      for (; i < ns; ++i) {
+        const float4 ov = __ldcg(reinterpret_cast<const float4*>(rg + i * rstride));
+        const float w = sw[i][g];
+        acc.x += w * ov.x;
+        acc.y += w * ov.y;
+        acc.z += w * ov.z;
+        acc.w += w * ov.w;
+      }
+      const float lam = sLam[g];
+      const float r[4] = {acc.x / lam, acc.y / lam, acc.z / lam, acc.w / lam};
       const size_t oi = ((size_t)s * p.H + hk * G + g) * D + d;
-      if (p.out_fp32) reinterpret_cast<float*>(p.out)[oi] = r;
-      else reinterpret_cast<__nv_bfloat16*>(p.out)[oi] = __float2bfloat16_rn(r);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (p.out_fp32) reinterpret_cast<float*>(p.out)[oi + k] = r[k];
+        else reinterpret_cast<__nv_bfloat16*>(p.out)[oi + k] = __float2bfloat16_rn(r[k]);
+      }
     }
   }
   // the last CTA to finish resets the work counter for the next launch

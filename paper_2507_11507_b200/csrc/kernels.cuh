@@ -32,7 +32,7 @@ struct AttnParams {
   const int32_t* n_units_dev;  // if set, the count is read here (CUDA-graph replays)
   int32_t H, H_kv, D;
   float scale_log2;            // log2(e) / sqrt(D) (already applied to q)
-  float* partial;              // [(pbase + split) * H + h][D + 2]
+  float* partial;              // [(pbase + split) * H + h][D + 4]: o, m, l, pad
   int32_t* tickets;            // [B * H_kv], zero between launches
   int32_t* sched;              // [2] dynamic item counter + finished CTAs, zero between launches
   void* out;                   // [B][H][D] fp32 or bf16

@@ -365,7 +365,7 @@ WsPlan ws_plan(const Shape& s, int Bm, int max_units) {
   w.y = (uint64_t)Bm * w.y_ld * 4;
   w.q = (uint64_t)Bm * s.H * s.D * 4;
   w.f = (uint64_t)Bm * s.f * 2;
-  w.partial = (uint64_t)max_units * s.H * (s.D + 2) * 4;
+  w.partial = (uint64_t)max_units * s.H * (s.D + 4) * 4;
   w.tickets = (uint64_t)Bm * s.Hk * 4 + 8;  // split tickets + the attention work counter
   w.argmax = (uint64_t)Bm * 4;
   return w;
@@ -626,8 +626,8 @@ int32_t gemm_lt(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf16* x
     CKB(c, cublasLtMatmulPreferenceCreate(&pref));
     const uint64_t ws = kCublasWs;
     CKB(c, cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws, sizeof ws));
-    constexpr int kCand = 12;
-    cublasLtMatmulHeuristicResult_t res[kCand];
+    static const int kCand = getenv("MIRAGE_GEMM_CANDIDATES") ? std::max(1, std::min(64, atoi(getenv("MIRAGE_GEMM_CANDIDATES")))) : 12;
+    cublasLtMatmulHeuristicResult_t res[64];
     int n = 0;
     cublasLtMatmulAlgoGetHeuristic(c->lt, pl.op, pl.a, pl.b, pl.d, pl.d, pref, kCand, res, &n);
     cublasLtMatmulPreferenceDestroy(pref);
