@@ -423,7 +423,9 @@ def run_mirage(args, rank, world):
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "attention_traffic.json")))
-        traffic = tr.get(wl.name, {}).get("dram_bytes_per_launch")
+        ent = tr.get(wl.name, {})
+        if ent.get("batch", 400 if wl.name == "c2" else None) == B:   # only for the captured workload
+            traffic = ent.get("dram_bytes_per_launch")
     except Exception:
         pass
     if rank != 0:

@@ -94,6 +94,10 @@ __device__ __forceinline__ void norm_row8(int family, int d, bool own, float (&v
                                           __nv_bfloat16* x, float* red) {
   const int e0 = threadIdx.x * 8;
   float gv[8], bv[8], out[8];
+  if (own) {  // issue the parameter loads before the reductions (one DRAM round trip less)
+    load8bf(g + e0, gv);
+    if (family == 0) load8bf(bta + e0, bv);
+  }
   if (family == 0) {
     float sm = 0.f;
     if (own)
@@ -106,8 +110,6 @@ __device__ __forceinline__ void norm_row8(int family, int d, bool own, float (&v
       for (int k = 0; k < 8; ++k) q += (v[k] - mean) * (v[k] - mean);
     const float r = rsqrtf(block_sum(q, red) / d + eps);
     if (own) {
-      load8bf(g + e0, gv);
-      load8bf(bta + e0, bv);
 #pragma unroll
       for (int k = 0; k < 8; ++k) out[k] = (v[k] - mean) * r * gv[k] + bv[k];
       *reinterpret_cast<uint4*>(x + e0) = pack8bf(out);
@@ -119,7 +121,6 @@ __device__ __forceinline__ void norm_row8(int family, int d, bool own, float (&v
       for (int k = 0; k < 8; ++k) q += v[k] * v[k];
     const float r = rsqrtf(block_sum(q, red) / d + eps);
     if (own) {
-      load8bf(g + e0, gv);
 #pragma unroll
       for (int k = 0; k < 8; ++k) out[k] = v[k] * r * gv[k];
       *reinterpret_cast<uint4*>(x + e0) = pack8bf(out);
@@ -244,7 +245,7 @@ qkv_post_kernel(int family, int H, int Hk, int D, const float* qkv, const __nv_b
                 const int32_t* positions, const int32_t* seq_off, const uint64_t* addrs,
                 uint64_t layer_off, float rope_theta, float q_scale, uint32_t* q) {
   extern __shared__ float cs[];  // [D/2] cos, [D/2] sin
-  const int b = blockIdx.x;
+  const int b = blockIdx.x;  // row; blockIdx.y = slice of the row's work items (one per thread)
   const int pos = positions[b];
   const int half = D / 2, hc = D / 16;  // chunks per half row
   const int W = (H + 2 * Hk) * D;
@@ -262,7 +263,7 @@ qkv_post_kernel(int family, int H, int Hk, int D, const float* qkv, const __nv_b
   char* kvbase = reinterpret_cast<char*>(addrs[seq_off[b] + (pos >> 4)] + layer_off);
   const int r = pos & 15;
   const int n_qk = (H + Hk) * hc, n_v = Hk * (D / 8);
-  for (int e = threadIdx.x; e < n_qk + n_v; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < n_qk + n_v; e += gridDim.y * blockDim.x) {
     if (e < n_qk) {
       const int hh = e / hc, c = e % hc;
       const int c0 = hh * D + c * 8, c1 = c0 + half;
@@ -499,7 +500,10 @@ cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float
                             const __nv_bfloat16* bias, const int32_t* positions,
                             const int32_t* seq_off, const uint64_t* addrs, uint64_t layer_off,
                             float rope_theta, float q_scale, uint32_t* q, cudaStream_t s) {
-  qkv_post_kernel<<<B, 256, D * sizeof(float), s>>>(family, H, Hk, D, qkv, bias, positions, seq_off,
+  // one thread per work item: all of a row's loads are in flight at once (the
+  // kernel is latency-bound at decode batch sizes)
+  const int items = (H + Hk) * (D / 16) + Hk * (D / 8);
+  qkv_post_kernel<<<dim3(B, (items + 255) / 256), 256, D * sizeof(float), s>>>(family, H, Hk, D, qkv, bias, positions, seq_off,
                                                     addrs, layer_off, rope_theta, q_scale, q);
   return cudaGetLastError();
 }
