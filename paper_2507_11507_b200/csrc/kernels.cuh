@@ -67,23 +67,6 @@ cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float
                             const __nv_bfloat16* bias, const int32_t* positions,
                             const int32_t* seq_off, const uint64_t* addrs, uint64_t layer_off,
                             float rope_theta, float q_scale, uint32_t* q, cudaStream_t s);
-// Decode-shaped GEMM (gemm_skinny.cu): y[M][N] = x[M][K] W[N][K]^T (+ bias, ReLU),
-// bf16 in, fp32 accumulate, for M <= 64. Split-K partials go to ws
-// ([splits][M][N] fp32); tickets [ceil(N / 128)] must be zero between launches.
-constexpr int kSkinnyMaxSplits = 16;
-struct SkinnyArgs {
-  const __nv_bfloat16* x;  // [M][K]
-  const __nv_bfloat16* W;  // [N][K]
-  void* y;                 // [M][N] fp32, or bf16 if out_bf16
-  const __nv_bfloat16* bias;  // [N] or nullptr
-  float* ws;
-  int32_t* tickets;
-  int M, N, K, k_per_split, out_bf16, relu;
-};
-bool skinny_gemm_ok(int M, int N, int K);
-int skinny_gemm_splits(int N, int K, int sms);
-cudaError_t launch_skinny_gemm(const SkinnyArgs& a, int splits, cudaStream_t s);
-
 // Block migration (mirage_migrate_region): copy `bytes` from src[i] to dst[i]
 // for i < n (device addresses, 16-byte aligned, bytes % 16 == 0).
 struct BlockMoves {

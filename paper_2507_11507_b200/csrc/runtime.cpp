@@ -37,8 +37,6 @@ constexpr int kMaxSplits = 128;        // split-K partitions per (sequence, kv h
 constexpr int kTargetCtas = 148 * 16;     // sizing bound for the attention work-item list
 constexpr uint64_t kAlign = 256;
 constexpr size_t kCublasWs = 32u << 20;
-constexpr size_t kSkinnyWs = 24u << 20;   // split-K partials of the skinny decode GEMM
-constexpr int kSkinnyTickets = 4096;      // N tiles of 128 features
 
 enum LayerState { RESIDENT = 0, SLOT = 1, RECLAIMED = 2 };
 
@@ -247,10 +245,7 @@ struct mirage_ctx {
   cublasHandle_t blas = nullptr;
   cublasLtHandle_t lt = nullptr;
   void* blas_ws = nullptr;
-  // skinny decode GEMM (gemm_skinny.cu) split-K workspace and per-tile tickets
-  float* skinny_ws = nullptr;
-  int32_t* skinny_tickets = nullptr;
-  int sms = 148;
+
   struct LtPlan {
     cublasLtMatmulDesc_t op = nullptr;
     cublasLtMatrixLayout_t a = nullptr, b = nullptr, d = nullptr;
@@ -610,17 +605,6 @@ void harvest_step_time(Model* M) {
 // epi: 0 none, 1 bias, 2 relu(+bias). out_bf16 selects the output type.
 int32_t gemm_lt(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf16* x, void* y, int out_bf16,
                 const bf16* bias, int epi) {
-  // small decode batches: the hand-written weight-streaming kernel (gemm_skinny.cu),
-  // chosen by a fixed rule so results never depend on timing noise
-  static const bool skinny_on = !getenv("MIRAGE_SKINNY_GEMM") || atoi(getenv("MIRAGE_SKINNY_GEMM")) != 0;
-  if (skinny_on && mirage::skinny_gemm_ok(B, N, K) && (N + 127) / 128 <= kSkinnyTickets) {
-    int splits = mirage::skinny_gemm_splits(N, K, c->sms);
-    while (splits > 1 && (size_t)splits * B * N * 4 > kSkinnyWs) --splits;
-    mirage::SkinnyArgs a{x, W, y, epi ? bias : nullptr, c->skinny_ws, c->skinny_tickets, B, N, K, 0, out_bf16,
-                         epi == 2};
-    KL(c, mirage::launch_skinny_gemm(a, splits, c->cs));
-    return MIRAGE_OK;
-  }
   auto key = std::make_tuple(B, N, K, out_bf16, epi);
   auto it = c->lt_plans.find(key);
   if (it == c->lt_plans.end()) {
@@ -779,11 +763,7 @@ int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
   if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) return bail(MIRAGE_ERR_CUDA);
   if (cublasLtCreate(&c->lt) != CUBLAS_STATUS_SUCCESS) return bail(MIRAGE_ERR_CUDA);
   if (cudaMalloc(&c->blas_ws, kCublasWs) != cudaSuccess) return bail(MIRAGE_ERR_CUDA);
-  if (cudaMalloc(reinterpret_cast<void**>(&c->skinny_ws), kSkinnyWs) != cudaSuccess ||
-      cudaMalloc(reinterpret_cast<void**>(&c->skinny_tickets), kSkinnyTickets * 4) != cudaSuccess ||
-      cudaMemset(c->skinny_tickets, 0, kSkinnyTickets * 4) != cudaSuccess)
-    return bail(MIRAGE_ERR_CUDA);
-  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->cfg.device);
+
   if (cublasSetWorkspace(c->blas, c->blas_ws, kCublasWs) != CUBLAS_STATUS_SUCCESS ||
       cublasSetStream(c->blas, c->cs) != CUBLAS_STATUS_SUCCESS)
     return bail(MIRAGE_ERR_CUDA);
@@ -859,8 +839,7 @@ void mirage_destroy(mirage_ctx* c) {
   }
   if (c->lt) cublasLtDestroy(c->lt);
   if (c->blas_ws) cudaFree(c->blas_ws);
-  if (c->skinny_ws) cudaFree(c->skinny_ws);
-  if (c->skinny_tickets) cudaFree(c->skinny_tickets);
+
   if (c->own_xs && c->xs) cudaStreamDestroy(c->xs);
   if (c->nccl) ncclCommDestroy(c->nccl);
   (void)cudaGetLastError();
