@@ -76,6 +76,12 @@ extern "C" {
                                 * over peer memory (NVLink) and applies the residual and
                                 * next norm (a one-shot all-reduce fused into its
                                 * consumer; fixed rank order, bit-identical on all ranks) */
+#define MIRAGE_FLAG_POISON 32u /* init flag (debug): when layers are reclaimed,
+                                * their bytes are filled with 0xFF (bf16 NaN) on the compute
+                                * stream before any block is handed out, so a kernel that
+                                * still read a reclaimed layer as weights would produce NaN.
+                                * Blocks carry KV before they are read, so outputs are
+                                * unchanged.                                               */
 #define MIRAGE_FLAG_HOST_ONLY 2u /* init flag: no device; allocator/remap/table/query
                                   * calls only (the arena pointer is used for address
                                   * arithmetic, never dereferenced); device calls

@@ -24,6 +24,7 @@ FLAG_HOST_ONLY = 2
 FLAG_SLOT_TAGS = 4
 FLAG_CUDA_GRAPHS = 8
 FLAG_TP_IPC = 16
+FLAG_POISON = 32
 MAX_CYCLE = 256
 
 _NAMES = {ERR_CONFIG: "CONFIG", ERR_CAPACITY: "CAPACITY", ERR_RANGE: "RANGE", ERR_STATE: "STATE",

@@ -1149,6 +1149,9 @@ int32_t mirage_remap_layers(mirage_ctx* c, int32_t donor, int32_t recipient, con
   D->donated_bytes += (uint64_t)Rl.size() * D->sz.S;
   for (int i = 0; i < beta; ++i) D->layer_state[cycle[i]] = SLOT;
   for (int32_t l : Rl) D->layer_state[l] = RECLAIMED;
+  if ((c->cfg.flags & MIRAGE_FLAG_POISON) && !c->host_only)  // debug: reclaimed bytes become NaN
+    for (auto& r : runs)
+      CK(c, cudaMemsetAsync(D->w_dev + (uint64_t)r.first * D->sz.S, 0xFF, (uint64_t)r.second * D->sz.S, c->cs));
   if (gained && !c->host_only)  // stream-ordered after every kernel that read these bytes as weights
     CK(c, cudaMemcpyAsync(R->bbase_dev + first_new, R->bbase_host.data() + first_new, gained * 8,
                           cudaMemcpyHostToDevice, c->cs));

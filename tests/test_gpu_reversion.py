@@ -29,10 +29,13 @@ def decode_and_check(ctx, mid, shape, seed, seqs, steps, t0=0):
         assert rel < 1e-2, (t, rel)
 
 
-def test_cycle_and_inactive_donor_reversion():
-    from paper_2507_11507_b200 import Context
+@pytest.mark.parametrize("poison", [False, True])
+def test_cycle_and_inactive_donor_reversion(poison):
+    """With MIRAGE_FLAG_POISON the reclaimed bytes are NaN-filled at remap time: any
+    kernel that still read a reclaimed layer as weights would poison the outputs."""
+    from paper_2507_11507_b200 import Context, _lib
     a, d = models.TOY, models.TOY_LLAMA
-    ctx = Context(harness.arena_for([(a, 8), (d, 8)], 8, 128), 8, 128)
+    ctx = Context(harness.arena_for([(a, 8), (d, 8)], 8, 128), 8, 128, flags=_lib.FLAG_POISON if poison else 0)
     ma = ctx.add_model(a, harness.make_blob(a, seed=7), 8)
     md = ctx.add_model(d, harness.make_blob(d, seed=8), 8)
     # self-remap cycle on A and a full reclaim of the inactive donor D into A
