@@ -209,3 +209,36 @@ def test_cold_start_reload_gated_per_layer():
     assert run_cold(None) == (1, 2)     # both donor layers reloaded, prefill bit-identical
     assert run_cold(4)[0] == 1          # slow link (20 ms per layer), waits kept: still exact
     assert run_cold(3)[0] == 0          # slow link, waits removed: the prefill reads KV bytes
+
+
+@pytest.mark.parametrize("shape", [models.TOY, models.TOY_LLAMA])
+def test_prefill_through_a_streaming_cycle(shape):
+    """A prefill on a model that re-streams a layer through one slot (C={0,1},
+    beta=1): every chunk is a step of the cycle; results match the oracle and a
+    non-remapped run bit for bit."""
+    from paper_2507_11507_b200 import Context
+    seqs = [0, 1, 2]
+    lens = [21, 9, 33]
+    outs = []
+    for remap in (True, False):
+        ctx = Context(harness.arena_for([(shape, 64)], 16, 128), 16, 128)
+        mid = ctx.add_model(shape, harness.make_blob(shape, seed=13), 8 if remap else 64)
+        if remap:
+            ctx.remap_layers(mid, mid, [0, 1], 1)
+        for s, n in zip(seqs, lens):
+            ctx.alloc_blocks(mid, s, harness.blocks_for(n + 1))
+        ctx.prefill(mid, seqs, [prompt(s, n, shape.vocab) for s, n in zip(seqs, lens)], argmax=False)
+        hid = torch.empty((3, shape.d_model), dtype=torch.bfloat16, device="cuda")
+        ctx.decode_step(mid, seqs, [5, 6, 7], lens, hidden_out=hid)
+        ctx.sync()
+        outs.append(hid.float().cpu().numpy())
+        if remap:
+            assert ctx.query(mid)["h2d_copies"] > 0
+        ctx.close()
+    assert np.array_equal(outs[0], outs[1])
+    dec = oracle_for(shape, 13)
+    for s, n in zip(seqs, lens):
+        for t, tok in enumerate(prompt(s, n, shape.vocab)):
+            dec.step_one(s, tok, t)
+    ref, _, _ = dec.step(seqs, [5, 6, 7], lens)
+    check(outs[0], ref, "prefill under a cycle")
