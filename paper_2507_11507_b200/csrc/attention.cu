@@ -72,6 +72,16 @@ __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(smem_u32(p)));
 }
+__device__ __forceinline__ void ldsm_x4_s(uint32_t (&r)[4], uint32_t saddr) {  // shared-window address
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(saddr));
+}
+__device__ __forceinline__ void ldsm_x4_t_s(uint32_t (&r)[4], uint32_t saddr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(saddr));
+}
 __device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -137,6 +147,7 @@ paged_attention_kernel(const AttnParams p) {
   __shared__ int slot_claim[QB];
   __shared__ unsigned long long slot_word[QB];  // ((k + 1) << 32) | item, published atomically
   __shared__ float sLam[GV];
+  __shared__ float sFw[kWarps][GV], sMg[GV], sLs[GV];  // per-item warp-merge weights
   // split-combine scratch aliases sm_acc (free once the partials are written)
   float(*sw)[GV] = reinterpret_cast<float(*)[GV]>(sm_accf);
   float(*sl)[GV] = reinterpret_cast<float(*)[GV]>(sm_accf + kMaxSplitsDev * GV);
@@ -241,9 +252,16 @@ paged_attention_kernel(const AttnParams p) {
   };
   pump(0);
 
-  // ldmatrix row addresses (byte offsets within a tile, before the swizzle)
+  // ldmatrix lane addresses within a K|V tile (swizzled), computed once per warp
   const int k_row = (lane & 7) + ((lane >> 3) & 1) * 8, k_cadd = lane >> 4;
   const int v_row = (lane & 7) + (lane >> 4) * 8, v_cadd = (lane >> 3) & 1;
+  const uint32_t ring_s = smem_u32(ring);
+  uint32_t koff[KS], voff[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    koff[ks] = k_row * ROW + (((2 * ks + k_cadd) ^ (k_row & 7)) << 4);
+    voff[ks] = TILE + v_row * ROW + (((2 * ks + v_cadd) ^ (v_row & 7)) << 4);
+  }
 
   for (int ck = 0;; ++ck) {
     pump(ck);  // the producer has now visited item ck (or the stream has ended there)
@@ -314,11 +332,11 @@ paged_attention_kernel(const AttnParams p) {
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int j = 0; j < 4; ++j) sacc[nt][j] = sacc2[nt][j] = 0.f;
+      const uint32_t tile_s = ring_s + st * 2 * TILE;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         uint32_t a[4];
-        const int c = 2 * ks + k_cadd;
-        ldsm_x4(a, tile + k_row * ROW + ((c ^ (k_row & 7)) << 4));
+        ldsm_x4_s(a, tile_s + koff[ks]);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) mma_bf16((ks & 1) ? sacc2[nt] : sacc[nt], a, qb[nt][ks]);
       }
@@ -376,8 +394,7 @@ paged_attention_kernel(const AttnParams p) {
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         uint32_t a[4];
-        const int c = 2 * ks + v_cadd;
-        ldsm_x4_t(a, tile + TILE + v_row * ROW + ((c ^ (v_row & 7)) << 4));
+        ldsm_x4_t_s(a, tile_s + voff[ks]);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) mma_bf16(o[nt][ks], a, pb[nt]);
       }
@@ -410,33 +427,60 @@ paged_attention_kernel(const AttnParams p) {
     }
     __syncthreads();
 
-    // merge the warps in fixed order; thread t handles (g, d) pairs
+    // merge the warps in fixed order. Per head first (one thread each): M = max_w m_w,
+    // fw_w = 2^(m_w - M) (0 for a warp that saw nothing), Ls = sum_w fw_w l_w; then
+    // every thread merges float4s of dims with the precomputed weights.
     const bool split = u.nsplit > 1;
-    for (int e = threadIdx.x; e < GV * D; e += kWarps * 32) {
-      const int g = e / D, d = e % D;
-      if (QP > 1 && g / G >= nq) continue;
+    if (threadIdx.x < GV) {
+      const int g = threadIdx.x;
       float M = sm_m[0][g];
 #pragma unroll
       for (int w = 1; w < kWarps; ++w) M = fmaxf(M, sm_m[w][g]);
-      float Ls = 0.f, ov = 0.f;
+      float Ls = 0.f;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) {
         const float fw = (sm_m[w][g] == -CUDART_INF_F) ? 0.f : exp2f(sm_m[w][g] - M);
+        sFw[w][g] = fw;
         Ls += fw * sm_l[w][g];
-        ov += fw * sm_acc[w][g][d];
+      }
+      sMg[g] = M;
+      sLs[g] = Ls;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < GV * D / 4; e += kWarps * 32) {
+      const int g = e / (D / 4), d = (e % (D / 4)) * 4;
+      if (QP > 1 && g / G >= nq) continue;
+      float4 ov = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const float fw = sFw[w][g];
+        const float4 a = *reinterpret_cast<const float4*>(&sm_acc[w][g][d]);
+        ov.x += fw * a.x;
+        ov.y += fw * a.y;
+        ov.z += fw * a.z;
+        ov.w += fw * a.w;
       }
       const int h = hk * G + g % G;
       if (!split) {
-        const float r = ov / Ls;
+        const float Ls = sLs[g];
         const size_t oi = ((size_t)(s + g / G) * p.H + h) * D + d;
-        if (p.out_fp32) reinterpret_cast<float*>(p.out)[oi] = r;
-        else reinterpret_cast<__nv_bfloat16*>(p.out)[oi] = __float2bfloat16_rn(r);
+        if (p.out_fp32) {
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oi) =
+              make_float4(ov.x / Ls, ov.y / Ls, ov.z / Ls, ov.w / Ls);
+        } else {
+          const __nv_bfloat162 lo2 = __floats2bfloat162_rn(ov.x / Ls, ov.y / Ls);
+          const __nv_bfloat162 hi2 = __floats2bfloat162_rn(ov.z / Ls, ov.w / Ls);
+          uint2 pk;
+          pk.x = *reinterpret_cast<const uint32_t*>(&lo2);
+          pk.y = *reinterpret_cast<const uint32_t*>(&hi2);
+          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + oi) = pk;
+        }
       } else {
         float* rec = p.partial + ((size_t)(u.pbase + u.split) * p.H + h) * (D + 4);
-        rec[d] = ov;
+        *reinterpret_cast<float4*>(rec + d) = ov;
         if (d == 0) {
-          rec[D] = M;
-          rec[D + 1] = Ls;
+          rec[D] = sMg[g];
+          rec[D + 1] = sLs[g];
         }
       }
     }
