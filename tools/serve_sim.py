@@ -324,7 +324,8 @@ def e4(args):
     """Table 1 C1 under round-robin temporal sharing: OPT-13b, Llama-2-13b
     and Llama-3-8b with the paper's GH200 reservations (35%/35%/20% of 96 GB).
     Each phase one model is active; at the phase end its running requests are
-    preempted and the next model activates (its donated layers are reloaded).
+    preempted and the next model activates (its donated layers are reloaded
+    asynchronously: the reload overlaps the phase's first prefill and steps).
     Controller with MRU (the paper's default) vs LRU vs no remap."""
     shapes = [models.OPT_13B, models.LLAMA2_13B, models.LLAMA3_8B]
     resv = [0.35, 0.35, 0.20]
@@ -372,6 +373,7 @@ def e4(args):
                         queues[m].append((nxt, t))
                         nxt += 1
                 q = queues[a]
+                admitted = []
                 while q and len(running) < 256:
                     sid, ta = q[0]
                     P = int(prompts[sid % len(prompts)])
@@ -382,11 +384,20 @@ def e4(args):
                         if e.code != _lib.ERR_NO_BLOCKS:
                             raise
                         break
-                    ctx.fill_kv(mid, sid, P, seed=sid)
+                    if args.prefill == "fill":
+                        ctx.fill_kv(mid, sid, P, seed=sid)
+                    else:
+                        admitted.append((sid, P))
                     q.pop(0)
                     running.append(sid)
                     pos[sid], left[sid], held[sid] = P, int(outs[sid % len(outs)]), harness.blocks_for(P + 1)
                     waits.append(t - ta)
+                f0 = torch.cuda.Event(enable_timing=True)
+                f0.record(ctx.stream)
+                if admitted:   # the phase's first prefill also absorbs the reload of reverted layers
+                    ctx.prefill(mid, [x for x, _ in admitted],
+                                [[workload.teacher_tokens(x, j, sh.vocab) for j in range(n)] for x, n in admitted],
+                                argmax=False)
                 for sid in list(running):
                     if sid not in running or harness.blocks_for(pos[sid] + 1) <= held[sid]:
                         continue
@@ -403,8 +414,7 @@ def e4(args):
                                 break
                 if not running:
                     continue
-                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                f0.record(ctx.stream)
+                f1 = torch.cuda.Event(enable_timing=True)
                 ctx.decode_step(mid, running, [workload.teacher_tokens(x, pos[x], sh.vocab) for x in running],
                                 [pos[x] for x in running], argmax=False)
                 f1.record(ctx.stream)
@@ -440,6 +450,8 @@ if __name__ == "__main__":
     ap.add_argument("--phase", type=int, default=150)
     ap.add_argument("--phases", type=int, default=9)
     ap.add_argument("--cap", type=float, default=1.0, help="max remapped fraction of an inactive model (P:387)")
+    ap.add_argument("--prefill", default="real", choices=["real", "fill"],
+                    help="E4 admission: real prefill (reloads overlap it) or random prompt KV")
     a = ap.parse_args()
     out = {}
     if "e1" in a.exp:
