@@ -1,0 +1,27 @@
+"""Host logic of bench.py (CPU): the nearest-rank percentile used for p50/p99
+TBT, checked against SPEC.md:474-476's examples ({10, 12} ms -> P99 = 12 ms;
+101 samples 1..101 -> P99 = 100, rank ceil(0.99 * 101) = 100)."""
+import importlib.util
+import os
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def load_bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def test_nearest_rank_percentiles():
+    b = load_bench()
+    xs = list(range(101))                       # 0..100, shuffled order must not matter
+    xs = xs[50:] + xs[:50]
+    assert b.nearest_rank(xs, 99) == 99         # ceil(0.99 * 101) = 100th smallest -> 99
+    assert b.nearest_rank(xs, 50) == 50         # ceil(50.5) = 51st smallest -> 50
+    assert b.nearest_rank(xs, 100) == 100
+    assert b.nearest_rank([7.0], 99) == 7.0
+    assert b.nearest_rank(list(range(1, 11)), 90) == 9
+    assert b.nearest_rank([10.0, 12.0], 99) == 12.0
+    assert b.nearest_rank(list(range(1, 102)), 99) == 100

@@ -144,6 +144,12 @@ def test_multirow_errors():
     with pytest.raises(MirageError):      # 17 tokens need 2 blocks
         ctx.prefill(mid, [0], [list(range(17))])
     assert ctx.seq_len(mid, 0) == 0       # nothing committed on error
+    with pytest.raises(MirageError):      # degenerate inputs: empty batch, empty prompt, too many rows
+        ctx.decode_step(mid, [], [], [])
+    with pytest.raises(MirageError):
+        ctx.prefill(mid, [0], [[]])
+    with pytest.raises(MirageError):
+        ctx.decode_step(mid, [0] * 9, list(range(9)), list(range(9)))
     ctx.prefill(mid, [0], [list(range(16))])
     assert ctx.seq_len(mid, 0) == 16
 
