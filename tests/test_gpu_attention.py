@@ -53,7 +53,7 @@ def oracle_alloc_mirror(shape, n_native, gained_layers, ops):
     return al, r
 
 
-@pytest.mark.parametrize("H,Hk,D", [(4, 4, 128), (8, 2, 128), (4, 4, 64), (8, 1, 64)])
+@pytest.mark.parametrize("H,Hk,D", [(4, 4, 128), (8, 2, 128), (4, 4, 64), (8, 1, 64), (8, 4, 64), (16, 2, 128)])
 def test_attention_matches_oracle(H, Hk, D):
     shape = small_shape(H, Hk, D)
     lens = [1, 15, 16, 17, 127, 128, 129, 700]
