@@ -357,7 +357,26 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
         ctx.sync()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     st2 = ctx.query(mid)
-    out = dict(step_ms=step_ms, total_ms=total_ms, launches=launches, clocks=clocks, e2e_ms=e2e_ms,
+    # the same attention launch alone (after the timed region, no DMA or GEMMs around it)
+    alone_gbs = None
+    try:
+        sh = tenants[0][0]
+        B = len(ctxs)
+        q = torch.randn((B, sh.n_heads, sh.head_dim), dtype=torch.float32, device=dev)
+        o = torch.empty((B, sh.n_heads, sh.head_dim), dtype=torch.bfloat16, device=dev)
+        for _ in range(3):
+            ctx.attn_only(mid, sh.n_layers - 1, list(range(B)), q, o)
+        ctx.sync()
+        a0 = ctx.query(mid)
+        for _ in range(10):
+            ctx.attn_only(mid, sh.n_layers - 1, list(range(B)), q, o)
+        ctx.sync()
+        a1 = ctx.query(mid)
+        if a1["attn_launches"] > a0["attn_launches"]:
+            alone_gbs = (a1["attn_bytes"] - a0["attn_bytes"]) / ((a1["attn_ms"] - a0["attn_ms"]) * 1e-3) / 1e9
+    except Exception:
+        alone_gbs = None
+    out = dict(step_ms=step_ms, alone_gbs=alone_gbs, total_ms=total_ms, launches=launches, clocks=clocks, e2e_ms=e2e_ms,
                attn_ms=st1["attn_ms"] - st0["attn_ms"], attn_launches=st1["attn_launches"] - st0["attn_launches"],
                attn_bytes=st1["attn_bytes"] - st0["attn_bytes"],
                h2d_ms=st1["h2d_ms"] - st0["h2d_ms"], h2d_bytes=st1["h2d_bytes"] - st0["h2d_bytes"],
@@ -454,6 +473,8 @@ def run_mirage(args, rank, world):
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": attn_bytes_launch, "avg_launch_ms": attn_avg_ms,
                      "launches": res["attn_launches"], "share_of_step": res["attn_ms"] / t_local,
+                     "kernel_alone_gbs": res.get("alone_gbs"),
+                     "kernel_alone_frac": (res["alone_gbs"] / hbm_peak) if res.get("alone_gbs") else None,
                      "peak_source": peak_src},
         "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": h2d_peak, "frac": (h2d_gbs / h2d_peak) if h2d_gbs else None,
                 "bytes_per_step": res["h2d_bytes"] / args.steps, "copies": res["h2d_copies"],
