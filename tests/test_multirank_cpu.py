@@ -1,4 +1,4 @@
-"""Multi-rank allocator checks over torch.distributed gloo (world sizes 2 and 4),
+"""Multi-rank allocator checks over torch.distributed gloo (world sizes 2, 4 and 8: the 1/2/4/8-GPU parity target),
 the CPU stand-in for 1/2/4/8 GPUs:
  * tenant/batch sharding: every rank replays its own op log; rank 0 replays all
    logs in the oracle and checks every rank's state hash bit-exactly;
@@ -46,7 +46,7 @@ def _worker(rank, world, port, results):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_gloo_ranks(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
