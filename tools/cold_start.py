@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--prompts", type=int, default=64)
     ap.add_argument("--n-list", type=int, nargs="*", default=[0, 2, 4, 8, 12, 16, 24, 32])
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--time-attn", action="store_true", help="also report the prefill's attention time (N=0 only)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -75,7 +76,8 @@ def main():
         for mode in (["prefill"] if N == 0 else ["reload", "serial", "overlapped"]):
             best = None
             for rep in range(a.reps):
-                ctx = _lib.Context(arena, rows, max_ctx, device=0)
+                ctx = _lib.Context(arena, rows, max_ctx, device=0,
+                                   flags=_lib.FLAG_TIME_ATTN if (a.time_attn and N == 0) else 0)
                 md = ctx.add_model(d, blob, need + 8)
                 mr = ctx.add_model(r, harness.make_blob(r, seed=1), 64)
                 # warm-up prefill of the same shapes (cuBLASLt plans are tuned per context)
@@ -103,6 +105,10 @@ def main():
                 e1.record(ctx.stream)
                 ctx.sync()
                 ms = e0.elapsed_time(e1)
+                if a.time_attn and N == 0:
+                    st = ctx.query(md)
+                    print(json.dumps({"prefill_attention_ms_total_incl_warmup": round(st["attn_ms"], 2),
+                                      "attention_launches": st["attn_launches"]}), flush=True)
                 ctx.close()
                 best = ms if best is None else min(best, ms)
             results.append({"N": N, "mode": mode, "ms": round(best, 2)})
