@@ -78,16 +78,23 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
 
-    def stop(self):
+    def stop(self, window=None):
+        """window = (t0, t1) host times of the timed region: keep the samples that
+        arrived inside it (a 200 ms sample lands shortly after it is taken); the
+        sampler runs from before the warm-up so short timed regions still get one."""
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(2)
             except Exception:
                 self.proc.kill()
-        rows = [r for r in self.rows if len(r) >= 9]
+        rows = [(t, r) for t, r in self.rows if len(r) >= 9]
+        if window and rows:
+            inside = [(t, r) for t, r in rows if window[0] <= t <= window[1] + 0.25]
+            rows = inside or [min(rows, key=lambda tr: abs(tr[0] - window[0]))]
+        rows = [r for _, r in rows]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
@@ -325,6 +332,8 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
         for i in range(B):
             pos[i] += 1
 
+    if clock:
+        clock.start()   # running before the timed region; stop() keeps the samples inside it
     for _ in range(warmup):
         step(False)
     ctx.sync()
@@ -334,8 +343,7 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
     if torch.distributed.is_initialized():
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
-    if clock:
-        clock.start()
+    t_timed0 = time.time()
     cs = ctx.stream
     torch.cuda.nvtx.range_push("timed")
     evs[0].record(cs)
@@ -345,7 +353,7 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
     ctx.sync()
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize(dev)
-    clocks = clock.stop() if clock else None
+    clocks = clock.stop((t_timed0, time.time())) if clock else None
     step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(steps)]
     total_ms = evs[0].elapsed_time(evs[steps])
     launches = ctx.kernel_launches() - l0

@@ -25,3 +25,16 @@ def test_nearest_rank_percentiles():
     assert b.nearest_rank(list(range(1, 11)), 90) == 9
     assert b.nearest_rank([10.0, 12.0], 99) == 12.0
     assert b.nearest_rank(list(range(1, 102)), 99) == 100
+
+
+def test_clock_sampler_keeps_samples_inside_the_timed_window():
+    b = load_bench()
+    cs = b.ClockSampler(0)
+    row = lambda mhz, cap: ["0", str(mhz), "1965", "900", "0x0", "Not Active", "Not Active", "Not Active", cap]
+    cs.rows = [(9.0, row(1000, "Active")), (10.1, row(1900, "Not Active")), (10.3, row(1800, "Active")),
+               (12.0, row(500, "Not Active"))]
+    got = cs.stop((10.0, 10.5))
+    assert got["sm_mhz"] == 1850 and got["samples"] == 2 and got["reasons"] == ["sw_power_cap"]
+    cs.rows = [(9.0, row(1000, "Not Active")), (10.9, row(1700, "Not Active"))]
+    got = cs.stop((10.0, 10.2))                  # none inside: the nearest sample to the start
+    assert got["sm_mhz"] == 1700 and got["samples"] == 1
