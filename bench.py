@@ -153,6 +153,59 @@ def oracle_leg(shape, ctxs, n_seqs=2, seed=0, steps=1):
                        f"LM head, fp64 numpy, scaled x{shape.n_layers} layers to tok/s")}
 
 
+def allocator_leg(n_ops=20000, seed=0):
+    """SURVEY §8(d) oracle item (1): the allocator oracle (c2, one thread) and the
+    library's C++ allocator (host-only context) replaying the same seeded op log:
+    a toy tenant with 40 native blocks, an inactive donor reclaimed into it, then
+    alloc/free traffic over 64 sequences. Returns ops/s of both."""
+    import random
+    from oracle import allocator as OA
+    from paper_2507_11507_b200 import _lib
+    from synth import models, weights
+    sh = models.TOY
+    bb = sh.n_layers * sh.n_kv_heads * 2 * 16 * sh.head_dim * 2
+    rng = random.Random(seed)
+    log = [("alloc" if rng.random() < 0.6 else "free", rng.randrange(64), rng.randint(1, 4)) for _ in range(n_ops)]
+    al = OA.Allocator()
+    r = al.add_model(sh.n_layers, weights.layer_bytes(sh), bb, 40)
+    d = al.add_model(sh.n_layers, weights.layer_bytes(sh), bb, 0)
+    al.set_active(d, False)
+    al.remap(d, r, [0, 1], 0)
+    t0 = time.perf_counter()
+    for op, seq, n in log:
+        try:
+            al.alloc(r, seq, n) if op == "alloc" else al.free_seq(r, seq)
+        except (OA.NoBlocks, OA.DoubleFree):
+            pass
+    t_or = time.perf_counter() - t0
+    ctx = _lib.Context.host_only(1 << 36, 64, 4096)
+    r2 = ctx.add_model_host_only(sh, 40)
+    d2 = ctx.add_model_host_only(sh, 0)
+    ctx.set_active(d2, False)
+    ctx.remap_layers(d2, r2, [0, 1], 0)
+    t0 = time.perf_counter()
+    for op, seq, n in log:
+        try:
+            ctx.alloc_blocks(r2, seq, n) if op == "alloc" else ctx.free_blocks(r2, seq)
+        except _lib.MirageError:
+            pass
+    t_lib = time.perf_counter() - t0
+    ctx.close()
+    return {"ops": n_ops, "oracle_ops_s": n_ops / t_or, "library_ops_s_incl_ctypes": n_ops / t_lib}
+
+
+def host_cpu():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model, "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -461,7 +514,12 @@ def run_mirage(args, rank, world):
     if world == 1 and not args.no_cpu_baseline:
         try:
             o = oracle_leg(wl.tenants[0][0], wl.ctxs, n_seqs=2, seed=args.seed, steps=1)
-            cpu = {"value": o["tok_s"], "unit": "tok/s", "cores": o["cores"], "kind": "oracle", "sample": o["sample"]}
+            cpu = {"value": o["tok_s"], "unit": "tok/s", "cores": o["cores"], "kind": "oracle", "sample": o["sample"],
+                   "host": host_cpu()}
+            try:
+                cpu["allocator"] = allocator_leg()
+            except Exception as e:
+                cpu["allocator"] = {"failed": str(e)[:200]}
         except Exception as e:  # the CPU leg must not hide the GPU number
             cpu = {"value": None, "unit": "tok/s", "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {e}"}
     step_med = statistics.median(res["step_ms"])

@@ -38,3 +38,10 @@ def test_clock_sampler_keeps_samples_inside_the_timed_window():
     cs.rows = [(9.0, row(1000, "Not Active")), (10.9, row(1700, "Not Active"))]
     got = cs.stop((10.0, 10.2))                  # none inside: the nearest sample to the start
     assert got["sm_mhz"] == 1700 and got["samples"] == 1
+
+
+def test_cpu_baseline_extras():
+    b = load_bench()
+    a = b.allocator_leg(2000)
+    assert a["ops"] == 2000 and a["oracle_ops_s"] > 0 and a["library_ops_s_incl_ctypes"] > 0
+    assert b.host_cpu()["nproc"] >= 1
