@@ -157,7 +157,8 @@ def allocator_leg(n_ops=20000, seed=0):
     """SURVEY §8(d) oracle item (1): the allocator oracle (c2, one thread) and the
     library's C++ allocator (host-only context) replaying the same seeded op log:
     a toy tenant with 40 native blocks, an inactive donor reclaimed into it, then
-    alloc/free traffic over 64 sequences. Returns ops/s of both."""
+    valid alloc/free traffic over 64 sequences (every op succeeds; the tables
+    of both are compared at the end). Returns ops/s of both."""
     import random
     from oracle import allocator as OA
     from paper_2507_11507_b200 import _lib
@@ -165,7 +166,19 @@ def allocator_leg(n_ops=20000, seed=0):
     sh = models.TOY
     bb = sh.n_layers * sh.n_kv_heads * 2 * 16 * sh.head_dim * 2
     rng = random.Random(seed)
-    log = [("alloc" if rng.random() < 0.6 else "free", rng.randrange(64), rng.randint(1, 4)) for _ in range(n_ops)]
+    cap = 40 + 2 * weights.layer_bytes(sh) // bb      # native + the reclaimed donor layers
+    live, free_n, log = {}, cap, []
+    while len(log) < n_ops:                            # a valid log: every op succeeds
+        n = rng.randint(1, 4)
+        if free_n >= n and (rng.random() < 0.6 or not live):
+            sq = rng.randrange(64)
+            live[sq] = live.get(sq, 0) + n
+            free_n -= n
+            log.append(("alloc", sq, n))
+        elif live:
+            sq = rng.choice(sorted(live))
+            free_n += live.pop(sq)
+            log.append(("free", sq, 0))
     al = OA.Allocator()
     r = al.add_model(sh.n_layers, weights.layer_bytes(sh), bb, 40)
     d = al.add_model(sh.n_layers, weights.layer_bytes(sh), bb, 0)
@@ -173,10 +186,7 @@ def allocator_leg(n_ops=20000, seed=0):
     al.remap(d, r, [0, 1], 0)
     t0 = time.perf_counter()
     for op, seq, n in log:
-        try:
-            al.alloc(r, seq, n) if op == "alloc" else al.free_seq(r, seq)
-        except (OA.NoBlocks, OA.DoubleFree):
-            pass
+        al.alloc(r, seq, n) if op == "alloc" else al.free_seq(r, seq)
     t_or = time.perf_counter() - t0
     ctx = _lib.Context.host_only(1 << 36, 64, 4096)
     r2 = ctx.add_model_host_only(sh, 40)
@@ -185,13 +195,12 @@ def allocator_leg(n_ops=20000, seed=0):
     ctx.remap_layers(d2, r2, [0, 1], 0)
     t0 = time.perf_counter()
     for op, seq, n in log:
-        try:
-            ctx.alloc_blocks(r2, seq, n) if op == "alloc" else ctx.free_blocks(r2, seq)
-        except _lib.MirageError:
-            pass
+        ctx.alloc_blocks(r2, seq, n) if op == "alloc" else ctx.free_blocks(r2, seq)
     t_lib = time.perf_counter() - t0
+    same = all(ctx.block_table(r2, sq) == al.table(r, sq) for sq in range(64) if sq in al.models[r].tables)
     ctx.close()
-    return {"ops": n_ops, "oracle_ops_s": n_ops / t_or, "library_ops_s_incl_ctypes": n_ops / t_lib}
+    return {"ops": n_ops, "oracle_ops_s": n_ops / t_or, "library_ops_s_incl_ctypes": n_ops / t_lib,
+            "tables_equal": same}
 
 
 def host_cpu():

@@ -43,5 +43,5 @@ def test_clock_sampler_keeps_samples_inside_the_timed_window():
 def test_cpu_baseline_extras():
     b = load_bench()
     a = b.allocator_leg(2000)
-    assert a["ops"] == 2000 and a["oracle_ops_s"] > 0 and a["library_ops_s_incl_ctypes"] > 0
+    assert a["ops"] == 2000 and a["oracle_ops_s"] > 0 and a["library_ops_s_incl_ctypes"] > 0 and a["tables_equal"]
     assert b.host_cpu()["nproc"] >= 1
