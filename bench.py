@@ -449,6 +449,7 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
     out = dict(step_ms=step_ms, alone_gbs=alone_gbs, total_ms=total_ms, launches=launches, clocks=clocks, e2e_ms=e2e_ms,
                attn_ms=st1["attn_ms"] - st0["attn_ms"], attn_launches=st1["attn_launches"] - st0["attn_launches"],
                attn_bytes=st1["attn_bytes"] - st0["attn_bytes"],
+               stall_ms=st1["stall_ms"] - st0["stall_ms"], stall_waits=st1["stall_waits"] - st0["stall_waits"],
                h2d_ms=st1["h2d_ms"] - st0["h2d_ms"], h2d_bytes=st1["h2d_bytes"] - st0["h2d_bytes"],
                h2d_copies=st1["h2d_copies"] - st0["h2d_copies"], meta_bytes=st2["last_meta_h2d_bytes"],
                units=st1["last_attn_units"], split_blocks=st1["last_split_blocks"], stats=st1)
@@ -551,6 +552,8 @@ def run_mirage(args, rank, world):
                      "kernel_alone_gbs": res.get("alone_gbs"),
                      "kernel_alone_frac": (res["alone_gbs"] / hbm_peak) if res.get("alone_gbs") else None,
                      "peak_source": peak_src},
+        "handoff": {"stall_ms_per_step": res["stall_ms"] / args.steps, "ready_waits": res["stall_waits"],
+                    "how": "events around each slot ready-wait on the compute stream (a5)"},
         "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": h2d_peak, "frac": (h2d_gbs / h2d_peak) if h2d_gbs else None,
                 "bytes_per_step": res["h2d_bytes"] / args.steps, "copies": res["h2d_copies"],
                 "peak_source": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this run"},

@@ -60,7 +60,8 @@ extern "C" {
 #define MIRAGE_BETA_2 2       /* double buffering          (Eq. 5, :478)  */
 #define MIRAGE_BETA_DYNAMIC 3 /* smallest m with zero predicted stall (reading #6) */
 
-#define MIRAGE_FLAG_TIME_ATTN 1u /* init flag: time every attention launch with events */
+#define MIRAGE_FLAG_TIME_ATTN 1u /* init flag: time every attention launch and every
+                                  * slot ready-wait (mirage_stats.stall_ms) with events */
 #define MIRAGE_FLAG_SLOT_TAGS 4u /* init flag: race detector for re-streaming. Behind every
                                   * layer DMA the copy stream writes a 4-byte tag
                                   * {0xA5, model, layer} into the slot's tag word; before
@@ -370,6 +371,11 @@ typedef struct mirage_stats {
                                  * before their weights had landed (must stay 0)     */
   int64_t tp_peer_timeouts;     /* MIRAGE_FLAG_TP_IPC: all-reduce waits that gave up
                                  * on a peer (must stay 0)                            */
+  /* with MIRAGE_FLAG_TIME_ATTN: the compute stream's measured stall on the slot
+   * handoff (a5): event time from reaching a cycled layer's ready-wait to passing
+   * it, summed over completed waits (0 when re-streaming is hidden)  */
+  int64_t stall_waits;
+  double stall_ms;
 } mirage_stats;
 
 int32_t mirage_query(mirage_ctx* ctx, int32_t model, mirage_stats* out);

@@ -72,7 +72,8 @@ class Stats(C.Structure):
                 ("steps", C.c_int64), ("attn_launches", C.c_int64), ("attn_ms", C.c_double),
                 ("attn_bytes", C.c_uint64), ("last_meta_h2d_bytes", C.c_uint64),
                 ("last_attn_units", C.c_int32), ("last_split_blocks", C.c_int32),
-                ("slot_tag_errors", C.c_int64), ("tp_peer_timeouts", C.c_int64)]
+                ("slot_tag_errors", C.c_int64), ("tp_peer_timeouts", C.c_int64),
+                ("stall_waits", C.c_int64), ("stall_ms", C.c_double)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "cycle"}

@@ -204,6 +204,9 @@ struct Model {
     uint64_t bytes;
   };
   std::deque<AttnTiming> attn_pending;
+  std::deque<AttnTiming> stall_pending;  // (before, after) a slot ready-wait on the compute stream
+  int64_t stall_waits = 0;
+  double stall_ms = 0;
   std::vector<cudaEvent_t> ev_pool;
   int64_t attn_launches = 0;
   double attn_ms = 0;
@@ -559,6 +562,21 @@ void harvest_copy_times(Model* M) {
   (void)cudaGetLastError();
 }
 
+void harvest_stall_times(Model* M) {
+  while (!M->stall_pending.empty()) {
+    auto& t = M->stall_pending.front();
+    if (cudaEventQuery(t.t1) != cudaSuccess) break;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t.t0, t.t1);
+    M->stall_ms += ms;
+    M->stall_waits += 1;
+    M->ev_pool.push_back(t.t0);
+    M->ev_pool.push_back(t.t1);
+    M->stall_pending.pop_front();
+  }
+  (void)cudaGetLastError();
+}
+
 void harvest_attn_times(Model* M) {
   while (!M->attn_pending.empty()) {
     auto& t = M->attn_pending.front();
@@ -811,6 +829,10 @@ void mirage_destroy(mirage_ctx* c) {
     if (M->slot_tag) cudaFree(M->slot_tag);
     if (M->tag_err) cudaFree(M->tag_err);
     if (M->host_tags) cudaFreeHost(M->host_tags);
+    for (auto& t : M->stall_pending) {
+      cudaEventDestroy(t.t0);
+      cudaEventDestroy(t.t1);
+    }
     for (auto& t : M->attn_pending) {
       cudaEventDestroy(t.t0);
       cudaEventDestroy(t.t1);
@@ -1549,8 +1571,17 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
       if (!dbg_nowait) CK(c, cudaStreamWaitEvent(cs, M->reload_ev[l], 0));
       M->reload_pending[l] = 0;
     }
-    if (!dbg_nowait && l < s.n && use_of[l] >= beta && use_of[l] >= 0)
-      CK(c, cudaStreamWaitEvent(cs, M->ready_ev[use_of[l] % beta], 0));
+    if (!dbg_nowait && l < s.n && use_of[l] >= beta && use_of[l] >= 0) {
+      if (c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) {  // measured stall of this handoff
+        Model::AttnTiming t{pool_event(M), pool_event(M), 0};
+        CK(c, cudaEventRecord(t.t0, cs));
+        CK(c, cudaStreamWaitEvent(cs, M->ready_ev[use_of[l] % beta], 0));
+        CK(c, cudaEventRecord(t.t1, cs));
+        M->stall_pending.push_back(t);
+      } else {
+        CK(c, cudaStreamWaitEvent(cs, M->ready_ev[use_of[l] % beta], 0));
+      }
+    }
     if (M->slot_tag && l < s.n && use_of[l] >= 0)  // SLOT_TAGS: the slot must hold layer l now
       KL(c, mirage::launch_tag_check(M->slot_tag + use_of[l] % beta, M->host_tags[l], M->tag_err, cs));
     return MIRAGE_OK;
@@ -1635,7 +1666,10 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   const bool time_attn = c->cfg.flags & MIRAGE_FLAG_TIME_ATTN;
   uint64_t attn_bytes = 0;
   for (int i = 0; i < B; ++i) attn_bytes += (uint64_t)hv.len[i] * 2 * Hk * D * 2;
-  if (time_attn) harvest_attn_times(M);
+  if (time_attn) {
+    harvest_attn_times(M);
+    harvest_stall_times(M);
+  }
   for (int l = 0; l < s.n; ++l) {
     const LayerW w = layer_ptrs(s, wptr[l]);
     const uint64_t layer_off = (uint64_t)l * Hk * 2 * kBlockTokens * D * 2;
@@ -1926,6 +1960,7 @@ int32_t mirage_query(mirage_ctx* c, int32_t model, mirage_stats* o) {
     harvest_copy_times(M);
     harvest_step_time(M);
     harvest_attn_times(M);
+    harvest_stall_times(M);
   }
   std::memset(o, 0, sizeof *o);
   o->native_blocks = M->n_native;
@@ -1947,6 +1982,8 @@ int32_t mirage_query(mirage_ctx* c, int32_t model, mirage_stats* o) {
   o->last_step_ms = M->last_step_ms;
   o->steps = M->steps;
   o->attn_launches = M->attn_launches;
+  o->stall_waits = M->stall_waits;
+  o->stall_ms = M->stall_ms;
   o->attn_ms = M->attn_ms;
   o->attn_bytes = M->attn_bytes;
   o->last_meta_h2d_bytes = M->last_meta;
