@@ -534,6 +534,15 @@ def run_mirage(args, rank, world):
             cpu = {"value": None, "unit": "tok/s", "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {e}"}
     step_med = statistics.median(res["step_ms"])
     h2d_gbs = res["h2d_bytes"] / (res["h2d_ms"] * 1e-3) / 1e9 if res["h2d_ms"] else None
+    # predicted handoff stall of this cycle (the planner's timeline, mirage_predict_stall) from the
+    # measured per-layer copy time T_T and per-layer compute time T_c = step / n
+    predicted_stall = None
+    if info.get("beta") and h2d_gbs:
+        from paper_2507_11507_b200 import _lib as L_
+        n_l = wl.tenants[0][0].n_layers
+        t_t = info["layer_bytes"] / (h2d_gbs * 1e9) * 1e9
+        t_c = step_med / n_l * 1e6
+        predicted_stall = L_.predict_stall(n_l, list(info["cycle"]), info["beta"], t_t, t_c) / 1e6
     config = {"workload": wl.desc, "batch_per_gpu": B, "ctx_mean": sum(wl.ctxs) / B, "ctx_max": max(wl.ctxs),
               "split_blocks": res["split_blocks"], "attention_units": res["units"],
               "l2": "inputs larger than L2 (weights + KV read every step)", "parallelism": f"tenant-replica x{world}"}
@@ -553,6 +562,7 @@ def run_mirage(args, rank, world):
                      "kernel_alone_frac": (res["alone_gbs"] / hbm_peak) if res.get("alone_gbs") else None,
                      "peak_source": peak_src},
         "handoff": {"stall_ms_per_step": res["stall_ms"] / args.steps, "ready_waits": res["stall_waits"],
+                    "predicted_stall_ms_per_step": predicted_stall,
                     "how": "events around each slot ready-wait on the compute stream (a5)"},
         "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": h2d_peak, "frac": (h2d_gbs / h2d_peak) if h2d_gbs else None,
                 "bytes_per_step": res["h2d_bytes"] / args.steps, "copies": res["h2d_copies"],

@@ -215,6 +215,14 @@ int32_t mirage_plan(int32_t n_layers, int32_t alpha, int32_t beta_policy,
                     uint64_t t_transfer_ns, uint64_t t_compute_layer_ns, int32_t anchor,
                     int32_t* cycle_out, int32_t* m_out, int32_t* beta_out);
 
+/* Predicted steady-state stall per decode step (ns) of an explicit cycle: the
+ * planner's event simulation of the copy-engine / compute timeline (PAPER.md
+ * :310-314, :463-482; the 8th simulated step minus n * t_compute). cycle:
+ * ascending layer ids, m entries, beta slots (0 = nothing streamed). Pure, no
+ * context. Errors: RANGE. */
+int32_t mirage_predict_stall(int32_t n_layers, const int32_t* cycle, int32_t m, int32_t beta,
+                             uint64_t t_transfer_ns, uint64_t t_compute_layer_ns, int64_t* stall_ns_out);
+
 /* Reclaim the parameter memory of R = cycle[beta..m) of `donor` as KV blocks of
  * `recipient`. R is split into maximal runs
  * of consecutive layers; each run yields floor(run_bytes / BB_recipient) blocks

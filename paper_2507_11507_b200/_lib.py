@@ -95,6 +95,7 @@ def _load():
         "mirage_last_error": (C.c_char_p, [P]),
         "mirage_add_model": (I32, [P, C.POINTER(ModelCfg), P, U64, I64, pI32]),
         "mirage_plan": (I32, [I32, I32, I32, U64, U64, I32, pI32, pI32, pI32]),
+        "mirage_predict_stall": (I32, [I32, pI32, I32, I32, U64, U64, pI64]),
         "mirage_remap_layers": (I32, [P, I32, I32, pI32, I32, I32, pI64, pU64]),
         "mirage_set_active": (I32, [P, I32, I32]),
         "mirage_alloc_blocks": (I32, [P, I32, I64, I32, pI32, pI32]),
@@ -140,7 +141,7 @@ EXPORTED = [
     "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches", "mirage_nccl_unique_id",
     "mirage_host_register", "mirage_host_unregister", "mirage_region_count", "mirage_region_info",
     "mirage_unremap", "mirage_swap_out", "mirage_swap_in", "mirage_set_weight_source", "mirage_tp_export",
-    "mirage_tp_import", "mirage_prefill", "mirage_migrate_region"]
+    "mirage_tp_import", "mirage_prefill", "mirage_migrate_region", "mirage_predict_stall"]
 
 
 def model_cfg(shape):
@@ -176,6 +177,16 @@ def plan(n_layers, alpha, beta_policy, t_transfer_ns, t_compute_layer_ns, anchor
     if rc:
         raise MirageError(rc, "plan")
     return list(cyc[: m.value]), m.value, beta.value
+
+
+def predict_stall(n_layers, cycle, beta, t_transfer_ns, t_compute_layer_ns):
+    """Predicted steady-state stall per step (ns) of an explicit cycle (mirage_predict_stall)."""
+    out = C.c_int64()
+    rc = LIB.mirage_predict_stall(n_layers, _i32(cycle) if cycle else None, len(cycle), beta, int(t_transfer_ns),
+                                  int(t_compute_layer_ns), C.byref(out))
+    if rc:
+        raise MirageError(rc, "predict_stall")
+    return out.value
 
 
 def nccl_unique_id():

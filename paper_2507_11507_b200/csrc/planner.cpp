@@ -98,3 +98,14 @@ extern "C" int32_t mirage_plan(int32_t n_layers, int32_t alpha, int32_t beta_pol
   }
   return beta_policy == MIRAGE_BETA_DYNAMIC ? MIRAGE_ERR_INFEASIBLE : MIRAGE_ERR_RANGE;
 }
+
+extern "C" int32_t mirage_predict_stall(int32_t n_layers, const int32_t* cycle, int32_t m, int32_t beta,
+                                        uint64_t t_transfer_ns, uint64_t t_compute_layer_ns, int64_t* stall_ns_out) {
+  if (n_layers <= 0 || m < 0 || m > n_layers || beta < 0 || beta > m || !stall_ns_out || (m && !cycle))
+    return MIRAGE_ERR_RANGE;
+  for (int32_t i = 0; i < m; ++i)
+    if (cycle[i] < 0 || cycle[i] >= n_layers || (i && cycle[i] <= cycle[i - 1])) return MIRAGE_ERR_RANGE;
+  const std::vector<int32_t> C(cycle, cycle + m);
+  *stall_ns_out = mirage::simulate_stall(n_layers, C, beta, t_transfer_ns, t_compute_layer_ns, 8);
+  return MIRAGE_OK;
+}

@@ -94,3 +94,21 @@ def test_slot_log():
     assert log == [(0, 0, 0, 0, False), (1, 0, 4, 0, True), (2, 1, 0, 0, True), (3, 1, 4, 0, True)]
     log = timeline.slot_log([0, 11, 22], 2, 1)
     assert [(k, l, s, c) for k, _, l, s, c in log] == [(0, 0, 0, False), (1, 11, 1, False), (2, 22, 0, True)]
+
+
+def test_library_stall_predictor_matches_oracle_timeline():
+    """mirage_predict_stall (the product planner's event simulation) equals the
+    oracle c5 timeline's last-step stall on random cycles and speed ratios."""
+    import random
+    from paper_2507_11507_b200 import _lib
+    rng = random.Random(3)
+    for _ in range(300):
+        n = rng.randint(2, 40)
+        m = rng.randint(1, n)
+        beta = rng.randint(1, min(2, m))
+        C = sorted(rng.sample(range(n), m))
+        tc = rng.randint(1, 1000)
+        tt = rng.randint(1, 20000)
+        dur, _, _ = timeline.simulate(n, C, beta, tt, tc, 8)
+        assert _lib.predict_stall(n, C, beta, tt, tc) == dur[-1] - n * tc
+    assert _lib.predict_stall(12, [], 0, 10**6, 5) == 0
