@@ -535,13 +535,13 @@ def run_mirage(args, rank, world):
     step_med = statistics.median(res["step_ms"])
     h2d_gbs = res["h2d_bytes"] / (res["h2d_ms"] * 1e-3) / 1e9 if res["h2d_ms"] else None
     # predicted handoff stall of this cycle (the planner's timeline, mirage_predict_stall) from the
-    # measured per-layer copy time T_T and per-layer compute time T_c = step / n
+    # measured per-layer copy time T_T and per-layer compute time T_c = (step - measured stall) / n
     predicted_stall = None
     if info.get("beta") and h2d_gbs:
         from paper_2507_11507_b200 import _lib as L_
         n_l = wl.tenants[0][0].n_layers
         t_t = info["layer_bytes"] / (h2d_gbs * 1e9) * 1e9
-        t_c = step_med / n_l * 1e6
+        t_c = max(step_med - res["stall_ms"] / args.steps, 1e-3) / n_l * 1e6   # compute only, stall removed
         predicted_stall = L_.predict_stall(n_l, list(info["cycle"]), info["beta"], t_t, t_c) / 1e6
     config = {"workload": wl.desc, "batch_per_gpu": B, "ctx_mean": sum(wl.ctxs) / B, "ctx_max": max(wl.ctxs),
               "split_blocks": res["split_blocks"], "attention_units": res["units"],
