@@ -33,6 +33,11 @@ CASES = {
     "llama3_8b_4x16k": (32, 32, 8, 128, 4, 16384),
     "llama70b_tp8_64x4k": (80, 8, 1, 128, 64, 4096),
 }
+# SURVEY §8(d) C4 grid: Llama-3-8B, L in {8k, 16k, 32k} x B in {1, 4, 16, 32}
+for _B in (1, 4, 16, 32):
+    for _L in (8192, 16384, 32768):
+        CASES.setdefault(f"llama3_8b_{_B}x{_L // 1024}k", (32, 32, 8, 128, _B, _L))
+C4_GRID = [f"llama3_8b_{b}x{l}k" for b in (1, 4, 16, 32) for l in (8, 16, 32)]
 
 
 def run(name, reps, seed=0, split=0):
@@ -75,11 +80,14 @@ def run(name, reps, seed=0, split=0):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--case", nargs="*", default=list(CASES))
+    ap.add_argument("--case", nargs="*", default=None, help="default: the named cases (--c4-grid: the C4 grid)")
+    ap.add_argument("--c4-grid", action="store_true")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--split", type=int, nargs="*", default=[0], help="split sizes in tokens (0 = planner)")
     a = ap.parse_args()
-    for c in a.case:
+    cases = a.case or (C4_GRID if a.c4_grid else [c for c in CASES if c not in C4_GRID or c in
+                                                     ("llama3_8b_32x8k", "llama3_8b_1x32k", "llama3_8b_4x16k")])
+    for c in cases:
         for sp in a.split:
             try:
                 r = run(c, a.reps, split=sp)
