@@ -522,13 +522,26 @@ paged_attention_kernel(const AttnParams p) {
       sLam[g] = Ls;
     }
     __syncthreads();
-    // (3) o = sum_i w_i o_i / Lambda: one float4 of dims per thread, 8 independent
+    // (3) o = sum_i w_i o_i / Lambda: one float4 of dims per thread, 16 (then 8) independent
     // 16-byte loads in flight (same per-element order of operations as a scalar loop)
     for (int e = threadIdx.x; e < G * D / 4; e += kWarps * 32) {
       const int g = e / (D / 4), d = (e % (D / 4)) * 4;
       const float* rg = rec0 + g * (D + 4) + d;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       int i = 0;
+      for (; i + 16 <= ns; i += 16) {  // 16 loads in flight (same summation order)
+        float4 ov[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) ov[k] = __ldcg(reinterpret_cast<const float4*>(rg + (i + k) * rstride));
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float w = sw[i + k][g];
+          acc.x += w * ov[k].x;
+          acc.y += w * ov[k].y;
+          acc.z += w * ov[k].z;
+          acc.w += w * ov[k].w;
+        }
+      }
       for (; i + 8 <= ns; i += 8) {
         float4 ov[8];
 #pragma unroll
