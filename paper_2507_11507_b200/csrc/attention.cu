@@ -10,9 +10,14 @@
 // Design (HBM-bound gather; AI = G flop/B):
 //   * a work item is (sequence, split, kv head); a CTA = 4 warps, warp w takes
 //     blocks w, w+4, ... of the item (placement independent). The grid is
-//     persistent (one wave of CTAs); CTA c takes items c, c + grid, ... in the
-//     host's longest-first order, and each warp's TMA ring streams straight
-//     across item boundaries, so no CTA launch/prologue bubbles remain.
+//     persistent (one wave of CTAs); CTAs claim items from a global counter in
+//     the host's longest-first order (greedy LPT), and each warp's TMA ring
+//     streams straight across item boundaries, so no CTA launch/prologue
+//     bubbles remain. In a prefill step (QP > 1) an item carries up to QP
+//     consecutive rows of one sequence as extra query columns, each with its
+//     own causal length, so one K|V pass serves QP rows.
+//   * q arrives scaled by log2(e)/sqrt(D) and split into bf16 hi|lo words in
+//     the MMA fragment order (qkv_post_kernel), staged per item by one bulk copy.
 //   * one 16-token block of one (layer, kv-head) is a contiguous 2*16*D*2-byte
 //     K|V tile, fetched whole by one cp.async.bulk (TMA engine) into shared
 //     memory; every warp runs its own NS-deep ring (mbarrier complete_tx), so
