@@ -257,3 +257,38 @@ def test_migrate_pins():
         check_invariants(al, r)
         al.unremap(r, reg)                             # the region is empty now
         assert M.regions[reg]["retired"]
+
+
+def test_remap_unremap_restores_state_except_next_id():
+    """SURVEY §8(c) c2 invariants I5/I6: the same op log gives the same state, and
+    remap followed by unremap restores everything except next_id (retired ids are
+    never handed out again, reading #13)."""
+    def run(log):
+        al = A.Allocator()
+        r = al.add_model(4, 300, 100, 5)
+        d = al.add_model(6, 300, 100, 0)
+        al.set_active(d, False)
+        for op in log:
+            if op[0] == "alloc":
+                al.alloc(r, op[1], op[2])
+            elif op[0] == "free":
+                al.free_seq(r, op[1])
+            elif op[0] == "remap":
+                al.remap(d, r, op[1], 0)
+            elif op[0] == "unremap":
+                al.unremap(r, op[1])
+        return al, r, d
+
+    def snapshot(al, r, d):
+        R, D = al.models[r], al.models[d]
+        return (sorted(R.free), {k: list(v) for k, v in R.tables.items()}, R.reclaimed_bytes,
+                list(D.layer_state), D.donated_bytes)
+
+    base = [("alloc", 0, 2), ("alloc", 1, 1)]
+    al0, r0, d0 = run(base)
+    al1, r1, d1 = run(base + [("remap", [1, 2, 4]), ("alloc", 2, 3), ("free", 2), ("unremap", 1), ("unremap", 0)])
+    assert snapshot(al0, r0, d0) == snapshot(al1, r1, d1)
+    assert al1.models[r1].next_id > al0.models[r0].next_id
+    assert all(g["retired"] for g in al1.models[r1].regions)
+    al2, r2, d2 = run(base + [("remap", [1, 2, 4]), ("alloc", 2, 3), ("free", 2), ("unremap", 1), ("unremap", 0)])
+    assert snapshot(al1, r1, d1) == snapshot(al2, r2, d2) and al1.models[r1].next_id == al2.models[r2].next_id
