@@ -20,9 +20,10 @@
 //     the MMA fragment order (qkv_post_kernel), staged per item by one bulk copy.
 //   * one 16-token block of one (layer, kv-head) is a contiguous 2*16*D*2-byte
 //     K|V tile, fetched whole by one cp.async.bulk (TMA engine) into shared
-//     memory; every warp runs its own NS-deep ring (mbarrier complete_tx), so
-//     NS tiles per warp are in flight while it computes; block addresses
-//     (table -> block_base) are resolved 32 at a time, one per lane.
+//     memory; every consumer warp has its own NS-deep ring (full/empty mbarrier
+//     pairs) that a fifth, producer warp keeps filled, so NS tiles per warp are
+//     in flight while it computes; block addresses (table -> block_base) are
+//     resolved 32 at a time, one per lane.
 //   * QK^T and PV run on the tensor cores (mma.sync m16n8k16 bf16 -> fp32) with
 //     q and p carried as bf16 hi+lo column pairs (near-fp32 accuracy); this cuts
 //     the per-tile instruction count ~6x versus CUDA-core dot products so the
@@ -117,6 +118,10 @@ constexpr int kMaxSplitsDev = 128;  // split-K partitions per (sequence, kv head
 template <int D, int G, int QP, int W, int NS>
 constexpr int smem_bytes() { return W * NS * 2 * (16 * D * 2) + (NS + 1) * G * QP * D * 4; }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // Tensor-core formulation per 16-token tile (one warp):
 //   S[16 tok x 8 col] = K[16 x D] * Qc[D x 8]      (D/16 mma.m16n8k16 per n-tile)
 //   O^T[D x 8]       += V^T[D x 16] * P[16 x 8]    (D/16 mma per n-tile)
@@ -128,8 +133,12 @@ constexpr int smem_bytes() { return W * NS * 2 * (16 * D * 2) + (NS + 1) * G * Q
 // own causal length len + pp, so one K|V tile serves QP query rows.
 // The KV tile is stored XOR-swizzled in 16-byte chunks (chunk ^ (row & 7), see
 // include/mirage.h), which makes every ldmatrix below bank-conflict free.
-template <int D, int G, int QP, int W, int NS>
-__global__ void __launch_bounds__(W * 32)
+// WS (warp-specialized): one extra producer warp claims the items, stages q and
+// issues every TMA tile for the W consumer warps (full/empty mbarrier pairs per
+// ring stage); the consumers only compute. Otherwise each warp runs its own
+// producer inline (pump).
+template <int D, int G, int QP, int W, int NS, bool WS>
+__global__ void __launch_bounds__((W + (WS ? 1 : 0)) * 32)
 paged_attention_kernel(const AttnParams p) {
   constexpr int GV = G * QP;          // query column groups (virtual heads) per item
   constexpr int kWarps = W;
@@ -143,6 +152,9 @@ paged_attention_kernel(const AttnParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[kWarps][NS];
   __shared__ __align__(8) uint64_t qbars[QB];
+  __shared__ __align__(8) uint64_t empty[WS ? kWarps : 1][NS];  // WS: consumer released the stage
+  __shared__ __align__(8) uint64_t slot_free[WS ? QB : 1];      // WS: all consumers read the slot's q
+  __shared__ int ptiles[WS ? kWarps : 1];                       // WS: tiles issued per consumer warp
   __shared__ float sm_m[kWarps][GV], sm_l[kWarps][GV];
   constexpr int ACC = (kWarps * D > 2 * kMaxSplitsDev ? kWarps * D : 2 * kMaxSplitsDev) * GV;
   __shared__ __align__(16) float sm_accf[ACC];
@@ -162,23 +174,33 @@ paged_attention_kernel(const AttnParams p) {
   const int gq = lane >> 2;  // mma group id (row / column index)
   const int tq = lane & 3;   // thread in group
   const int n_flat = (p.n_units_dev ? *p.n_units_dev : p.n_units) * p.H_kv;  // item f = unit * H_kv + kv head
-  uint8_t* ring = smem + (size_t)warp * NS * 2 * TILE;
+  uint8_t* ring = smem + (size_t)(warp < kWarps ? warp : 0) * NS * 2 * TILE;
   // q staging (dynamic smem after the rings): [QB][G][2][D/2] packed bf16 hi|lo words, one copy per CTA item
   uint32_t(*qbuf)[GV * D] = reinterpret_cast<uint32_t(*)[GV * D]>(smem + (size_t)kWarps * NS * 2 * TILE);
 
-  if (lane == 0) {
+  if (lane == 0 && warp < kWarps) {
 #pragma unroll
-    for (int i = 0; i < NS; ++i) mbar_init(&bars[warp][i], 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&bars[warp][i], 1);
+      if (WS) mbar_init(&empty[WS ? warp : 0][i], 1);
+    }
+    if (WS) ptiles[WS ? warp : 0] = 0;
     if (warp == 0)
 #pragma unroll
       for (int i = 0; i < QB; ++i) {
         mbar_init(&qbars[i], 1);
+        if (WS) mbar_init(&slot_free[WS ? i : 0], kWarps);
         slot_word[i] = 0ull;
         slot_claim[i] = i - QB;
       }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();  // q barriers and item slots are shared by the CTA
+  // consumer-only CTA barrier (named barrier 1) when a producer warp is present
+  auto csync = [&]() {
+    if (WS) asm volatile("bar.sync 1, %0;" ::"r"(kWarps * 32) : "memory");
+    else __syncthreads();
+  };
 
   // ---- work items are claimed dynamically from a global counter (items are in
   // longest-first order, so this is greedy LPT). The first warp of the CTA to
@@ -220,6 +242,7 @@ paged_attention_kernel(const AttnParams p) {
   const uint64_t* p_tbl = nullptr;
   uint64_t p_off = 0, my_addr = 0;
   auto pump = [&](int ck) {
+    if (WS) return;
     while (pt < rc + NS && !p_done) {
       if (p_it >= p_n) {
         if (pk + 1 > ck + QB - 1) return;  // slot window
@@ -255,6 +278,51 @@ paged_attention_kernel(const AttnParams p) {
       }
     }
   };
+  if (WS && warp == kWarps) {
+    // ---- producer warp: claim items in order, stage q, then issue every tile of
+    // the item to its consumer warp's ring (block j -> warp (j - b0) % W), waiting
+    // on that stage's empty barrier once the ring has wrapped ----
+    for (int k = 0;; ++k) {
+      const int sl_ = k % QB;
+      int item = 0;
+      if (lane == 0) {
+        if (k >= QB) mbar_wait(&slot_free[WS ? sl_ : 0], ((k / QB) - 1) & 1);
+        item = atomicAdd(p.sched, 1);
+        if (item < n_flat) {
+          const AttnUnit u = p.units[item / p.H_kv];
+          const int nq = QP == 1 ? 1 : u.nq;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&qbars[sl_], nq * G * D * 4);
+          for (int pp = 0; pp < nq; ++pp)
+            bulk_g2s(&qbuf[sl_][pp * G * D], p.q + ((size_t)(u.seq + pp) * p.H + (item % p.H_kv) * G) * D,
+                     G * D * 4, &qbars[sl_]);
+        }
+        atomicExch(&slot_word[sl_], ((unsigned long long)(k + 1) << 32) | (unsigned int)item);
+      }
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= n_flat) break;
+      const AttnUnit u = p.units[item / p.H_kv];
+      const uint64_t off = p.layer_off + (uint64_t)(item % p.H_kv) * (2 * TILE);
+      const uint64_t* tbl = p.addrs + u.addr_off;
+      for (int base = u.b0; base < u.b1; base += 32) {
+        const int j = base + lane;
+        const uint64_t a = j < u.b1 ? tbl[j] + off : 0;
+        const int cnt = min(32, u.b1 - base);
+        for (int i = 0; i < cnt; ++i) {
+          const uint64_t ai = __shfl_sync(0xffffffffu, a, i);
+          if (lane == 0) {
+            const int w = (base + i - u.b0) % kWarps;
+            const int t = ptiles[WS ? w : 0]++;
+            const int st = t % NS;
+            if (t >= NS) mbar_wait(&empty[WS ? w : 0][st], ((t / NS) - 1) & 1);
+            uint8_t* dst = smem + (size_t)w * NS * 2 * TILE + st * 2 * TILE;
+            mbar_expect_tx(&bars[w][st], 2 * TILE);
+            bulk_g2s(dst, reinterpret_cast<const void*>(ai), 2 * TILE, &bars[w][st]);
+          }
+        }
+      }
+    }
+  } else {
   pump(0);
 
   // ldmatrix lane addresses within a K|V tile (swizzled), computed once per warp
@@ -270,8 +338,16 @@ paged_attention_kernel(const AttnParams p) {
 
   for (int ck = 0;; ++ck) {
     pump(ck);  // the producer has now visited item ck (or the stream has ended there)
-    const int f = __shfl_sync(
-        0xffffffffu, lane == 0 ? (int)(unsigned int)(atomicAdd(&slot_word[ck % QB], 0ull) & 0xffffffffull) : 0, 0);
+    int f_ = 0;
+    if (lane == 0) {
+      unsigned long long w_;
+      if (WS)  // the producer warp publishes item ck in slot ck % QB
+        while (((w_ = atomicAdd(&slot_word[ck % QB], 0ull)) >> 32) != (unsigned long long)(ck + 1)) __nanosleep(32);
+      else
+        w_ = atomicAdd(&slot_word[ck % QB], 0ull);
+      f_ = (int)(unsigned int)(w_ & 0xffffffffull);
+    }
+    const int f = __shfl_sync(0xffffffffu, f_, 0);
     if (f >= n_flat) break;
     const AttnUnit u = p.units[f / p.H_kv];
     const int hk = f % p.H_kv;
@@ -301,6 +377,10 @@ paged_attention_kernel(const AttnParams p) {
           qb[nt][ks][0] = qb[nt][ks][1] = 0u;
         }
       }
+    }
+    if (WS) {  // this warp holds item ck's q in registers: its slot may be reused
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&slot_free[WS ? ck % QB : 0]);
     }
     // per lane: softmax state of head nt*4 + tq; O^T accumulators (dims ks*16+gq,+8)
     float m[NT], l[NT], o[NT][KS][4];
@@ -404,6 +484,13 @@ paged_attention_kernel(const AttnParams p) {
         for (int nt = 0; nt < NT; ++nt) mma_bf16(o[nt][ks], a, pb[nt]);
       }
       ++rc;
+      if (WS) {  // hand the stage back to the producer warp
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes (V zeroing) -> TMA
+          mbar_arrive(&empty[WS ? warp : 0][st]);
+        }
+      }
       pump(ck);  // refill the freed stage with the tile NS ahead in the stream
     }
     // l: sum the lane partials over the 8 token groups
@@ -414,7 +501,7 @@ paged_attention_kernel(const AttnParams p) {
       l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 16);
     }
 
-    __syncthreads();  // the previous item's merge has finished reading sm_*
+    csync();  // the previous item's merge has finished reading sm_*
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int hh = nt * 4 + tq;
@@ -430,7 +517,7 @@ paged_attention_kernel(const AttnParams p) {
         }
       }
     }
-    __syncthreads();
+    csync();
 
     // merge the warps in fixed order. Per head first (one thread each): M = max_w m_w,
     // fw_w = 2^(m_w - M) (0 for a warp that saw nothing), Ls = sum_w fw_w l_w; then
@@ -451,7 +538,7 @@ paged_attention_kernel(const AttnParams p) {
       sMg[g] = M;
       sLs[g] = Ls;
     }
-    __syncthreads();
+    csync();
     for (int e = threadIdx.x; e < GV * D / 4; e += kWarps * 32) {
       const int g = e / (D / 4), d = (e % (D / 4)) * 4;
       if (QP > 1 && g / G >= nq) continue;
@@ -493,14 +580,14 @@ paged_attention_kernel(const AttnParams p) {
 
     // ---- split-K combine by the last-arriving CTA of this (seq, kv head) ----
     __threadfence();
-    __syncthreads();
+    csync();
     if (threadIdx.x == 0) {
       int* t = p.tickets + (size_t)s * p.H_kv + hk;
       const int prev = atomicAdd(t, 1);
       am_last = (prev == u.nsplit - 1);
       if (am_last) *t = 0;  // reset for the next launch
     }
-    __syncthreads();
+    csync();
     if (!am_last) continue;
     __threadfence();
     const size_t rstride = (size_t)p.H * (D + 4);
@@ -512,7 +599,7 @@ paged_attention_kernel(const AttnParams p) {
       sw[i][g] = __ldcg(rec0 + i * rstride + g * (D + 4) + D);
       sl[i][g] = __ldcg(rec0 + i * rstride + g * (D + 4) + D + 1);
     }
-    __syncthreads();
+    csync();
     // (2) per head: M = max_i m_i, w_i = 2^(m_i - M), Lambda = sum_i w_i l_i (fixed order)
     if (threadIdx.x < G) {
       const int g = threadIdx.x;
@@ -526,7 +613,7 @@ paged_attention_kernel(const AttnParams p) {
       }
       sLam[g] = Ls;
     }
-    __syncthreads();
+    csync();
     // (3) o = sum_i w_i o_i / Lambda: one float4 of dims per thread, 16 (then 8) independent
     // 16-byte loads in flight (same per-element order of operations as a scalar loop)
     for (int e = threadIdx.x; e < G * D / 4; e += kWarps * 32) {
@@ -578,6 +665,7 @@ paged_attention_kernel(const AttnParams p) {
       }
     }
   }
+  }  // consumer warps
   // the last CTA to finish resets the work counter for the next launch
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -589,17 +677,18 @@ paged_attention_kernel(const AttnParams p) {
   }
 }
 
-template <int D, int G, int QP, int W, int NS>
+template <int D, int G, int QP, int W, int NS, bool WS>
 int grid_ctas() {  // persistent grid: as many CTAs as fit on the GPU at once
   constexpr int SMEM = smem_bytes<D, G, QP, W, NS>();
+  constexpr int THREADS = (W + (WS ? 1 : 0)) * 32;
   static int ctas = 0;
   if (!ctas) {
-    if (cudaFuncSetAttribute(paged_attention_kernel<D, G, QP, W, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(paged_attention_kernel<D, G, QP, W, NS, WS>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
       return -1;
     int per_sm = 0, dev = 0, sms = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, paged_attention_kernel<D, G, QP, W, NS>, W * 32,
-                                                      SMEM) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, paged_attention_kernel<D, G, QP, W, NS, WS>,
+                                                      THREADS, SMEM) != cudaSuccess)
       return -1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -608,9 +697,9 @@ int grid_ctas() {  // persistent grid: as many CTAs as fit on the GPU at once
   return ctas;
 }
 
-template <int D, int G, int QP, int W, int NS>
+template <int D, int G, int QP, int W, int NS, bool WS = false>
 cudaError_t launch_v(const AttnParams& p, cudaStream_t s, bool query, int* grid_out) {
-  const int ctas = grid_ctas<D, G, QP, W, NS>();
+  const int ctas = grid_ctas<D, G, QP, W, NS, WS>();
   if (ctas < 0) return cudaErrorInvalidValue;
   if (query) {
     *grid_out = ctas;
@@ -618,11 +707,14 @@ cudaError_t launch_v(const AttnParams& p, cudaStream_t s, bool query, int* grid_
   }
   const long items = (long)p.n_units * p.H_kv;
   const int grid = (int)std::min<long>(items, ctas);
-  paged_attention_kernel<D, G, QP, W, NS><<<grid, W * 32, smem_bytes<D, G, QP, W, NS>(), s>>>(p);
+  paged_attention_kernel<D, G, QP, W, NS, WS>
+      <<<grid, (W + (WS ? 1 : 0)) * 32, smem_bytes<D, G, QP, W, NS>(), s>>>(p);
   return cudaGetLastError();
 }
 
-// tuning hook: MIRAGE_ATTN_VARIANT selects (warps, stages) alternatives
+// tuning hook: MIRAGE_ATTN_VARIANT selects alternatives (1: 3-deep rings, inline
+// producers; 3: inline producers). Default: a producer warp per CTA for decode
+// items (C2 in-step 6.02 vs 5.94 TB/s, alone 6.55 vs 6.49; two alternating runs)
 int variant() {
   static int v = -1;
   if (v < 0) {
@@ -639,7 +731,8 @@ cudaError_t launch_dg(const AttnParams& p, cudaStream_t s, bool query, int* grid
   constexpr int QP = G < 8 ? 8 / G : 1;  // prefill rows per item: 8 virtual heads per kv head
   if (p.qp > 1 && QP > 1) return launch_v<D, G, QP, 4, NS>(p, s, query, grid_out);
   if (D == 128 && variant() == 1) return launch_v<D, G, 1, 4, 3>(p, s, query, grid_out);
-  return launch_v<D, G, 1, 4, NS>(p, s, query, grid_out);
+  if (variant() == 3) return launch_v<D, G, 1, 4, NS>(p, s, query, grid_out);
+  return launch_v<D, G, 1, 4, NS, true>(p, s, query, grid_out);
 }
 
 template <int D>
