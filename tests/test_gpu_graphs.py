@@ -55,12 +55,16 @@ def test_graphs_cut_small_batch_step_time():
         ctx = Context(harness.arena_for([(shape, 64)], 8, 256), 8, 256, flags=flags)
         mid = ctx.add_model(shape, harness.make_blob(shape, seed=3), 64)
         for s in range(8):
-            ctx.alloc_blocks(mid, s, 4)
-        for t in range(40):
-            if t == 10:
+            ctx.alloc_blocks(mid, s, 7)
+        best = None
+        for t in range(100):             # three 30-step windows after a warm-up; keep the fastest
+            if t in (10, 40, 70):
                 ctx.sync()
+                if t > 10:
+                    w = (time.perf_counter() - t0) / 30
+                    best = w if best is None else min(best, w)
                 t0 = time.perf_counter()
             ctx.decode_step(mid, list(range(8)), [1] * 8, [t] * 8, argmax=False)
         ctx.sync()
-        times[flags] = (time.perf_counter() - t0) / 30
+        times[flags] = min(best, (time.perf_counter() - t0) / 30)
     assert times[_lib.FLAG_CUDA_GRAPHS] < times[0]
