@@ -118,6 +118,14 @@ constexpr int kMaxSplitsDev = 128;  // split-K partitions per (sequence, kv head
 template <int D, int G, int QP, int W, int NS>
 constexpr int smem_bytes() { return W * NS * 2 * (16 * D * 2) + (NS + 1) * G * QP * D * 4; }
 
+// 2^x on the MUFU with flush-to-zero: the softmax arguments are <= 0 after the max
+// subtraction, and a probability below 2^-126 adds nothing to l >= 1
+__device__ __forceinline__ float exp2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -441,14 +449,14 @@ paged_attention_kernel(const AttnParams p) {
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
         const float m_new = fmaxf(m[nt], bm);
-        pA[nt] = exp2f(s0 - m_new);
-        pB[nt] = exp2f(s1 - m_new);
+        pA[nt] = exp2_ftz(s0 - m_new);
+        pB[nt] = exp2_ftz(s1 - m_new);
         if (QP > 1 && m_new == -CUDART_INF_F) pA[nt] = pB[nt] = 0.f;  // a row that sees none of this tile
         // rescale only when some head's running max moved (alpha == 1 otherwise:
         // skipping the multiply by exactly 1 leaves every bit unchanged)
         if (__any_sync(0xffffffffu, m_new != m[nt])) {
           // (a prefill row that has seen no token yet keeps m = -inf: alpha = 1, not NaN)
-          const float alpha = (QP > 1 && m_new == -CUDART_INF_F) ? 1.f : exp2f(m[nt] - m_new);
+          const float alpha = (QP > 1 && m_new == -CUDART_INF_F) ? 1.f : exp2_ftz(m[nt] - m_new);
           l[nt] *= alpha;
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks)
