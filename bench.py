@@ -234,6 +234,24 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------- mirage arm ---
+def measure_copy_peak(torch, dev, elems=1 << 30):
+    """A device-to-device bf16 copy of 1 Gi elements, read + write bytes over the best
+    of 5 (the same recipe as MEASURED_PEAKS.json's hbm_gbs), measured in this run."""
+    a = torch.empty(elems, dtype=torch.bfloat16, device=dev)
+    b = torch.empty_like(a)
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * elems * 2 / best / 1e6
+
+
 def measure_h2d_peak(torch, dev, nbytes=1 << 30):
     h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
@@ -476,6 +494,7 @@ def run_mirage(args, rank, world):
     peak_src = ("MEASURED_PEAKS.json hbm_gbs (copy, of measured)" if "hbm_gbs" in peaks
                 else "B200_PROFILING.md fallback 6.65 TB/s (of fallback; MEASURED_PEAKS.json absent)")
     h2d_peak = measure_h2d_peak(torch, dev)
+    copy_peak_run = measure_copy_peak(torch, dev)
     t0 = time.time()
     blobs = {}
     for sh, seed, _ in wl.tenants:
@@ -559,6 +578,8 @@ def run_mirage(args, rank, world):
                      "algorithmic_bytes_per_launch": attn_bytes_launch, "avg_launch_ms": attn_avg_ms,
                      "launches": res["attn_launches"], "share_of_step": res["attn_ms"] / t_local,
                      "kernel_alone_gbs": res.get("alone_gbs"),
+                     "copy_peak_this_run_gbs": copy_peak_run,
+                     "frac_of_copy_peak_this_run": achieved / copy_peak_run,
                      "kernel_alone_frac": (res["alone_gbs"] / hbm_peak) if res.get("alone_gbs") else None,
                      "peak_source": peak_src},
         "handoff": {"stall_ms_per_step": res["stall_ms"] / args.steps, "ready_waits": res["stall_waits"],
