@@ -57,3 +57,23 @@ def test_sizes_match_synth_spec():
         assert S == weights.layer_bytes(m) and G == weights.global_bytes(m)
         assert BB == m.n_layers * m.n_kv_heads * 2 * 16 * m.head_dim * 2
         assert S % 256 == 0
+
+
+def test_header_is_plain_c99():
+    """include/mirage.h is a C ABI: it must compile as C99 (no C++ or torch types)."""
+    import os
+    import shutil
+    import subprocess
+    import tempfile
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        import pytest
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "h.c")
+        with open(src, "w") as f:
+            f.write('#include "mirage.h"\nint main(void) { mirage_stats s; (void)s; return 0; }\n')
+        r = subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-fsyntax-only", "-I",
+                            os.path.join(root, "include"), src], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
