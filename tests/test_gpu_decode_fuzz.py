@@ -62,3 +62,58 @@ def test_random_remapped_decode_matches_oracle(seed):
         ref, _, _ = dec.step(list(range(B)), [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)], [t] * B)
         rel = np.sqrt(((got[t] - ref) ** 2).mean() / (ref ** 2).mean())
         assert rel <= REL_RMS and np.abs(got[t] - ref).max() <= MAX_ABS, (t, rel, cycle, beta)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_prefill_and_extend_match_oracle(seed):
+    """Random shapes (G in 1, 2, 4, 8; D in 64, 128), ragged prompts, a random
+    max_batch that splits prompts across chunks, then a second, unaligned extend and
+    one decode step: every row's final hidden of the extend step and the decode step
+    vs oracle c4 token by token."""
+    from paper_2507_11507_b200 import Context
+    rng = random.Random(900 + seed)
+    D = rng.choice([64, 128])
+    G = rng.choice([1, 2, 4, 8])
+    Hk = rng.choice([1, 2])
+    H = G * Hk
+    family = models.LLAMA if G > 1 or rng.random() < 0.5 else models.OPT
+    d = max(128, H * D) if family == models.LLAMA else H * D
+    if family == models.OPT and d % 128:
+        family, d = models.LLAMA, 128 * ((H * D + 127) // 128)
+    shape = models.ModelShape(f"fz-pf-{seed}", family, 2, d, H, Hk if family == models.LLAMA else H, D, 256, 512,
+                              512, *(() if family == models.OPT else (1e-5, 10000.0)))
+    B = rng.randint(1, 4)
+    lens = [rng.randint(1, 40) for _ in range(B)]
+    ext = [rng.randint(1, 9) for _ in range(B)]
+    rows = rng.choice([8, 16, 64])
+    ctx = Context(harness.arena_for([(shape, 64)], max(rows, sum(ext)), 128), max(rows, sum(ext)), 128)
+    mid = ctx.add_model(shape, harness.make_blob(shape, seed=seed), 64)
+    dec = Decoder(shape, [weights.layer_tensors(shape, l, seed) for l in range(2)], weights.global_tensors(shape, seed))
+    for s, (n, e) in enumerate(zip(lens, ext)):
+        ctx.alloc_blocks(mid, s, harness.blocks_for(n + e + 1))
+    prompts = [[workload.teacher_tokens(s, t, shape.vocab) for t in range(n)] for s, n in enumerate(lens)]
+    ctx.prefill(mid, list(range(B)), prompts, argmax=False)
+    for s, p in enumerate(prompts):
+        for t, tok in enumerate(p):
+            dec.step_one(s, tok, t)
+    # an unaligned extend as rows of ONE step (several rows per sequence)
+    rs = [s for s in range(B) for _ in range(ext[s])]
+    rp = [lens[s] + j for s in range(B) for j in range(ext[s])]
+    rt = [workload.teacher_tokens(s, 100 + p, shape.vocab) for s, p in zip(rs, rp)]
+    hid = torch.empty((len(rs), shape.d_model), dtype=torch.bfloat16, device="cuda")
+    ctx.decode_step(mid, rs, rt, rp, hidden_out=hid)
+    ctx.sync()
+    got = hid.float().cpu().numpy()
+    for i, (s, t, p) in enumerate(zip(rs, rt, rp)):
+        x, _ = dec.step_one(s, t, p)
+        rel = np.sqrt(((got[i] - x) ** 2).mean() / (x ** 2).mean())
+        assert rel <= REL_RMS and np.abs(got[i] - x).max() <= MAX_ABS, (i, s, p, rel)
+    pos = [n + e for n, e in zip(lens, ext)]
+    h2 = torch.empty((B, shape.d_model), dtype=torch.bfloat16, device="cuda")
+    ctx.decode_step(mid, list(range(B)), [3] * B, pos, hidden_out=h2)
+    ctx.sync()
+    ref, _, _ = dec.step(list(range(B)), [3] * B, pos)
+    g2 = h2.float().cpu().numpy()
+    rel = np.sqrt(((g2 - ref) ** 2).mean() / (ref ** 2).mean())
+    assert rel <= REL_RMS and np.abs(g2 - ref).max() <= MAX_ABS, rel
+    ctx.close()
