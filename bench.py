@@ -396,21 +396,23 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
         ctx.alloc_blocks(mid, i, harness.blocks_for(L))
         ctx.fill_kv(mid, i, L, seed=args.seed * 7919 + i)
     ctx.sync()
-    pos = list(ctxs)
+    import numpy as np
+    pos = np.array(list(ctxs), dtype=np.int64)
+    seqs = np.arange(B, dtype=np.int64)
     seq_c = (C.c_int64 * B)(*range(B))
     tok_c = (C.c_int32 * B)()
     pos_c = (C.c_int32 * B)()
     am_c = (C.c_int32 * B)()
+    tok_v = np.frombuffer(tok_c, dtype=np.int32)     # views: the ctypes arrays are filled in place
+    pos_v = np.frombuffer(pos_c, dtype=np.int32)
 
     def step(read_back):
-        for i in range(B):
-            if pos[i] % 16 == 0:
-                ctx.alloc_blocks(mid, i, 1)
-            tok_c[i] = workload.teacher_tokens(i, pos[i], shape.vocab)
-            pos_c[i] = pos[i]
+        for i in np.nonzero(pos % 16 == 0)[0]:      # a sequence crossing into a new block
+            ctx.alloc_blocks(mid, int(i), 1)
+        tok_v[:] = (7919 * seqs + 104729 * pos) % shape.vocab   # workload.teacher_tokens, vectorised
+        pos_v[:] = pos
         ctx.decode_step_raw(mid, B, seq_c, tok_c, pos_c, None, am_c if read_back else None)
-        for i in range(B):
-            pos[i] += 1
+        pos[:] += 1                                  # in place (pos is the enclosing array)
 
     if clock:
         clock.start()   # running before the timed region; stop() keeps the samples inside it
