@@ -203,6 +203,33 @@ def allocator_leg(n_ops=20000, seed=0):
             "tables_equal": same}
 
 
+def attention_oracle_leg(shape, ctxs, n_seqs=64, seed=0):
+    """SURVEY §8(d) oracle item (2): oracle c3 attention (fp64 numpy, one thread per
+    BLAS pool) for one layer of the first n_seqs sequences of the batch, all heads;
+    reported as KV bytes (bf16, the kernel's algorithmic bytes) processed per second."""
+    import numpy as np
+    from oracle import attention as OAT
+    from oracle import kvgen
+    rng = np.random.default_rng(seed)
+    Hk, D, G = shape.n_kv_heads, shape.head_dim, shape.n_heads // shape.n_kv_heads
+    sample = [min(int(c), 4096) for c in list(ctxs)[:n_seqs]]
+    kv = [[(kvgen.kv_values(seed, i, shape.n_layers, Hk, D, 0, h, 0, range(L)),
+            kvgen.kv_values(seed, i, shape.n_layers, Hk, D, 0, h, 1, range(L))) for h in range(Hk)]
+          for i, L in enumerate(sample)]
+    q = rng.standard_normal((len(sample), shape.n_heads, D))
+    dt = 1e30
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for i in range(len(sample)):
+            for h in range(shape.n_heads):
+                K, V = kv[i][h // G]
+                OAT.attend(q[i, h], K, V)
+        dt = min(dt, time.perf_counter() - t0)
+    nbytes = sum(sample) * 2 * Hk * D * 2
+    return {"kv_gbs": nbytes / dt / 1e9, "seconds": dt, "sample": f"{len(sample)} seqs (ctx mean "
+            f"{sum(sample) / len(sample):.0f}), 1 layer, {shape.n_heads} heads, oracle c3 fp64, best of 3"}
+
+
 def host_cpu():
     model = None
     try:
@@ -551,6 +578,10 @@ def run_mirage(args, rank, world):
                 cpu["allocator"] = allocator_leg()
             except Exception as e:
                 cpu["allocator"] = {"failed": str(e)[:200]}
+            try:
+                cpu["attention"] = attention_oracle_leg(wl.tenants[0][0], wl.ctxs, seed=args.seed)
+            except Exception as e:
+                cpu["attention"] = {"failed": str(e)[:200]}
         except Exception as e:  # the CPU leg must not hide the GPU number
             cpu = {"value": None, "unit": "tok/s", "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {e}"}
     step_med = statistics.median(res["step_ms"])

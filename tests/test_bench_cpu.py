@@ -45,3 +45,6 @@ def test_cpu_baseline_extras():
     a = b.allocator_leg(2000)
     assert a["ops"] == 2000 and a["oracle_ops_s"] > 0 and a["library_ops_s_incl_ctypes"] > 0 and a["tables_equal"]
     assert b.host_cpu()["nproc"] >= 1
+    from synth import models
+    at = b.attention_oracle_leg(models.TOY, [20, 33, 5], n_seqs=3)
+    assert at["kv_gbs"] > 0
