@@ -13,7 +13,10 @@ readings #1, #11-#15 (listed in DESIGN.md):
 * remap(d, r, C, beta): R = sorted(C[beta:]) split into maximal runs of
   consecutive layer ids; each run of |run| * S_d bytes yields floor(len / BB_r)
   blocks at byte offsets first*S_d + i*BB_r of the donor's weight arena;
-* alloc(r, seq, n): the n lowest free ids, ascending, all-or-nothing;
+* alloc(r, seq, n): the n lowest free ids, ascending, all-or-nothing; a
+  sequence's table never exceeds max_blocks = max_ctx / 16 ids (RangeError,
+  checked after the free-count check and before any state changes, like every
+  other error: a failed call leaves the state exactly as it was);
 * free(r, seq): return all of seq's blocks; unknown seq -> DoubleFree.
 
 * unremap(r, region) (NEXT-1, Dynamic Reversion): all of the region's ids free
@@ -78,15 +81,24 @@ class Model:
 
 
 class Allocator:
-    def __init__(self):
+    def __init__(self, max_blocks=None):
+        """max_blocks: cap on one sequence's table (max_ctx / 16); None = no cap."""
         self.models = []
+        self.max_blocks = max_blocks
 
     def add_model(self, n_layers, layer_bytes, block_bytes, n_native):
         self.models.append(Model(n_layers, layer_bytes, block_bytes, n_native))
         return len(self.models) - 1
 
     def set_active(self, model, active):
-        self.models[model].active = bool(active)
+        """A model can run only if every reclaimed layer of it is streamed through
+        its own cycle (its other reclaimed bytes are somebody's KV blocks)."""
+        m = self.models[model]
+        if active and not m.active:
+            for l, st in enumerate(m.layer_state):
+                if st == RECLAIMED and l not in m.cycle:
+                    raise StateError(f"layer {l} is reclaimed outside the model's cycle")
+        m.active = bool(active)
 
     def remap(self, donor, recipient, C, beta):
         """Returns the number of blocks added to the recipient's pool."""
@@ -207,6 +219,8 @@ class Allocator:
             raise RangeError("n")
         if n > len(r.free):
             raise NoBlocks(n - len(r.free))
+        if self.max_blocks is not None and len(r.tables.get(seq, [])) + n > self.max_blocks:
+            raise RangeError(f"table of seq {seq} would exceed max_ctx")
         ids = sorted(r.free)[:n]
         for i in ids:
             r.free.remove(i)

@@ -45,13 +45,16 @@ class Controller:
         for m in sorted(self.n):
             if m == self.active or len(self.taken[m]) >= self.limit(m):
                 continue
+            if len(self.taken[m]) + len(self.al.models[m].cycle) >= self.n[m]:
+                continue
             key = (self.prio[m], self.sign * self.last_act[m], m)
             if best is None or key < best[0]:
                 best = (key, m)
         if best is None:
             return None
         m = best[1]
-        remaining = [l for l in range(self.n[m] - 1, -1, -1) if l not in self.taken[m]]
+        own = set(self.al.models[m].cycle)       # its own streaming cycle is not donatable
+        remaining = [l for l in range(self.n[m] - 1, -1, -1) if l not in self.taken[m] and l not in own]
         layers = sorted(remaining[: min(self.k, self.limit(m) - len(self.taken[m]))])
         gained = self.al.remap(m, self.active, layers, 0)
         self.taken[m] |= set(layers)
@@ -79,19 +82,22 @@ class Controller:
             g = regs[idx]
             if g["retired"]:
                 continue
-            ids = range(g["first_id"], g["first_id"] + g["n_blocks"])
+            # the regions of a streaming cycle revert as one (allocator.unremap)
+            ids = self.al._region_ids(self.al.models[self.active], idx)
             live = sum(1 for i in ids if i not in self.al.models[self.active].free)
             if live > migrate_max:
                 continue
-            if len(self.al.models[self.active].free) - g["n_blocks"] < headroom:
+            if len(self.al.models[self.active].free) - len(ids) < headroom:
                 continue
+            n_layers = (sum(r["n_layers"] for r in regs if r["cycle"] and r["donor"] == g["donor"] and not r["retired"])
+                        if g["cycle"] else g["n_layers"])
             if live:
                 moves = self.al.migrate(self.active, idx)
                 self.log.append(("migrate", idx, len(moves)))
                 out.append(self.log[-1])
             self.al.unremap(self.active, idx)
             self.taken[g["donor"]] -= set(range(g["first_layer"], g["first_layer"] + g["n_layers"]))
-            entry = ("revert", idx, g["donor"], g["n_layers"])
+            entry = ("revert", idx, g["donor"], n_layers)
             self.log.append(entry)
             out.append(entry)
         return out

@@ -16,7 +16,15 @@ Host-side policy, as in the paper (a Python component of the serving system):
   parameters must be resident to run).
 
 Layer choice for an inactive donor (unstated by the paper, reading in
-DESIGN.md): highest remaining layer index first, ``layers_per_call`` at a time.
+DESIGN.md): highest remaining layer index first, ``layers_per_call`` at a time;
+layers of the donor's own streaming cycle (if it self-remapped while active)
+are never donated.
+
+``cap`` defaults to 1.0, a deliberate reading (#8): P:387 enforces a maximum
+remapping threshold so enough parameters stay resident for a cold start, but
+Alg. 1 removes a model only at remapped == layers and BASELINE C3 asks
+for a fully remapped inactive tenant. The price of cap = 1.0 is the cold start:
+every layer must be reloaded before (or, NEXT-4b, while) the tenant prefills.
 
 Active-model self-remap (streaming), when no inactive model is left: with
 ``self_remap="auto"`` the controller applies §5.3: with T_T the
@@ -48,12 +56,18 @@ class RemappingController:
     def enable_remap(self):
         return any(not r["retired"] for r in self.ctx.regions(self.active))
 
+    def _cycled(self, m):
+        """Layers of m's own streaming cycle (slots and streamed layers): not donatable."""
+        return set(self.ctx.query(m)["cycle"])
+
     def _candidates(self):
         out = []
         for m, i in self.info.items():
             if m == self.active:
                 continue
             if len(i["remapped"]) >= int(self.cap * i["layers"] + 1e-9):
+                continue
+            if len(i["remapped"]) + len(self._cycled(m)) >= i["layers"]:
                 continue
             prio = i["prio"] if i["prio"] is not None else 0
             rec = -i["act"] if self.order == "mru" else i["act"]
@@ -74,7 +88,7 @@ class RemappingController:
             return None
         m = cands[0]
         i = self.info[m]
-        left = [l for l in range(i["layers"]) if l not in i["remapped"]]
+        left = [l for l in range(i["layers"]) if l not in i["remapped"] and l not in self._cycled(m)]
         limit = int(self.cap * i["layers"] + 1e-9) - len(i["remapped"])
         take = sorted(left, reverse=True)[: min(self.per_call, limit)]
         layers = sorted(take)
@@ -126,12 +140,19 @@ class RemappingController:
         done = []
         regs = self.ctx.regions(self.active)
         for idx in range(len(regs) - 1, -1, -1):
-            r = self.ctx.regions(self.active)[idx]
-            live = r["n_blocks"] - r["n_free"]
-            if r["retired"] or live > migrate_max:
+            regs = self.ctx.regions(self.active)
+            r = regs[idx]
+            if r["retired"]:
+                continue
+            # a streaming cycle's regions revert (and migrate) together: count them all
+            group = ([g for g in regs if g["cycle"] and g["donor"] == r["donor"] and not g["retired"]]
+                     if r["cycle"] else [r])
+            live = sum(g["n_blocks"] - g["n_free"] for g in group)
+            n_blocks = sum(g["n_blocks"] for g in group)
+            if live > migrate_max:
                 continue
             free = self.ctx.query(self.active)["free_blocks"]
-            if free - r["n_blocks"] < headroom:
+            if free - n_blocks < headroom:
                 continue
             if live:
                 moved = self.ctx.migrate_region(self.active, idx)
@@ -142,7 +163,7 @@ class RemappingController:
             if r["donor"] in self.info:
                 i = self.info[r["donor"]]
                 i["remapped"] = [l for l in i["remapped"] if l not in lay]
-            act = ("revert", idx, r["donor"], r["n_layers"])
+            act = ("revert", idx, r["donor"], sum(g["n_layers"] for g in group))
             self.log.append(act)
             done.append(act)
         return done

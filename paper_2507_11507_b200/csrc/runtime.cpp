@@ -1096,9 +1096,10 @@ int32_t mirage_set_active(mirage_ctx* c, int32_t model, int32_t active) {
   Model* M = get_model(c, model);
   if (!M) return fail(c, MIRAGE_ERR_RANGE, "set_active: model %d", model);
   if (active && !M->active) {
-    for (int st : M->layer_state)
-      if (st == RECLAIMED && M->cycle.empty())
-        return fail(c, MIRAGE_ERR_STATE, "set_active: model %d has reclaimed layers", model);
+    // a reclaimed layer runs only if it is streamed through this model's own cycle
+    for (int32_t l = 0; l < M->shp.n; ++l)
+      if (M->layer_state[l] == RECLAIMED && M->cyc_index[l] < 0)
+        return fail(c, MIRAGE_ERR_STATE, "set_active: model %d layer %d is reclaimed outside its cycle", model, l);
   }
   M->active = active != 0;
   return MIRAGE_OK;
@@ -1350,9 +1351,12 @@ int32_t mirage_alloc_blocks(mirage_ctx* c, int32_t model, int64_t seq_id, int32_
     if (shortfall_out) *shortfall_out = n - (int32_t)M->free_ids.size();
     return fail(c, MIRAGE_ERR_NO_BLOCKS, "alloc: shortfall %d", n - (int32_t)M->free_ids.size());
   }
-  auto& t = M->tables[seq_id];
-  if ((int64_t)t.size() + n > c->max_blk)
+  // every check before any state changes: a failed call leaves no table behind
+  const auto found = M->tables.find(seq_id);
+  const int64_t have = found == M->tables.end() ? 0 : (int64_t)found->second.size();
+  if (have + n > c->max_blk)
     return fail(c, MIRAGE_ERR_RANGE, "alloc: table of seq %lld would exceed max_ctx", (long long)seq_id);
+  auto& t = M->tables[seq_id];
   for (int i = 0; i < n; ++i) {
     const int32_t id = *M->free_ids.begin();
     M->free_ids.erase(M->free_ids.begin());
@@ -1470,9 +1474,9 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     return fail(c, MIRAGE_ERR_RANGE, "step: batch %d", B);
   const Shape& s = M->shp;
   if (!M->active) return fail(c, MIRAGE_ERR_STATE, "step: model %d inactive", model);
-  for (int st : M->layer_state)
-    if (st == RECLAIMED && M->cycle.empty())
-      return fail(c, MIRAGE_ERR_STATE, "step: model %d has reclaimed layers and no cycle", model);
+  for (int32_t l = 0; l < s.n; ++l)
+    if (M->layer_state[l] == RECLAIMED && M->cyc_index[l] < 0)
+      return fail(c, MIRAGE_ERR_STATE, "step: model %d layer %d is reclaimed outside its cycle", model, l);
   // ---- validate (before any enqueue) ----
   // A row is one token. Several rows may belong to one sequence (a prefill or
   // extend chunk): in row order they must take consecutive positions starting at

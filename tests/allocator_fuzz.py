@@ -39,9 +39,9 @@ def make_log(seed, n_ops=300, n_seqs=12):
     return log
 
 
-def replay_lib(log, shape=models.TOY):
+def replay_lib(log, shape=models.TOY, max_ctx=4096):
     from paper_2507_11507_b200 import _lib
-    ctx = _lib.Context.host_only(1 << 36, 64, 4096)
+    ctx = _lib.Context.host_only(1 << 36, 64, max_ctx)
     out = []
     for op in log:
         try:
@@ -80,9 +80,9 @@ def replay_lib(log, shape=models.TOY):
     return out, state
 
 
-def replay_oracle(log, shape=models.TOY):
+def replay_oracle(log, shape=models.TOY, max_ctx=4096):
     from paper_2507_11507_b200 import _lib   # error codes only
-    al = OA.Allocator()
+    al = OA.Allocator(max_blocks=max_ctx // 16)
     S, BB = weights.layer_bytes(shape), bb(shape)
     out = []
     for op in log:

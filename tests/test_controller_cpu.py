@@ -160,3 +160,70 @@ def test_product_controller_matches_oracle(seed, prios, order):
         for s, t in al.models[m].tables.items():
             assert ctx.block_table(m, s) == t
         assert ctx.query(m)["free_blocks"] == len(al.models[m].free)
+
+
+def _both(native, donors, active_layers=DONOR):
+    """The same setup in the oracle and in a host-only libmirage context."""
+    from paper_2507_11507_b200 import _lib
+    al = OA.Allocator()
+    a = al.add_model(active_layers.n_layers, weights.layer_bytes(active_layers), bb(active_layers), native)
+    spec = {a: (active_layers.n_layers, None)}
+    ctx = _lib.Context.host_only(1 << 38, 64, 4096)
+    ctx.add_model_host_only(active_layers, native)
+    for p in donors:
+        d = al.add_model(DONOR.n_layers, weights.layer_bytes(DONOR), bb(DONOR), 0)
+        ctx.add_model_host_only(DONOR, 0)
+        spec[d] = (DONOR.n_layers, p)
+    return al, ctx, spec
+
+
+def test_revert_counts_every_region_of_a_streaming_cycle():
+    """A self-remap cycle [0, 3, 6] (beta = 1) reclaims two separate regions
+    (layers 3 and 6) that revert and migrate together. With the newest region
+    empty but its sibling holding KV, revert() must skip the cycle (not fail)
+    unless the live blocks of BOTH regions fit migrate_max; the headroom check
+    counts both regions' blocks. Product and oracle agree."""
+    from paper_2507_11507_b200 import _lib
+    from paper_2507_11507_b200.controller import RemappingController
+    al, ctx, spec = _both(8, [])
+    octl = OracleController(al, spec, active=0)
+    pctl = RemappingController(ctx, spec, active=0)
+    for c in (octl, pctl):
+        if c is octl:
+            al.remap(0, 0, [0, 3, 6], 1)
+        else:
+            ctx.remap_layers(0, 0, [0, 3, 6], 1)
+        c.alloc(0, 8)                             # the native pool
+        c.alloc(1, 2)                             # 2 blocks of region 0 (layer 3)
+        c.free(0)
+        assert c.revert(headroom=0) == []         # region 1 is empty, region 0 is not: skip, no error
+        assert c.revert(headroom=0, migrate_max=1) == []
+        assert c.revert(headroom=7, migrate_max=2) == []   # free - (both regions' blocks) = 6 < 7
+    assert pctl.log == octl.log
+    po = pctl.revert(headroom=0, migrate_max=2)
+    oo = octl.revert(headroom=0, migrate_max=2)
+    assert po == oo and oo[0][0] == "migrate" and oo[1] == ("revert", 1, 0, 2)
+    assert ctx.query(0)["m"] == 0 and al.models[0].cycle == []
+
+
+def test_victim_never_donates_its_own_cycle():
+    """A model that self-remapped (cycle [1, 5], beta = 1) and then went inactive
+    is picked as a victim: its cycled layers must not be offered (the library
+    would refuse them with STATE); the controller takes its other layers."""
+    from paper_2507_11507_b200.controller import RemappingController
+    al, ctx, spec = _both(2, [None], active_layers=TOY)
+    octl = OracleController(al, spec, active=1)
+    pctl = RemappingController(ctx, spec, active=1)
+    al.remap(1, 1, [1, 5], 1)
+    ctx.remap_layers(1, 1, [1, 5], 1)
+    octl.activate(0)
+    pctl.activate(0)
+    for c in (octl, pctl):
+        taken = []
+        while True:
+            e = c.remapping()
+            if e is None:
+                break
+            taken += list(e[2])
+        assert sorted(taken) == [0, 2, 3, 4, 6, 7]
+    assert pctl.log == octl.log

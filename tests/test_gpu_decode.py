@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 import torch
 
+import c4_bounds as CB
 import harness
 from oracle import timeline as OT
 from oracle.decode import Decoder
@@ -12,7 +13,7 @@ from synth import models, weights, workload
 
 pytestmark = pytest.mark.gpu
 
-REL_RMS, MAX_ABS = 1e-2, 5e-2     # DESIGN.md reading #19 (end-to-end bf16 decode)
+REL_RMS, MAX_ABS = 1e-2, 5e-2     # vs the bf16-point twin; the derived bound vs the exact decoder: c4_bounds
 
 
 def run_gpu(shape, steps, B, n_native, remap=None, seed=3, max_ctx=256):
@@ -38,18 +39,15 @@ def run_gpu(shape, steps, B, n_native, remap=None, seed=3, max_ctx=256):
     return H, A, ctx, mid
 
 
-def run_oracle(shape, steps, B, seed=3):
-    layers = [weights.layer_tensors(shape, l, seed) for l in range(shape.n_layers)]
-    dec = Decoder(shape, layers, weights.global_tensors(shape, seed), round_points=True)
-    H, A, M = [], [], []
-    for t in range(steps):
-        toks = [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)]
-        h, logits, am = dec.step(list(range(B)), toks, [t] * B)
-        srt = np.sort(logits, axis=1)
-        H.append(h)
-        A.append(am)
-        M.append(srt[:, -1] - srt[:, -2])
-    return H, A, M
+def oracle_script(shape, steps, B):
+    def script(dec):
+        out = []
+        for t in range(steps):
+            toks = [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)]
+            h, logits, _ = dec.step(list(range(B)), toks, [t] * B)
+            out.append((h, logits))
+        return out
+    return script
 
 
 @pytest.mark.parametrize("shape,remap", [
@@ -64,14 +62,24 @@ def test_decode_matches_oracle_and_remap_is_invisible(shape, remap):
     for t in range(steps):   # remapping moves memory, never math
         assert np.array_equal(Hg[t], Hn[t]), t
         assert Ag[t] == An[t]
-    Ho, Ao, Mo = run_oracle(shape, steps, B)
+    layers = [weights.layer_tensors(shape, l, 3) for l in range(shape.n_layers)]
+    glob = weights.global_tensors(shape, 3)
+    script = oracle_script(shape, steps, B)
+    exact, bounds = CB.predict(shape, layers, glob, script)     # exact decoder + derived bound
+    twin = script(Decoder(shape, layers, glob, round_points=True))
+    E = CB.lm_head(shape, glob)
+    decided = 0
     for t in range(steps):
-        ref = Ho[t]
+        CB.check(Hg[t], exact[t][0], bounds[t], t)
+        ref = twin[t][0]
         rel = np.sqrt(((Hg[t] - ref) ** 2).mean() / (ref ** 2).mean())
         assert rel <= REL_RMS and np.abs(Hg[t] - ref).max() <= MAX_ABS, (t, rel)
+        ok = CB.argmax_decidable(E, Hg[t], exact[t][0], exact[t][1])
         for s in range(B):
-            if Mo[t][s] > 0.5:
-                assert Ag[t][s] == Ao[t][s], (t, s)
+            if ok[s]:
+                decided += 1
+                assert Ag[t][s] == int(np.argmax(exact[t][1][s])), (t, s)
+    assert decided >= steps * B // 2
     # slot-assignment log == oracle c5 schedule
     C, beta = remap[1], remap[2]
     log = ctx.slot_log(mid)
@@ -132,23 +140,37 @@ def test_long_prompt_decode_uses_split_k_and_matches_oracle():
     ctx = Context(harness.arena_for([(shape, 400)], B, 4096), B, 4096)
     mid = ctx.add_model(shape, harness.make_blob(shape, seed=6), 400)
     layers = [weights.layer_tensors(shape, l, 6) for l in range(shape.n_layers)]
-    dec = Decoder(shape, layers, weights.global_tensors(shape, 6))
+    glob = weights.global_tensors(shape, 6)
+    kvs = []
     for i in range(B):
         kv = workload.logical_kv(shape.n_layers, shape.n_kv_heads, shape.head_dim, P - i * 700, seed=2, seq=i)
         ctx.alloc_blocks(mid, i, harness.blocks_for(P + 8))
         ctx.write_kv(mid, i, kv)
         kvf = kv.float().double().numpy()
-        dec.set_kv(i, [(kvf[l, :, 0], kvf[l, :, 1]) for l in range(shape.n_layers)])
+        kvs.append([(kvf[l, :, 0], kvf[l, :, 1]) for l in range(shape.n_layers)])
     hid = torch.empty((B, shape.d_model), dtype=torch.bfloat16, device="cuda")
-    pos = [P - i * 700 for i in range(B)]
+    pos0 = [P - i * 700 for i in range(B)]
+    toks = [[workload.teacher_tokens(i, pos0[i] + t, shape.vocab) for i in range(B)] for t in range(4)]
+    got = []
     for t in range(4):
-        toks = [workload.teacher_tokens(i, pos[i], shape.vocab) for i in range(B)]
-        ctx.decode_step(mid, list(range(B)), toks, pos, hidden_out=hid)
-        ref, _, _ = dec.step(list(range(B)), toks, pos)
+        ctx.decode_step(mid, list(range(B)), toks[t], [p + t for p in pos0], hidden_out=hid)
         ctx.sync()
-        got = hid.float().cpu().numpy()
-        rel = np.sqrt(((got - ref) ** 2).mean() / (ref ** 2).mean())
-        assert rel <= REL_RMS and np.abs(got - ref).max() <= MAX_ABS, (t, rel)
-        pos = [p + 1 for p in pos]
+        got.append(hid.float().cpu().numpy().copy())
+
+    def script(dec):
+        for i in range(B):
+            dec.set_kv(i, kvs[i])
+        out = []
+        for t in range(4):
+            h, lg, _ = dec.step(list(range(B)), toks[t], [p + t for p in pos0])
+            out.append((h, lg))
+        return out
+    exact, bounds = CB.predict(shape, layers, glob, script)
+    twin = script(Decoder(shape, layers, glob))
+    for t in range(4):
+        CB.check(got[t], exact[t][0], bounds[t], t)
+        ref = twin[t][0]
+        rel = np.sqrt(((got[t] - ref) ** 2).mean() / (ref ** 2).mean())
+        assert rel <= REL_RMS and np.abs(got[t] - ref).max() <= MAX_ABS, (t, rel)
     st = ctx.query(mid)
     assert st["last_split_blocks"] < (P + 15) // 16 and st["last_attn_units"] > B   # split-K active

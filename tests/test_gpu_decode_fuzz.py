@@ -1,14 +1,17 @@
 """Seeded random sweep of the full decode step under a streaming self-remap
 (a1-a9): random family, depth, head geometry, cycle and beta; every step's final
-hidden vs oracle c4 (reading #19 tolerance) and bit-identical to the same model
-run without the remap (remapping moves memory, never math: PAPER.md:88-91, :874).
-GPU only."""
+hidden vs the exact decoder (oracle c4, fp64, HF-pinned) within the bound
+derived from bf16 rounding (tests/c4_bounds.py, reading #19), vs the bf16-point
+oracle twin, argmax wherever the logit error bound decides it, and bit-identical
+to the same model run without the remap (remapping moves memory, never math:
+PAPER.md:88-91, :874). GPU only."""
 import random
 
 import numpy as np
 import pytest
 import torch
 
+import c4_bounds as CB
 import harness
 from oracle.decode import Decoder
 from synth import models, weights, workload
@@ -19,49 +22,89 @@ REL_RMS, MAX_ABS = 1e-2, 5e-2
 
 def run(shape, seed, steps, B, cycle, beta):
     from paper_2507_11507_b200 import Context
-    native = 64 if cycle is None or len(cycle) == beta else 4   # reclaimed blocks must hold KV
+    # with reclaimed layers the native pool holds one block per sequence only, so
+    # every sequence's later KV lands in reclaimed parameter memory
+    native = 64 if cycle is None or len(cycle) == beta else B
     ctx = Context(harness.arena_for([(shape, 64)], B, 128), B, 128)
     mid = ctx.add_model(shape, harness.make_blob(shape, seed=seed), native)
     if cycle is not None:
         ctx.remap_layers(mid, mid, cycle, beta)
     hid = torch.empty((B, shape.d_model), dtype=torch.bfloat16, device="cuda")
-    out = []
+    out, am = [], []
     for t in range(steps):
         if t % 16 == 0:
             for s in range(B):
                 ctx.alloc_blocks(mid, s, 1)
-        ctx.decode_step(mid, list(range(B)), [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)],
-                        [t] * B, hidden_out=hid)
+        a = ctx.decode_step(mid, list(range(B)), [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)],
+                            [t] * B, hidden_out=hid)
         ctx.sync()
         out.append(hid.float().cpu().numpy().copy())
+        am.append(list(a))
+    if cycle is not None and len(cycle) > beta:   # KV really sits in reclaimed memory
+        assert all(ctx.block_location(mid, i)[0] == mid for s in range(B) for i in ctx.block_table(mid, s)[1:])
     ctx.close()
-    return out
+    return out, am
 
 
-@pytest.mark.parametrize("seed", [0, 1, 3, 4, 5, 8, 10, 11])   # MHA and GQA (G = 2, 4), OPT and Llama
-def test_random_remapped_decode_matches_oracle(seed):
+def fuzz_case(seed):
+    """Seeds 0-15: random family / depth / GQA / cycle / beta (seeds 2, 3, 6 and 13
+    cycle EVERY layer, m = n; 7, 9, 14 are prefetch-only, m = beta). Seeds 16-19:
+    G = 4 and G = 8 at D = 64 and 128 with reclaimed KV."""
     rng = random.Random(500 + seed)
-    family = rng.choice([models.OPT, models.LLAMA])
-    n = rng.randint(2, 5)
-    H = rng.choice([2, 4])
-    Hk = H if family == models.OPT else rng.choice([1, H // 2 if H > 1 else 1, H])
-    D = 64
+    if seed < 16:
+        family = rng.choice([models.OPT, models.LLAMA])
+        n = rng.randint(2, 5)
+        H = rng.choice([2, 4])
+        Hk = H if family == models.OPT else rng.choice([1, H // 2 if H > 1 else 1, H])
+        D = 64
+        m = rng.randint(1, n)
+        beta = rng.randint(1, min(2, m))
+        cycle = sorted(rng.sample(range(n), m))
+    else:
+        family = models.LLAMA
+        G, D = [(4, 64), (8, 64), (4, 128), (8, 128)][seed - 16]
+        Hk = 2 if D == 64 else 1
+        H = G * Hk
+        n = 4
+        beta = 1 + seed % 2
+        cycle = [0, 2, 3] if beta == 1 else [0, 1, 2, 3]
     shape = models.ModelShape(f"fz-dec-{seed}", family, n, H * D, H, Hk, D, 384, 512, 256,
                               *(() if family == models.OPT else (1e-5, 10000.0)))
-    m = rng.randint(1, n)
-    beta = rng.randint(1, min(2, m))
-    cycle = sorted(rng.sample(range(n), m))
+    return shape, cycle, beta
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_remapped_decode_matches_oracle(seed):
+    shape, cycle, beta = fuzz_case(seed)
+    n = shape.n_layers
     steps, B = 20, 4
-    got = run(shape, 40 + seed, steps, B, cycle, beta)
-    ref_gpu = run(shape, 40 + seed, steps, B, None, 0)
+    got, am = run(shape, 40 + seed, steps, B, cycle, beta)
+    ref_gpu, am_n = run(shape, 40 + seed, steps, B, None, 0)
     for t in range(steps):
         assert np.array_equal(got[t], ref_gpu[t]), (t, cycle, beta)
-    dec = Decoder(shape, [weights.layer_tensors(shape, l, 40 + seed) for l in range(n)],
-                  weights.global_tensors(shape, 40 + seed))
+        assert am[t] == am_n[t]
+    layers = [weights.layer_tensors(shape, l, 40 + seed) for l in range(n)]
+    glob = weights.global_tensors(shape, 40 + seed)
+
+    def script(dec):
+        out = []
+        for t in range(steps):
+            h, lg, _ = dec.step(list(range(B)), [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)],
+                                [t] * B)
+            out.append((h, lg))
+        return out
+    exact, bounds = CB.predict(shape, layers, glob, script)
+    twin = script(Decoder(shape, layers, glob))
+    E = CB.lm_head(shape, glob)
     for t in range(steps):
-        ref, _, _ = dec.step(list(range(B)), [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)], [t] * B)
+        CB.check(got[t], exact[t][0], bounds[t], (t, cycle, beta))
+        ref = twin[t][0]
         rel = np.sqrt(((got[t] - ref) ** 2).mean() / (ref ** 2).mean())
         assert rel <= REL_RMS and np.abs(got[t] - ref).max() <= MAX_ABS, (t, rel, cycle, beta)
+        ok = CB.argmax_decidable(E, got[t], exact[t][0], exact[t][1])
+        for s in range(B):
+            if ok[s]:
+                assert am[t][s] == int(np.argmax(exact[t][1][s])), (t, s)
 
 
 @pytest.mark.parametrize("seed", range(6))

@@ -109,3 +109,41 @@ def test_rounding_points_are_small_perturbation():
         hb, _, _ = b.step([0], [t * 3], [t])
     rel = np.sqrt(((ha - hb) ** 2).mean() / (hb ** 2).mean())
     assert 0 < rel < 2e-2
+
+
+@pytest.mark.parametrize("shape", [models.TOY, models.TOY_LLAMA])
+def test_noise_model_bound_covers_real_bf16_rounding(shape):
+    """The end-to-end tolerance is derived from the first-order bf16 noise model
+    (tests/c4_bounds.py). Check the model against real round-to-nearest-even bf16
+    at the same points (the rounded twin): the derived bound must cover it, and
+    sigma -> 0 must reproduce the exact decoder bit for bit."""
+    import c4_bounds as CB
+    layers = [weights.layer_tensors(shape, l, seed=4) for l in range(shape.n_layers)]
+    glob = weights.global_tensors(shape, seed=4)
+    B, steps = 4, 12
+
+    def script(dec):
+        out = []
+        for t in range(steps):
+            h, lg, _ = dec.step(list(range(B)), [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)],
+                                [t] * B)
+            out.append((h, lg))
+        return out
+    exact, bounds = CB.predict(shape, layers, glob, script)
+    rounded = script(Decoder(shape, layers, glob, round_points=True))
+    for t in range(steps):
+        rel, mx = CB.check(rounded[t][0], exact[t][0], bounds[t], t)
+        assert rel > 0
+    zero = script(Decoder(shape, layers, glob, noise=(0.0, np.random.default_rng(0), "survey")))
+    for t in range(steps):
+        assert np.array_equal(zero[t][0], exact[t][0])
+    # an all-bf16 implementation (every SURVEY c4 point) is predicted to be noisier
+    _, b_survey = CB.predict(shape, layers, glob, script, draws=2, points="survey")
+    assert b_survey[-1][0] > bounds[-1][0]
+    # argmax decidability is sound: where decidable, the rounded twin's argmax is the exact one
+    E = CB.lm_head(shape, glob)
+    for t in range(steps):
+        ok = CB.argmax_decidable(E, rounded[t][0], exact[t][0], exact[t][1])
+        for s in range(B):
+            if ok[s]:
+                assert np.argmax(E @ rounded[t][0][s]) == np.argmax(exact[t][1][s])
