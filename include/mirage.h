@@ -427,6 +427,17 @@ int32_t mirage_host_unregister(void* ptr);
 /* Number of kernels this ctx has launched (its own kernels, not cuBLAS). */
 int64_t mirage_kernel_launches(const mirage_ctx* ctx);
 
+/* Profiling hook. With the environment variable MIRAGE_ATTN_TRACE set when the
+ * ctx is created, every attention launch of mirage_attn_only records 16
+ * %globaltimer slots per CTA (ns: entry, first tiles issued, first tile
+ * landed, last tile consumed, last output written, last split combine, exit;
+ * slot 7 = items processed; 8-10 = phases of the last combine: ticket taken,
+ * (m, l) staged, weights). This call synchronizes the compute stream and
+ * copies the last launch's [n_ctas][16] uint64 slots to host_out (capacity
+ * cap_ctas CTAs). Errors: STATE (tracing off), RANGE (cap too small; *n_ctas
+ * still receives the count), CUDA. */
+int32_t mirage_attn_trace(mirage_ctx* ctx, uint64_t* host_out, int32_t cap_ctas, int32_t* n_ctas);
+
 #ifdef __cplusplus
 }
 #endif

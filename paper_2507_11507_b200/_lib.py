@@ -112,6 +112,7 @@ def _load():
         "mirage_fill_kv": (I32, [P, I32, I64, I32, U64]),
         "mirage_write_kv": (I32, [P, I32, I64, I32, P]),
         "mirage_kernel_launches": (I64, [P]),
+        "mirage_attn_trace": (I32, [P, pU64, I32, pI32]),
         "mirage_nccl_unique_id": (I32, [P]),
         "mirage_host_register": (I32, [P, U64]),
         "mirage_region_count": (I32, [P, I32, pI32]),
@@ -141,7 +142,8 @@ EXPORTED = [
     "mirage_fill_kv", "mirage_write_kv", "mirage_kernel_launches", "mirage_nccl_unique_id",
     "mirage_host_register", "mirage_host_unregister", "mirage_region_count", "mirage_region_info",
     "mirage_unremap", "mirage_swap_out", "mirage_swap_in", "mirage_set_weight_source", "mirage_tp_export",
-    "mirage_tp_import", "mirage_prefill", "mirage_migrate_region", "mirage_predict_stall"]
+    "mirage_tp_import", "mirage_prefill", "mirage_migrate_region", "mirage_predict_stall",
+    "mirage_attn_trace"]
 
 
 def model_cfg(shape):
@@ -445,3 +447,12 @@ class Context:
 
     def kernel_launches(self):
         return LIB.mirage_kernel_launches(self._ctx)
+
+    def attn_trace(self):
+        """[n_ctas][16] %globaltimer slots of the last attn_only launch (MIRAGE_ATTN_TRACE)."""
+        n = C.c_int32()
+        LIB.mirage_attn_trace(self._ctx, None, 0, C.byref(n))
+        buf = (C.c_uint64 * max(16 * n.value, 1))()
+        self._check(LIB.mirage_attn_trace(self._ctx, buf, n.value, C.byref(n)), "attn_trace")
+        v = list(buf[: 16 * n.value])
+        return [v[i: i + 16] for i in range(0, len(v), 16)]

@@ -126,6 +126,20 @@ __device__ __forceinline__ float exp2_ftz(float x) {
   return y;
 }
 
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// trace slots per CTA (16): 0 entry, 1 first tiles issued, 2 first tile landed
+// (warp 0), 3 last tile consumed (warp 0), 4 last item's output / partial written,
+// 5 last combine done, 6 exit, 7 items processed; combine phases of the last
+// combine: 8 ticket taken, 9 (m, l) staged, 10 weights computed
+#define ATTN_TRACE(slot, val)                                              \
+  do {                                                                     \
+    if (p.trace) p.trace[(size_t)blockIdx.x * 16 + (slot)] = (val);        \
+  } while (0)
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -145,8 +159,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // issues every TMA tile for the W consumer warps (full/empty mbarrier pairs per
 // ring stage); the consumers only compute. Otherwise each warp runs its own
 // producer inline (pump).
+// resident CTAs per SM the register budget must allow (the shared-memory rings
+// decide the rest): 3 for MHA decode (G = 1), 2 otherwise
+template <int G, int QP>
+constexpr int min_ctas() { return (G == 1 && QP == 1) ? 3 : 2; }
+
 template <int D, int G, int QP, int W, int NS, bool WS>
-__global__ void __launch_bounds__((W + (WS ? 1 : 0)) * 32)
+__global__ void __launch_bounds__((W + (WS ? 1 : 0)) * 32, min_ctas<G, QP>())
 paged_attention_kernel(const AttnParams p) {
   constexpr int GV = G * QP;          // query column groups (virtual heads) per item
   constexpr int kWarps = W;
@@ -156,6 +175,13 @@ paged_attention_kernel(const AttnParams p) {
   constexpr int NT = (2 * GV + 7) / 8; // n8 tiles of (head, part) columns
 
   constexpr int QB = NS + 1;           // q staging buffers per CTA (warp 0's producer runs ahead)
+  // FA: G = 8 decode puts the query side on the MMA's M dimension (rows = 8 heads x
+  // {hi, lo} bf16 parts of q, or of p): S[16 x tok] = Qc K^T leaves each lane the
+  // scores of ONE head for 4 tokens, so the row max needs 2 shuffles and P feeds
+  // the PV MMA as its A operand straight from the accumulator registers (no
+  // transposing shuffles): ~100 instead of ~260 instructions per 16-token tile,
+  // same HMMA count (16 + 16).
+  constexpr bool FA = G == 8 && QP == 1 && WS;
 
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[kWarps][NS];
@@ -164,18 +190,15 @@ paged_attention_kernel(const AttnParams p) {
   __shared__ __align__(8) uint64_t slot_free[WS ? QB : 1];      // WS: all consumers read the slot's q
   __shared__ int ptiles[WS ? kWarps : 1];                       // WS: tiles issued per consumer warp
   __shared__ float sm_m[kWarps][GV], sm_l[kWarps][GV];
-  constexpr int ACC = (kWarps * D > 2 * kMaxSplitsDev ? kWarps * D : 2 * kMaxSplitsDev) * GV;
+  // per-warp O partials of an item; reused by the split combine for the weights
+  constexpr int ACC_C = (kMaxSplitsDev + 1) * G;
+  constexpr int ACC = kWarps * D * GV > ACC_C ? kWarps * D * GV : ACC_C;
   __shared__ __align__(16) float sm_accf[ACC];
   float(*sm_acc)[GV][D] = reinterpret_cast<float(*)[GV][D]>(sm_accf);
   __shared__ int am_last;
   // dynamic item queue: CTA item k (in claim order) lives in slot k % QB
   __shared__ int slot_claim[QB];
   __shared__ unsigned long long slot_word[QB];  // ((k + 1) << 32) | item, published atomically
-  __shared__ float sLam[GV];
-  __shared__ float sFw[kWarps][GV], sMg[GV], sLs[GV];  // per-item warp-merge weights
-  // split-combine scratch aliases sm_acc (free once the partials are written)
-  float(*sw)[GV] = reinterpret_cast<float(*)[GV]>(sm_accf);
-  float(*sl)[GV] = reinterpret_cast<float(*)[GV]>(sm_accf + kMaxSplitsDev * GV);
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -186,6 +209,7 @@ paged_attention_kernel(const AttnParams p) {
   // q staging (dynamic smem after the rings): [QB][G][2][D/2] packed bf16 hi|lo words, one copy per CTA item
   uint32_t(*qbuf)[GV * D] = reinterpret_cast<uint32_t(*)[GV * D]>(smem + (size_t)kWarps * NS * 2 * TILE);
 
+  if (threadIdx.x == 0) ATTN_TRACE(0, gtimer());
   if (lane == 0 && warp < kWarps) {
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
@@ -219,7 +243,7 @@ paged_attention_kernel(const AttnParams p) {
     int item = 0;
     if (lane == 0) {
       if (atomicCAS(&slot_claim[sl], k - QB, k) == k - QB) {
-        item = atomicAdd(p.sched, 1);
+        item = k == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(p.sched, 1);
         if (item < n_flat) {
           const AttnUnit u = p.units[item / p.H_kv];
           const int nq = QP == 1 ? 1 : u.nq;  // rows u.seq .. u.seq + nq - 1, G heads each
@@ -295,7 +319,9 @@ paged_attention_kernel(const AttnParams p) {
       int item = 0;
       if (lane == 0) {
         if (k >= QB) mbar_wait(&slot_free[WS ? sl_ : 0], ((k / QB) - 1) & 1);
-        item = atomicAdd(p.sched, 1);
+        // the first item is static (CTA b takes item b: no atomic on the critical
+        // path of the first tiles); later ones come from the counter, in order
+        item = k == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(p.sched, 1);
         if (item < n_flat) {
           const AttnUnit u = p.units[item / p.H_kv];
           const int nq = QP == 1 ? 1 : u.nq;
@@ -309,6 +335,7 @@ paged_attention_kernel(const AttnParams p) {
       }
       item = __shfl_sync(0xffffffffu, item, 0);
       if (item >= n_flat) break;
+      if (k == 0 && lane == 0) ATTN_TRACE(1, gtimer());
       const AttnUnit u = p.units[item / p.H_kv];
       const uint64_t off = p.layer_off + (uint64_t)(item % p.H_kv) * (2 * TILE);
       const uint64_t* tbl = p.addrs + u.addr_off;
@@ -366,194 +393,316 @@ paged_attention_kernel(const AttnParams p) {
     const int first = u.b0 + warp;
     const int n_it = first < u.b1 ? (u.b1 - first + kWarps - 1) / kWarps : 0;
 
-    // B fragments of the query columns: column n = gq (+8 nt): head nt*4 + gq/2, part gq&1.
-    // q arrives pre-scaled and pre-split (qkv_post): word i of (head, part) packs
-    // elements 2i, 2i+1, so a fragment is two shared-memory words.
-    uint32_t qb[NT][KS][2];
-    const uint32_t* qs = &qbuf[ck % QB][0];
-    if (n_it > 0) mbar_wait(&qbars[ck % QB], (ck / QB) & 1);
+    if constexpr (FA) {
+      // ---- G = 8 decode, query heads as the M side (see the comment at FA) ----
+      // A fragments of q: row gq = head gq's hi part, row gq + 8 = its lo part
+      uint32_t qa[KS][4];
+      const uint32_t* qs = &qbuf[ck % QB][0];
+      if (n_it > 0) mbar_wait(&qbars[ck % QB], (ck / QB) & 1);
+      {
+        const uint32_t* qw = qs + gq * D + tq;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int hh = nt * 4 + (gq >> 1);
-      const uint32_t* qw = qs + hh * D + (gq & 1) * (D / 2) + tq;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        if (hh < GV && hh / G < nq && n_it > 0) {
-          qb[nt][ks][0] = qw[ks * 8];
-          qb[nt][ks][1] = qw[ks * 8 + 4];
-        } else {
-          qb[nt][ks][0] = qb[nt][ks][1] = 0u;
+        for (int ks = 0; ks < KS; ++ks) {
+          qa[ks][0] = n_it > 0 ? qw[ks * 8] : 0u;                  // hi, dims 16ks + 2tq, +1
+          qa[ks][1] = n_it > 0 ? qw[D / 2 + ks * 8] : 0u;          // lo
+          qa[ks][2] = n_it > 0 ? qw[ks * 8 + 4] : 0u;              // hi, dims 16ks + 8 + 2tq, +1
+          qa[ks][3] = n_it > 0 ? qw[D / 2 + ks * 8 + 4] : 0u;      // lo
         }
       }
-    }
-    if (WS) {  // this warp holds item ck's q in registers: its slot may be reused
       __syncwarp();
       if (lane == 0) mbar_arrive(&slot_free[WS ? ck % QB : 0]);
-    }
-    // per lane: softmax state of head nt*4 + tq; O^T accumulators (dims ks*16+gq,+8)
-    float m[NT], l[NT], o[NT][KS][4];
-    int Lv[NT];  // causal length of the lane's (virtual) head: row v / G of the item
+      // per lane: softmax state of head gq; O rows gq (hi) and gq + 8 (lo), dims 8n + 2tq, +1
+      float mh = -CUDART_INF_F, lh = 0.f;
+      float oa[D / 8][4];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) Lv[nt] = L + min((nt * 4 + tq) / G, nq - 1);
+      for (int n = 0; n < D / 8; ++n)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      m[nt] = -CUDART_INF_F;
-      l[nt] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) o[nt][ks][j] = 0.f;
-    }
-
-    for (int it = 0; it < n_it; ++it) {
-      const int st = rc % NS;
-      const uint32_t phase = (rc / NS) & 1;
-      const int blk = first + kWarps * it;
-      mbar_wait(&bars[warp][st], phase);
-      uint8_t* tile = ring + st * 2 * TILE;
-      const int valid_rows = min(16, Lmax - blk * 16);
-      if (valid_rows < 16) {  // rows past the context may hold any bytes: zero V there
-        for (int e = lane; e < (16 - valid_rows) * (ROW / 16); e += 32) {
-          const int r = valid_rows + e / (ROW / 16), c = e % (ROW / 16);
-          *reinterpret_cast<uint4*>(tile + TILE + r * ROW + c * 16) = make_uint4(0, 0, 0, 0);
+        for (int j = 0; j < 4; ++j) oa[n][j] = 0.f;
+      for (int it = 0; it < n_it; ++it) {
+        const int st = rc % NS;
+        const uint32_t phase = (rc / NS) & 1;
+        const int blk = first + kWarps * it;
+        mbar_wait(&bars[warp][st], phase);
+        if (rc == 0 && warp == 0 && lane == 0) ATTN_TRACE(2, gtimer());
+        uint8_t* tile = ring + st * 2 * TILE;
+        const int valid_rows = min(16, Lmax - blk * 16);
+        if (valid_rows < 16) {  // rows past the context may hold any bytes: zero V there
+          for (int e = lane; e < (16 - valid_rows) * (ROW / 16); e += 32) {
+            const int r = valid_rows + e / (ROW / 16), c = e % (ROW / 16);
+            *reinterpret_cast<uint4*>(tile + TILE + r * ROW + c * 16) = make_uint4(0, 0, 0, 0);
+          }
+          __syncwarp();
         }
-        __syncwarp();
-      }
-      // ---- S = K Qc (two independent accumulation chains: even / odd k-slices) ----
-      float sacc[NT][4], sacc2[NT][4];
+        const uint32_t tile_s = ring_s + st * 2 * TILE;
+        // ---- S[16 x 16 tok] = Qc K^T: one accumulator chain per 8-token n-tile ----
+        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+        for (int ks = 0; ks < KS; ++ks) {
+          uint32_t bk[4];  // (tok 0-7, dims lo), (tok 0-7, hi), (tok 8-15, lo), (tok 8-15, hi)
+          ldsm_x4_s(bk, tile_s + voff[ks] - TILE);
+          const uint32_t b0[2] = {bk[0], bk[1]}, b1[2] = {bk[2], bk[3]};
+          mma_bf16(s0, qa[ks], b0);
+          mma_bf16(s1, qa[ks], b1);
+        }
+        // head gq's scores of tokens 2tq, 2tq + 1, 8 + 2tq, 9 + 2tq (hi row + lo row)
+        float sc[4] = {s0[0] + s0[2], s0[1] + s0[3], s1[0] + s1[2], s1[1] + s1[3]};
+        if (valid_rows < 16) {
+          const int t0 = 2 * tq;
+          if (t0 >= valid_rows) sc[0] = -CUDART_INF_F;
+          if (t0 + 1 >= valid_rows) sc[1] = -CUDART_INF_F;
+          if (t0 + 8 >= valid_rows) sc[2] = -CUDART_INF_F;
+          if (t0 + 9 >= valid_rows) sc[3] = -CUDART_INF_F;
+        }
+        float bm = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
+        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+        const float m_new = fmaxf(mh, bm);
+        float pv[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) sacc[nt][j] = sacc2[nt][j] = 0.f;
-      const uint32_t tile_s = ring_s + st * 2 * TILE;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        uint32_t a[4];
-        ldsm_x4_s(a, tile_s + koff[ks]);
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) mma_bf16((ks & 1) ? sacc2[nt] : sacc[nt], a, qb[nt][ks]);
-      }
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) sacc[nt][j] += sacc2[nt][j];
-      // ---- online softmax (base 2) per head nt*4+tq; rows gq and gq+8 ----
-      float pA[NT], pB[NT];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int vr = QP == 1 ? valid_rows : Lv[nt] - blk * 16;  // rows of this tile the head sees
-        const float s0 = (gq < vr) ? sacc[nt][0] + sacc[nt][1] : -CUDART_INF_F;
-        const float s1 = (gq + 8 < vr) ? sacc[nt][2] + sacc[nt][3] : -CUDART_INF_F;
-        float bm = fmaxf(s0, s1);
-        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 4));
-        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
-        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
-        const float m_new = fmaxf(m[nt], bm);
-        pA[nt] = exp2_ftz(s0 - m_new);
-        pB[nt] = exp2_ftz(s1 - m_new);
-        if (QP > 1 && m_new == -CUDART_INF_F) pA[nt] = pB[nt] = 0.f;  // a row that sees none of this tile
+        for (int j = 0; j < 4; ++j) pv[j] = exp2_ftz(sc[j] - m_new);
         // rescale only when some head's running max moved (alpha == 1 otherwise:
         // skipping the multiply by exactly 1 leaves every bit unchanged)
-        if (__any_sync(0xffffffffu, m_new != m[nt])) {
-          // (a prefill row that has seen no token yet keeps m = -inf: alpha = 1, not NaN)
-          const float alpha = (QP > 1 && m_new == -CUDART_INF_F) ? 1.f : exp2_ftz(m[nt] - m_new);
-          l[nt] *= alpha;
+        if (__any_sync(0xffffffffu, m_new != mh)) {
+          const float alpha = exp2_ftz(mh - m_new);
+          lh *= alpha;
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks)
+          for (int n = 0; n < D / 8; ++n)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) o[nt][ks][j] *= alpha;
+            for (int j = 0; j < 4; ++j) oa[n][j] *= alpha;
         }
-        l[nt] = l[nt] + pA[nt] + pB[nt];
-        m[nt] = m_new;
-      }
-      // ---- P as B fragments: lane needs P[2tq, 2tq+1, 2tq+8, 2tq+9][column gq] ----
-      uint32_t pb[NT][2];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int src0 = 8 * tq + (gq >> 1), src1 = src0 + 4;
-        const float a0 = __shfl_sync(0xffffffffu, pA[nt], src0);  // P[2tq]
-        const float a8 = __shfl_sync(0xffffffffu, pB[nt], src0);  // P[2tq+8]
-        const float c0 = __shfl_sync(0xffffffffu, pA[nt], src1);  // P[2tq+1]
-        const float c8 = __shfl_sync(0xffffffffu, pB[nt], src1);  // P[2tq+9]
-        const int part = gq & 1;
-        if (nt * 4 + (gq >> 1) < GV) {
-          pb[nt][0] = pack_bf16(bf16_part(a0, part), bf16_part(c0, part));
-          pb[nt][1] = pack_bf16(bf16_part(a8, part), bf16_part(c8, part));
-        } else {
-          pb[nt][0] = pb[nt][1] = 0u;
+        mh = m_new;
+        lh += (pv[0] + pv[1]) + (pv[2] + pv[3]);
+        // P as the A operand: rows gq = bf16 hi of p, gq + 8 = bf16(p - hi)
+        uint32_t pa[4];
+        {
+          const __nv_bfloat162 h01 = __floats2bfloat162_rn(pv[0], pv[1]);
+          const __nv_bfloat162 h89 = __floats2bfloat162_rn(pv[2], pv[3]);
+          const float2 f01 = __bfloat1622float2(h01), f89 = __bfloat1622float2(h89);
+          const __nv_bfloat162 l01 = __floats2bfloat162_rn(pv[0] - f01.x, pv[1] - f01.y);
+          const __nv_bfloat162 l89 = __floats2bfloat162_rn(pv[2] - f89.x, pv[3] - f89.y);
+          pa[0] = *reinterpret_cast<const uint32_t*>(&h01);
+          pa[1] = *reinterpret_cast<const uint32_t*>(&l01);
+          pa[2] = *reinterpret_cast<const uint32_t*>(&h89);
+          pa[3] = *reinterpret_cast<const uint32_t*>(&l89);
         }
-      }
-      // ---- O^T += V^T P ----
+        // ---- O[16 x D] += P V: V^T fragments by ldmatrix.trans, two 8-dim n-tiles each ----
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        uint32_t a[4];
-        ldsm_x4_t_s(a, tile_s + voff[ks]);
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) mma_bf16(o[nt][ks], a, pb[nt]);
-      }
-      ++rc;
-      if (WS) {  // hand the stage back to the producer warp
+        for (int ks = 0; ks < KS; ++ks) {
+          uint32_t bv[4];  // (tok 0-7, dims 16ks..+7), (tok 8-15, same), (tok 0-7, +8..), (tok 8-15, +8..)
+          ldsm_x4_t_s(bv, tile_s + koff[ks] + TILE);
+          const uint32_t b0[2] = {bv[0], bv[1]}, b1[2] = {bv[2], bv[3]};
+          mma_bf16(oa[2 * ks], pa, b0);
+          mma_bf16(oa[2 * ks + 1], pa, b1);
+        }
+        ++rc;
         __syncwarp();
         if (lane == 0) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes (V zeroing) -> TMA
           mbar_arrive(&empty[WS ? warp : 0][st]);
         }
       }
-      pump(ck);  // refill the freed stage with the tile NS ahead in the stream
-    }
-    // l: sum the lane partials over the 8 token groups
+      lh += __shfl_xor_sync(0xffffffffu, lh, 1);
+      lh += __shfl_xor_sync(0xffffffffu, lh, 2);
+      if (warp == 0 && lane == 0) {
+        ATTN_TRACE(3, gtimer());
+        ATTN_TRACE(7, ck + 1);
+      }
+      csync();  // the previous item's merge has finished reading sm_*
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 4);
-      l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 8);
-      l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 16);
-    }
-
-    csync();  // the previous item's merge has finished reading sm_*
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int hh = nt * 4 + tq;
-      if (hh < GV) {
-#pragma unroll
+      for (int n = 0; n < D / 8; ++n)
+        *reinterpret_cast<float2*>(&sm_acc[warp][gq][8 * n + 2 * tq]) =
+            make_float2(oa[n][0] + oa[n][2], oa[n][1] + oa[n][3]);
+      if (tq == 0) {
+        sm_m[warp][gq] = mh;
+        sm_l[warp][gq] = lh;
+      }
+      csync();
+    } else {
+    // B fragments of the query columns: column n = gq (+8 nt): head nt*4 + gq/2, part gq&1.
+      // q arrives pre-scaled and pre-split (qkv_post): word i of (head, part) packs
+      // elements 2i, 2i+1, so a fragment is two shared-memory words.
+      uint32_t qb[NT][KS][2];
+      const uint32_t* qs = &qbuf[ck % QB][0];
+      if (n_it > 0) mbar_wait(&qbars[ck % QB], (ck / QB) & 1);
+  #pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int hh = nt * 4 + (gq >> 1);
+        const uint32_t* qw = qs + hh * D + (gq & 1) * (D / 2) + tq;
+  #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
-          sm_acc[warp][hh][ks * 16 + gq] = o[nt][ks][0] + o[nt][ks][1];
-          sm_acc[warp][hh][ks * 16 + gq + 8] = o[nt][ks][2] + o[nt][ks][3];
-        }
-        if (gq == 0) {
-          sm_m[warp][hh] = m[nt];
-          sm_l[warp][hh] = l[nt];
+          if (hh < GV && hh / G < nq && n_it > 0) {
+            qb[nt][ks][0] = qw[ks * 8];
+            qb[nt][ks][1] = qw[ks * 8 + 4];
+          } else {
+            qb[nt][ks][0] = qb[nt][ks][1] = 0u;
+          }
         }
       }
+      if (WS) {  // this warp holds item ck's q in registers: its slot may be reused
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&slot_free[WS ? ck % QB : 0]);
+      }
+      // per lane: softmax state of head nt*4 + tq; O^T accumulators (dims ks*16+gq,+8)
+      float m[NT], l[NT], o[NT][KS][4];
+      int Lv[NT];  // causal length of the lane's (virtual) head: row v / G of the item
+  #pragma unroll
+      for (int nt = 0; nt < NT; ++nt) Lv[nt] = L + min((nt * 4 + tq) / G, nq - 1);
+  #pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        m[nt] = -CUDART_INF_F;
+        l[nt] = 0.f;
+  #pragma unroll
+        for (int ks = 0; ks < KS; ++ks)
+  #pragma unroll
+          for (int j = 0; j < 4; ++j) o[nt][ks][j] = 0.f;
+      }
+  
+      for (int it = 0; it < n_it; ++it) {
+        const int st = rc % NS;
+        const uint32_t phase = (rc / NS) & 1;
+        const int blk = first + kWarps * it;
+        mbar_wait(&bars[warp][st], phase);
+        if (rc == 0 && warp == 0 && lane == 0) ATTN_TRACE(2, gtimer());
+        uint8_t* tile = ring + st * 2 * TILE;
+        const int valid_rows = min(16, Lmax - blk * 16);
+        if (valid_rows < 16) {  // rows past the context may hold any bytes: zero V there
+          for (int e = lane; e < (16 - valid_rows) * (ROW / 16); e += 32) {
+            const int r = valid_rows + e / (ROW / 16), c = e % (ROW / 16);
+            *reinterpret_cast<uint4*>(tile + TILE + r * ROW + c * 16) = make_uint4(0, 0, 0, 0);
+          }
+          __syncwarp();
+        }
+        // ---- S = K Qc (two independent accumulation chains: even / odd k-slices) ----
+        float sacc[NT][4], sacc2[NT][4];
+  #pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+  #pragma unroll
+          for (int j = 0; j < 4; ++j) sacc[nt][j] = sacc2[nt][j] = 0.f;
+        const uint32_t tile_s = ring_s + st * 2 * TILE;
+  #pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          uint32_t a[4];
+          ldsm_x4_s(a, tile_s + koff[ks]);
+  #pragma unroll
+          for (int nt = 0; nt < NT; ++nt) mma_bf16((ks & 1) ? sacc2[nt] : sacc[nt], a, qb[nt][ks]);
+        }
+  #pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+  #pragma unroll
+          for (int j = 0; j < 4; ++j) sacc[nt][j] += sacc2[nt][j];
+        // ---- online softmax (base 2) per head nt*4+tq; rows gq and gq+8 ----
+        float pA[NT], pB[NT];
+  #pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int vr = QP == 1 ? valid_rows : Lv[nt] - blk * 16;  // rows of this tile the head sees
+          const float s0 = (gq < vr) ? sacc[nt][0] + sacc[nt][1] : -CUDART_INF_F;
+          const float s1 = (gq + 8 < vr) ? sacc[nt][2] + sacc[nt][3] : -CUDART_INF_F;
+          float bm = fmaxf(s0, s1);
+          bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 4));
+          bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
+          bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
+          const float m_new = fmaxf(m[nt], bm);
+          pA[nt] = exp2_ftz(s0 - m_new);
+          pB[nt] = exp2_ftz(s1 - m_new);
+          if (QP > 1 && m_new == -CUDART_INF_F) pA[nt] = pB[nt] = 0.f;  // a row that sees none of this tile
+          // rescale only when some head's running max moved (alpha == 1 otherwise:
+          // skipping the multiply by exactly 1 leaves every bit unchanged)
+          if (__any_sync(0xffffffffu, m_new != m[nt])) {
+            // (a prefill row that has seen no token yet keeps m = -inf: alpha = 1, not NaN)
+            const float alpha = (QP > 1 && m_new == -CUDART_INF_F) ? 1.f : exp2_ftz(m[nt] - m_new);
+            l[nt] *= alpha;
+  #pragma unroll
+            for (int ks = 0; ks < KS; ++ks)
+  #pragma unroll
+              for (int j = 0; j < 4; ++j) o[nt][ks][j] *= alpha;
+          }
+          l[nt] = l[nt] + pA[nt] + pB[nt];
+          m[nt] = m_new;
+        }
+        // ---- P as B fragments: lane needs P[2tq, 2tq+1, 2tq+8, 2tq+9][column gq] ----
+        uint32_t pb[NT][2];
+  #pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int src0 = 8 * tq + (gq >> 1), src1 = src0 + 4;
+          const float a0 = __shfl_sync(0xffffffffu, pA[nt], src0);  // P[2tq]
+          const float a8 = __shfl_sync(0xffffffffu, pB[nt], src0);  // P[2tq+8]
+          const float c0 = __shfl_sync(0xffffffffu, pA[nt], src1);  // P[2tq+1]
+          const float c8 = __shfl_sync(0xffffffffu, pB[nt], src1);  // P[2tq+9]
+          const int part = gq & 1;
+          if (nt * 4 + (gq >> 1) < GV) {
+            pb[nt][0] = pack_bf16(bf16_part(a0, part), bf16_part(c0, part));
+            pb[nt][1] = pack_bf16(bf16_part(a8, part), bf16_part(c8, part));
+          } else {
+            pb[nt][0] = pb[nt][1] = 0u;
+          }
+        }
+        // ---- O^T += V^T P ----
+  #pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          uint32_t a[4];
+          ldsm_x4_t_s(a, tile_s + voff[ks]);
+  #pragma unroll
+          for (int nt = 0; nt < NT; ++nt) mma_bf16(o[nt][ks], a, pb[nt]);
+        }
+        ++rc;
+        if (WS) {  // hand the stage back to the producer warp
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes (V zeroing) -> TMA
+            mbar_arrive(&empty[WS ? warp : 0][st]);
+          }
+        }
+        pump(ck);  // refill the freed stage with the tile NS ahead in the stream
+      }
+      if (warp == 0 && lane == 0) {
+        ATTN_TRACE(3, gtimer());
+        ATTN_TRACE(7, ck + 1);
+      }
+      // l: sum the lane partials over the 8 token groups
+  #pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 4);
+        l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 8);
+        l[nt] += __shfl_xor_sync(0xffffffffu, l[nt], 16);
+      }
+  
+      csync();  // the previous item's merge has finished reading sm_*
+  #pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int hh = nt * 4 + tq;
+        if (hh < GV) {
+  #pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            sm_acc[warp][hh][ks * 16 + gq] = o[nt][ks][0] + o[nt][ks][1];
+            sm_acc[warp][hh][ks * 16 + gq + 8] = o[nt][ks][2] + o[nt][ks][3];
+          }
+          if (gq == 0) {
+            sm_m[warp][hh] = m[nt];
+            sm_l[warp][hh] = l[nt];
+          }
+        }
+      }
+      csync();
+  
     }
-    csync();
 
-    // merge the warps in fixed order. Per head first (one thread each): M = max_w m_w,
-    // fw_w = 2^(m_w - M) (0 for a warp that saw nothing), Ls = sum_w fw_w l_w; then
-    // every thread merges float4s of dims with the precomputed weights.
+    // merge the warps in fixed order (w = 0..W-1); every thread derives its head's
+    // weights itself: M = max_w m_w, fw_w = 2^(m_w - M) (0 for a warp that saw
+    // nothing), Ls = sum_w fw_w l_w, then merges float4s of dims
     const bool split = u.nsplit > 1;
-    if (threadIdx.x < GV) {
-      const int g = threadIdx.x;
+#pragma unroll 1
+    for (int e = threadIdx.x; e < GV * D / 4; e += kWarps * 32) {
+      const int g = e / (D / 4), d = (e % (D / 4)) * 4;
+      if (QP > 1 && g / G >= nq) continue;
       float M = sm_m[0][g];
 #pragma unroll
       for (int w = 1; w < kWarps; ++w) M = fmaxf(M, sm_m[w][g]);
       float Ls = 0.f;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const float fw = (sm_m[w][g] == -CUDART_INF_F) ? 0.f : exp2f(sm_m[w][g] - M);
-        sFw[w][g] = fw;
-        Ls += fw * sm_l[w][g];
-      }
-      sMg[g] = M;
-      sLs[g] = Ls;
-    }
-    csync();
-    for (int e = threadIdx.x; e < GV * D / 4; e += kWarps * 32) {
-      const int g = e / (D / 4), d = (e % (D / 4)) * 4;
-      if (QP > 1 && g / G >= nq) continue;
       float4 ov = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) {
-        const float fw = sFw[w][g];
+        const float fw = (sm_m[w][g] == -CUDART_INF_F) ? 0.f : exp2f(sm_m[w][g] - M);
+        Ls += fw * sm_l[w][g];
         const float4 a = *reinterpret_cast<const float4*>(&sm_acc[w][g][d]);
         ov.x += fw * a.x;
         ov.y += fw * a.y;
@@ -562,7 +711,6 @@ paged_attention_kernel(const AttnParams p) {
       }
       const int h = hk * G + g % G;
       if (!split) {
-        const float Ls = sLs[g];
         const size_t oi = ((size_t)(s + g / G) * p.H + h) * D + d;
         if (p.out_fp32) {
           *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oi) =
@@ -578,77 +726,84 @@ paged_attention_kernel(const AttnParams p) {
       } else {
         float* rec = p.partial + ((size_t)(u.pbase + u.split) * p.H + h) * (D + 4);
         *reinterpret_cast<float4*>(rec + d) = ov;
-        if (d == 0) {
-          rec[D] = sMg[g];
-          rec[D + 1] = sLs[g];
-        }
+        if (d == 0) *reinterpret_cast<float2*>(rec + D) = make_float2(M, Ls);
       }
     }
+    if (threadIdx.x == 0) ATTN_TRACE(4, gtimer());
     if (QP > 1 || !split) continue;  // prefill items are never split (host guarantees nsplit == 1)
 
-    // ---- split-K combine by the last-arriving CTA of this (seq, kv head) ----
-    __threadfence();
+    // ---- split-K combine: o = sum_i w_i o_i / sum_i w_i l_i over the splits i of
+    // this (seq, kv head), w_i = 2^(m_i - M), M = max_i m_i; the reduction order
+    // depends only on nsplit, so the result is deterministic and independent of
+    // where the blocks live.
+    // Publication: the barrier orders every consumer thread's partial stores before
+    // thread 0's release-acquire ticket (cumulativity, as in CUTLASS's split-K
+    // semaphore); the last arriver's barrier then orders its threads' loads after them.
+    const int ns = u.nsplit;  // <= kMaxSplitsDev
+    const size_t rstride = (size_t)p.H * (D + 4);
+    const float* rec0 = p.partial + ((size_t)u.pbase * p.H + hk * G) * (D + 4);
     csync();
+    // The last-arriving CTA of this (seq, kv head) folds everything. (A cooperative
+    // variant in which the ns CTAs wait for each other and each fold a slice of the
+    // columns measured slower on B200: 19.0 vs 16.8 us per 1 x 8k launch.)
     if (threadIdx.x == 0) {
       int* t = p.tickets + (size_t)s * p.H_kv + hk;
-      const int prev = atomicAdd(t, 1);
-      am_last = (prev == u.nsplit - 1);
-      if (am_last) *t = 0;  // reset for the next launch
+      int prev;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(t) : "memory");
+      am_last = (prev == ns - 1);
+      if (am_last) *t = 0;  // every split has arrived: reset for the next launch
     }
     csync();
     if (!am_last) continue;
-    __threadfence();
-    const size_t rstride = (size_t)p.H * (D + 4);
-    const float* rec0 = p.partial + ((size_t)u.pbase * p.H + hk * G) * (D + 4);
-    const int ns = u.nsplit;  // <= kMaxSplitsDev
-    // (1) stage every split's (m, l) in shared memory
-    for (int e = threadIdx.x; e < ns * G; e += kWarps * 32) {
-      const int i = e / G, g = e % G;
-      sw[i][g] = __ldcg(rec0 + i * rstride + g * (D + 4) + D);
-      sl[i][g] = __ldcg(rec0 + i * rstride + g * (D + 4) + D + 1);
-    }
-    csync();
-    // (2) per head: M = max_i m_i, w_i = 2^(m_i - M), Lambda = sum_i w_i l_i (fixed order)
-    if (threadIdx.x < G) {
-      const int g = threadIdx.x;
+    if (threadIdx.x == 0) ATTN_TRACE(8, gtimer());
+    // (1) per head (one warp each): M = max_i m_i, w_i = 2^(m_i - M), Lambda =
+    // sum_i w_i l_i by a fixed shuffle tree; the w_i go to shared memory
+    float* sw = sm_accf;                          // [kMaxSplitsDev][G]
+    float* sLam = sm_accf + kMaxSplitsDev * G;    // [G]
+    for (int g = warp; g < G; g += kWarps) {
+      float mv[kMaxSplitsDev / 32], lv[kMaxSplitsDev / 32];
       float M = -CUDART_INF_F;
-      for (int i = 0; i < ns; ++i) M = fmaxf(M, sw[i][g]);
-      float Ls = 0.f;
-      for (int i = 0; i < ns; ++i) {
-        const float w = exp2f(sw[i][g] - M);
-        sw[i][g] = w;
-        Ls += w * sl[i][g];
+#pragma unroll
+      for (int k = 0; k < kMaxSplitsDev / 32; ++k) {
+        const int i = lane + 32 * k;
+        mv[k] = -CUDART_INF_F;
+        lv[k] = 0.f;
+        if (i < ns) {
+          const float2 v = __ldcg(reinterpret_cast<const float2*>(rec0 + i * rstride + g * (D + 4) + D));
+          mv[k] = v.x;
+          lv[k] = v.y;
+        }
+        M = fmaxf(M, mv[k]);
       }
-      sLam[g] = Ls;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      float Ls = 0.f;
+#pragma unroll
+      for (int k = 0; k < kMaxSplitsDev / 32; ++k) {
+        const int i = lane + 32 * k;
+        const float w = i < ns ? exp2f(mv[k] - M) : 0.f;
+        if (i < ns) sw[i * G + g] = w;
+        Ls += w * lv[k];
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, o);
+      if (lane == 0) sLam[g] = Ls;
     }
     csync();
-    // (3) o = sum_i w_i o_i / Lambda: one float4 of dims per thread, 16 (then 8) independent
-    // 16-byte loads in flight (same per-element order of operations as a scalar loop)
+    // (2) o = sum_i w_i o_i / Lambda: one float4 of dims per thread, 16 (then 8)
+    // independent 16-byte loads in flight (same per-element order as a scalar loop)
     for (int e = threadIdx.x; e < G * D / 4; e += kWarps * 32) {
       const int g = e / (D / 4), d = (e % (D / 4)) * 4;
       const float* rg = rec0 + g * (D + 4) + d;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       int i = 0;
-      for (; i + 16 <= ns; i += 16) {  // 16 loads in flight (same summation order)
+      for (; i + 16 <= ns; i += 16) {
         float4 ov[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) ov[k] = __ldcg(reinterpret_cast<const float4*>(rg + (i + k) * rstride));
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const float w = sw[i + k][g];
-          acc.x += w * ov[k].x;
-          acc.y += w * ov[k].y;
-          acc.z += w * ov[k].z;
-          acc.w += w * ov[k].w;
-        }
-      }
-      for (; i + 8 <= ns; i += 8) {
-        float4 ov[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) ov[k] = __ldcg(reinterpret_cast<const float4*>(rg + (i + k) * rstride));
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float w = sw[i + k][g];
+          const float w = sw[(i + k) * G + g];
           acc.x += w * ov[k].x;
           acc.y += w * ov[k].y;
           acc.z += w * ov[k].z;
@@ -657,7 +812,7 @@ paged_attention_kernel(const AttnParams p) {
       }
       for (; i < ns; ++i) {
         const float4 ov = __ldcg(reinterpret_cast<const float4*>(rg + i * rstride));
-        const float w = sw[i][g];
+        const float w = sw[i * G + g];
         acc.x += w * ov.x;
         acc.y += w * ov.y;
         acc.z += w * ov.z;
@@ -672,11 +827,13 @@ paged_attention_kernel(const AttnParams p) {
         else reinterpret_cast<__nv_bfloat16*>(p.out)[oi + k] = __float2bfloat16_rn(r[k]);
       }
     }
+    if (threadIdx.x == 0) ATTN_TRACE(5, gtimer());
   }
   }  // consumer warps
   // the last CTA to finish resets the work counter for the next launch
   __syncthreads();
   if (threadIdx.x == 0) {
+    ATTN_TRACE(6, gtimer());
     __threadfence();
     if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
       atomicExch(p.sched, 0);

@@ -202,6 +202,7 @@ struct Model {
   struct AttnTiming {
     cudaEvent_t t0, t1;
     uint64_t bytes;
+    int reps = 1;  // launches between t0 and t1
   };
   std::deque<AttnTiming> attn_pending;
   std::deque<AttnTiming> stall_pending;  // (before, after) a slot ready-wait on the compute stream
@@ -263,6 +264,9 @@ struct mirage_ctx {
   int stage_i = 0;
   char* meta_dev = nullptr;
   int max_units = 0;
+  static constexpr int kTraceCtas = 4096;
+  uint64_t* attn_trace = nullptr;  // MIRAGE_ATTN_TRACE: [kTraceCtas][8] stamps of the last attn_only launch
+  int32_t attn_trace_ctas = 0;
   int max_blk = 0;
   std::string err;
   int32_t sticky = MIRAGE_OK;
@@ -585,7 +589,7 @@ void harvest_attn_times(Model* M) {
     cudaEventElapsedTime(&ms, t.t0, t.t1);
     M->attn_ms += ms;
     M->attn_bytes += t.bytes;
-    M->attn_launches += 1;
+    M->attn_launches += t.reps;
     M->ev_pool.push_back(t.t0);
     M->ev_pool.push_back(t.t1);
     M->attn_pending.pop_front();
@@ -792,6 +796,9 @@ int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
         cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming) != cudaSuccess)
       return bail(MIRAGE_ERR_CUDA);
   }
+  if (getenv("MIRAGE_ATTN_TRACE") &&
+      cudaMalloc(reinterpret_cast<void**>(&c->attn_trace), (size_t)mirage_ctx::kTraceCtas * 16 * 8) != cudaSuccess)
+    c->attn_trace = nullptr;
   if (cudaMalloc(reinterpret_cast<void**>(&c->meta_dev), c->meta_bytes) != cudaSuccess)
     return bail(MIRAGE_ERR_CUDA);
   c->tp = cfg->tp_size;
@@ -852,6 +859,7 @@ void mirage_destroy(mirage_ctx* c) {
     if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
   }
   if (c->meta_dev) cudaFree(c->meta_dev);
+  if (c->attn_trace) cudaFree(c->attn_trace);
   if (c->blas) cublasDestroy(c->blas);
   for (auto& kv : c->lt_plans) {
     cublasLtMatmulDescDestroy(kv.second.op);
@@ -871,6 +879,17 @@ void mirage_destroy(mirage_ctx* c) {
 const char* mirage_last_error(const mirage_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
 
 int64_t mirage_kernel_launches(const mirage_ctx* c) { return c ? c->launches : 0; }
+
+
+int32_t mirage_attn_trace(mirage_ctx* c, uint64_t* host_out, int32_t cap_ctas, int32_t* n_ctas) {
+  GUARD(c);
+  if (!c->attn_trace) return fail(c, MIRAGE_ERR_STATE, "attn_trace: set MIRAGE_ATTN_TRACE before mirage_init");
+  if (n_ctas) *n_ctas = c->attn_trace_ctas;
+  if (!host_out || cap_ctas < c->attn_trace_ctas) return fail(c, MIRAGE_ERR_RANGE, "attn_trace: capacity");
+  CK(c, cudaStreamSynchronize(c->cs));
+  CK(c, cudaMemcpy(host_out, c->attn_trace, (size_t)c->attn_trace_ctas * 16 * 8, cudaMemcpyDeviceToHost));
+  return MIRAGE_OK;
+}
 
 int32_t mirage_add_model(mirage_ctx* c, const mirage_model_cfg* mc, const void* host_blob,
                          uint64_t host_bytes, int64_t native_kv_blocks, int32_t* model_id) {
@@ -1883,13 +1902,26 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
   ap.sched = M->tickets + (size_t)c->cfg.max_batch * s.Hk;
   ap.out = out_dev;
   ap.out_fp32 = out_fp32;
+  if (c->attn_trace) {
+    const int ctas = mirage::attention_grid_ctas(s.H, s.Hk, s.D);
+    c->attn_trace_ctas = std::min(mirage_ctx::kTraceCtas, std::min(ctas, n_units * s.Hk));
+    CK(c, cudaMemsetAsync(c->attn_trace, 0, (size_t)mirage_ctx::kTraceCtas * 16 * 8, c->cs));
+    ap.trace = c->attn_trace;
+  }
   if (c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) {  // kernel-only time, excluding the metadata upload
     harvest_attn_times(M);
     uint64_t nbytes = 0;
     for (int i = 0; i < B; ++i) nbytes += (uint64_t)hv.len[i] * 2 * s.Hk * s.D * 2;
-    Model::AttnTiming at{pool_event(M), pool_event(M), nbytes};
+    // MIRAGE_ATTN_REPEAT=R (bench hook): R back-to-back launches over layers
+    // layer, layer+1, ... (mod n: every launch reads other HBM) inside one timed
+    // pair of events, reported as R launches (per-launch time = total / R)
+    static const int reps = getenv("MIRAGE_ATTN_REPEAT") ? std::max(1, atoi(getenv("MIRAGE_ATTN_REPEAT"))) : 1;
+    Model::AttnTiming at{pool_event(M), pool_event(M), nbytes * reps, reps};
     CK(c, cudaEventRecord(at.t0, c->cs));
-    KL(c, mirage::launch_paged_attention(ap, c->cs));
+    for (int r = 0; r < reps; ++r) {
+      ap.layer_off = (uint64_t)((layer + r) % s.n) * s.Hk * 2 * kBlockTokens * s.D * 2;
+      KL(c, mirage::launch_paged_attention(ap, c->cs));
+    }
     CK(c, cudaEventRecord(at.t1, c->cs));
     M->attn_pending.push_back(at);
     return MIRAGE_OK;

@@ -72,10 +72,32 @@ def run(name, reps, seed=0, split=0):
     nbytes = sum(lens) * 2 * Hk * D * 2
     st = ctx_.query(mid)
     k_ms = (st["attn_ms"] - q0["attn_ms"]) / max(1, st["attn_launches"] - q0["attn_launches"])
+    trace = None
+    if os.environ.get("MIRAGE_ATTN_TRACE"):
+        ctx_.attn_only(mid, layers[reps % L], list(range(B)), q, out, split_tokens=split)
+        trace = trace_summary(ctx_.attn_trace())
     ctx_.close()
     return {"case": name, "split_blocks": st["last_split_blocks"], "units": st["last_attn_units"], "batch": B, "ctx_sum": sum(lens), "bytes": nbytes, "median_ms": med, "best_ms": ms[0],
             "gbs_median": nbytes / med / 1e6, "gbs_best": nbytes / ms[0] / 1e6,
-            "kernel_ms": k_ms, "gbs_kernel": nbytes / k_ms / 1e6}
+            "kernel_ms": k_ms, "gbs_kernel": nbytes / k_ms / 1e6, **({"trace": trace} if trace else {})}
+
+
+def trace_summary(tr):
+    """Per-CTA %globaltimer stamps (us after the earliest entry): median / max of
+    entry, first tiles issued, first tile landed, last tile consumed, last output,
+    last combine, exit; items per CTA."""
+    import numpy as np
+    a = np.array(tr, dtype=np.float64)
+    t0 = a[:, 0][a[:, 0] > 0].min()
+    out = {"ctas": len(a)}
+    for i, nm in [(0, "entry"), (1, "issued"), (2, "landed"), (3, "consumed"), (4, "written"), (8, "ticket"),
+                  (9, "staged"), (10, "weights"), (5, "combined"), (6, "exit")]:
+        v = a[:, i]
+        v = (v[v > 0] - t0) / 1e3
+        if len(v):
+            out[nm] = [round(float(np.percentile(v, 5)), 2), round(float(np.median(v)), 2), round(float(v.max()), 2)]
+    out["items"] = [int(a[:, 7].min()), int(a[:, 7].max())]
+    return out
 
 
 if __name__ == "__main__":
