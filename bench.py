@@ -36,8 +36,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mirage", choices=["mirage", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"],
-                    help="BASELINE.json configs[1..3]; c2 is the headline")
+    ap.add_argument("--config", default="c2", choices=["c2", "c2p", "c3", "c4"],
+                    help="BASELINE.json configs[1..3]; c2 is the headline (P-full: ~400 seqs); c2p = C2 at the "
+                         "paper's KV pressure (P-paper: Table 1's 35%% reservation of a 96 GB GPU, ~29 seqs)")
     ap.add_argument("--batch", type=int, default=0, help="0 = config default (c2: 400, c4: 32)")
     ap.add_argument("--ctx", type=int, default=0, help="c4 context length (default 32768)")
     ap.add_argument("--alpha", type=int, default=1)
@@ -50,6 +51,8 @@ def parse():
     ap.add_argument("--no-resident-arm", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--graphs", action="store_true",
+                    help="capture the step in CUDA graphs (MIRAGE_FLAG_CUDA_GRAPHS); no per-launch attention timing")
     return ap.parse_args()
 
 
@@ -113,7 +116,6 @@ def oracle_leg(shape, ctxs, n_seqs=2, seed=0, steps=1):
     generator. Scaled to tok/s of the full model:
       t_token = (n_layers * (t_layer_step - t_head) + t_head) / n."""
     import numpy as np
-    import torch
     from oracle import kvgen
     from oracle.decode import Decoder
     from synth import weights, workload
@@ -127,13 +129,13 @@ def oracle_leg(shape, ctxs, n_seqs=2, seed=0, steps=1):
         V = np.stack([kvgen.kv_values(seed, i, shape.n_layers, Hk, D, 0, h, 1, range(L)) for h in range(Hk)])
         dec.set_kv(i, [(K, V)])
     setup = time.perf_counter() - t0
-    threads = torch.get_num_threads()
+    threads = None
     try:
         from threadpoolctl import threadpool_info
-        threads = max([threads] + [i.get("num_threads", 0) for i in threadpool_info()])
+        threads = max([1] + [i.get("num_threads", 0) for i in threadpool_info()])
     except Exception:
         pass
-    per_step = []
+    per_step, walls = [], []
     for s in range(steps):
         pos = [L + s for L in sample]
         toks = [workload.teacher_tokens(i, p, shape.vocab) for i, p in enumerate(pos)]
@@ -147,8 +149,9 @@ def oracle_leg(shape, ctxs, n_seqs=2, seed=0, steps=1):
             head @ x
         t_head = time.perf_counter() - t2
         per_step.append((shape.n_layers * (t_step - t_head) + t_head) / len(sample))
+        walls.append(t_step)
     return {"tok_s": 1.0 / statistics.median(per_step), "t_token_s": statistics.median(per_step),
-            "cores": threads, "setup_s": setup, "per_step_token_s": per_step,
+            "cores": threads, "setup_s": setup, "per_step_token_s": per_step, "per_step_wall_s": walls,
             "sample": (f"oracle c4 decode of {len(sample)} seqs (ctx {sample}) through 1 {shape.name} layer + "
                        f"LM head, fp64 numpy, scaled x{shape.n_layers} layers to tok/s")}
 
@@ -242,20 +245,70 @@ def host_cpu():
     return {"nproc": os.cpu_count(), "model": model, "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
 
 
+def c4_toy_leg(steps=128, B=8, seed=0):
+    """SURVEY §8(d) oracle item (3): oracle c4 decoding the C1 toy (2-layer d=256
+    decoder, 8 sequences x 128 teacher-forced steps from position 0), one thread."""
+    from oracle.decode import Decoder
+    from synth import models, weights, workload
+    sh = models.TOY
+    dec = Decoder(sh, [weights.layer_tensors(sh, l, seed) for l in range(sh.n_layers)],
+                  weights.global_tensors(sh, seed))
+    t0 = time.perf_counter()
+    for t in range(steps):
+        dec.step(list(range(B)), [workload.teacher_tokens(s, t, sh.vocab) for s in range(B)], [t] * B)
+    dt = time.perf_counter() - t0
+    return {"seconds": dt, "tok_s": B * steps / dt, "threads": 1,
+            "sample": f"C1 toy, {B} seqs x {steps} decode steps, oracle c4 fp64 numpy"}
+
+
+def single_thread():
+    """Pin the BLAS pools to one thread: the oracle's loops are single-threaded
+    Python, and the reported core count must be the threads actually used."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(1)
+    except Exception:
+        import contextlib
+        return contextlib.nullcontext()
+
+
+def workload_config(wl, info, world):
+    """The config object both arms report (workload-defining keys only)."""
+    B = len(wl.ctxs)
+    c = {"workload": wl.desc, "batch_per_gpu": B, "ctx_mean": sum(wl.ctxs) / B, "ctx_max": max(wl.ctxs),
+         "l2": "inputs larger than L2 (weights + KV read every step)", "parallelism": f"tenant-replica x{world}"}
+    c.update(info)
+    return c
+
+
 def run_reference(args, rank, world):
+    """The oracle arm: oracle/ as it stands (fp64 numpy, one thread), never the
+    library. One step = one oracle decode step of a bounded sample of the same
+    workload: 2 of the batch's sequences (contexts capped at 4096) through ONE
+    hidden layer of the model plus the LM head. ms_per_step is that sample's
+    measured wall time; value extrapolates it to the full model's tok/s:
+    t_token = (n_layers * (t_step - t_head) + t_head) / 2."""
     if rank != 0:
         return
-    wl, _ = build_workload(args, rank, args.warmup + args.steps + args.e2e_steps + 1)
-    res = oracle_leg(wl.tenants[0][0], wl.ctxs, n_seqs=2, seed=args.seed, steps=args.warmup + args.steps)
+    total = args.warmup + args.steps + args.e2e_steps + 1
+    wl, info = build_workload(args, rank, total, impl="reference")
+    with single_thread():
+        res = oracle_leg(wl.tenants[0][0], wl.ctxs, n_seqs=2, seed=args.seed, steps=args.warmup + args.steps)
+        toy = c4_toy_leg()
     times = res["per_step_token_s"][args.warmup:]
+    walls = res["per_step_wall_s"][args.warmup:]
     tok_s = 1.0 / statistics.median(times)
+    sample = res["sample"]
     line = {"impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tok/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded random-init weights, counter-based KV, ShareGPT-shaped lengths)",
-            "config": {"workload": wl.desc + " (bounded oracle sample)"},
-            "cpu_baseline": {"value": tok_s, "unit": "tok/s", "cores": res["cores"], "kind": "oracle",
-                             "sample": res["sample"]},
+            "config": workload_config(wl, info, world),
+            "reference_sample": {"step": sample, "ms_per_step_is": "wall time of that sample step (what ran)",
+                                 "value_is": "full-model tok/s extrapolated from it: (n_layers * (t_step - "
+                                             "t_head) + t_head) / n_seqs per token"},
+            "cpu_baseline": {"value": tok_s, "unit": "tok/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             "c4_toy": toy, "host": host_cpu()},
             "e2e": {"value": tok_s, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -319,31 +372,86 @@ def reclaimed_blocks(S_donor, BB_recipient, R):
     return sum(len(r) * S_donor // BB_recipient for r in runs)
 
 
-def plan_cycle(shape, alpha, beta, placement):
-    from paper_2507_11507_b200 import _lib
+class Sizes:
+    """Layer bytes S, block bytes BB and the planner's cycle for a workload. The
+    mirage arm asks the library (mirage_model_sizes, mirage_plan); the reference
+    arm asks the oracle / synth (bit-exact with the library: tests/test_abi_cpu.py),
+    so the oracle arm never loads libmirage."""
+
+    def __init__(self, impl):
+        self.impl = impl
+
+    def sizes(self, shape):
+        if self.impl == "mirage":
+            from paper_2507_11507_b200 import _lib
+            S, _, BB = _lib.model_sizes(shape)
+            return S, BB
+        from synth import weights
+        return weights.layer_bytes(shape), shape.n_layers * shape.n_kv_heads * 2 * 16 * shape.head_dim * 2
+
+    def plan(self, n, alpha, beta):
+        if self.impl == "mirage":
+            from paper_2507_11507_b200 import _lib
+            cycle, _, b = _lib.plan(n, alpha, beta, 0, 1)
+        else:
+            from oracle import planner
+            cycle, _, b = planner.plan(n, alpha, beta, 0, 1)
+        return list(cycle), b
+
+
+def plan_cycle(sz, shape, alpha, beta, placement):
     if alpha == 0:
         return [], 0
     if placement == "uniform":   # PAPER.md §5.4 uniform-interval placement
-        cycle, m, b = _lib.plan(shape.n_layers, alpha, beta, 0, 1)
-        return cycle, b
+        return sz.plan(shape.n_layers, alpha, beta)
     m = alpha + beta             # last alpha layers reclaimed, the beta before them are slots
     return list(range(shape.n_layers - m, shape.n_layers)), beta
 
 
-def build_workload(args, rank, total_steps):
-    from paper_2507_11507_b200 import _lib
+def ppaper_batch(shape, S, BB, seed, total_steps, extra_blocks=0):
+    """C2 P-paper: the native pool of Table 1's 35% reservation
+    (PAPER.md:599) of GH200's 96 GB (:635) minus the active model's parameters;
+    the ShareGPT trace is admitted in order while it fits (+ extra_blocks)."""
+    from synth import weights, workload
+    params = shape.n_layers * S + weights.global_bytes(shape)
+    native = int((0.35 * 96e9 - params) // BB)
+    trace = workload.mid_generation_contexts(4096, seed=seed, max_ctx=shape.max_pos)
+    out, used = [], 0
+    for c in trace:
+        c = int(min(c, shape.max_pos - total_steps - 1))
+        nb = (c + total_steps + 15) // 16
+        if used + nb > native + extra_blocks:
+            break
+        out.append(c)
+        used += nb
+    return out, native
+
+
+def build_workload(args, rank, total_steps, impl="mirage"):
     from synth import models, workload
+    sz = Sizes(impl)
     cfg = args.config
-    if cfg in ("c2", "c4"):
-        if cfg == "c2":
+    if cfg in ("c2", "c2p", "c4"):
+        if cfg in ("c2", "c2p"):
             shape = models.OPT_13B
-            B = args.batch or 400
-            ctxs = workload.mid_generation_contexts(B, seed=args.seed + 1000 * rank, max_ctx=shape.max_pos)
-            ctxs = [int(min(c, shape.max_pos - total_steps - 1)) for c in ctxs]
             beta_pol = args.beta or 1
-            desc = ("C2: OPT-13B-shaped decode, ShareGPT-shaped contexts, {a} layer(s) remapped to KV "
-                    "({p} placement, beta={b}); native pool sized so the batch fits only with the reclaimed blocks")
             kernel = "paged_attention_kernel<128,1>"
+            if cfg == "c2":
+                B = args.batch or 400
+                ctxs = workload.mid_generation_contexts(B, seed=args.seed + 1000 * rank, max_ctx=shape.max_pos)
+                ctxs = [int(min(c, shape.max_pos - total_steps - 1)) for c in ctxs]
+                desc = ("C2: OPT-13B-shaped decode, ShareGPT-shaped contexts, {a} layer(s) remapped to KV "
+                        "({p} placement, beta={b}); native pool sized so the batch fits only with the reclaimed "
+                        "blocks")
+            else:
+                S0, BB0 = sz.sizes(shape)
+                cyc0, b0 = plan_cycle(sz, shape, args.alpha, beta_pol, args.placement)
+                gained = reclaimed_blocks(S0, BB0, cyc0[b0:])
+                ctxs, native0 = ppaper_batch(shape, S0, BB0, args.seed + 1000 * rank, total_steps, gained)
+                desc = ("C2 P-paper: OPT-13B-shaped decode at the paper's KV pressure (native pool = 35%% x 96 GB - "
+                        "params = %d blocks, PAPER.md:599/:635), ShareGPT-shaped trace admitted while it fits the "
+                        "native + reclaimed blocks; {a} layer(s) remapped ({p} placement, beta={b}); the PCIe link "
+                        "carries m*S per step: LINK-BOUND by construction (SURVEY §8(d))" % native0)
         else:
             shape = models.LLAMA3_8B
             B = args.batch or 32
@@ -354,8 +462,8 @@ def build_workload(args, rank, total_steps):
                     "{a} layer(s) remapped ({p} placement, beta={b}); native pool sized so the batch fits only "
                     "with the reclaimed blocks" % (B, L))
             kernel = "paged_attention_kernel<128,4>"
-        S, G, BB = _lib.model_sizes(shape)
-        cycle, beta = plan_cycle(shape, args.alpha, beta_pol, args.placement)
+        S, BB = sz.sizes(shape)
+        cycle, beta = plan_cycle(sz, shape, args.alpha, beta_pol, args.placement)
         reclaimed = reclaimed_blocks(S, BB, cycle[beta:])
         need = sum((c + total_steps + 15) // 16 for c in ctxs)
         tenants = [(shape, args.seed, need - reclaimed)]
@@ -366,11 +474,12 @@ def build_workload(args, rank, total_steps):
                                                           "native_blocks": need - reclaimed, "block_bytes": BB,
                                                           "layer_bytes": S}
     if cfg == "c3":
+        from synth import weights
         act, don = models.OPT_13B, models.LLAMA2_7B
-        Sa, Ga, BBa = _lib.model_sizes(act)
-        Sd, _, _ = _lib.model_sizes(don)
+        Sa, BBa = sz.sizes(act)
+        Sd, _ = sz.sizes(don)
         # Table 1 reservation on GH200's 96 GB (:635): 35% minus the active params
-        native = int((0.35 * 96e9 - (act.n_layers * Sa + Ga)) // BBa)
+        native = int((0.35 * 96e9 - (act.n_layers * Sa + weights.global_bytes(act))) // BBa)
         gained = reclaimed_blocks(Sd, BBa, range(don.n_layers))
         trace = workload.mid_generation_contexts(4096, seed=args.seed + 1000 * rank, max_ctx=act.max_pos)
         trace = [int(min(c, act.max_pos - total_steps - 1)) for c in trace]
@@ -407,7 +516,8 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
     from synth import workload
     B = len(ctxs)
     arena = harness.arena_for([(sh, nat) for sh, _, nat in tenants], B, max_ctx)
-    ctx = _lib.Context(arena, B, max_ctx, device=dev.index, flags=_lib.FLAG_TIME_ATTN)
+    ctx = _lib.Context(arena, B, max_ctx, device=dev.index,
+                       flags=_lib.FLAG_CUDA_GRAPHS if getattr(args, "graphs", False) else _lib.FLAG_TIME_ATTN)
     mids = [ctx.add_model(sh, blobs[(sh.name, seed)], nat) for sh, seed, nat in tenants]
     if args.weight_source == "device" and remaps:
         dev_copy = blobs[(tenants[0][0].name, tenants[0][1])].to(dev)
@@ -526,12 +636,21 @@ def run_mirage(args, rank, world):
     copy_peak_run = measure_copy_peak(torch, dev)
     t0 = time.time()
     blobs = {}
+    node = harness.gpu_numa_node(dev.index)
+    blob_info = {"numa_node": node, "shared": world > 1}
     for sh, seed, _ in wl.tenants:
         if world == 1:
-            blobs[(sh.name, seed)] = harness.make_blob(sh, seed=seed, model_idx=0, gen_device=dev)
-        else:  # replicas of one model share one page-locked host copy (PAPER.md:555 fn.)
-            blobs[(sh.name, seed)] = harness.shared_blob(sh, seed, 0, "bench", lr == 0,
-                                                         torch.distributed.barrier, gen_device=dev)
+            with harness.numa_bind(node):   # first touch on the GPU's own NUMA node
+                blobs[(sh.name, seed)] = harness.make_blob(sh, seed=seed, model_idx=0, gen_device=dev)
+        else:
+            # replicas share one page-locked host copy PER NUMA NODE (PAPER.md:555 fn.): the
+            # lowest local rank of each node writes it with its threads bound to that node
+            # (first-touch placement), so every GPU pulls over its own socket's PCIe root
+            nodes = [None] * world
+            torch.distributed.all_gather_object(nodes, (node, lr))
+            creator = lr == min(l for n, l in nodes if n == node)
+            blobs[(sh.name, seed)] = harness.shared_blob(sh, seed, 0, f"bench_n{node}", creator,
+                                                         torch.distributed.barrier, gen_device=dev, numa_node=node)
     setup_blob_s = time.time() - t0
     clock = ClockSampler(lr)
     res = run_arm(args, torch, dev, wl.tenants, wl.remaps, wl.ctxs, wl.max_ctx, blobs, args.steps, args.warmup,
@@ -557,7 +676,7 @@ def run_mirage(args, rank, world):
     e2e_med = statistics.median(res["e2e_ms"]) if res["e2e_ms"] else None
     attn_avg_ms = res["attn_ms"] / max(1, res["attn_launches"])
     attn_bytes_launch = res["attn_bytes"] / max(1, res["attn_launches"])
-    achieved = attn_bytes_launch / (attn_avg_ms * 1e-3) / 1e9
+    achieved = attn_bytes_launch / (attn_avg_ms * 1e-3) / 1e9 if attn_avg_ms > 0 else None
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "attention_traffic.json")))
@@ -571,19 +690,19 @@ def run_mirage(args, rank, world):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            o = oracle_leg(wl.tenants[0][0], wl.ctxs, n_seqs=2, seed=args.seed, steps=1)
-            cpu = {"value": o["tok_s"], "unit": "tok/s", "cores": o["cores"], "kind": "oracle", "sample": o["sample"],
-                   "host": host_cpu()}
-            try:
-                cpu["allocator"] = allocator_leg()
-            except Exception as e:
-                cpu["allocator"] = {"failed": str(e)[:200]}
-            try:
-                cpu["attention"] = attention_oracle_leg(wl.tenants[0][0], wl.ctxs, seed=args.seed)
-            except Exception as e:
-                cpu["attention"] = {"failed": str(e)[:200]}
+            with single_thread():
+                o = oracle_leg(wl.tenants[0][0], wl.ctxs, n_seqs=2, seed=args.seed, steps=1)
+                cpu = {"value": o["tok_s"], "unit": "tok/s", "cores": o["cores"] or 1, "kind": "oracle",
+                       "sample": o["sample"] + "; one thread", "host": host_cpu()}
+                for key, fn in (("allocator", allocator_leg),
+                                ("attention", lambda: attention_oracle_leg(wl.tenants[0][0], wl.ctxs, seed=args.seed)),
+                                ("c4_toy", c4_toy_leg)):
+                    try:
+                        cpu[key] = fn()
+                    except Exception as e:
+                        cpu[key] = {"failed": str(e)[:200]}
         except Exception as e:  # the CPU leg must not hide the GPU number
-            cpu = {"value": None, "unit": "tok/s", "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {e}"}
+            cpu = {"value": None, "unit": "tok/s", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
     step_med = statistics.median(res["step_ms"])
     h2d_gbs = res["h2d_bytes"] / (res["h2d_ms"] * 1e-3) / 1e9 if res["h2d_ms"] else None
     # predicted handoff stall of this cycle (the planner's timeline, mirage_predict_stall) from the
@@ -595,10 +714,7 @@ def run_mirage(args, rank, world):
         t_t = info["layer_bytes"] / (h2d_gbs * 1e9) * 1e9
         t_c = max(step_med - res["stall_ms"] / args.steps, 1e-3) / n_l * 1e6   # compute only, stall removed
         predicted_stall = L_.predict_stall(n_l, list(info["cycle"]), info["beta"], t_t, t_c) / 1e6
-    config = {"workload": wl.desc, "batch_per_gpu": B, "ctx_mean": sum(wl.ctxs) / B, "ctx_max": max(wl.ctxs),
-              "split_blocks": res["split_blocks"], "attention_units": res["units"],
-              "l2": "inputs larger than L2 (weights + KV read every step)", "parallelism": f"tenant-replica x{world}"}
-    config.update(info)
+    config = workload_config(wl, info, world)
     line = {
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_all / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -607,12 +723,12 @@ def run_mirage(args, rank, world):
         "config": config,
         "p99_tbt_ms": nearest_rank(res["step_ms"], 99), "p50_tbt_ms": nearest_rank(res["step_ms"], 50),
         "roofline": {"kernel": wl.kernel, "bound": "hbm", "achieved": achieved,
-                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
                      "algorithmic_bytes_per_launch": attn_bytes_launch, "avg_launch_ms": attn_avg_ms,
                      "launches": res["attn_launches"], "share_of_step": res["attn_ms"] / t_local,
                      "kernel_alone_gbs": res.get("alone_gbs"),
                      "copy_peak_this_run_gbs": copy_peak_run,
-                     "frac_of_copy_peak_this_run": achieved / copy_peak_run,
+                     "frac_of_copy_peak_this_run": achieved / copy_peak_run if achieved else None,
                      "kernel_alone_frac": (res["alone_gbs"] / hbm_peak) if res.get("alone_gbs") else None,
                      "peak_source": peak_src},
         "handoff": {"stall_ms_per_step": res["stall_ms"] / args.steps, "ready_waits": res["stall_waits"],
@@ -629,14 +745,29 @@ def run_mirage(args, rank, world):
                 "ms_per_step": e2e_med, "how": "host-timed mirage_decode_step with host token/position arrays, "
                                                "argmax read back to host and stream sync every step"},
         "gpu_launches": res["launches"], "setup_blob_s": setup_blob_s,
+        "kernel_plan": {"split_blocks": res["split_blocks"], "attention_units": res["units"]},
+        "host_blob": blob_info,
     }
     print(json.dumps(line), flush=True)
 
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `bench.py --gpus N` outside torchrun: start the N ranks ourselves, the way the
+        # driver does (one process per GPU, rendezvous on 127.0.0.1)
+        import socket
+        so = socket.socket()
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+        so.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     if world > 1:
         # replicas share nothing on the data path; the bench's own barrier and
         # max-over-ranks reduction are tiny host-side collectives (gloo)

@@ -70,10 +70,60 @@ def make_shard_blob(shape, rank, tp, seed=0, model_idx=0):
     return blob
 
 
-def shared_blob(shape, seed, model_idx, tag, creator, barrier, gen_device="cpu"):
-    """A weight blob in a file mapping shared by all replicas on the node (the
-    paper's single host copy of the parameters, PAPER.md:555 fn.), page-locked in
-    every process. `creator` (local rank 0) generates it; `barrier()` syncs."""
+def gpu_numa_node(index):
+    """NUMA node of CUDA device `index` (its PCI function's numa_node in sysfs;
+    0 when unknown or on a single-node host)."""
+    try:
+        p = torch.cuda.get_device_properties(index)
+        path = "/sys/bus/pci/devices/%04x:%02x:%02x.0/numa_node" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+        return max(0, int(open(path).read().strip()))
+    except Exception:
+        return 0
+
+
+def _node_cpus(node):
+    out = set()
+    try:
+        for part in open(f"/sys/devices/system/node/node{node}/cpulist").read().strip().split(","):
+            lo, _, hi = part.partition("-")
+            out.update(range(int(lo), int(hi or lo) + 1))
+    except Exception:
+        pass
+    return out
+
+
+class numa_bind:
+    """Bind the calling thread to the CPUs of NUMA node `node` for the block, so
+    host pages it first-touches (a pinned blob's allocation, a shared blob's
+    writes) land on that node; restores the previous affinity."""
+
+    def __init__(self, node):
+        self.cpus = _node_cpus(node) if node is not None else set()
+
+    def __enter__(self):
+        import os
+        self.prev = None
+        if self.cpus and hasattr(os, "sched_setaffinity"):
+            try:
+                self.prev = os.sched_getaffinity(0)
+                os.sched_setaffinity(0, self.cpus & self.prev or self.cpus)
+            except OSError:
+                self.prev = None
+        return self
+
+    def __exit__(self, *exc):
+        import os
+        if self.prev is not None:
+            os.sched_setaffinity(0, self.prev)
+        return False
+
+
+def shared_blob(shape, seed, model_idx, tag, creator, barrier, gen_device="cpu", numa_node=None):
+    """A weight blob in a file mapping shared by the replicas of one NUMA node
+    (the paper's single host copy of the parameters, PAPER.md:555 fn., kept
+    local to the socket whose PCIe root the GPUs use), page-locked in every
+    process. `creator` generates it with its thread bound to `numa_node`;
+    `barrier()` syncs."""
     import os
     S, G, _ = _lib.model_sizes(shape)
     n = shape.n_layers * S + G
@@ -87,11 +137,12 @@ def shared_blob(shape, seed, model_idx, tag, creator, barrier, gen_device="cpu")
     if creator:
         with open(path, "wb") as f:
             f.truncate(n)
-        t = torch.from_file(path, shared=True, size=n, dtype=torch.uint8)
-        for l in range(shape.n_layers):
-            t[l * S:(l + 1) * S].copy_(layer_bytes_tensor(shape, l, seed, model_idx, gen_device))
-        t[shape.n_layers * S:].copy_(global_bytes_tensor(shape, seed, model_idx, gen_device))
-        del t
+        with numa_bind(numa_node):
+            t = torch.from_file(path, shared=True, size=n, dtype=torch.uint8)
+            for l in range(shape.n_layers):
+                t[l * S:(l + 1) * S].copy_(layer_bytes_tensor(shape, l, seed, model_idx, gen_device))
+            t[shape.n_layers * S:].copy_(global_bytes_tensor(shape, seed, model_idx, gen_device))
+            del t
     barrier()
     t = torch.from_file(path, shared=True, size=n, dtype=torch.uint8)
     _lib.host_register(t)

@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <numeric>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -214,13 +215,22 @@ struct Model {
   uint64_t attn_bytes = 0;
   uint64_t last_meta = 0;
   int32_t last_units = 0, last_split = 0;
-  // ---- CUDA graphs of the decode step (MIRAGE_FLAG_CUDA_GRAPHS, models without a cycle) ----
+  // ---- CUDA graphs of the decode step (MIRAGE_FLAG_CUDA_GRAPHS) ----
+  // Key: batch size and, for a streaming cycle, the slot parity of the step's first
+  // use (uses % lcm(m, beta)): the slots and copy sources of a step repeat with it.
+  // A graph of a cycling model holds the copy stream's re-streaming DMAs as a
+  // captured branch (fork on the free events, join before the graph ends).
   struct Graph {
     cudaGraphExec_t exec;
     int64_t kernels;
   };
-  std::map<int, Graph> graphs;  // by batch size
-  std::set<int> graph_seen;     // batch sizes run once eagerly (plans/autotune done)
+  std::map<int64_t, Graph> graphs;
+  std::set<int64_t> graph_seen;  // keys run once eagerly (plans/autotune done)
+  cudaEvent_t join_ev = nullptr; // the copy branch rejoins the compute stream at the end of a capture
+  // slot events used inside captures (an event recorded in a capture cannot be
+  // waited on outside it, so the eager ready/free events stay separate)
+  std::vector<cudaEvent_t> cap_ready_ev, cap_free_ev;
+  uint64_t graph_copies = 0;     // re-streaming DMAs run inside graphs (not individually timed)
   // ---- tensor parallelism over peer memory (MIRAGE_FLAG_TP_IPC) ----
   char* xfer = nullptr;               // [flag u64 | pad][partial par 0][partial par 1]
   size_t xfer_part = 0;               // bytes of one partial buffer (max_batch * d * 4)
@@ -321,10 +331,13 @@ int32_t fail(mirage_ctx* c, int32_t code, const char* fmt, ...) {
                   __LINE__);                                                                       \
   } while (0)
 
+// every call makes the ctx's device current on the calling thread (a process may
+// drive several GPUs, e.g. a peer-HBM weight source on another device)
 #define GUARD(ctx)                                                      \
   do {                                                                  \
     if (!(ctx)) return MIRAGE_ERR_CONFIG;                               \
     if ((ctx)->sticky) return (ctx)->sticky;                            \
+    if (!(ctx)->host_only) cudaSetDevice((ctx)->cfg.device);            \
   } while (0)
 
 Shape shape_of(const mirage_model_cfg* m) {
@@ -597,6 +610,25 @@ void harvest_attn_times(Model* M) {
   (void)cudaGetLastError();
 }
 
+// MIRAGE_COPY_MODE (experiment): 0 = cudaMemcpyAsync on the copy stream (default),
+// 1 = cudaMemcpyBatchAsync with cudaMemcpyFlagPreferOverlapWithCompute
+int copy_mode() {
+  static const int v = getenv("MIRAGE_COPY_MODE") ? atoi(getenv("MIRAGE_COPY_MODE")) : 0;
+  return v;
+}
+
+// The captured graphs of M bake in its weight/slot pointers and copy sources:
+// drop them whenever its cycle or weight source changes.
+void drop_graphs(Model* M) {
+  for (auto& g : M->graphs) cudaGraphExecDestroy(g.second.exec);
+  M->graphs.clear();
+  M->graph_seen.clear();
+  for (auto e : M->cap_ready_ev) cudaEventDestroy(e);
+  for (auto e : M->cap_free_ev) cudaEventDestroy(e);
+  M->cap_ready_ev.clear();
+  M->cap_free_ev.clear();
+}
+
 int prefetch_debug() {
   static const int v = getenv("MIRAGE_PREFETCH_DEBUG") ? atoi(getenv("MIRAGE_PREFETCH_DEBUG")) : 0;
   return v;
@@ -845,7 +877,8 @@ void mirage_destroy(mirage_ctx* c) {
       cudaEventDestroy(t.t1);
     }
     for (auto e : M->ev_pool) cudaEventDestroy(e);
-    for (auto& g : M->graphs) cudaGraphExecDestroy(g.second.exec);
+    drop_graphs(M);
+    if (M->join_ev) cudaEventDestroy(M->join_ev);
     for (size_t r = 0; r < M->peer_base.size(); ++r)
       if (M->peer_base[r] && M->peer_base[r] != M->xfer) cudaIpcCloseMemHandle(M->peer_base[r]);
     if (M->xfer) cudaFree(M->xfer);
@@ -1060,6 +1093,7 @@ int32_t mirage_set_weight_source(mirage_ctx* c, int32_t model, const void* src, 
     CK(c, cudaStreamSynchronize(c->xs));  // no copy from the old source is in flight
   }
   M->host = reinterpret_cast<const char*>(src);
+  drop_graphs(M);  // captured copies read the old source
   return MIRAGE_OK;
 }
 
@@ -1214,6 +1248,7 @@ int32_t mirage_remap_layers(mirage_ctx* c, int32_t donor, int32_t recipient, con
       D->ready_ev.push_back(a);
       D->free_ev.push_back(b);
     }
+    if (beta > 0) drop_graphs(D);
   }
   if (gained && !c->host_only) CK(c, cudaStreamSynchronize(c->cs));  // the host staging above is a pageable vector
   if (blocks_gained) *blocks_gained = gained;
@@ -1306,6 +1341,7 @@ int32_t mirage_unremap(mirage_ctx* c, int32_t recipient, int32_t region) {
     }
     D->ready_ev.clear();
     D->free_ev.clear();
+    drop_graphs(D);
   }
   return MIRAGE_OK;
 }
@@ -1589,12 +1625,16 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   static const int dbg_nowait = prefetch_debug() == 2 || prefetch_debug() == 3;
   bool reloading = false;
   for (char r : M->reload_pending) reloading |= r != 0;
+  bool capturing = false;  // this step's body is being captured into a CUDA graph
   auto gate = [&](int l) -> int32_t {  // wait until layer l's weights are in its slot
     if (reloading && l < s.n && M->reload_pending[l]) {  // an asynchronous reload (mirage_unremap)
       if (!dbg_nowait) CK(c, cudaStreamWaitEvent(cs, M->reload_ev[l], 0));
       M->reload_pending[l] = 0;
     }
-    if (!dbg_nowait && l < s.n && use_of[l] >= beta && use_of[l] >= 0) {
+    // (inside a graph capture, a copy issued by an earlier step is covered by the
+    // pre-capture waits and, on replays, by the previous graph's joined copy branch)
+    const bool prior_copy = use_of[l] - beta < (int64_t)M->uses;
+    if (!dbg_nowait && l < s.n && use_of[l] >= beta && use_of[l] >= 0 && !(capturing && prior_copy)) {
       if (c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) {  // measured stall of this handoff
         Model::AttnTiming t{pool_event(M), pool_event(M), 0};
         CK(c, cudaEventRecord(t.t0, cs));
@@ -1602,7 +1642,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
         CK(c, cudaEventRecord(t.t1, cs));
         M->stall_pending.push_back(t);
       } else {
-        CK(c, cudaStreamWaitEvent(cs, M->ready_ev[use_of[l] % beta], 0));
+        CK(c, cudaStreamWaitEvent(cs, (capturing ? M->cap_ready_ev : M->ready_ev)[use_of[l] % beta], 0));
       }
     }
     if (M->slot_tag && l < s.n && use_of[l] >= 0)  // SLOT_TAGS: the slot must hold layer l now
@@ -1615,47 +1655,89 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     const int slot = (int)(u % beta);
     M->slot_log.insert(M->slot_log.end(),
                        {(int64_t)u, M->cyc_steps, l, slot, (int64_t)(u >= (uint64_t)beta)});
-    CK(c, cudaEventRecord(M->free_ev[slot], cs));
+    cudaEvent_t fev = (capturing ? M->cap_free_ev : M->free_ev)[slot];
+    CK(c, cudaEventRecord(fev, cs));
     const uint64_t nu = u + beta;
     const int nl = M->cycle[nu % m];
-    CK(c, cudaStreamWaitEvent(c->xs, M->free_ev[slot], 0));
-    CopyTiming t{pool_event(M), pool_event(M), M->sz.S};
-    if (!t.t0 || !t.t1) return fail(c, MIRAGE_ERR_CUDA, "release: event pool");
-    CK(c, cudaEventRecord(t.t0, c->xs));
+    CK(c, cudaStreamWaitEvent(c->xs, fev, 0));  // (in a capture: forks the copy branch)
+    CopyTiming t{nullptr, nullptr, M->sz.S};
+    if (!capturing) {  // copy timing events are per step: eager steps only
+      t = CopyTiming{pool_event(M), pool_event(M), M->sz.S};
+      if (!t.t0 || !t.t1) return fail(c, MIRAGE_ERR_CUDA, "release: event pool");
+      CK(c, cudaEventRecord(t.t0, c->xs));
+    }
     const int dbg_mode = prefetch_debug();
     if (dbg_mode == 3 || dbg_mode == 4) KL(c, mirage::launch_spin(20000000ull, c->xs));  // a slow link
-    if (dbg_mode != 1)  // experiment hook: 1 = events only, no DMA
-      CK(c, cudaMemcpyAsync(M->w_dev + (uint64_t)M->cycle[slot] * M->sz.S,
-                            M->host + (uint64_t)nl * M->sz.S, M->sz.S, cudaMemcpyDefault, c->xs));
+    if (dbg_mode != 1) {  // experiment hook: 1 = events only, no DMA
+      void* dst = M->w_dev + (uint64_t)M->cycle[slot] * M->sz.S;
+      const void* src = M->host + (uint64_t)nl * M->sz.S;
+      if (copy_mode() == 1) {  // batch API with the overlap-with-compute hint (CUDA 12.8+)
+        void* dsts[1] = {dst};
+        void* srcs[1] = {const_cast<void*>(src)};
+        size_t sizes[1] = {M->sz.S}, aidx[1] = {0}, fail_idx = 0;
+        cudaMemcpyAttributes at{};
+        at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+        CK(c, cudaMemcpyBatchAsync(dsts, srcs, sizes, 1, &at, aidx, 1, &fail_idx, c->xs));
+      } else {
+        CK(c, cudaMemcpyAsync(dst, src, M->sz.S, cudaMemcpyDefault, c->xs));
+      }
+    }
     if (M->slot_tag)  // same stream, after the weights: a correct tag proves they landed
       CK(c, cudaMemcpyAsync(M->slot_tag + slot, M->host_tags + nl, 4, cudaMemcpyHostToDevice, c->xs));
-    CK(c, cudaEventRecord(t.t1, c->xs));
-    CK(c, cudaEventRecord(M->ready_ev[slot], c->xs));
-    M->pending.push_back(t);
+    if (!capturing) {
+      CK(c, cudaEventRecord(t.t1, c->xs));
+      M->pending.push_back(t);
+    } else {
+      M->graph_copies += 1;
+    }
+    CK(c, cudaEventRecord((capturing ? M->cap_ready_ev : M->ready_ev)[slot], c->xs));
     return MIRAGE_OK;
   };
 
   // CUDA graph of the step body (embed ... argmax): models without a streaming
   // cycle, one graph per batch size, captured on the second step of that size
   // (the first runs eagerly so cuBLASLt plans/autotuning happen outside capture)
-  const bool graphable = (c->cfg.flags & MIRAGE_FLAG_CUDA_GRAPHS) && m == 0 && !reloading && qp == 1 &&
-                         !(c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) && !M->tp_ready;
+  const bool graphable = (c->cfg.flags & MIRAGE_FLAG_CUDA_GRAPHS) && !reloading && qp == 1 &&
+                         !(c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) && !M->tp_ready && !dbg_nowait &&
+                         prefetch_debug() == 0 && !M->slot_tag;
   if (c->tp > 1 && !c->nccl && !M->tp_ready)
     return fail(c, MIRAGE_ERR_STATE, "step: tensor parallel model without a collective (tp_import first)");
-  bool body_done = false, capturing = false;
+  bool body_done = false;
   int64_t l0 = 0;
+  const int64_t par_period = m ? (int64_t)std::lcm(m, beta) : 1;
+  const int64_t gkey = (int64_t)B * 64 + (m ? (int64_t)(M->uses % par_period) : 0);
   if (graphable) {
-    auto g = M->graphs.find(B);
+    auto g = M->graphs.find(gkey);
+    if (g != M->graphs.end() || M->graph_seen.count(gkey)) {
+      // a cycling model: copies issued by earlier (eager) steps must land before the graph
+      for (int sl = 0; sl < beta; ++sl) CK(c, cudaStreamWaitEvent(cs, M->ready_ev[sl], 0));
+    }
     if (g != M->graphs.end()) {
       CK(c, cudaGraphLaunch(g->second.exec, cs));
       c->launches += g->second.kernels;
       body_done = true;
-    } else if (M->graph_seen.count(B)) {
+      // host bookkeeping of the replayed step: the slot log and the copy count
+      for (int l = 0; l < s.n; ++l)
+        if (use_of[l] >= 0) {
+          const uint64_t u = (uint64_t)use_of[l];
+          M->slot_log.insert(M->slot_log.end(),
+                             {(int64_t)u, M->cyc_steps, l, (int64_t)(u % beta), (int64_t)(u >= (uint64_t)beta)});
+          M->graph_copies += 1;
+        }
+    } else if (M->graph_seen.count(gkey)) {
+      while ((int)M->cap_ready_ev.size() < beta) {
+        cudaEvent_t a, b;
+        CK(c, cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CK(c, cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        M->cap_ready_ev.push_back(a);
+        M->cap_free_ev.push_back(b);
+      }
       CK(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
       capturing = true;
       l0 = c->launches;
     } else {
-      M->graph_seen.insert(B);
+      M->graph_seen.insert(gkey);
     }
   }
   if (!body_done) {
@@ -1778,12 +1860,17 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   if (int32_t e = gemm_lt(c, B, s.V, d, gw.lm_head, M->x, M->y, 0, nullptr, 0)) return e;
   KL(c, mirage::launch_argmax(B, s.V, M->y, M->argmax, cs));
   if (capturing) {
+    if (m) {  // rejoin the copy branch: the graph ends when its DMAs have landed
+      if (!M->join_ev) CK(c, cudaEventCreateWithFlags(&M->join_ev, cudaEventDisableTiming));
+      CK(c, cudaEventRecord(M->join_ev, c->xs));
+      CK(c, cudaStreamWaitEvent(cs, M->join_ev, 0));
+    }
     cudaGraph_t graph;
     CK(c, cudaStreamEndCapture(cs, &graph));
     cudaGraphExec_t exec;
     CK(c, cudaGraphInstantiate(&exec, graph, 0));
     cudaGraphDestroy(graph);
-    M->graphs[B] = Model::Graph{exec, c->launches - l0};
+    M->graphs[gkey] = Model::Graph{exec, c->launches - l0};
     CK(c, cudaGraphLaunch(exec, cs));
   }
   }  // !body_done

@@ -48,3 +48,32 @@ def test_cpu_baseline_extras():
     from synth import models
     at = b.attention_oracle_leg(models.TOY, [20, 33, 5], n_seqs=3)
     assert at["kv_gbs"] > 0
+
+
+def test_reference_arm_never_loads_the_library():
+    """--impl reference runs the oracle only: building its workload and timing the
+    oracle must not load libmirage (the arm is compared against the product)."""
+    import subprocess
+    import sys
+    code = ("import sys, json; sys.argv=['bench.py','--impl','reference','--steps','1','--warmup','0','--config',"
+            "'c2','--batch','4']; import importlib.util as u; s=u.spec_from_file_location('b','%s/bench.py'); "
+            "b=u.module_from_spec(s); s.loader.exec_module(b); a=b.parse(); wl,info=b.build_workload(a,0,3,'reference');"
+            "print(json.dumps({'libs':[m for m in sys.modules if 'paper_2507' in m],'cycle':info['cycle']}))" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    import json
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["libs"] == [] and d["cycle"] == [0, 20]
+
+
+def test_both_arms_report_the_same_config():
+    b = load_bench()
+
+    class A:
+        config, batch, ctx, alpha, beta, placement, seed = "c2", 8, 0, 1, 0, "uniform", 0
+    wl_m, info_m = b.build_workload(A, 0, 10, "mirage")
+    wl_r, info_r = b.build_workload(A, 0, 10, "reference")
+    assert b.workload_config(wl_m, info_m, 1) == b.workload_config(wl_r, info_r, 1)
+    A.config = "c2p"
+    wl_p, info_p = b.build_workload(A, 0, 10, "reference")
+    assert 20 <= len(wl_p.ctxs) <= 40          # SURVEY §8(d): the P-paper pressure admits ~29 sequences

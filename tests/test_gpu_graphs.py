@@ -68,3 +68,39 @@ def test_graphs_cut_small_batch_step_time():
         ctx.sync()
         times[flags] = min(best, (time.perf_counter() - t0) / 30)
     assert times[_lib.FLAG_CUDA_GRAPHS] < times[0]
+
+
+def run_cycle(flags, shape, cycle, beta, steps, B=4, unremap_at=None):
+    from paper_2507_11507_b200 import Context
+    ctx = Context(harness.arena_for([(shape, 64)], 8, 256), 8, 256, flags=flags)
+    mid = ctx.add_model(shape, harness.make_blob(shape, seed=4), B)   # KV lands in reclaimed memory
+    ctx.remap_layers(mid, mid, cycle, beta)
+    hid = torch.empty((B, shape.d_model), dtype=torch.bfloat16, device="cuda")
+    outs = []
+    for t in range(steps):
+        if t % 16 == 0:
+            for s in range(B):
+                ctx.alloc_blocks(mid, s, 1)
+        am = ctx.decode_step(mid, list(range(B)), [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)],
+                             [t] * B, hidden_out=hid)
+        ctx.sync()
+        outs.append((hid.float().cpu().numpy().copy(), list(am)))
+    log = ctx.slot_log(mid)
+    return outs, log, ctx.kernel_launches()
+
+
+@pytest.mark.parametrize("cycle,beta", [([0, 2], 1), ([0, 2, 3], 1), ([0, 1, 3], 2), ([1, 2, 3], 2)])
+def test_streaming_cycle_graph_replays_bit_identical(cycle, beta):
+    """a0 with a streaming cycle: the copy-stream DMAs are a captured branch of the
+    step graph (fork on the slot-free events, join at the end); m mod beta != 0
+    ([0,1,3] with beta 2) alternates the slot parity, so two graphs alternate.
+    Replays equal eager steps bit for bit, with the same slot log (oracle c5 order)."""
+    from paper_2507_11507_b200 import _lib
+    from oracle import timeline as OT
+    shape = models.TOY_LLAMA.with_layers(4)
+    a, la_log, la = run_cycle(0, shape, cycle, beta, 24)
+    b, lb_log, lb = run_cycle(_lib.FLAG_CUDA_GRAPHS, shape, cycle, beta, 24)
+    for t, ((ha, aa), (hb, ab)) in enumerate(zip(a, b)):
+        assert np.array_equal(ha, hb) and aa == ab, t
+    assert la_log == lb_log == [(k, st, l, sl, int(cp)) for k, st, l, sl, cp in OT.slot_log(cycle, beta, 24)]
+    assert la == lb

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--ctx", type=int, default=4096)
     ap.add_argument("--graphs", action="store_true", help="MIRAGE_FLAG_CUDA_GRAPHS (no attention timing)")
+    ap.add_argument("--alpha", type=int, default=0, help="remapped layers per rank (planner, uniform placement)")
+    ap.add_argument("--beta", type=int, default=2)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     B, L0 = a.batch, a.ctx
@@ -40,6 +42,10 @@ def main():
         blob = harness.make_blob(shape, seed=3, gen_device=dev)
         ctx = _lib.Context(arena, B, max_ctx, flags=_lib.FLAG_CUDA_GRAPHS if a.graphs else _lib.FLAG_TIME_ATTN)
         mid = ctx.add_model(shape, blob, nblk)
+        cycle = []
+        if a.alpha:   # alpha = 1, beta = 2 per rank
+            cycle, _, beta = _lib.plan(shape.n_layers, a.alpha, a.beta, 0, 1)
+            ctx.remap_layers(mid, mid, cycle, beta)
         for s in range(B):
             ctx.alloc_blocks(mid, s, harness.blocks_for(L0 + a.steps + 8))
             ctx.fill_kv(mid, s, L0, seed=s)
@@ -66,7 +72,7 @@ def main():
         ar_bytes = 2 * shape.n_layers * B * shape.d_model * 4
         print(json.dumps({
             "tp": tp, "shape": {"n_heads": shape.n_heads, "n_kv_heads": shape.n_kv_heads, "ffn": shape.ffn_dim},
-            "batch": B, "ctx": L0, "cuda_graphs": a.graphs, "step_ms": round(ms, 3), "tok_s_per_rank_group": round(B / (ms / 1e3), 1),
+            "batch": B, "ctx": L0, "cuda_graphs": a.graphs, "cycle": cycle, "step_ms": round(ms, 3), "tok_s_per_rank_group": round(B / (ms / 1e3), 1),
             "attention_ms_per_step": round(attn_ms, 3), "attention_share": round(attn_ms / ms, 3),
             "attention_gbs": round(attn_bytes / (attn_ms / launches * 1e-3) / 1e9, 1),
             "weights_gb_per_rank": round((shape.n_layers * S + G) / 1e9, 2),
