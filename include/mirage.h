@@ -68,9 +68,14 @@ extern "C" {
                                   * the first kernel of a cycled layer a check kernel
                                   * compares it (mirage_stats.slot_tag_errors).      */
 #define MIRAGE_FLAG_CUDA_GRAPHS 8u /* init flag: capture the decode-step body (embed .. argmax)
-                                    * into one CUDA graph per batch size for models without
-                                    * a streaming cycle (captured on the second step of a
-                                    * size; ignored with MIRAGE_FLAG_TIME_ATTN)          */
+                                    * into CUDA graphs, one per batch size and, for a
+                                    * streaming cycle, per slot parity (uses mod
+                                    * lcm(m, beta)); the re-streaming DMAs are a captured
+                                    * branch forked from the slot-free events and joined
+                                    * before the graph ends (captured on the second step
+                                    * of a key; ignored with MIRAGE_FLAG_TIME_ATTN,
+                                    * MIRAGE_FLAG_SLOT_TAGS, during reloads and for
+                                    * prefill steps)                                     */
 #define MIRAGE_FLAG_TP_IPC 16u /* init flag: tensor parallelism without NCCL: after
                                 * mirage_tp_export/import, each partial O-/down-projection
                                 * is summed by one kernel that reads the peers' partials
@@ -83,6 +88,16 @@ extern "C" {
                                 * still read a reclaimed layer as weights would produce NaN.
                                 * Blocks carry KV before they are read, so outputs are
                                 * unchanged.                                               */
+#define MIRAGE_FLAG_TC_GEMM 64u /* init flag: the row-parallel projections (O-proj and
+                                 * FC2/down, batch <= 256) run on the library's tcgen05
+                                 * decode GEMM (see mirage_decode_gemm) instead of
+                                 * cuBLASLt; its split-K slices are summed in fixed order
+                                 * by the residual kernel. With MIRAGE_FLAG_TP_IPC the
+                                 * GEMM's epilogue stores each partial tile straight into
+                                 * every rank's exchange buffer and bumps that rank's
+                                 * arrival counter (GEMM fused with a one-shot all-reduce,
+                                 * SURVEY NEXT-4); the consumer then reads only local
+                                 * memory, in fixed rank order.                        */
 #define MIRAGE_FLAG_HOST_ONLY 2u /* init flag: no device; allocator/remap/table/query
                                   * calls only (the arena pointer is used for address
                                   * arithmetic, never dereferenced); device calls
@@ -426,6 +441,17 @@ int32_t mirage_host_unregister(void* ptr);
 
 /* Number of kernels this ctx has launched (its own kernels, not cuBLAS). */
 int64_t mirage_kernel_launches(const mirage_ctx* ctx);
+
+/* Test/bench hook: the decode GEMM of the step on the 5th-generation tensor
+ * cores (tcgen05 + TMEM, TMA-fed; SURVEY §8(a) a6 supporting row, NEXT-4):
+ * Y_s[b][n] = sum over split s's share of K of X[b][k] * W[n][k], for
+ * W = w_dev bf16 [N][K] and X = x_dev bf16 [B][K] (row-major, device memory,
+ * K % 8 == 0, 1 <= B <= 256), written to y_dev fp32 [splits][B][N]; the splits
+ * partition K in order and sum to Y. splits = 0 picks the library's choice
+ * (about one wave of CTAs) and reports it in *splits_out. Enqueued on `stream`
+ * (a cudaStream_t; NULL = legacy default stream). Errors: RANGE, CUDA. */
+int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
+                           float* y_dev, int32_t splits, int32_t* splits_out);
 
 /* Profiling hook. With the environment variable MIRAGE_ATTN_TRACE set when the
  * ctx is created, every attention launch of mirage_attn_only records 16

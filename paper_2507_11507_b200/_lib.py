@@ -25,6 +25,7 @@ FLAG_SLOT_TAGS = 4
 FLAG_CUDA_GRAPHS = 8
 FLAG_TP_IPC = 16
 FLAG_POISON = 32
+FLAG_TC_GEMM = 64
 MAX_CYCLE = 256
 
 _NAMES = {ERR_CONFIG: "CONFIG", ERR_CAPACITY: "CAPACITY", ERR_RANGE: "RANGE", ERR_STATE: "STATE",
@@ -113,6 +114,7 @@ def _load():
         "mirage_write_kv": (I32, [P, I32, I64, I32, P]),
         "mirage_kernel_launches": (I64, [P]),
         "mirage_attn_trace": (I32, [P, pU64, I32, pI32]),
+        "mirage_decode_gemm": (I32, [P, P, I32, I32, P, I32, P, I32, pI32]),
         "mirage_nccl_unique_id": (I32, [P]),
         "mirage_host_register": (I32, [P, U64]),
         "mirage_region_count": (I32, [P, I32, pI32]),
@@ -143,7 +145,7 @@ EXPORTED = [
     "mirage_host_register", "mirage_host_unregister", "mirage_region_count", "mirage_region_info",
     "mirage_unremap", "mirage_swap_out", "mirage_swap_in", "mirage_set_weight_source", "mirage_tp_export",
     "mirage_tp_import", "mirage_prefill", "mirage_migrate_region", "mirage_predict_stall",
-    "mirage_attn_trace"]
+    "mirage_attn_trace", "mirage_decode_gemm"]
 
 
 def model_cfg(shape):
@@ -189,6 +191,24 @@ def predict_stall(n_layers, cycle, beta, t_transfer_ns, t_compute_layer_ns):
     if rc:
         raise MirageError(rc, "predict_stall")
     return out.value
+
+
+def decode_gemm(w, x, splits=0, stream=None):
+    """Y slices [splits][B][N] fp32 of x [B][K] @ w[N][K]^T on the tcgen05 decode GEMM
+    (mirage_decode_gemm); both bf16 CUDA tensors. Returns (slices, splits)."""
+    assert w.dtype == torch.bfloat16 and x.dtype == torch.bfloat16 and w.is_cuda and x.is_cuda
+    w, x = w.contiguous(), x.contiguous()
+    N, K = w.shape
+    B = x.shape[0]
+    n = splits or 16
+    y = torch.empty((n, B, N), dtype=torch.float32, device=w.device)
+    got = C.c_int32()
+    st = stream if stream is not None else torch.cuda.current_stream(w.device)
+    rc = LIB.mirage_decode_gemm(st.cuda_stream, w.data_ptr(), N, K, x.data_ptr(), B, y.data_ptr(), int(splits),
+                                C.byref(got))
+    if rc:
+        raise MirageError(rc, "decode_gemm")
+    return y[: got.value], got.value
 
 
 def nccl_unique_id():

@@ -17,7 +17,7 @@ except Exception:  # pragma: no cover
     NCCL_DIR = "/usr"
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I" + os.path.join(NCCL_DIR, "include")]
-SOURCES = ["attention.cu", "layer_kernels.cu", "runtime.cpp", "planner.cpp"]
+SOURCES = ["attention.cu", "decode_gemm.cu", "layer_kernels.cu", "runtime.cpp", "planner.cpp"]
 
 
 def _compile(src):

@@ -1,0 +1,339 @@
+// Decode GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+//   Y[b][n] = sum_k X[b][k] * W[n][k]      (y = x W^T; W row-major [N][K] bf16, X [B][K] bf16)
+//
+// A decode step multiplies a skinny activation block (B rows, B <= 256) by the
+// layer's weights, so the GEMM is weight-streaming bound (AI ~ B flop/B). It is
+// computed swapped, Y^T = W X^T: the 128 weight rows of a tile are the MMA's M
+// side and the batch is its N side (N = B rounded up to 16), so one
+// tcgen05.mma.cta_group::1.kind::f16 M=128 x N=Bn x K=16 consumes 4 KB of weights
+// straight from shared memory while the fp32 accumulator tile lives in TMEM
+// (128 lanes x Bn columns).
+//
+// One CTA = one (128-row tile, K split). Warp roles: lane 0 of warp 0 issues the
+// TMA loads (cp.async.bulk.tensor, 128B swizzle: 128 x 64 weight box + Bn x 64
+// activation box per stage, an NS-deep full/empty mbarrier ring); lane 0 of warp
+// 1 issues the MMAs (4 per stage, K = 16 each) and releases a stage with
+// tcgen05.commit; warp 2 owns the TMEM allocation. After the last commit all 4
+// warps drain TMEM (tcgen05.ld 32x32b: warp w reads lanes 32w..32w+31 = rows of
+// the tile) and store the split's fp32 slice Y_s[b][n]. Split slices are summed
+// in fixed order by the consumer (the residual kernel), so results are
+// deterministic; with `peer` destinations the epilogue writes the slice straight
+// into every tensor-parallel rank's exchange buffer (the fused all-reduce, a10).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "kernels.cuh"
+
+namespace mirage {
+namespace {
+
+constexpr int kTileM = 128;  // weight rows per tile (MMA M)
+constexpr int kTileK = 64;   // K per stage: one 128-byte swizzle row of bf16
+// ring depth: ~96-104 KB of stages per CTA, so two CTAs share an SM (two tiles
+// streaming per SM: the grid of a decode GEMM is ~1-2 waves of small tiles)
+template <int BN>
+constexpr int stages() { return BN <= 32 ? 5 : (BN <= 64 ? 4 : (BN <= 128 ? 3 : 2)); }
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          su32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(su32(bar))
+      : "memory");
+}
+// UMMA shared-memory descriptor, K-major operand in the 128B-swizzle canonical
+// layout (rows of 128 bytes, 8-row groups 1024 bytes apart): start >> 4 in
+// [0,14), LBO = 1 (unused for swizzled K-major) in [16,30), SBO = 1024 >> 4 in
+// [32,46), version 1 (Blackwell) at 46, layout SWIZZLE_128B (2) in [61,64).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+
+// Instruction descriptor, kind::f16: D fp32 (bits 4-5 = 1), A and B bf16 (7-9 = 1,
+// 10-12 = 1), both K-major (15, 16 = 0), N >> 3 in [17,23), M >> 4 in [24,29).
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+struct GemmArgs {
+  float* out;          // split s, row b, column n at out + s * slice + b * ldo + n
+  long long slice;     // floats between split slices
+  int ldo, N, K, B;
+  int kb_per_split;    // 64-wide K blocks per split
+  int n_kb;            // total K blocks
+  // fused tensor-parallel epilogue: also store the slice into every rank's exchange
+  // buffer (peer pointers); peer_slot = this rank's slot offset (floats) there
+  float* const* peers;
+  int n_peers;
+  long long peer_slot;
+  // arrival counters bumped (release, system scope) once the CTA's stores landed:
+  // one per destination rank of a fused tensor-parallel GEMM
+  unsigned long long* const* cnt;
+  int n_cnt;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(128, 2)
+decode_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, const GemmArgs g) {
+  constexpr int A_BYTES = kTileM * kTileK * 2;  // 16 KB
+  constexpr int B_BYTES = BN * kTileK * 2;
+  constexpr int STAGE = A_BYTES + B_BYTES;
+  constexpr int TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  constexpr int kStages = stages<BN>();
+  extern __shared__ __align__(1024) uint8_t dsmem[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[stages<BN>()], empty[stages<BN>()], done;
+  __shared__ uint32_t tmem_base;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * kTileM;
+  const int split = blockIdx.y;
+  const int kb0 = split * g.kb_per_split;
+  const int kb1 = min(g.n_kb, kb0 + g.kb_per_split);
+  const int nkb = kb1 - kb0;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mb_init(&full[i], 1);
+      mb_init(&empty[i], 1);
+    }
+    mb_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+  }
+  if (warp == 2) {  // TMEM accumulator: 128 lanes x TMEM_COLS fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_d = tmem_base;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    for (int i = 0; i < nkb; ++i) {
+      const int st = i % kStages;
+      if (i >= kStages) mb_wait(&empty[st], ((i / kStages) - 1) & 1);
+      uint8_t* a = smem + st * STAGE;
+      mb_expect_tx(&full[st], STAGE);
+      tma_2d(a, &tmW, (kb0 + i) * kTileK, n0, &full[st]);
+      tma_2d(a + A_BYTES, &tmX, (kb0 + i) * kTileK, 0, &full[st]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer (one thread) ----
+    constexpr uint32_t idesc = idesc_bf16(kTileM, BN);
+    for (int i = 0; i < nkb; ++i) {
+      const int st = i % kStages;
+      mb_wait(&full[st], (i / kStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a = su32(smem + st * STAGE), b = a + A_BYTES;
+#pragma unroll
+      for (int k = 0; k < kTileK / 16; ++k)  // K = 16 per MMA: +32 bytes inside the swizzle row
+        umma_f16(tmem_d, sw128_desc(a + 32 * k), sw128_desc(b + 32 * k), idesc, (i | k) != 0);
+      umma_commit(&empty[st]);  // the stage is free once these MMAs have read it
+    }
+    umma_commit(&done);
+  }
+  __syncwarp();
+
+  // ---- epilogue: TMEM -> registers -> global (all 4 warps; warp w owns lanes 32w..) ----
+  mb_wait(&done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int n = n0 + warp * 32 + lane;
+  const uint32_t taddr = tmem_d + ((uint32_t)(warp * 32) << 16);
+  float* dst = g.out + (long long)split * g.slice;
+  // compact epilogue (one copy of the 16-column body: the unrolled form spent most
+  // of its time fetching instructions)
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    uint32_t v[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr + c0));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int nb = min(16, g.B - c0);
+    if (n < g.N && nb > 0) {
+      const long long off = (long long)c0 * g.ldo + n;
+#pragma unroll 1
+      for (int r = -1; r < g.n_peers; ++r) {  // r = -1: the local slice; r >= 0: fused TP push to rank r
+        float* d = (r < 0 ? dst : g.peers[r] + g.peer_slot + (long long)split * g.slice) + off;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < nb) d[(long long)j * g.ldo] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "n"(TMEM_COLS) : "memory");
+  // fused all-reduce: the barrier above orders every thread's tile stores (local
+  // and peer) before thread 0's system-scope release increments (cumulativity);
+  // a consumer that acquires a counter value sees this tile in every slot.
+  if (threadIdx.x == 0 && g.n_cnt) {
+    __threadfence_system();
+    for (int r = 0; r < g.n_cnt; ++r)
+      asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(g.cnt[r]) : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map of a row-major [rows][cols] matrix (row pitch ld elements),
+// box [box_rows][64] with 128-byte swizzle; cached by its arguments.
+bool tensor_map(CUtensorMap* out, const void* base, int rows, int cols, int ld, int box_rows) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, int, int>, CUtensorMap> cache;
+  const auto key = std::make_tuple(base, rows, cols, ld, box_rows);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kTileK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMap m;
+  if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, m);
+  *out = m;
+  return true;
+}
+
+template <int BN>
+cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const GemmArgs& g, int tiles, int splits,
+                      cudaStream_t s) {
+  constexpr int SMEM = stages<BN>() * (kTileM * kTileK * 2 + BN * kTileK * 2) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  decode_gemm_kernel<BN><<<dim3(tiles, splits), 128, SMEM, s>>>(tw, tx, g);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int decode_gemm_splits(int N, int K, int B, int sms) {
+  // Per-SM load model of a one-tile-per-CTA grid at two resident CTAs per SM:
+  // ceil(tiles * s / sms) CTAs per SM, each streaming ceil(kb / s) stages of
+  // (weights + activations), plus the split slices every split writes and the
+  // consumer reads back (2 * B * N * 4 bytes per split, spread over the SMs).
+  const int tiles = (N + kTileM - 1) / kTileM;
+  const int n_kb = (K + kTileK - 1) / kTileK;
+  const int bn = B <= 32 ? 32 : (B <= 64 ? 64 : (B <= 128 ? 128 : 256));
+  double best = 1e300;
+  int best_s = 1;
+  for (int s = 1; s <= kMaxGemmSplits && (s == 1 || n_kb / s >= 2); ++s) {
+    const int per = (n_kb + s - 1) / s;
+    const int used = (n_kb + per - 1) / per;  // splits that actually hold K blocks
+    if (used != s) continue;
+    // CTAs on the busiest SM; a CTA alone on an SM keeps only half the bytes in flight
+    // (~0.6 of the SM's rate, measured by the split sweep of tools/gemm_bench.py)
+    const int on_sm = (tiles * s + sms - 1) / sms;
+    const double cost = (on_sm >= 2 ? on_sm : on_sm / 0.6) * per * (kTileM * kTileK * 2.0 + bn * kTileK * 2.0) +
+                        (s > 1 ? 2.0 * s * B * N * 4.0 / sms : 0.0);
+    if (cost < best * 0.995) {
+      best = cost;
+      best_s = s;
+    }
+  }
+  return best_s;
+}
+
+cudaError_t launch_decode_gemm(const __nv_bfloat16* W, int N, int K, int ldw, const __nv_bfloat16* X, int B, int ldx,
+                               float* out, int ldo, long long slice, int splits, float* const* peers, int n_peers,
+                               long long peer_slot, cudaStream_t s, unsigned long long* const* cnt, int n_cnt) {
+  if (B <= 0 || B > 256 || N <= 0 || K <= 0 || splits < 1 || splits > kMaxGemmSplits || (ldw % 8) || (ldx % 8))
+    return cudaErrorInvalidValue;
+  const int BN = ((B + 15) / 16) * 16;
+  const int bn = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  CUtensorMap tw, tx;
+  if (!tensor_map(&tw, W, N, K, ldw, kTileM) || !tensor_map(&tx, X, B, K, ldx, bn)) return cudaErrorInvalidValue;
+  GemmArgs g{};
+  g.out = out;
+  g.slice = slice;
+  g.ldo = ldo;
+  g.N = N;
+  g.K = K;
+  g.B = B;
+  g.n_kb = (K + kTileK - 1) / kTileK;
+  g.kb_per_split = (g.n_kb + splits - 1) / splits;
+  g.peers = peers;
+  g.n_peers = peers ? n_peers : 0;
+  g.peer_slot = peer_slot;
+  g.cnt = cnt;
+  g.n_cnt = cnt ? n_cnt : 0;
+  const int tiles = (N + kTileM - 1) / kTileM;
+  switch (bn) {
+    case 32: return launch_bn<32>(tw, tx, g, tiles, splits, s);
+    case 64: return launch_bn<64>(tw, tx, g, tiles, splits, s);
+    case 128: return launch_bn<128>(tw, tx, g, tiles, splits, s);
+    default: return launch_bn<256>(tw, tx, g, tiles, splits, s);
+  }
+}
+
+}  // namespace mirage

@@ -49,6 +49,24 @@ int attention_grid_ctas(int H, int H_kv, int D, int qp = 1);
 int attention_prefill_rows(int H, int H_kv);
 int attention_cta_warps(int H_kv);
 
+// ---- decode GEMM on tcgen05 (decode_gemm.cu) ---------------------------------
+// Y_s[b][n] = sum over split s's K range of X[b][k] W[n][k]: W [N][ldw] and X
+// [B][ldx] bf16 row-major, 1 <= B <= 256; split slice s at out + s * slice, row b
+// at + b * ldo. peers (device array of n_peers float*, or null): the slices are
+// also stored at peers[r] + peer_slot + (same offsets) -- the fused TP all-reduce.
+constexpr int kMaxGemmSplits = 16;
+// cnt (device array of n_cnt counters, or null): each CTA increments every one of
+// them (release, system scope) after its stores -- the arrival signal of the
+// fused tensor-parallel all-reduce (one increment per tile per destination).
+cudaError_t launch_decode_gemm(const __nv_bfloat16* W, int N, int K, int ldw, const __nv_bfloat16* X, int B, int ldx,
+                               float* out, int ldo, long long slice, int splits, float* const* peers, int n_peers,
+                               long long peer_slot, cudaStream_t s, unsigned long long* const* cnt = nullptr,
+                               int n_cnt = 0);
+// tiles (CTAs per split) of a decode GEMM with N output rows
+inline int decode_gemm_tiles(int N) { return (N + 127) / 128; }
+// K splits for a B-row decode GEMM on `sms` SMs (per-SM load model, decode_gemm.cu)
+int decode_gemm_splits(int N, int K, int B, int sms);
+
 // ---- dense-layer support kernels -------------------------------------------
 // h[b] = E[tok] (+ P[pos + 2] for OPT); x[b] = bf16(norm(h[b])).
 cudaError_t launch_embed_norm(int family, int B, int d, const int32_t* tokens,
@@ -56,11 +74,12 @@ cudaError_t launch_embed_norm(int family, int B, int d, const int32_t* tokens,
                               const __nv_bfloat16* pos_embed, const __nv_bfloat16* g,
                               const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
                               cudaStream_t s);
-// h[b] += y[b] (+ bias); x[b] = bf16(norm(h[b])). y row stride ldy.
+// h[b] += y[b] (+ bias); x[b] = bf16(norm(h[b])). y row stride ldy; y may hold
+// nsplit split-K slices `slice` floats apart (summed in slice order first).
 cudaError_t launch_residual_norm(int family, int B, int d, const float* y, int ldy,
                                  const __nv_bfloat16* bias, const __nv_bfloat16* g,
                                  const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
-                                 cudaStream_t s);
+                                 cudaStream_t s, int nsplit = 1, long long slice = 0);
 // qkv [B][(H+2Hk)D] fp32 (+bias, +RoPE) -> q in the attention kernel's split
 // format (AttnParams::q, scaled by q_scale); K/V bf16 appended to the paged cache
 // at positions[b] (block address addrs[seq_off[b] + pos / 16]).
@@ -94,6 +113,16 @@ cudaError_t launch_tp_residual_norm(int family, int B, int d, const float* const
                                     unsigned int* err, const __nv_bfloat16* bias, const __nv_bfloat16* g,
                                     const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
                                     cudaStream_t s);
+
+// Fused variant (MIRAGE_FLAG_TC_GEMM + TP_IPC): every rank's decode GEMM pushed its
+// partial rows into slot r of THIS rank's exchange buffer and bumped cnt[r]; wait
+// until cnt[r] >= expect for every r (bounded spin: err++ on a lost peer), then
+// h += sum_r slots[r] (fixed rank order) (+ bias); x = norm(h) if g. Local reads only.
+cudaError_t launch_tp_push_residual_norm(int family, int B, int d, const float* const* slots, int tp,
+                                         const unsigned long long* cnt, unsigned long long expect, unsigned int* err,
+                                         const __nv_bfloat16* bias, const __nv_bfloat16* g,
+                                         const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
+                                         cudaStream_t s);
 
 // ---- slot tags (MIRAGE_FLAG_SLOT_TAGS): race detector for the copy engine ----
 // errors[0] += 1 and errors[1] = got if *tag != expected.

@@ -162,10 +162,12 @@ embed_norm_kernel(int family, int d, const int32_t* tokens, const int32_t* posit
 }
 
 // h[b] += y[b] (+ bias) if y != nullptr; then x[b] = bf16(norm(h[b])) if g != nullptr.
+// y may hold nsplit split-K slices (the tcgen05 decode GEMM's output), `slice`
+// floats apart: they are summed in slice order, then added.
 __global__ void __launch_bounds__(1024)
-residual_norm_kernel(int family, int d, const float* y, int ldy, const __nv_bfloat16* bias,
-                     const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps, float* h,
-                     __nv_bfloat16* x) {
+residual_norm_kernel(int family, int d, const float* y, int ldy, int nsplit, long long slice,
+                     const __nv_bfloat16* bias, const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps,
+                     float* h, __nv_bfloat16* x) {
   __shared__ __align__(16) float red[32];
   const int b = blockIdx.x;
   const int e0 = threadIdx.x * 8;
@@ -176,6 +178,12 @@ residual_norm_kernel(int family, int d, const float* y, int ldy, const __nv_bflo
     if (y) {
       float yv[8];
       load8(y + (size_t)b * ldy + e0, yv);
+      for (int s_ = 1; s_ < nsplit; ++s_) {
+        float ys[8];
+        load8(y + s_ * slice + (size_t)b * ldy + e0, ys);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) yv[k] += ys[k];
+      }
 #pragma unroll
       for (int k = 0; k < 8; ++k) v[k] += yv[k];
       if (bias) {
@@ -232,6 +240,51 @@ tp_residual_norm_kernel(int family, int d, const float* const* parts, int tp, in
     for (int r = 0; r < tp; ++r) {  // fixed order: every rank computes the same sum
       float pv[8];
       load8(parts[r] + (size_t)b * d + e0, pv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] += pv[k];
+    }
+    if (bias) {
+      float bv[8];
+      load8bf(bias + e0, bv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] += bv[k];
+    }
+    store8(h + (size_t)b * d + e0, v);
+  }
+  if (g) norm_row8(family, d, own, v, g, bta, eps, x + (size_t)b * d, red);
+}
+
+__global__ void __launch_bounds__(1024)
+tp_push_residual_norm_kernel(int family, int d, const float* const* slots, int tp, const unsigned long long* cnt,
+                             unsigned long long expect, unsigned int* err, const __nv_bfloat16* bias,
+                             const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps, float* h,
+                             __nv_bfloat16* x) {
+  __shared__ __align__(16) float red[32];
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < tp; ++r) {  // every rank's tiles of this GEMM have landed here
+      long long n = 0;
+      while (ld_acquire_sys(cnt + r) < expect) {
+        if (++n > (1ll << 26)) {
+          atomicAdd(err, 1u);
+          break;
+        }
+        __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+  const int e0 = threadIdx.x * 8;
+  const bool own = e0 < d;
+  float v[8];
+  if (own) {
+    load8(h + (size_t)b * d + e0, v);
+    for (int r = 0; r < tp; ++r) {  // fixed order: every rank computes the same sum
+      float pv[8];
+      const float4* src = reinterpret_cast<const float4*>(slots[r] + (size_t)b * d + e0);
+      const float4 p0 = __ldcg(src), p1 = __ldcg(src + 1);
+      pv[0] = p0.x; pv[1] = p0.y; pv[2] = p0.z; pv[3] = p0.w;
+      pv[4] = p1.x; pv[5] = p1.y; pv[6] = p1.z; pv[7] = p1.w;
 #pragma unroll
       for (int k = 0; k < 8; ++k) v[k] += pv[k];
     }
@@ -500,9 +553,10 @@ cudaError_t launch_embed_norm(int family, int B, int d, const int32_t* tokens,
 cudaError_t launch_residual_norm(int family, int B, int d, const float* y, int ldy,
                                  const __nv_bfloat16* bias, const __nv_bfloat16* g,
                                  const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
-                                 cudaStream_t s) {
-  if (d % 8 || d > 8192) return cudaErrorInvalidValue;
-  residual_norm_kernel<<<B, ((d / 8 + 31) / 32) * 32, 0, s>>>(family, d, y, ldy, bias, g, bta, eps, h, x);
+                                 cudaStream_t s, int nsplit, long long slice) {
+  if (d % 8 || d > 8192 || nsplit < 1) return cudaErrorInvalidValue;
+  residual_norm_kernel<<<B, ((d / 8 + 31) / 32) * 32, 0, s>>>(family, d, y, ldy, nsplit, slice, bias, g, bta, eps,
+                                                               h, x);
   return cudaGetLastError();
 }
 
@@ -550,6 +604,17 @@ cudaError_t launch_act(int family, int B, int f, const float* y, const __nv_bflo
 
 cudaError_t launch_argmax(int B, int V, const float* logits, int32_t* out, cudaStream_t s) {
   argmax_kernel<<<B, 1024, 0, s>>>(V, logits, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tp_push_residual_norm(int family, int B, int d, const float* const* slots, int tp,
+                                         const unsigned long long* cnt, unsigned long long expect, unsigned int* err,
+                                         const __nv_bfloat16* bias, const __nv_bfloat16* g,
+                                         const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
+                                         cudaStream_t s) {
+  if (d % 8 || d > 8192) return cudaErrorInvalidValue;
+  tp_push_residual_norm_kernel<<<B, ((d / 8 + 31) / 32) * 32, 0, s>>>(family, d, slots, tp, cnt, expect, err, bias,
+                                                                       g, bta, eps, h, x);
   return cudaGetLastError();
 }
 

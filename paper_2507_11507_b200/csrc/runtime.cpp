@@ -232,8 +232,15 @@ struct Model {
   std::vector<cudaEvent_t> cap_ready_ev, cap_free_ev;
   uint64_t graph_copies = 0;     // re-streaming DMAs run inside graphs (not individually timed)
   // ---- tensor parallelism over peer memory (MIRAGE_FLAG_TP_IPC) ----
-  char* xfer = nullptr;               // [flag u64 | pad][partial par 0][partial par 1]
+  // pull (TP_IPC): [flag u64 | pad][partial par 0][partial par 1];
+  // push (TP_IPC + TC_GEMM): [flag | cnt[tp] u64 | pad][par 0: tp slots][par 1: tp slots]
+  char* xfer = nullptr;
   size_t xfer_part = 0;               // bytes of one partial buffer (max_batch * d * 4)
+  bool tp_push = false;               // fused GEMM + all-reduce (the GEMM pushes to every rank)
+  float** push_dst_dev = nullptr;     // device [2][tp-1]: my slot in each OTHER rank's buffer
+  float** local_slots_dev = nullptr;  // device [2][tp]: the tp slots of my own buffer
+  unsigned long long** push_cnt_dev = nullptr;  // device [tp]: my arrival counter in every rank's header
+  unsigned long long push_expect = 0; // tiles each counter has received once the last GEMM lands
   std::vector<char*> peer_base;       // rank -> base of its xfer (own or IPC-opened)
   float** parts_dev = nullptr;        // device [2][tp]
   unsigned long long** flags_dev = nullptr;  // device [tp]
@@ -274,6 +281,7 @@ struct mirage_ctx {
   int stage_i = 0;
   char* meta_dev = nullptr;
   int max_units = 0;
+  int sms = 148;  // multiprocessors of the device (split planning)
   static constexpr int kTraceCtas = 4096;
   uint64_t* attn_trace = nullptr;  // MIRAGE_ATTN_TRACE: [kTraceCtas][8] stamps of the last attn_only launch
   int32_t attn_trace_ctas = 0;
@@ -655,6 +663,39 @@ void harvest_step_time(Model* M) {
   (void)cudaGetLastError();
 }
 
+// The row-parallel projections (O-proj, FC2/down) of a decode step: with
+// MIRAGE_FLAG_TC_GEMM the tcgen05 decode GEMM (decode_gemm.cu) writing split-K
+// slices that the residual kernel sums (*nsplit of them); otherwise, or above 256
+// rows, cuBLASLt (one fp32 output).
+
+int32_t gemm_lt(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf16* x, void* y, int out_bf16,
+                const bf16* bias, int epi);
+
+int32_t gemm_rowpar(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf16* x, float* y, long long y_cap,
+                    int* nsplit) {
+  *nsplit = 1;
+  if (!(c->cfg.flags & MIRAGE_FLAG_TC_GEMM) || B > 256 || K % 8) return gemm_lt(c, B, N, K, W, x, y, 0, nullptr, 0);
+  int s = mirage::decode_gemm_splits(N, K, B, c->sms);
+  s = (int)std::max<long long>(1, std::min<long long>(s, y_cap / ((long long)B * N)));
+  KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, y, N, (long long)B * N, s, nullptr, 0, 0, c->cs));
+  *nsplit = s;
+  return MIRAGE_OK;
+}
+
+// NEXT-4: the row-parallel GEMM of a tensor-parallel rank, fused with the one-shot
+// all-reduce: one K split (so each rank sends B x N once), the epilogue stores the
+// partial tile into this rank's own slot and into its slot of every other rank's
+// exchange buffer (parity ep & 1), then bumps each rank's arrival counter for this
+// rank; every counter therefore gains `tiles` per GEMM (push_expect).
+int32_t tp_push_gemm(mirage_ctx* c, Model* M, int B, int N, int K, const bf16* W, const bf16* x, uint64_t ep) {
+  const int par = (int)(ep & 1);
+  float* mine = reinterpret_cast<float*>(M->xfer + kAlign + (par * c->tp + c->tp_rank) * M->xfer_part);
+  KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, mine, N, 0, 1, M->push_dst_dev + par * (c->tp - 1),
+                                   c->tp - 1, 0, c->cs, M->push_cnt_dev, c->tp));
+  M->push_expect += (unsigned long long)mirage::decode_gemm_tiles(N);
+  return MIRAGE_OK;
+}
+
 // y[B][N] = epilogue(x[B][K] W[N][K]^T (+ bias[N])), fp32 accumulate, via cuBLASLt.
 // epi: 0 none, 1 bias, 2 relu(+bias). out_bf16 selects the output type.
 int32_t gemm_lt(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf16* x, void* y, int out_bf16,
@@ -807,6 +848,7 @@ int32_t mirage_init(const mirage_init_cfg* cfg, mirage_ctx** out) {
     return MIRAGE_OK;
   }
   if (cudaSetDevice(cfg->device) != cudaSuccess) return bail(MIRAGE_ERR_CUDA);
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, cfg->device);
   if (cfg->copy_stream) {
     c->xs = reinterpret_cast<cudaStream_t>(cfg->copy_stream);
   } else {
@@ -882,6 +924,9 @@ void mirage_destroy(mirage_ctx* c) {
     for (size_t r = 0; r < M->peer_base.size(); ++r)
       if (M->peer_base[r] && M->peer_base[r] != M->xfer) cudaIpcCloseMemHandle(M->peer_base[r]);
     if (M->xfer) cudaFree(M->xfer);
+    if (M->push_dst_dev) cudaFree(M->push_dst_dev);
+    if (M->local_slots_dev) cudaFree(M->local_slots_dev);
+    if (M->push_cnt_dev) cudaFree(M->push_cnt_dev);
     if (M->parts_dev) cudaFree(M->parts_dev);
     if (M->flags_dev) cudaFree(M->flags_dev);
     if (M->tp_err) cudaFree(M->tp_err);
@@ -913,6 +958,24 @@ const char* mirage_last_error(const mirage_ctx* c) { return c ? c->err.c_str() :
 
 int64_t mirage_kernel_launches(const mirage_ctx* c) { return c ? c->launches : 0; }
 
+
+int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
+                           float* y_dev, int32_t splits, int32_t* splits_out) {
+  if (!w_dev || !x_dev || !y_dev || N <= 0 || K <= 0 || K % 8 || B <= 0 || B > 256 || splits < 0 ||
+      splits > mirage::kMaxGemmSplits)
+    return MIRAGE_ERR_RANGE;
+  if (splits == 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    splits = mirage::decode_gemm_splits(N, K, B, sms);
+  }
+  if (splits_out) *splits_out = splits;
+  const cudaError_t e = mirage::launch_decode_gemm(
+      reinterpret_cast<const bf16*>(w_dev), N, K, K, reinterpret_cast<const bf16*>(x_dev), B, K, y_dev, N,
+      (long long)B * N, splits, nullptr, 0, 0, reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? MIRAGE_OK : MIRAGE_ERR_CUDA;
+}
 
 int32_t mirage_attn_trace(mirage_ctx* c, uint64_t* host_out, int32_t cap_ctas, int32_t* n_ctas) {
   GUARD(c);
@@ -1025,8 +1088,10 @@ int32_t mirage_tp_export(mirage_ctx* c, int32_t model, void* handle_out) {
     return fail(c, MIRAGE_ERR_CONFIG, "tp_export: needs MIRAGE_FLAG_TP_IPC");
   if (!M->xfer) {
     M->xfer_part = align_up((uint64_t)c->cfg.max_batch * M->shp.d * 4, kAlign);
-    CK(c, cudaMalloc(reinterpret_cast<void**>(&M->xfer), kAlign + 2 * M->xfer_part));
-    CK(c, cudaMemset(M->xfer, 0, kAlign + 2 * M->xfer_part));
+    M->tp_push = (c->cfg.flags & MIRAGE_FLAG_TC_GEMM) && c->cfg.max_batch <= 256;
+    const size_t bytes = kAlign + 2 * (M->tp_push ? (size_t)c->tp : 1) * M->xfer_part;
+    CK(c, cudaMalloc(reinterpret_cast<void**>(&M->xfer), bytes));
+    CK(c, cudaMemset(M->xfer, 0, bytes));
   }
   cudaIpcMemHandle_t h;
   CK(c, cudaIpcGetMemHandle(&h, M->xfer));
@@ -1057,6 +1122,28 @@ int32_t mirage_tp_import(mirage_ctx* c, int32_t model, const void* handles) {
     flags[r] = reinterpret_cast<unsigned long long*>(M->peer_base[r]);
     for (int par = 0; par < 2; ++par)
       parts[par * tp + r] = reinterpret_cast<float*>(M->peer_base[r] + kAlign + par * M->xfer_part);
+  }
+  if (M->tp_push) {  // fused GEMM + all-reduce: where my GEMM pushes, where I read, whom I signal
+    const int me = c->tp_rank;
+    std::vector<float*> dst(2 * (tp - 1)), mine(2 * tp);
+    std::vector<unsigned long long*> cnt(tp);
+    for (int par = 0; par < 2; ++par) {
+      int k = 0;
+      for (int r = 0; r < tp; ++r) {
+        mine[par * tp + r] = reinterpret_cast<float*>(M->xfer + kAlign + (par * tp + r) * M->xfer_part);
+        if (r != me)
+          dst[par * (tp - 1) + k++] =
+              reinterpret_cast<float*>(M->peer_base[r] + kAlign + (par * tp + me) * M->xfer_part);
+      }
+    }
+    for (int r = 0; r < tp; ++r) cnt[r] = reinterpret_cast<unsigned long long*>(M->peer_base[r] + 8 + 8 * me);
+    CK(c, cudaMalloc(reinterpret_cast<void**>(&M->push_dst_dev), std::max<size_t>(1, dst.size()) * sizeof(float*)));
+    CK(c, cudaMalloc(reinterpret_cast<void**>(&M->local_slots_dev), mine.size() * sizeof(float*)));
+    CK(c, cudaMalloc(reinterpret_cast<void**>(&M->push_cnt_dev), cnt.size() * sizeof(void*)));
+    if (!dst.empty())
+      CK(c, cudaMemcpy(M->push_dst_dev, dst.data(), dst.size() * sizeof(float*), cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpy(M->local_slots_dev, mine.data(), mine.size() * sizeof(float*), cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpy(M->push_cnt_dev, cnt.data(), cnt.size() * sizeof(void*), cudaMemcpyHostToDevice));
   }
   CK(c, cudaMalloc(reinterpret_cast<void**>(&M->parts_dev), parts.size() * sizeof(float*)));
   CK(c, cudaMalloc(reinterpret_cast<void**>(&M->flags_dev), flags.size() * sizeof(void*)));
@@ -1604,6 +1691,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   const GlobalW gw = global_ptrs(s, M->w_dev + (uint64_t)s.n * M->sz.S);
   const int d = s.d, H = s.H, Hk = s.Hk, D = s.D, qkvN = (H + 2 * Hk) * D;
   const bool opt = s.family == MIRAGE_FAMILY_OPT;
+  const long long y_cap = (long long)c->cfg.max_batch * M->y_ld_max;  // floats of the y workspace
   const int m = (int)M->cycle.size();
   const int beta = M->beta;
   // weights of layer l for this step (slot if cycled) and its use index
@@ -1791,7 +1879,14 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     } else {
       KL(c, mirage::launch_paged_attention(ap, cs));
     }
-    if (M->tp_ready) {  // a10 over peer memory: partial O-proj -> fused all-reduce + residual + norm
+    if (M->tp_ready && M->tp_push) {  // NEXT-4: the O-proj GEMM pushes its partial to every rank
+      const uint64_t ep = ++M->tp_epoch;
+      if (int32_t e = tp_push_gemm(c, M, B, d, H * D, w.w_o, M->x, ep)) return e;
+      KL(c, mirage::launch_tp_push_residual_norm(s.family, B, d, M->local_slots_dev + (ep & 1) * c->tp, c->tp,
+                                                reinterpret_cast<unsigned long long*>(M->xfer + 8), M->push_expect,
+                                                M->tp_err, opt ? w.b_o : nullptr, w.n2_g, opt ? w.n2_b : nullptr,
+                                                s.eps, M->h, M->x, cs));
+    } else if (M->tp_ready) {  // a10 over peer memory: partial O-proj -> fused all-reduce + residual + norm
       const uint64_t ep = ++M->tp_epoch;
       float* part = reinterpret_cast<float*>(M->xfer + kAlign + (ep & 1) * M->xfer_part);
       if (int32_t e = gemm_lt(c, B, d, H * D, w.w_o, M->x, part, 0, nullptr, 0)) return e;
@@ -1799,11 +1894,16 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
                                            M->flags_dev, ep, M->tp_err, opt ? w.b_o : nullptr, w.n2_g,
                                            opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs));
     } else {
-      if (int32_t e = gemm_lt(c, B, d, H * D, w.w_o, M->x, M->y, 0, nullptr, 0)) return e;
-      if (c->nccl)  // a10: sum the heads' partial O-projections over the TP ranks
+      int ns_o = 1;
+      if (c->nccl) {
+        if (int32_t e = gemm_lt(c, B, d, H * D, w.w_o, M->x, M->y, 0, nullptr, 0)) return e;
+        // a10: sum the heads' partial O-projections over the TP ranks
         CKN(c, ncclAllReduce(M->y, M->y, (size_t)B * d, ncclFloat32, ncclSum, c->nccl, cs));
+      } else if (int32_t e = gemm_rowpar(c, B, d, H * D, w.w_o, M->x, M->y, y_cap, &ns_o)) {
+        return e;
+      }
       KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_o : nullptr, w.n2_g,
-                                        opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs));
+                                        opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs, ns_o, (long long)B * d));
     }
     if (opt) {
       // FC1 + bias + ReLU fused in the GEMM epilogue, bf16 out (one rounding, as before)
@@ -1813,22 +1913,33 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
       KL(c, mirage::launch_act(s.family, B, s.f, M->y, nullptr, M->f, cs));
     }
     uint64_t ep2 = 0;
-    if (M->tp_ready) {
+    int ns_2 = 1;
+    if (M->tp_ready && M->tp_push) {
+      ep2 = ++M->tp_epoch;
+      if (int32_t e = tp_push_gemm(c, M, B, d, s.f, w.w_2, M->f, ep2)) return e;
+    } else if (M->tp_ready) {
       ep2 = ++M->tp_epoch;
       float* part = reinterpret_cast<float*>(M->xfer + kAlign + (ep2 & 1) * M->xfer_part);
       if (int32_t e = gemm_lt(c, B, d, s.f, w.w_2, M->f, part, 0, nullptr, 0)) return e;
-    } else {
+    } else if (c->nccl) {
       if (int32_t e = gemm_lt(c, B, d, s.f, w.w_2, M->f, M->y, 0, nullptr, 0)) return e;
+    } else if (int32_t e = gemm_rowpar(c, B, d, s.f, w.w_2, M->f, M->y, y_cap, &ns_2)) {
+      return e;
     }
     if (c->nccl)  // a10: sum the FFN shards' partial down-projections
       CKN(c, ncclAllReduce(M->y, M->y, (size_t)B * d, ncclFloat32, ncclSum, c->nccl, cs));
     // residual of layer l (+ the next norm): plain, or fused with the peer all-reduce
     auto residual = [&](const bf16* bias2, const bf16* g2, const bf16* b2) -> int32_t {
-      if (M->tp_ready) {
+      if (M->tp_ready && M->tp_push) {
+        KL(c, mirage::launch_tp_push_residual_norm(s.family, B, d, M->local_slots_dev + (ep2 & 1) * c->tp, c->tp,
+                                                  reinterpret_cast<unsigned long long*>(M->xfer + 8),
+                                                  M->push_expect, M->tp_err, bias2, g2, b2, s.eps, M->h, M->x, cs));
+      } else if (M->tp_ready) {
         KL(c, mirage::launch_tp_residual_norm(s.family, B, d, M->parts_dev + (ep2 & 1) * c->tp, c->tp, c->tp_rank,
                                              M->flags_dev, ep2, M->tp_err, bias2, g2, b2, s.eps, M->h, M->x, cs));
       } else {
-        KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, bias2, g2, b2, s.eps, M->h, M->x, cs));
+        KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, bias2, g2, b2, s.eps, M->h, M->x, cs, ns_2,
+                                          (long long)B * d));
       }
       return MIRAGE_OK;
     };

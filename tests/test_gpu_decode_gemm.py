@@ -1,0 +1,48 @@
+"""The tcgen05 decode GEMM (decode_gemm.cu) against a
+plain PyTorch reference of the same op (y = x W^T in float64 on the same bf16
+values): ragged N, K and batch, forced and planned K splits, every batch width
+the kernel instantiates (N side 32 / 64 / 128 / 256). The split slices must sum
+to the product and each slice must be the product over its own K range. GPU only."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def ref(w, x):
+    return x.double() @ w.double().T
+
+
+@pytest.mark.parametrize("N,K,B,splits", [
+    (256, 256, 4, 1), (128, 64, 1, 1), (1000, 776, 37, 0), (1000, 776, 37, 3), (5120, 5120, 64, 0),
+    (15360, 5120, 29, 0), (4096, 14336, 64, 0), (8192, 1024, 64, 0), (512, 1024, 256, 2), (700, 2048, 200, 0),
+    (384, 4096, 16, 16), (130, 520, 130, 0)])
+def test_decode_gemm_matches_reference(N, K, B, splits):
+    from paper_2507_11507_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(N * 7 + K * 3 + B)
+    w = (torch.randn((N, K), generator=g, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    x = torch.randn((B, K), generator=g, device="cuda").to(torch.bfloat16)
+    y, ns = _lib.decode_gemm(w, x, splits)
+    torch.cuda.synchronize()
+    assert ns >= 1 and (splits == 0 or ns == splits)
+    r = ref(w, x)
+    got = y.double().sum(0)
+    scale = r.abs().max().item()
+    assert (got - r).abs().max().item() <= 2e-5 * scale + 1e-6 * K ** 0.5
+    # each slice is the product over its own K range (64-wide blocks, split in order)
+    n_kb = (K + 63) // 64
+    per = (n_kb + ns - 1) // ns
+    for s in range(ns):
+        k0, k1 = min(K, s * per * 64), min(K, (s + 1) * per * 64)
+        rs = ref(w[:, k0:k1], x[:, k0:k1]) if k1 > k0 else torch.zeros_like(r)
+        assert (y[s].double() - rs).abs().max().item() <= 2e-5 * scale + 1e-6 * K ** 0.5
+
+
+def test_decode_gemm_is_deterministic():
+    from paper_2507_11507_b200 import _lib
+    w = torch.randn((4096, 4096), device="cuda").to(torch.bfloat16)
+    x = torch.randn((64, 4096), device="cuda").to(torch.bfloat16)
+    a, _ = _lib.decode_gemm(w, x)
+    b, _ = _lib.decode_gemm(w, x)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)

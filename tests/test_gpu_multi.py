@@ -7,7 +7,9 @@ test_gpu_tp.py and test_gpu_reversion.py):
   * head-sharded TP at tp = 2 over NCCL (one process per GPU): ranks bit-identical,
     equal to the FULL model's exact decoder within the derived bf16 bound;
   * the fused one-shot all-reduce over peer memory (MIRAGE_FLAG_TP_IPC) across two
-    GPUs (the peers' partial rows read over NVLink): the same checks;
+    GPUs (the peers' partial rows read over NVLink), and its NEXT-4 form in which
+    the tcgen05 GEMM's epilogue pushes each tile to the peer over NVLink
+    (MIRAGE_FLAG_TC_GEMM): the same checks;
   * NEXT-2: re-streaming from a weight copy in the PEER GPU's HBM (NVLink) gives
     bit-identical outputs to streaming from the pinned host copy.
 GPU only."""
@@ -64,10 +66,10 @@ def _tp_rank(rank, tp, port, mode, q):
         dist.broadcast_object_list(ids, src=0)
         kw["nccl_id"] = ids[0]
     else:
-        kw["flags"] = _lib.FLAG_TP_IPC
+        kw["flags"] = _lib.FLAG_TP_IPC | (_lib.FLAG_TC_GEMM if mode == "push" else 0)
     ctx = Context(harness.arena_for([(sh, 16)], B, 128), B, 128, **kw)
     mid = ctx.add_model(shape, harness.make_shard_blob(shape, rank, tp, seed=SEED), 16)
-    if mode == "ipc":
+    if mode in ("ipc", "push"):
         handles = [None] * tp
         dist.all_gather_object(handles, ctx.tp_export(mid))
         ctx.tp_import(mid, handles)
@@ -123,7 +125,7 @@ def _check_full_model(got):
         CB.check(got[t], exact[t][0], bounds[t], t)
 
 
-@pytest.mark.parametrize("mode", ["nccl", "ipc"])
+@pytest.mark.parametrize("mode", ["nccl", "ipc", "push"])
 def test_tp2_two_gpus_matches_full_model(mode):
     res = _run_tp(mode)
     assert np.array_equal(res[0], res[1])          # every rank holds the same all-reduced state

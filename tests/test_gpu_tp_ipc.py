@@ -22,7 +22,7 @@ def _port():
     return p
 
 
-def _rank(rank, tp, port, q):
+def _rank(rank, tp, port, q, push=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -35,7 +35,8 @@ def _rank(rank, tp, port, q):
     from synth import models, workload
     shape = models.ModelShape("tp-llama", models.LLAMA, 2, 256, 8, 4, 64, 512, 1024, 256)
     sh = harness.shard_shape(shape, tp)
-    ctx = Context(harness.arena_for([(sh, 16)], 4, 128), 4, 128, flags=_lib.FLAG_TP_IPC, tp_rank=rank, tp_size=tp)
+    flags = _lib.FLAG_TP_IPC | (_lib.FLAG_TC_GEMM if push else 0)
+    ctx = Context(harness.arena_for([(sh, 16)], 4, 128), 4, 128, flags=flags, tp_rank=rank, tp_size=tp)
     mid = ctx.add_model(shape, harness.make_shard_blob(shape, rank, tp, seed=13), 16)
     handles = [None] * tp
     dist.all_gather_object(handles, ctx.tp_export(mid))
@@ -57,14 +58,11 @@ def _rank(rank, tp, port, q):
     dist.destroy_process_group()
 
 
-def test_two_rank_tp_over_peer_memory_matches_oracle():
-    from oracle.decode import Decoder
-    from synth import models, weights, workload
-    tp = 2
+def run_ranks(tp, push):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_rank, args=(r, tp, port, q)) for r in range(tp)]
+    ps = [ctx.Process(target=_rank, args=(r, tp, port, q, push)) for r in range(tp)]
     for p in ps:
         p.start()
     res = {}
@@ -74,12 +72,38 @@ def test_two_rank_tp_over_peer_memory_matches_oracle():
     for p in ps:
         p.join(120)
     assert all(p.exitcode == 0 for p in ps)
+    return res
+
+
+@pytest.mark.parametrize("push", [False, True], ids=["pull-consumer", "fused-gemm-push"])
+def test_two_rank_tp_over_peer_memory_matches_oracle(push):
+    """pull: cuBLASLt partial GEMM, then one kernel reads the peers' partials (a10).
+    fused-gemm-push (MIRAGE_FLAG_TC_GEMM, NEXT-4): the tcgen05 decode GEMM's
+    epilogue stores each partial tile into every rank's exchange buffer and bumps
+    the rank's arrival counter; the consumer reads local memory only."""
+    import c4_bounds as CB
+    from oracle.decode import Decoder
+    from synth import models, weights, workload
+    tp = 2
+    res = run_ranks(tp, push)
     assert res[0][1] == 0 and res[1][1] == 0                   # no lost-peer timeouts
     assert np.array_equal(res[0][0], res[1][0])                 # fixed-order sum: identical ranks
     shape = models.ModelShape("tp-llama", models.LLAMA, 2, 256, 8, 4, 64, 512, 1024, 256)
-    dec = Decoder(shape, [weights.layer_tensors(shape, l, 13) for l in range(2)], weights.global_tensors(shape, 13))
+    layers = [weights.layer_tensors(shape, l, 13) for l in range(2)]
+    glob = weights.global_tensors(shape, 13)
+    dec = Decoder(shape, layers, glob)
     for t in range(12):
         ref, _, _ = dec.step([0, 1, 2, 3], [workload.teacher_tokens(s, t, shape.vocab) for s in range(4)], [t] * 4)
         got = res[0][0][t]
         rel = np.sqrt(((got - ref) ** 2).mean() / (ref ** 2).mean())
         assert rel < 1e-2, (t, rel)
+
+    def script(d):
+        out = []
+        for t in range(12):
+            h, lg, _ = d.step([0, 1, 2, 3], [workload.teacher_tokens(s, t, shape.vocab) for s in range(4)], [t] * 4)
+            out.append((h, lg))
+        return out
+    exact, bounds = CB.predict(shape, layers, glob, script)
+    for t in range(12):
+        CB.check(res[0][0][t], exact[t][0], bounds[t], t)

@@ -31,6 +31,10 @@ def main():
     ap.add_argument("--graphs", action="store_true", help="MIRAGE_FLAG_CUDA_GRAPHS (no attention timing)")
     ap.add_argument("--alpha", type=int, default=0, help="remapped layers per rank (planner, uniform placement)")
     ap.add_argument("--beta", type=int, default=2)
+    ap.add_argument("--ipc", choices=["none", "pull", "push"], default="none",
+                    help="run the rank's all-reduce machinery at tp_size 1 (no peers): pull = cuBLASLt + "
+                         "the consumer that reads partials (a10); push = the tcgen05 GEMM whose epilogue "
+                         "pushes its tile + arrival counters, consumer reads locally (NEXT-4)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     B, L0 = a.batch, a.ctx
@@ -40,8 +44,13 @@ def main():
         max_ctx = L0 + a.steps + 16
         arena = harness.arena_for([(shape, nblk)], B, max_ctx, slack=256 << 20)
         blob = harness.make_blob(shape, seed=3, gen_device=dev)
-        ctx = _lib.Context(arena, B, max_ctx, flags=_lib.FLAG_CUDA_GRAPHS if a.graphs else _lib.FLAG_TIME_ATTN)
+        flags = _lib.FLAG_CUDA_GRAPHS if a.graphs else _lib.FLAG_TIME_ATTN
+        if a.ipc != "none":
+            flags = _lib.FLAG_TIME_ATTN | _lib.FLAG_TP_IPC | (_lib.FLAG_TC_GEMM if a.ipc == "push" else 0)
+        ctx = _lib.Context(arena, B, max_ctx, flags=flags)
         mid = ctx.add_model(shape, blob, nblk)
+        if a.ipc != "none":
+            ctx.tp_import(mid, [ctx.tp_export(mid)])
         cycle = []
         if a.alpha:   # alpha = 1, beta = 2 per rank
             cycle, _, beta = _lib.plan(shape.n_layers, a.alpha, a.beta, 0, 1)
@@ -72,7 +81,7 @@ def main():
         ar_bytes = 2 * shape.n_layers * B * shape.d_model * 4
         print(json.dumps({
             "tp": tp, "shape": {"n_heads": shape.n_heads, "n_kv_heads": shape.n_kv_heads, "ffn": shape.ffn_dim},
-            "batch": B, "ctx": L0, "cuda_graphs": a.graphs, "cycle": cycle, "step_ms": round(ms, 3), "tok_s_per_rank_group": round(B / (ms / 1e3), 1),
+            "batch": B, "ctx": L0, "cuda_graphs": a.graphs, "cycle": cycle, "ipc": a.ipc, "step_ms": round(ms, 3), "tok_s_per_rank_group": round(B / (ms / 1e3), 1),
             "attention_ms_per_step": round(attn_ms, 3), "attention_share": round(attn_ms / ms, 3),
             "attention_gbs": round(attn_bytes / (attn_ms / launches * 1e-3) / 1e9, 1),
             "weights_gb_per_rank": round((shape.n_layers * S + G) / 1e9, 2),
