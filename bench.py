@@ -677,12 +677,14 @@ def run_mirage(args, rank, world):
     attn_avg_ms = res["attn_ms"] / max(1, res["attn_launches"])
     attn_bytes_launch = res["attn_bytes"] / max(1, res["attn_launches"])
     achieved = attn_bytes_launch / (attn_avg_ms * 1e-3) / 1e9 if attn_avg_ms > 0 else None
-    traffic = None
+    traffic, traffic_capture = None, None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "attention_traffic.json")))
         ent = tr.get(wl.name, {})
         if ent.get("batch", 400 if wl.name == "c2" else None) == B:   # only for the captured workload
             traffic = ent.get("dram_bytes_per_launch")
+            traffic_capture = {k: ent.get(k) for k in ("algorithmic_bytes_per_launch", "traffic_over_algorithmic",
+                                                       "source")}
     except Exception:
         pass
     if rank != 0:
@@ -726,6 +728,7 @@ def run_mirage(args, rank, world):
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
                      "algorithmic_bytes_per_launch": attn_bytes_launch, "avg_launch_ms": attn_avg_ms,
                      "launches": res["attn_launches"], "share_of_step": res["attn_ms"] / t_local,
+                     "traffic_capture": traffic_capture,
                      "kernel_alone_gbs": res.get("alone_gbs"),
                      "copy_peak_this_run_gbs": copy_peak_run,
                      "frac_of_copy_peak_this_run": achieved / copy_peak_run if achieved else None,

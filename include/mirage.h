@@ -448,10 +448,14 @@ int64_t mirage_kernel_launches(const mirage_ctx* ctx);
  * W = w_dev bf16 [N][K] and X = x_dev bf16 [B][K] (row-major, device memory,
  * K % 8 == 0, 1 <= B <= 256), written to y_dev fp32 [splits][B][N]; the splits
  * partition K in order and sum to Y. splits = 0 picks the library's choice
- * (about one wave of CTAs) and reports it in *splits_out. Enqueued on `stream`
- * (a cudaStream_t; NULL = legacy default stream). Errors: RANGE, CUDA. */
+ * (a per-SM load model) and reports it in *splits_out. reduce != 0: splits
+ * of a tile run as one thread-block cluster and are summed in split order
+ * through distributed shared memory inside the kernel (at most 8 splits,
+ * B <= 128), so y_dev receives ONE slice [B][N] and *splits_out is set to 1.
+ * Enqueued on `stream` (a cudaStream_t; NULL = legacy default stream).
+ * Errors: RANGE, CUDA. */
 int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
-                           float* y_dev, int32_t splits, int32_t* splits_out);
+                           float* y_dev, int32_t splits, int32_t reduce, int32_t* splits_out);
 
 /* Profiling hook. With the environment variable MIRAGE_ATTN_TRACE set when the
  * ctx is created, every attention launch of mirage_attn_only records 16

@@ -114,7 +114,7 @@ def _load():
         "mirage_write_kv": (I32, [P, I32, I64, I32, P]),
         "mirage_kernel_launches": (I64, [P]),
         "mirage_attn_trace": (I32, [P, pU64, I32, pI32]),
-        "mirage_decode_gemm": (I32, [P, P, I32, I32, P, I32, P, I32, pI32]),
+        "mirage_decode_gemm": (I32, [P, P, I32, I32, P, I32, P, I32, I32, pI32]),
         "mirage_nccl_unique_id": (I32, [P]),
         "mirage_host_register": (I32, [P, U64]),
         "mirage_region_count": (I32, [P, I32, pI32]),
@@ -193,9 +193,10 @@ def predict_stall(n_layers, cycle, beta, t_transfer_ns, t_compute_layer_ns):
     return out.value
 
 
-def decode_gemm(w, x, splits=0, stream=None):
+def decode_gemm(w, x, splits=0, stream=None, reduce=False):
     """Y slices [splits][B][N] fp32 of x [B][K] @ w[N][K]^T on the tcgen05 decode GEMM
-    (mirage_decode_gemm); both bf16 CUDA tensors. Returns (slices, splits)."""
+    (mirage_decode_gemm); both bf16 CUDA tensors. reduce: the splits are summed in
+    the kernel (one slice). Returns (slices, number of slices)."""
     assert w.dtype == torch.bfloat16 and x.dtype == torch.bfloat16 and w.is_cuda and x.is_cuda
     w, x = w.contiguous(), x.contiguous()
     N, K = w.shape
@@ -205,7 +206,7 @@ def decode_gemm(w, x, splits=0, stream=None):
     got = C.c_int32()
     st = stream if stream is not None else torch.cuda.current_stream(w.device)
     rc = LIB.mirage_decode_gemm(st.cuda_stream, w.data_ptr(), N, K, x.data_ptr(), B, y.data_ptr(), int(splits),
-                                C.byref(got))
+                                int(bool(reduce)), C.byref(got))
     if rc:
         raise MirageError(rc, "decode_gemm")
     return y[: got.value], got.value

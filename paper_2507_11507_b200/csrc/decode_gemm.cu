@@ -35,6 +35,7 @@ namespace {
 
 constexpr int kTileM = 128;  // weight rows per tile (MMA M)
 constexpr int kTileK = 64;   // K per stage: one 128-byte swizzle row of bf16
+constexpr int kMaxClusterSplits = 8;  // portable cluster size
 // ring depth: ~96-104 KB of stages per CTA, so two CTAs share an SM (two tiles
 // streaming per SM: the grid of a decode GEMM is ~1-2 waves of small tiles)
 template <int BN>
@@ -106,6 +107,12 @@ struct GemmArgs {
   // one per destination rank of a fused tensor-parallel GEMM
   unsigned long long* const* cnt;
   int n_cnt;
+  // cluster split reduction: the grid's K splits of a tile form one thread-block
+  // cluster (1 x S); each CTA parks its fp32 partial tile in its (now idle) stage
+  // ring, and after a cluster barrier CTA r sums rows b in [r B / S, (r+1) B / S)
+  // over the S partials through distributed shared memory, in split order, and
+  // stores the final rows (one slice, no workspace)
+  int creduce;
 };
 
 template <int BN>
@@ -182,6 +189,49 @@ decode_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
   const int n = n0 + warp * 32 + lane;
   const uint32_t taddr = tmem_d + ((uint32_t)(warp * 32) << 16);
   float* dst = g.out + (long long)split * g.slice;
+  if (g.creduce) {
+    float* part = reinterpret_cast<float*>(smem);  // [b][128] fp32; the ring is idle after `done`
+    const int row = warp * 32 + lane;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t v[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr + c0));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < g.B) part[(c0 + j) * kTileM + row] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    const int S = gridDim.y;
+    const int b0 = split * g.B / S, b1 = (split + 1) * g.B / S;
+    uint32_t rbase[kMaxClusterSplits];
+    const uint32_t mine = su32(part + row);
+#pragma unroll
+    for (int r = 0; r < kMaxClusterSplits; ++r)
+      if (r < S) asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbase[r]) : "r"(mine), "r"(r));
+    if (n < g.N) {
+#pragma unroll 1
+      for (int b = b0; b < b1; ++b) {
+        float acc = 0.f;
+#pragma unroll
+        for (int r = 0; r < kMaxClusterSplits; ++r) {  // split order: deterministic
+          if (r < S) {
+            float x;
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(rbase[r] + (uint32_t)(b * kTileM * 4)));
+            acc += x;
+          }
+        }
+        g.out[(long long)b * g.ldo + n] = acc;
+        for (int r = 0; r < g.n_peers; ++r) g.peers[r][g.peer_slot + (long long)b * g.ldo + n] = acc;
+      }
+    }
+    // no CTA may leave (and release its shared memory) while the others still read it
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else
   // compact epilogue (one copy of the 16-column body: the unrolled form spent most
   // of its time fetching instructions)
 #pragma unroll 1
@@ -262,17 +312,35 @@ bool tensor_map(CUtensorMap* out, const void* base, int rows, int cols, int ld, 
 }
 
 template <int BN>
+constexpr int smem_of() { return stages<BN>() * (kTileM * kTileK * 2 + BN * kTileK * 2) + 1024; }
+
+template <int BN>
 cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const GemmArgs& g, int tiles, int splits,
                       cudaStream_t s) {
-  constexpr int SMEM = stages<BN>() * (kTileM * kTileK * 2 + BN * kTileK * 2) + 1024;
+  constexpr int SMEM = smem_of<BN>();
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(decode_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  decode_gemm_kernel<BN><<<dim3(tiles, splits), 128, SMEM, s>>>(tw, tx, g);
-  return cudaGetLastError();
+  if (!g.creduce) {
+    decode_gemm_kernel<BN><<<dim3(tiles, splits), 128, SMEM, s>>>(tw, tx, g);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(tiles, splits);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = splits;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decode_gemm_kernel<BN>, tw, tx, g);
 }
 
 }  // namespace
@@ -306,7 +374,8 @@ int decode_gemm_splits(int N, int K, int B, int sms) {
 
 cudaError_t launch_decode_gemm(const __nv_bfloat16* W, int N, int K, int ldw, const __nv_bfloat16* X, int B, int ldx,
                                float* out, int ldo, long long slice, int splits, float* const* peers, int n_peers,
-                               long long peer_slot, cudaStream_t s, unsigned long long* const* cnt, int n_cnt) {
+                               long long peer_slot, cudaStream_t s, unsigned long long* const* cnt, int n_cnt,
+                               bool reduce, int* slices_out) {
   if (B <= 0 || B > 256 || N <= 0 || K <= 0 || splits < 1 || splits > kMaxGemmSplits || (ldw % 8) || (ldx % 8))
     return cudaErrorInvalidValue;
   const int BN = ((B + 15) / 16) * 16;
@@ -327,6 +396,10 @@ cudaError_t launch_decode_gemm(const __nv_bfloat16* W, int N, int K, int ldw, co
   g.peer_slot = peer_slot;
   g.cnt = cnt;
   g.n_cnt = cnt ? n_cnt : 0;
+  // the partial tile parks in the stage ring: B x 128 fp32 must fit there (bn <= 128)
+  g.creduce = reduce && splits > 1 && splits <= kMaxClusterSplits && bn <= 128 &&
+              B * kTileM * 4 <= smem_of<128>() - 1024;
+  if (slices_out) *slices_out = g.creduce ? 1 : splits;
   const int tiles = (N + kTileM - 1) / kTileM;
   switch (bn) {
     case 32: return launch_bn<32>(tw, tx, g, tiles, splits, s);

@@ -61,7 +61,10 @@ constexpr int kMaxGemmSplits = 16;
 cudaError_t launch_decode_gemm(const __nv_bfloat16* W, int N, int K, int ldw, const __nv_bfloat16* X, int B, int ldx,
                                float* out, int ldo, long long slice, int splits, float* const* peers, int n_peers,
                                long long peer_slot, cudaStream_t s, unsigned long long* const* cnt = nullptr,
-                               int n_cnt = 0);
+                               int n_cnt = 0, bool reduce = false, int* slices_out = nullptr);
+// reduce = true: up to 8 splits of a tile (batch <= 128) are summed inside the GEMM
+// through a thread-block cluster's distributed shared memory, so `out` receives
+// ONE slice (*slices_out = 1); otherwise *slices_out = splits.
 // tiles (CTAs per split) of a decode GEMM with N output rows
 inline int decode_gemm_tiles(int N) { return (N + 127) / 128; }
 // K splits for a B-row decode GEMM on `sms` SMs (per-SM load model, decode_gemm.cu)

@@ -676,9 +676,12 @@ int32_t gemm_rowpar(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf1
   *nsplit = 1;
   if (!(c->cfg.flags & MIRAGE_FLAG_TC_GEMM) || B > 256 || K % 8) return gemm_lt(c, B, N, K, W, x, y, 0, nullptr, 0);
   int s = mirage::decode_gemm_splits(N, K, B, c->sms);
+  if (B <= 128) s = std::min(s, 8);  // summed inside the GEMM (cluster DSMEM reduction): one slice out
   s = (int)std::max<long long>(1, std::min<long long>(s, y_cap / ((long long)B * N)));
-  KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, y, N, (long long)B * N, s, nullptr, 0, 0, c->cs));
-  *nsplit = s;
+  int slices = s;
+  KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, y, N, (long long)B * N, s, nullptr, 0, 0, c->cs, nullptr, 0,
+                                   true, &slices));
+  *nsplit = slices;
   return MIRAGE_OK;
 }
 
@@ -690,9 +693,14 @@ int32_t gemm_rowpar(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf1
 int32_t tp_push_gemm(mirage_ctx* c, Model* M, int B, int N, int K, const bf16* W, const bf16* x, uint64_t ep) {
   const int par = (int)(ep & 1);
   float* mine = reinterpret_cast<float*>(M->xfer + kAlign + (par * c->tp + c->tp_rank) * M->xfer_part);
-  KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, mine, N, 0, 1, M->push_dst_dev + par * (c->tp - 1),
-                                   c->tp - 1, 0, c->cs, M->push_cnt_dev, c->tp));
-  M->push_expect += (unsigned long long)mirage::decode_gemm_tiles(N);
+  // K splits are summed inside the GEMM (cluster reduction) before the push, so
+  // every rank still receives B x N once; without it (B > 128) one split
+  int s = B <= 128 ? std::min(8, mirage::decode_gemm_splits(N, K, B, c->sms)) : 1;
+  int slices = 1;
+  KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, mine, N, 0, s, M->push_dst_dev + par * (c->tp - 1),
+                                   c->tp - 1, 0, c->cs, M->push_cnt_dev, c->tp, true, &slices));
+  if (slices != 1) return fail(c, MIRAGE_ERR_STATE, "tp push GEMM: split not reduced");
+  M->push_expect += (unsigned long long)mirage::decode_gemm_tiles(N) * s;  // every CTA signals
   return MIRAGE_OK;
 }
 
@@ -960,7 +968,7 @@ int64_t mirage_kernel_launches(const mirage_ctx* c) { return c ? c->launches : 0
 
 
 int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
-                           float* y_dev, int32_t splits, int32_t* splits_out) {
+                           float* y_dev, int32_t splits, int32_t reduce, int32_t* splits_out) {
   if (!w_dev || !x_dev || !y_dev || N <= 0 || K <= 0 || K % 8 || B <= 0 || B > 256 || splits < 0 ||
       splits > mirage::kMaxGemmSplits)
     return MIRAGE_ERR_RANGE;
@@ -970,10 +978,13 @@ int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     splits = mirage::decode_gemm_splits(N, K, B, sms);
   }
-  if (splits_out) *splits_out = splits;
+  if (reduce) splits = std::min(splits, 8);
+  int slices = splits;
   const cudaError_t e = mirage::launch_decode_gemm(
       reinterpret_cast<const bf16*>(w_dev), N, K, K, reinterpret_cast<const bf16*>(x_dev), B, K, y_dev, N,
-      (long long)B * N, splits, nullptr, 0, 0, reinterpret_cast<cudaStream_t>(stream));
+      (long long)B * N, splits, nullptr, 0, 0, reinterpret_cast<cudaStream_t>(stream), nullptr, 0, reduce != 0,
+      &slices);
+  if (splits_out) *splits_out = slices;
   return e == cudaSuccess ? MIRAGE_OK : MIRAGE_ERR_CUDA;
 }
 

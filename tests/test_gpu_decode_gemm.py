@@ -38,6 +38,30 @@ def test_decode_gemm_matches_reference(N, K, B, splits):
         assert (y[s].double() - rs).abs().max().item() <= 2e-5 * scale + 1e-6 * K ** 0.5
 
 
+@pytest.mark.parametrize("N,K,B,splits", [(5120, 5120, 64, 0), (1000, 776, 37, 3), (8192, 1024, 128, 4),
+                                          (384, 4096, 16, 8), (700, 2048, 100, 0), (4096, 14336, 64, 2)])
+def test_decode_gemm_cluster_reduce_equals_the_slice_sum(N, K, B, splits):
+    """reduce: the K splits of a tile are summed inside the kernel through the
+    cluster's distributed shared memory, in split order -- bit-identical to
+    summing the unreduced slices in slice order, as the residual kernel does."""
+    from paper_2507_11507_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(N + K + B)
+    w = (torch.randn((N, K), generator=g, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    x = torch.randn((B, K), generator=g, device="cuda").to(torch.bfloat16)
+    s_plain, ns = _lib.decode_gemm(w, x, splits)
+    s_red, one = _lib.decode_gemm(w, x, min(ns, 8) if splits == 0 else splits, reduce=True)
+    torch.cuda.synchronize()
+    assert one == 1
+    if splits == 0:
+        s_plain, ns = _lib.decode_gemm(w, x, min(ns, 8))
+    acc = s_plain[0].clone()
+    for i in range(1, ns):
+        acc += s_plain[i]
+    assert torch.equal(s_red[0], acc)
+    r = ref(w, x)
+    assert (s_red[0].double() - r).abs().max().item() <= 2e-5 * r.abs().max().item() + 1e-6 * K ** 0.5
+
+
 def test_decode_gemm_is_deterministic():
     from paper_2507_11507_b200 import _lib
     w = torch.randn((4096, 4096), device="cuda").to(torch.bfloat16)

@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--batch", type=int, nargs="*", default=[16, 64, 128, 256])
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--shape", nargs="*", default=list(SHAPES))
+    ap.add_argument("--reduce", action="store_true", help="sum the K splits in the kernel (cluster DSMEM)")
     a = ap.parse_args()
     for name in a.shape:
         N, K = SHAPES[name]
@@ -57,7 +58,7 @@ def main():
 
             def ours(i):
                 _lib.LIB.mirage_decode_gemm(st.cuda_stream, ws[i % copies].data_ptr(), N, K, x.data_ptr(), B,
-                                            y.data_ptr(), 0, C.byref(got))
+                                            y.data_ptr(), 0, int(a.reduce and B <= 128), C.byref(got))
 
             def cublas(i):
                 torch.nn.functional.linear(x, ws[i % copies])

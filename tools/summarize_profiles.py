@@ -73,9 +73,24 @@ if __name__ == "__main__":
             for k, (v, u) in m.items():
                 f.write(f"  {k:62s} {v} {u}\n")
     traffic = [to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m["dram__bytes_write.sum"]) for m in ms]
+    # algorithmic bytes of the captured launches (sum_s L_s * 2 * H_kv * D * 2): the
+    # first timed step of `bench.py --config cfg --steps 2 --warmup 1` attends over ctx + 2 tokens
+    sys.path.insert(0, ROOT)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bm = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bm)
+
+    class A:
+        config, batch, ctx, alpha, beta, placement, seed = cfg, 0, 0, 1, 0, "uniform", 0
+    wl, _ = bm.build_workload(A, 0, 1 + 2 + 0 + 1, "reference")
+    sh = wl.tenants[0][0]
+    alg = sum(c + 2 for c in wl.ctxs) * 2 * sh.n_kv_heads * sh.head_dim * 2
     tpath = os.path.join(prof, "attention_traffic.json")
     t = json.load(open(tpath)) if os.path.exists(tpath) else {}
     t[cfg] = {"dram_bytes_per_launch": sum(traffic) / len(traffic), "launches": len(traffic),
+              "algorithmic_bytes_per_launch": alg, "traffic_over_algorithmic": sum(traffic) / len(traffic) / alg,
+              "batch": len(wl.ctxs),
               "source": f"profiles/{tag}_attention_ncu_{cfg}.txt (dram__bytes_read.sum + dram__bytes_write.sum)"}
     json.dump(t, open(tpath, "w"), indent=1)
     print(open(os.path.join(prof, f"{tag}_launch_shares_{cfg}.txt")).read())
