@@ -676,12 +676,11 @@ int32_t gemm_rowpar(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf1
   *nsplit = 1;
   if (!(c->cfg.flags & MIRAGE_FLAG_TC_GEMM) || B > 256 || K % 8) return gemm_lt(c, B, N, K, W, x, y, 0, nullptr, 0);
   int s = mirage::decode_gemm_splits(N, K, B, c->sms);
-  if (B <= 128) s = std::min(s, 8);  // summed inside the GEMM (cluster DSMEM reduction): one slice out
   s = (int)std::max<long long>(1, std::min<long long>(s, y_cap / ((long long)B * N)));
-  int slices = s;
-  KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, y, N, (long long)B * N, s, nullptr, 0, 0, c->cs, nullptr, 0,
-                                   true, &slices));
-  *nsplit = slices;
+  // the slices are summed by the residual kernel (the in-kernel cluster reduction
+  // measured slower: decode_gemm.cu)
+  KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, y, N, (long long)B * N, s, nullptr, 0, 0, c->cs));
+  *nsplit = s;
   return MIRAGE_OK;
 }
 
@@ -693,14 +692,12 @@ int32_t gemm_rowpar(mirage_ctx* c, int B, int N, int K, const bf16* W, const bf1
 int32_t tp_push_gemm(mirage_ctx* c, Model* M, int B, int N, int K, const bf16* W, const bf16* x, uint64_t ep) {
   const int par = (int)(ep & 1);
   float* mine = reinterpret_cast<float*>(M->xfer + kAlign + (par * c->tp + c->tp_rank) * M->xfer_part);
-  // K splits are summed inside the GEMM (cluster reduction) before the push, so
-  // every rank still receives B x N once; without it (B > 128) one split
-  int s = B <= 128 ? std::min(8, mirage::decode_gemm_splits(N, K, B, c->sms)) : 1;
-  int slices = 1;
-  KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, mine, N, 0, s, M->push_dst_dev + par * (c->tp - 1),
-                                   c->tp - 1, 0, c->cs, M->push_cnt_dev, c->tp, true, &slices));
-  if (slices != 1) return fail(c, MIRAGE_ERR_STATE, "tp push GEMM: split not reduced");
-  M->push_expect += (unsigned long long)mirage::decode_gemm_tiles(N) * s;  // every CTA signals
+  // one K split, so every rank receives B x N exactly once (summing the splits in
+  // the kernel through a cluster's distributed shared memory first measured slower:
+  // 13.1 vs 12.4 ms per 70B-TP8 shard step, profiles/r02_tp_push_vs_pull_per_rank.jsonl)
+  KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, mine, N, 0, 1, M->push_dst_dev + par * (c->tp - 1),
+                                   c->tp - 1, 0, c->cs, M->push_cnt_dev, c->tp));
+  M->push_expect += (unsigned long long)mirage::decode_gemm_tiles(N);  // every CTA signals once
   return MIRAGE_OK;
 }
 
