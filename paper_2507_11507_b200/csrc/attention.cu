@@ -140,6 +140,12 @@ __device__ __forceinline__ uint64_t gtimer() {
     if (p.trace) p.trace[(size_t)blockIdx.x * 16 + (slot)] = (val);        \
   } while (0)
 
+// Programmatic dependent launch: let the next kernel of the stream start its
+// prologue now / wait until the previous kernel's results are visible (no-ops
+// when the launch carries no programmatic dependency)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -209,6 +215,7 @@ paged_attention_kernel(const AttnParams p) {
   // q staging (dynamic smem after the rings): [QB][G][2][D/2] packed bf16 hi|lo words, one copy per CTA item
   uint32_t(*qbuf)[GV * D] = reinterpret_cast<uint32_t(*)[GV * D]>(smem + (size_t)kWarps * NS * 2 * TILE);
 
+  pdl_trigger();  // every CTA is resident (one wave): the next launch may start its prologue
   if (threadIdx.x == 0) ATTN_TRACE(0, gtimer());
   if (lane == 0 && warp < kWarps) {
 #pragma unroll
@@ -314,6 +321,18 @@ paged_attention_kernel(const AttnParams p) {
     // ---- producer warp: claim items in order, stage q, then issue every tile of
     // the item to its consumer warp's ring (block j -> warp (j - b0) % W), waiting
     // on that stage's empty barrier once the ring has wrapped ----
+    // The static first item's unit record and first 32 block addresses depend only
+    // on this step's metadata: fetch them before waiting for the previous kernel
+    // (qkv_post writes q and the new token's K/V), so under programmatic dependent
+    // launch these loads overlap that kernel's tail.
+    AttnUnit u_first{};
+    uint64_t a_first = 0;
+    if ((int)blockIdx.x < n_flat) {
+      u_first = p.units[blockIdx.x / p.H_kv];
+      const int j = u_first.b0 + lane;
+      a_first = j < u_first.b1 ? p.addrs[u_first.addr_off + j] : 0;
+    }
+    pdl_wait();
     for (int k = 0;; ++k) {
       const int sl_ = k % QB;
       int item = 0;
@@ -323,7 +342,7 @@ paged_attention_kernel(const AttnParams p) {
         // path of the first tiles); later ones come from the counter, in order
         item = k == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(p.sched, 1);
         if (item < n_flat) {
-          const AttnUnit u = p.units[item / p.H_kv];
+          const AttnUnit u = k == 0 ? u_first : p.units[item / p.H_kv];
           const int nq = QP == 1 ? 1 : u.nq;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           mbar_expect_tx(&qbars[sl_], nq * G * D * 4);
@@ -336,12 +355,12 @@ paged_attention_kernel(const AttnParams p) {
       item = __shfl_sync(0xffffffffu, item, 0);
       if (item >= n_flat) break;
       if (k == 0 && lane == 0) ATTN_TRACE(1, gtimer());
-      const AttnUnit u = p.units[item / p.H_kv];
+      const AttnUnit u = k == 0 ? u_first : p.units[item / p.H_kv];
       const uint64_t off = p.layer_off + (uint64_t)(item % p.H_kv) * (2 * TILE);
       const uint64_t* tbl = p.addrs + u.addr_off;
       for (int base = u.b0; base < u.b1; base += 32) {
         const int j = base + lane;
-        const uint64_t a = j < u.b1 ? tbl[j] + off : 0;
+        const uint64_t a = j < u.b1 ? ((k == 0 && base == u.b0) ? a_first : tbl[j]) + off : 0;
         const int cnt = min(32, u.b1 - base);
         for (int i = 0; i < cnt; ++i) {
           const uint64_t ai = __shfl_sync(0xffffffffu, a, i);
@@ -358,6 +377,7 @@ paged_attention_kernel(const AttnParams p) {
       }
     }
   } else {
+  pdl_wait();  // (inline-producer variants: no early prologue)
   pump(0);
 
   // ldmatrix lane addresses within a K|V tile (swizzled), computed once per warp
@@ -872,9 +892,17 @@ cudaError_t launch_v(const AttnParams& p, cudaStream_t s, bool query, int* grid_
   }
   const long items = (long)p.n_units * p.H_kv;
   const int grid = (int)std::min<long>(items, ctas);
-  paged_attention_kernel<D, G, QP, W, NS, WS>
-      <<<grid, (W + (WS ? 1 : 0)) * 32, smem_bytes<D, G, QP, W, NS>(), s>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3((W + (WS ? 1 : 0)) * 32);
+  cfg.dynamicSmemBytes = smem_bytes<D, G, QP, W, NS>();
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, paged_attention_kernel<D, G, QP, W, NS, WS>, p);
 }
 
 // tuning hook: MIRAGE_ATTN_VARIANT selects alternatives (1: 3-deep rings, inline

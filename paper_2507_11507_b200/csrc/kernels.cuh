@@ -38,7 +38,9 @@ struct AttnParams {
   void* out;                   // [B][H][D] fp32 or bf16
   int32_t out_fp32;
   int32_t qp;                  // rows per unit the launch was planned for (1, or 8 / G for prefill)
-  uint64_t* trace;             // optional [grid][8] %globaltimer stamps per CTA (MIRAGE_ATTN_TRACE), else null
+  uint64_t* trace;             // optional [grid][16] %globaltimer stamps per CTA (MIRAGE_ATTN_TRACE), else null
+  int32_t pdl;                 // launch with a programmatic dependency on the previous kernel (which
+                               // must call griddepcontrol.launch_dependents early, as qkv_post does)
 };
 
 cudaError_t launch_paged_attention(const AttnParams& p, cudaStream_t s);

@@ -40,6 +40,7 @@ __device__ __forceinline__ void store_q_split(uint32_t* p, const float (&v)[8], 
 }
 
 __global__ void q_split_kernel(int64_t n8, int D, const float* q, float sc, uint32_t* out) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the attention launch may start its prologue
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i * 8, row = e / D;
     const int col = (int)(e % D);
@@ -307,6 +308,9 @@ __global__ void __launch_bounds__(256)
 qkv_post_kernel(int family, int H, int Hk, int D, const float* qkv, const __nv_bfloat16* bias,
                 const int32_t* positions, const int32_t* seq_off, const uint64_t* addrs,
                 uint64_t layer_off, float rope_theta, float q_scale, uint32_t* q) {
+  // the attention launch that follows may start its prologue (barriers, its first
+  // work item's metadata) now; it waits (griddepcontrol.wait) before reading q / K / V
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ float cs[];  // [D/2] cos, [D/2] sin
   const int b = blockIdx.x;  // row; blockIdx.y = slice of the row's work items (one per thread)
   const int pos = positions[b];

@@ -1,10 +1,9 @@
 python -c "import __graft_entry__ as g; g.build()" >/dev/null
-python -m pytest tests/test_gpu_decode_gemm.py tests/test_gpu_tp_ipc.py -q -p no:cacheprovider 2>&1 | tail -4
-timeout 300 python tools/gemm_bench.py --batch 16 64 128 --reduce > gpurun_out/r02_gemm_bench_reduce.jsonl 2>&1; cat gpurun_out/r02_gemm_bench_reduce.jsonl | python -c "
+python -m pytest tests -m gpu -q -p no:cacheprovider -x 2>&1 | tail -3
+for P in 0 1; do MIRAGE_PDL=$P MIRAGE_ATTN_REPEAT=8 python tools/attn_bench.py --case llama3_8b_1x8k llama3_8b_1x32k llama3_8b_4x16k llama70b_tp8_64x4k opt13b_b29 opt13b_b400 --reps 10 | python -c "
 import sys,json
 for l in sys.stdin:
-    try:
-        d=json.loads(l); print(d['shape'], d['B'], d['splits'], d['tcgen05_gbs'], d['cublas_gbs'], d['speedup'])
-    except Exception: print(l[:300])"
-for m in pull push; do python tools/tp_shard_step.py --tp 8 --steps 30 --ipc $m; done > gpurun_out/r02f_tp_ipc.jsonl 2>&1
-cat gpurun_out/r02f_tp_ipc.jsonl | cut -c1-250
+    d=json.loads(l); print('pdl=$P', d['case'], round(d['kernel_ms']*1e3,1), round(d['gbs_kernel']))"; done
+for P in 0 1; do for cfg in "--config c4 --batch 1 --alpha 0" "--config c4 --batch 4 --ctx 16384 --alpha 0" "--config c2" ; do MIRAGE_PDL=$P python bench.py $cfg --graphs --steps 30 --warmup 5 --no-cpu-baseline --no-resident-arm --e2e-steps 0 2>/dev/null | python -c "
+import sys,json
+d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('pdl=$P', '$cfg', round(d['ms_per_step'],3), round(d['value']))"; done; done
