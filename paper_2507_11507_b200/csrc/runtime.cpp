@@ -618,8 +618,7 @@ void harvest_attn_times(Model* M) {
   (void)cudaGetLastError();
 }
 
-// MIRAGE_COPY_MODE (experiment): 0 = cudaMemcpyAsync on the copy stream (default),
-// 1 = cudaMemcpyBatchAsync with cudaMemcpyFlagPreferOverlapWithCompute
+// MIRAGE_COPY_MODE (experiment): 0 = cudaMemcpyAsync on the copy stream (default)
 int copy_mode() {
   static const int v = getenv("MIRAGE_COPY_MODE") ? atoi(getenv("MIRAGE_COPY_MODE")) : 0;
   return v;
@@ -1773,15 +1772,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     if (dbg_mode != 1) {  // experiment hook: 1 = events only, no DMA
       void* dst = M->w_dev + (uint64_t)M->cycle[slot] * M->sz.S;
       const void* src = M->host + (uint64_t)nl * M->sz.S;
-      if (copy_mode() == 1) {  // batch API with the overlap-with-compute hint (CUDA 12.8+)
-        void* dsts[1] = {dst};
-        void* srcs[1] = {const_cast<void*>(src)};
-        size_t sizes[1] = {M->sz.S}, aidx[1] = {0}, fail_idx = 0;
-        cudaMemcpyAttributes at{};
-        at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        at.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-        CK(c, cudaMemcpyBatchAsync(dsts, srcs, sizes, 1, &at, aidx, 1, &fail_idx, c->xs));
-      } else {
+      {
         CK(c, cudaMemcpyAsync(dst, src, M->sz.S, cudaMemcpyDefault, c->xs));
       }
     }
