@@ -73,6 +73,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// the same with an L2 cache policy (createpolicy), e.g. evict_first for K|V tiles
+// that are read exactly once per launch
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -133,8 +149,9 @@ __device__ __forceinline__ uint64_t gtimer() {
 }
 // trace slots per CTA (16): 0 entry, 1 first tiles issued, 2 first tile landed
 // (warp 0), 3 last tile consumed (warp 0), 4 last item's output / partial written,
-// 5 last combine done, 6 exit, 7 items processed; combine phases of the last
-// combine: 8 ticket taken, 9 (m, l) staged, 10 weights computed
+// 5 last combine done, 6 exit, 7 items processed, 9 every consumer warp done with
+// the last item (merge starts); combine phases of the last combine: 8 ticket
+// taken, 10 weights computed
 #define ATTN_TRACE(slot, val)                                              \
   do {                                                                     \
     if (p.trace) p.trace[(size_t)blockIdx.x * 16 + (slot)] = (val);        \
@@ -212,6 +229,11 @@ paged_attention_kernel(const AttnParams p) {
   const int tq = lane & 3;   // thread in group
   const int n_flat = (p.n_units_dev ? *p.n_units_dev : p.n_units) * p.H_kv;  // item f = unit * H_kv + kv head
   uint8_t* ring = smem + (size_t)(warp < kWarps ? warp : 0) * NS * 2 * TILE;
+  // items past the static first ones come from the global counter; when the grid
+  // covers every item (the small-batch regime) nobody claims, and the counter
+  // needs no reset at exit
+  const bool dyn = n_flat > (int)gridDim.x;
+  auto claim = [&]() -> int { return dyn ? (int)gridDim.x + atomicAdd(p.sched, 1) : n_flat; };
   // q staging (dynamic smem after the rings): [QB][G][2][D/2] packed bf16 hi|lo words, one copy per CTA item
   uint32_t(*qbuf)[GV * D] = reinterpret_cast<uint32_t(*)[GV * D]>(smem + (size_t)kWarps * NS * 2 * TILE);
 
@@ -250,7 +272,7 @@ paged_attention_kernel(const AttnParams p) {
     int item = 0;
     if (lane == 0) {
       if (atomicCAS(&slot_claim[sl], k - QB, k) == k - QB) {
-        item = k == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(p.sched, 1);
+        item = k == 0 ? (int)blockIdx.x : claim();
         if (item < n_flat) {
           const AttnUnit u = p.units[item / p.H_kv];
           const int nq = QP == 1 ? 1 : u.nq;  // rows u.seq .. u.seq + nq - 1, G heads each
@@ -332,6 +354,7 @@ paged_attention_kernel(const AttnParams p) {
       const int j = u_first.b0 + lane;
       a_first = j < u_first.b1 ? p.addrs[u_first.addr_off + j] : 0;
     }
+    const uint64_t kv_pol = policy_evict_first();
     pdl_wait();
     for (int k = 0;; ++k) {
       const int sl_ = k % QB;
@@ -340,7 +363,7 @@ paged_attention_kernel(const AttnParams p) {
         if (k >= QB) mbar_wait(&slot_free[WS ? sl_ : 0], ((k / QB) - 1) & 1);
         // the first item is static (CTA b takes item b: no atomic on the critical
         // path of the first tiles); later ones come from the counter, in order
-        item = k == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(p.sched, 1);
+        item = k == 0 ? (int)blockIdx.x : claim();
         if (item < n_flat) {
           const AttnUnit u = k == 0 ? u_first : p.units[item / p.H_kv];
           const int nq = QP == 1 ? 1 : u.nq;
@@ -371,7 +394,8 @@ paged_attention_kernel(const AttnParams p) {
             if (t >= NS) mbar_wait(&empty[WS ? w : 0][st], ((t / NS) - 1) & 1);
             uint8_t* dst = smem + (size_t)w * NS * 2 * TILE + st * 2 * TILE;
             mbar_expect_tx(&bars[w][st], 2 * TILE);
-            bulk_g2s(dst, reinterpret_cast<const void*>(ai), 2 * TILE, &bars[w][st]);
+            if (p.fold_mode & 1) bulk_g2s_hint(dst, reinterpret_cast<const void*>(ai), 2 * TILE, &bars[w][st], kv_pol);
+            else bulk_g2s(dst, reinterpret_cast<const void*>(ai), 2 * TILE, &bars[w][st]);
           }
         }
       }
@@ -706,6 +730,7 @@ paged_attention_kernel(const AttnParams p) {
   
     }
 
+    if (threadIdx.x == 0) ATTN_TRACE(9, gtimer());
     // merge the warps in fixed order (w = 0..W-1); every thread derives its head's
     // weights itself: M = max_w m_w, fw_w = 2^(m_w - M) (0 for a warp that saw
     // nothing), Ls = sum_w fw_w l_w, then merges float4s of dims
@@ -776,75 +801,120 @@ paged_attention_kernel(const AttnParams p) {
     csync();
     if (!am_last) continue;
     if (threadIdx.x == 0) ATTN_TRACE(8, gtimer());
-    // (1) per head (one warp each): M = max_i m_i, w_i = 2^(m_i - M), Lambda =
-    // sum_i w_i l_i by a fixed shuffle tree; the w_i go to shared memory
-    float* sw = sm_accf;                          // [kMaxSplitsDev][G]
+    // Every load of the fold is issued ahead of its use, with nothing serial in
+    // between: (0) each thread issues its first two batches of partial o loads
+    // (they do not depend on the weights), (1) one warp per head loads (m_i, l_i)
+    // and derives M, the w_i (zero past ns) and Lambda, (2) o = sum_i w_i o_i /
+    // Lambda, one batch at a time, the batch after next loading meanwhile (double
+    // buffer), with branch-free FMAs (o and w are zero past ns). Arithmetic and
+    // order are those of reading #30 (per column: i = 0..ns-1).
+    constexpr int NCOL = G * D / 4;                                // float4 columns of the G heads
+    constexpr int CPT = (NCOL + kWarps * 32 - 1) / (kWarps * 32);  // columns per thread
+    constexpr int NB = 8 / CPT;                                    // splits per load batch
+    float4 ov0[CPT][NB], ov1[CPT][NB];
+    auto load_batch = [&](float4 (&ov)[CPT][NB], int i0) {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const int e = threadIdx.x + c * kWarps * 32;
+        const float* rg = rec0 + (e / (D / 4)) * (D + 4) + (e % (D / 4)) * 4;
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+          ov[c][k] = (e < NCOL && i0 + k < ns)
+                         ? ((p.fold_mode & 2) ? *reinterpret_cast<const float4*>(rg + (i0 + k) * rstride)
+                                              : __ldcg(reinterpret_cast<const float4*>(rg + (i0 + k) * rstride)))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    float* sw = sm_accf;                          // [G][kMaxSplitsDev], zero past ns
     float* sLam = sm_accf + kMaxSplitsDev * G;    // [G]
-    for (int g = warp; g < G; g += kWarps) {
-      float mv[kMaxSplitsDev / 32], lv[kMaxSplitsDev / 32];
-      float M = -CUDART_INF_F;
+    constexpr int GI = (G + kWarps - 1) / kWarps;  // heads per warp
+    float mv[GI][kMaxSplitsDev / 32], lv[GI][kMaxSplitsDev / 32];
+#pragma unroll
+    for (int gi = 0; gi < GI; ++gi) {  // the (m, l) loads first: they gate the weights
+      const int g = warp + gi * kWarps;
 #pragma unroll
       for (int k = 0; k < kMaxSplitsDev / 32; ++k) {
         const int i = lane + 32 * k;
-        mv[k] = -CUDART_INF_F;
-        lv[k] = 0.f;
-        if (i < ns) {
+        mv[gi][k] = -CUDART_INF_F;
+        lv[gi][k] = 0.f;
+        if (g < G && i < ns) {
           const float2 v = __ldcg(reinterpret_cast<const float2*>(rec0 + i * rstride + g * (D + 4) + D));
-          mv[k] = v.x;
-          lv[k] = v.y;
+          mv[gi][k] = v.x;
+          lv[gi][k] = v.y;
         }
-        M = fmaxf(M, mv[k]);
       }
+    }
+    load_batch(ov0, 0);
+    load_batch(ov1, NB);
+#pragma unroll
+    for (int gi = 0; gi < GI; ++gi) {
+      const int g = warp + gi * kWarps;
+      if (g >= G) break;
+      float M = -CUDART_INF_F;
+#pragma unroll
+      for (int k = 0; k < kMaxSplitsDev / 32; ++k) M = fmaxf(M, mv[gi][k]);
 #pragma unroll
       for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
       float Ls = 0.f;
 #pragma unroll
       for (int k = 0; k < kMaxSplitsDev / 32; ++k) {
         const int i = lane + 32 * k;
-        const float w = i < ns ? exp2f(mv[k] - M) : 0.f;
-        if (i < ns) sw[i * G + g] = w;
-        Ls += w * lv[k];
+        const float w = i < ns ? exp2f(mv[gi][k] - M) : 0.f;
+        sw[g * kMaxSplitsDev + i] = w;
+        Ls += w * lv[gi][k];
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, o);
       if (lane == 0) sLam[g] = Ls;
     }
+    if (threadIdx.x == 0) ATTN_TRACE(10, gtimer());
     csync();
-    // (2) o = sum_i w_i o_i / Lambda: one float4 of dims per thread, 16 (then 8)
-    // independent 16-byte loads in flight (same per-element order as a scalar loop)
-    for (int e = threadIdx.x; e < G * D / 4; e += kWarps * 32) {
-      const int g = e / (D / 4), d = (e % (D / 4)) * 4;
-      const float* rg = rec0 + g * (D + 4) + d;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      int i = 0;
-      for (; i + 16 <= ns; i += 16) {
-        float4 ov[16];
+    float4 acc[CPT];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) ov[k] = __ldcg(reinterpret_cast<const float4*>(rg + (i + k) * rstride));
+    for (int c = 0; c < CPT; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto fma_batch = [&](const float4 (&ov)[CPT][NB], int i0) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const float w = sw[(i + k) * G + g];
-          acc.x += w * ov[k].x;
-          acc.y += w * ov[k].y;
-          acc.z += w * ov[k].z;
-          acc.w += w * ov[k].w;
+      for (int c = 0; c < CPT; ++c) {
+        const int g = min((int)(threadIdx.x + c * kWarps * 32) / (D / 4), G - 1);
+#pragma unroll
+        for (int k4 = 0; k4 < NB / 4; ++k4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(&sw[g * kMaxSplitsDev + i0 + 4 * k4]);
+          const float wk[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4& o = ov[c][4 * k4 + j];
+            acc[c].x += wk[j] * o.x;
+            acc[c].y += wk[j] * o.y;
+            acc[c].z += wk[j] * o.z;
+            acc[c].w += wk[j] * o.w;
+          }
         }
       }
-      for (; i < ns; ++i) {
-        const float4 ov = __ldcg(reinterpret_cast<const float4*>(rg + i * rstride));
-        const float w = sw[i * G + g];
-        acc.x += w * ov.x;
-        acc.y += w * ov.y;
-        acc.z += w * ov.z;
-        acc.w += w * ov.w;
-      }
-      const float lam = sLam[g];
-      const float r[4] = {acc.x / lam, acc.y / lam, acc.z / lam, acc.w / lam};
-      const size_t oi = ((size_t)s * p.H + hk * G + g) * D + d;
+    };
+    for (int i0 = 0; i0 < ns; i0 += 2 * NB) {
+      fma_batch(ov0, i0);
+      if (i0 + 2 * NB < ns) load_batch(ov0, i0 + 2 * NB);
+      if (i0 + NB >= ns) break;
+      fma_batch(ov1, i0 + NB);
+      if (i0 + 3 * NB < ns) load_batch(ov1, i0 + 3 * NB);
+    }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (p.out_fp32) reinterpret_cast<float*>(p.out)[oi + k] = r[k];
-        else reinterpret_cast<__nv_bfloat16*>(p.out)[oi + k] = __float2bfloat16_rn(r[k]);
+    for (int c = 0; c < CPT; ++c) {
+      const int e = threadIdx.x + c * kWarps * 32;
+      if (e >= NCOL) continue;
+      const int g = e / (D / 4), d = (e % (D / 4)) * 4;
+      const float lam = sLam[g];
+      const float4 r = make_float4(acc[c].x / lam, acc[c].y / lam, acc[c].z / lam, acc[c].w / lam);
+      const size_t oi = ((size_t)s * p.H + hk * G + g) * D + d;
+      if (p.out_fp32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oi) = r;
+      } else {
+        const __nv_bfloat162 lo2 = __floats2bfloat162_rn(r.x, r.y);
+        const __nv_bfloat162 hi2 = __floats2bfloat162_rn(r.z, r.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<const uint32_t*>(&lo2);
+        pk.y = *reinterpret_cast<const uint32_t*>(&hi2);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + oi) = pk;
       }
     }
     if (threadIdx.x == 0) ATTN_TRACE(5, gtimer());
@@ -852,8 +922,8 @@ paged_attention_kernel(const AttnParams p) {
   }  // consumer warps
   // the last CTA to finish resets the work counter for the next launch
   __syncthreads();
-  if (threadIdx.x == 0) {
-    ATTN_TRACE(6, gtimer());
+  if (threadIdx.x == 0) ATTN_TRACE(6, gtimer());
+  if (dyn && threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
       atomicExch(p.sched, 0);

@@ -636,6 +636,12 @@ void drop_graphs(Model* M) {
   M->cap_free_ev.clear();
 }
 
+// MIRAGE_ATTN_FOLD (experiment bits, see AttnParams::fold_mode)
+int attn_fold_mode() {
+  static const int v = getenv("MIRAGE_ATTN_FOLD") ? atoi(getenv("MIRAGE_ATTN_FOLD")) : 1;
+  return v;
+}
+
 // MIRAGE_PDL=0 disables programmatic dependent launch of the attention kernel
 int use_pdl() {
   static const int v = !(getenv("MIRAGE_PDL") && atoi(getenv("MIRAGE_PDL")) == 0);
@@ -1862,6 +1868,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   ap.out_fp32 = 0;
   ap.qp = qp;
   ap.pdl = use_pdl();  // programmatic dependency on qkv_post (which precedes it in the stream)
+  ap.fold_mode = attn_fold_mode();
   const bool time_attn = c->cfg.flags & MIRAGE_FLAG_TIME_ATTN;
   uint64_t attn_bytes = 0;
   for (int i = 0; i < B; ++i) attn_bytes += (uint64_t)hv.len[i] * 2 * Hk * D * 2;
@@ -2107,6 +2114,7 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
   ap.out = out_dev;
   ap.out_fp32 = out_fp32;
   ap.pdl = use_pdl();  // programmatic dependency on q_split (or the previous repeat)
+  ap.fold_mode = attn_fold_mode();
   if (c->attn_trace) {
     const int ctas = mirage::attention_grid_ctas(s.H, s.Hk, s.D);
     c->attn_trace_ctas = std::min(mirage_ctx::kTraceCtas, std::min(ctas, n_units * s.Hk));

@@ -91,7 +91,7 @@ def trace_summary(tr):
     t0 = a[:, 0][a[:, 0] > 0].min()
     out = {"ctas": len(a)}
     for i, nm in [(0, "entry"), (1, "issued"), (2, "landed"), (3, "consumed"), (4, "written"), (8, "ticket"),
-                  (9, "staged"), (10, "weights"), (5, "combined"), (6, "exit")]:
+                  (9, "warps_done"), (10, "weights"), (11, "fold1"), (12, "fold2"), (5, "combined"), (6, "exit")]:
         v = a[:, i]
         v = (v[v > 0] - t0) / 1e3
         if len(v):
