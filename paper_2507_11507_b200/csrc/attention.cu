@@ -151,7 +151,8 @@ __device__ __forceinline__ uint64_t gtimer() {
 // (warp 0), 3 last tile consumed (warp 0), 4 last item's output / partial written,
 // 5 last combine done, 6 exit, 7 items processed, 9 every consumer warp done with
 // the last item (merge starts); combine phases of the last combine: 8 ticket
-// taken, 10 weights computed
+// taken, 10 weights computed; 12-15 SM cycles from the merge start to the ticket,
+// M of head 0, the weights barrier and the end of the fold
 #define ATTN_TRACE(slot, val)                                              \
   do {                                                                     \
     if (p.trace) p.trace[(size_t)blockIdx.x * 16 + (slot)] = (val);        \
@@ -730,7 +731,11 @@ paged_attention_kernel(const AttnParams p) {
   
     }
 
-    if (threadIdx.x == 0) ATTN_TRACE(9, gtimer());
+    uint64_t c9 = 0;  // trace: SM clock at the merge start (fold phases below in cycles from here)
+    if (threadIdx.x == 0 && p.trace) {
+      ATTN_TRACE(9, gtimer());
+      c9 = clock64();
+    }
     // merge the warps in fixed order (w = 0..W-1); every thread derives its head's
     // weights itself: M = max_w m_w, fw_w = 2^(m_w - M) (0 for a warp that saw
     // nothing), Ls = sum_w fw_w l_w, then merges float4s of dims
@@ -800,7 +805,10 @@ paged_attention_kernel(const AttnParams p) {
     }
     csync();
     if (!am_last) continue;
-    if (threadIdx.x == 0) ATTN_TRACE(8, gtimer());
+    if (threadIdx.x == 0) {
+      ATTN_TRACE(8, gtimer());
+      ATTN_TRACE(12, clock64() - c9);
+    }
     // Every load of the fold is issued ahead of its use, with nothing serial in
     // between: (0) each thread issues its first two batches of partial o loads
     // (they do not depend on the weights), (1) one warp per head loads (m_i, l_i)
@@ -855,6 +863,7 @@ paged_attention_kernel(const AttnParams p) {
       for (int k = 0; k < kMaxSplitsDev / 32; ++k) M = fmaxf(M, mv[gi][k]);
 #pragma unroll
       for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      if (threadIdx.x == 0 && gi == 0) ATTN_TRACE(13, clock64() - c9);
       float Ls = 0.f;
 #pragma unroll
       for (int k = 0; k < kMaxSplitsDev / 32; ++k) {
@@ -869,6 +878,7 @@ paged_attention_kernel(const AttnParams p) {
     }
     if (threadIdx.x == 0) ATTN_TRACE(10, gtimer());
     csync();
+    if (threadIdx.x == 0) ATTN_TRACE(14, clock64() - c9);
     float4 acc[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -917,7 +927,10 @@ paged_attention_kernel(const AttnParams p) {
         *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + oi) = pk;
       }
     }
-    if (threadIdx.x == 0) ATTN_TRACE(5, gtimer());
+    if (threadIdx.x == 0) {
+      ATTN_TRACE(15, clock64() - c9);
+      ATTN_TRACE(5, gtimer());
+    }
   }
   }  // consumer warps
   // the last CTA to finish resets the work counter for the next launch

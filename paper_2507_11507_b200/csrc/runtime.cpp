@@ -506,7 +506,8 @@ int choose_split(const int32_t* lens, int B, int Hk, int G, int grid, int warps)
     return (double)n * Hk;
   };
   int P = std::max(p_lo, max_nb);
-  if (items(P) < grid) {
+  const bool lpt = items(P) >= grid;  // the unsplit batch already has an item for every CTA
+  if (!lpt) {
     // Fewer items than resident CTAs: split until the items just fill the grid
     // (the smallest P with items(P) <= grid). Every CTA then holds one item, so
     // the SMs carry equal loads (ncu on 1 x 32k: SMs with 2 CTAs ran ~1.6x
@@ -522,6 +523,16 @@ int choose_split(const int32_t* lens, int B, int Hk, int G, int grid, int warps)
   while (P > p_lo && items(P) < need) {
     const int next = std::max(p_lo, std::min(P - 1, (int)(P * 0.97)));
     P = next;
+  }
+  // a skewed batch (ShareGPT lengths at small B): with enough items for the grid,
+  // the longest item still bounds the LPT makespan, so no item may exceed 0.6 of
+  // the average load per CTA (C2 P-paper B=29, OPT-13B: split 95 -> 33 blocks,
+  // 41.9 -> ~37 us per launch in the tools/attn_bench.py --split sweep)
+  if (lpt) {
+    int64_t total = 0;
+    for (int b = 0; b < B; ++b) total += nbs[b];
+    const int cap = (int)std::ceil(0.6 * (double)total * Hk / std::max(grid, 1));
+    P = std::max(p_lo, std::min(P, std::max(cap, 1)));
   }
   // equalise the longest sequence's splits (no runt last split)
   const int ns = (max_nb + P - 1) / P;

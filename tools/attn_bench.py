@@ -91,11 +91,16 @@ def trace_summary(tr):
     t0 = a[:, 0][a[:, 0] > 0].min()
     out = {"ctas": len(a)}
     for i, nm in [(0, "entry"), (1, "issued"), (2, "landed"), (3, "consumed"), (4, "written"), (8, "ticket"),
-                  (9, "warps_done"), (10, "weights"), (11, "fold1"), (12, "fold2"), (5, "combined"), (6, "exit")]:
+                  (9, "warps_done"), (10, "weights"), (5, "combined"), (6, "exit")]:
         v = a[:, i]
         v = (v[v > 0] - t0) / 1e3
         if len(v):
             out[nm] = [round(float(np.percentile(v, 5)), 2), round(float(np.median(v)), 2), round(float(v.max()), 2)]
+    for i, nm in [(12, "cyc_ticket"), (13, "cyc_M"), (14, "cyc_weights"), (15, "cyc_fold")]:
+        v = a[:, i]
+        v = v[(v > 0) & (v < 1e7)]  # SM cycles from the merge start (fold CTAs of this launch)
+        if len(v):
+            out[nm] = [int(np.median(v)), int(v.max())]
     out["items"] = [int(a[:, 7].min()), int(a[:, 7].max())]
     return out
 

@@ -3,7 +3,8 @@ the per-CTA stamps (median / max, us after the first CTA entry)."""
 import json
 import sys
 
-KEYS = ["issued", "landed", "consumed", "warps_done", "written", "ticket", "weights", "combined", "exit"]
+KEYS = ["issued", "landed", "consumed", "warps_done", "written", "ticket", "weights", "combined", "exit",
+        "cyc_ticket", "cyc_M", "cyc_weights", "cyc_fold"]
 for f in sys.argv[1:] or ["gpurun_out/trace.jsonl", "gpurun_out/grid_b2b.jsonl"]:
     try:
         lines = open(f).readlines()
@@ -16,5 +17,5 @@ for f in sys.argv[1:] or ["gpurun_out/trace.jsonl", "gpurun_out/grid_b2b.jsonl"]
         t = r.get("trace")
         s = f"{tag}{r['case']:20s} {r['kernel_ms'] * 1e3:6.1f} us {r['gbs_kernel']:6.0f} GB/s"
         if t:
-            s += "  " + " ".join(f"{k}={t[k][1]}/{t[k][2]}" for k in KEYS if k in t)
+            s += "  " + " ".join(f"{k}={t[k][-2]}/{t[k][-1]}" for k in KEYS if k in t)
         print(s)
