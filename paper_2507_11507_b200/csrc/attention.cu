@@ -394,9 +394,20 @@ paged_attention_kernel(const AttnParams p) {
             const int st = t % NS;
             if (t >= NS) mbar_wait(&empty[WS ? w : 0][st], ((t / NS) - 1) & 1);
             uint8_t* dst = smem + (size_t)w * NS * 2 * TILE + st * 2 * TILE;
-            mbar_expect_tx(&bars[w][st], 2 * TILE);
-            if (p.fold_mode & 1) bulk_g2s_hint(dst, reinterpret_cast<const void*>(ai), 2 * TILE, &bars[w][st], kv_pol);
-            else bulk_g2s(dst, reinterpret_cast<const void*>(ai), 2 * TILE, &bars[w][st]);
+            // the last, partly filled block of a sequence: fetch only its valid token
+            // rows of K and of V (the consumer masks the scores of the other rows and
+            // zeroes their V rows), so DRAM traffic equals the algorithmic bytes
+            const int vr = min(16, u.len + (QP > 1 ? u.nq - 1 : 0) - (base + i) * 16);
+            const uint32_t part = vr < 16 ? (uint32_t)vr * ROW : 2u * TILE;
+            mbar_expect_tx(&bars[w][st], vr < 16 ? 2 * part : part);
+            const char* src = reinterpret_cast<const char*>(ai);
+            if (p.fold_mode & 1) {
+              bulk_g2s_hint(dst, src, part, &bars[w][st], kv_pol);
+              if (vr < 16) bulk_g2s_hint(dst + TILE, src + TILE, part, &bars[w][st], kv_pol);
+            } else {
+              bulk_g2s(dst, src, part, &bars[w][st]);
+              if (vr < 16) bulk_g2s(dst + TILE, src + TILE, part, &bars[w][st]);
+            }
           }
         }
       }
