@@ -416,7 +416,8 @@ int32_t mirage_sync(mirage_ctx* ctx);
 /* Paged attention of one layer only (a8+a9), over the sequences' current
  * cached lengths. q_dev: device fp32 [batch, H, D]; out_dev: device [batch, H,
  * D] fp32 (out_fp32 = 1) or bf16. split_tokens_override > 0 forces the split
- * size (multiple of 16). Errors: RANGE, STATE (a sequence with 0 tokens). */
+ * size (multiple of 16); -1 forces the balanced-range schedule.
+ * Errors: RANGE, STATE (a sequence with 0 tokens). */
 int32_t mirage_attn_only(mirage_ctx* ctx, int32_t model, int32_t layer, int32_t batch,
                          const int64_t* seq_ids, const float* q_dev, void* out_dev,
                          int32_t out_fp32, int32_t split_tokens_override);

@@ -233,8 +233,22 @@ paged_attention_kernel(const AttnParams p) {
   // items past the static first ones come from the global counter; when the grid
   // covers every item (the small-batch regime) nobody claims, and the counter
   // needs no reset at exit
-  const bool dyn = n_flat > (int)gridDim.x;
+  // Balanced ranges (schedule 1, decode): CTA b runs the units of range b / H_kv,
+  // in order, for kv head b % H_kv; no queue
+  const bool rmode = p.hdr != nullptr && p.hdr[1] == 1;
+  int r_first = 0, r_end = 0, r_kvh = 0;
+  if (rmode) {
+    r_first = p.rfirst[blockIdx.x / p.H_kv];
+    r_end = p.rfirst[blockIdx.x / p.H_kv + 1];
+    r_kvh = blockIdx.x % p.H_kv;
+  }
+  const bool dyn = !rmode && n_flat > (int)gridDim.x;
   auto claim = [&]() -> int { return dyn ? (int)gridDim.x + atomicAdd(p.sched, 1) : n_flat; };
+  // the CTA's k-th work item (item f = unit * H_kv + kv head)
+  auto item_at = [&](int k) -> int {
+    if (rmode) return r_first + k < r_end ? (r_first + k) * p.H_kv + r_kvh : n_flat;
+    return k == 0 ? (int)blockIdx.x : claim();
+  };
   // q staging (dynamic smem after the rings): [QB][G][2][D/2] packed bf16 hi|lo words, one copy per CTA item
   uint32_t(*qbuf)[GV * D] = reinterpret_cast<uint32_t(*)[GV * D]>(smem + (size_t)kWarps * NS * 2 * TILE);
 
@@ -273,7 +287,7 @@ paged_attention_kernel(const AttnParams p) {
     int item = 0;
     if (lane == 0) {
       if (atomicCAS(&slot_claim[sl], k - QB, k) == k - QB) {
-        item = k == 0 ? (int)blockIdx.x : claim();
+        item = item_at(k);
         if (item < n_flat) {
           const AttnUnit u = p.units[item / p.H_kv];
           const int nq = QP == 1 ? 1 : u.nq;  // rows u.seq .. u.seq + nq - 1, G heads each
@@ -350,8 +364,8 @@ paged_attention_kernel(const AttnParams p) {
     // launch these loads overlap that kernel's tail.
     AttnUnit u_first{};
     uint64_t a_first = 0;
-    if ((int)blockIdx.x < n_flat) {
-      u_first = p.units[blockIdx.x / p.H_kv];
+    if (rmode ? r_first < r_end : (int)blockIdx.x < n_flat) {
+      u_first = p.units[rmode ? r_first : blockIdx.x / p.H_kv];
       const int j = u_first.b0 + lane;
       a_first = j < u_first.b1 ? p.addrs[u_first.addr_off + j] : 0;
     }
@@ -364,7 +378,7 @@ paged_attention_kernel(const AttnParams p) {
         if (k >= QB) mbar_wait(&slot_free[WS ? sl_ : 0], ((k / QB) - 1) & 1);
         // the first item is static (CTA b takes item b: no atomic on the critical
         // path of the first tiles); later ones come from the counter, in order
-        item = k == 0 ? (int)blockIdx.x : claim();
+        item = item_at(k);
         if (item < n_flat) {
           const AttnUnit u = k == 0 ? u_first : p.units[item / p.H_kv];
           const int nq = QP == 1 ? 1 : u.nq;

@@ -30,6 +30,10 @@ struct AttnParams {
   const AttnUnit* units;       // [n_units], longest first
   int32_t n_units;             // host count (sizes the grid)
   const int32_t* n_units_dev;  // if set, the count is read here (CUDA-graph replays)
+  const int32_t* hdr;          // step metadata header: [1] = schedule (0 = longest-first queue,
+                               // 1 = balanced ranges: CTA b runs units rfirst[b / H_kv] ..
+                               // rfirst[b / H_kv + 1] - 1 for kv head b % H_kv; grid = R * H_kv)
+  const int32_t* rfirst;       // [R + 1] first unit of each range (schedule 1)
   int32_t H, H_kv, D;
   float scale_log2;            // log2(e) / sqrt(D) (already applied to q)
   float* partial;              // [(pbase + split) * H + h][D + 4]: o, m, l, pad

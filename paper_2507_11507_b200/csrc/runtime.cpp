@@ -431,9 +431,11 @@ Model* get_model(mirage_ctx* c, int32_t id) {
 // the host (addrs[seq_off[i] + j] = block_base[table[i][j]]), so the kernels
 // need no dependent table lookups. The KV hooks reuse the address region for a
 // plain int32 table row.
+constexpr int kMaxRanges = 512;  // balanced-range mode: ranges (= grid / H_kv) per launch
 struct MetaView {
-  int32_t* hdr;  // [4]: n_units, ...
+  int32_t* hdr;  // [4]: n_units, attention mode (0 = LPT queue, 1 = balanced ranges), ...
   int32_t *tokens, *pos, *len, *seq_off;
+  int32_t* rfirst;  // [kMaxRanges + 1]: first unit of each balanced range (mode 1)
   mirage::AttnUnit* units;
   uint64_t* addrs;
   int32_t* tables;  // aliases addrs (fill/write hooks only)
@@ -448,6 +450,7 @@ MetaView meta_view(mirage_ctx* c, char* base) {
   v.pos = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
   v.len = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
   v.seq_off = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)Bm * 4, 16);
+  v.rfirst = reinterpret_cast<int32_t*>(p); p += align_up((uint64_t)(kMaxRanges + 1) * 4, 16);
   v.units = reinterpret_cast<mirage::AttnUnit*>(p); p += align_up((uint64_t)c->max_units * sizeof(mirage::AttnUnit), 16);
   v.addrs = reinterpret_cast<uint64_t*>(p);
   v.tables = reinterpret_cast<int32_t*>(p);
@@ -456,7 +459,7 @@ MetaView meta_view(mirage_ctx* c, char* base) {
 
 size_t meta_size(mirage_ctx* c) {
   const int Bm = c->cfg.max_batch;
-  return 16 + 4 * align_up((uint64_t)Bm * 4, 16) + align_up((uint64_t)c->max_units * sizeof(mirage::AttnUnit), 16) +
+  return 16 + 4 * align_up((uint64_t)Bm * 4, 16) + align_up((uint64_t)(kMaxRanges + 1) * 4, 16) + align_up((uint64_t)c->max_units * sizeof(mirage::AttnUnit), 16) +
          (uint64_t)Bm * c->max_blk * 8;
 }
 
@@ -539,10 +542,101 @@ int choose_split(const int32_t* lens, int B, int Hk, int G, int grid, int warps)
   return std::max(1, (max_nb + ns - 1) / ns);
 }
 
+bool ranges_enabled();
+
+// Balanced ranges (stream-K over the batch): when the one-item-per-CTA split of
+// choose_split leaves CTAs idle (e.g. 70B-TP8, 64 sequences x 1 kv head: 256
+// equal items on 296 CTAs, so 40 SMs carry one CTA and 108 carry two), the
+// concatenated block stream of the batch (sequence order) is cut into
+// R = grid / Hk equal ranges instead; range r runs on the Hk CTAs r*Hk ..
+// r*Hk + Hk - 1 (one per kv head) as the one or more pieces (units) of the
+// sequences it overlaps. A sequence's pieces are its splits, in order, folded by
+// the same split-K combine. Depends on logical lengths only (placement
+// independent). Returns the unit count (units in range order, rfirst[r] = the
+// first unit of range r, rfirst[R] = count) or -1.
+int build_units_ranges(const int32_t* lens, const int32_t* seq_off, int B, int Hk, int grid,
+                       mirage::AttnUnit* units, int max_units, int32_t* rfirst) {
+  const int R = grid / Hk;
+  if (R < 1 || R > kMaxRanges) return -1;
+  std::vector<int> nbs(B), pieces(B, 0), pbase(B, 0);
+  int64_t T = 0;
+  for (int b = 0; b < B; ++b) {
+    nbs[b] = (lens[b] + kBlockTokens - 1) / kBlockTokens;
+    T += nbs[b];
+  }
+  int n = 0, b = 0;
+  int64_t seq_start = 0;  // stream offset of sequence b's block 0
+  for (int r = 0; r < R; ++r) {
+    const int64_t lo = T * r / R, hi = T * (r + 1) / R;
+    rfirst[r] = n;
+    while (b < B && seq_start + nbs[b] <= lo) seq_start += nbs[b++];  // (only empty sequences)
+    int64_t at = lo;
+    int bb = b;
+    int64_t st = seq_start;
+    while (at < hi && bb < B) {
+      const int64_t end = std::min(hi, st + nbs[bb]);
+      if (end > at) {
+        if (n >= max_units) return -1;
+        units[n++] = mirage::AttnUnit{bb, (int16_t)pieces[bb], 0, 0, lens[bb], (int32_t)(at - st), (int32_t)(end - st),
+                                      seq_off[bb], 1};
+        ++pieces[bb];
+        at = end;
+      }
+      if (at >= st + nbs[bb]) {
+        st += nbs[bb];
+        ++bb;
+      }
+    }
+  }
+  rfirst[R] = n;
+  int pb = 0;
+  for (int q = 0; q < B; ++q) {
+    if (pieces[q] > kMaxSplits) return -1;
+    pbase[q] = pb;
+    if (pieces[q] > 1) pb += pieces[q];
+  }
+  for (int i = 0; i < n; ++i) {
+    const int q = units[i].seq;
+    units[i].nsplit = (int16_t)pieces[q];
+    units[i].pbase = pieces[q] > 1 ? pbase[q] : 0;
+  }
+  return n;
+}
+
+// Use balanced ranges? Only when choose_split's one-item-per-CTA plan fills less
+// than 0.97 of the grid (decode steps, grid a multiple of Hk) and every range is
+// long (>= 256 blocks): a CTA's second piece costs a merge during which its TMA
+// rings stall, which outweighs the balance gain on short ranges (70B-TP8 64 x 4k,
+// 55 blocks per range: 32.9 -> 35.1 us; 32 x 32k, 1771 blocks: 601.8 -> 595.6 us,
+// 16 x 16k: 159.0 -> 157.4 us; profiles/r02g_attn_ranges_b2b.jsonl).
+bool want_ranges(const int32_t* lens, int B, int Hk, int grid, int P) {
+  if (grid % Hk || grid / Hk > kMaxRanges || B < 1) return false;
+  int64_t items = 0, T = 0;
+  for (int b = 0; b < B; ++b) {
+    const int nb = (lens[b] + kBlockTokens - 1) / kBlockTokens;
+    items += (nb + P - 1) / P;
+    T += nb;
+  }
+  items *= Hk;
+  return items < grid && items < (int64_t)(0.97 * grid) && T >= 256ll * (grid / Hk);
+}
+
 int build_units(const int32_t* lens, const int32_t* seq_off, int B, int Hk, int G, int grid, int warps,
-                int override_blocks, mirage::AttnUnit* units, int max_units, int* split_blocks) {
+                int override_blocks, mirage::AttnUnit* units, int max_units, int* split_blocks,
+                int32_t* mode = nullptr, int32_t* rfirst = nullptr) {
   int P = choose_split(lens, B, Hk, G, grid, warps);
   if (override_blocks > 0) P = override_blocks;
+  if (mode) *mode = 0;
+  // (override_blocks < 0: the test hook that forces the balanced-range schedule)
+  if (mode && rfirst && (override_blocks < 0 || (override_blocks == 0 && ranges_enabled() &&
+                                                  want_ranges(lens, B, Hk, grid, P)))) {
+    const int n = build_units_ranges(lens, seq_off, B, Hk, grid, units, max_units, rfirst);
+    if (n > 0) {
+      *mode = 1;
+      *split_blocks = 0;
+      return n;
+    }
+  }
   int n = 0, pbase = 0;
   for (int b = 0; b < B; ++b) {
     const int nb = (lens[b] + kBlockTokens - 1) / kBlockTokens;
@@ -645,6 +739,12 @@ void drop_graphs(Model* M) {
   for (auto e : M->cap_free_ev) cudaEventDestroy(e);
   M->cap_ready_ev.clear();
   M->cap_free_ev.clear();
+}
+
+// MIRAGE_ATTN_RANGES=0 disables the balanced-range attention schedule
+bool ranges_enabled() {
+  static const bool v = !(getenv("MIRAGE_ATTN_RANGES") && atoi(getenv("MIRAGE_ATTN_RANGES")) == 0);
+  return v;
 }
 
 // MIRAGE_ATTN_FOLD (experiment bits, see AttnParams::fold_mode)
@@ -1701,12 +1801,15 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   bool multi_row = false;  // a prefill / extend step: some sequence has several rows
   for (int i = 0; i < B && !multi_row; ++i) multi_row = first_row[i] != i;
   const int qp = multi_row ? mirage::attention_prefill_rows(s.H, s.Hk) : 1;
+  int32_t attn_mode = 0;
   const int n_units =
       qp > 1 ? build_units_rows(hv.len, hv.seq_off, seq_ids, B, qp, hv.units, c->max_units)
              : build_units(hv.len, hv.seq_off, B, s.Hk, s.H / s.Hk, mirage::attention_grid_ctas(s.H, s.Hk, s.D),
-                           mirage::attention_cta_warps(s.Hk), 0, hv.units, c->max_units, &split_blocks);
+                           mirage::attention_cta_warps(s.Hk), 0, hv.units, c->max_units, &split_blocks, &attn_mode,
+                           hv.rfirst);
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "step: too many attention units");
   hv.hdr[0] = n_units;
+  hv.hdr[1] = attn_mode;
   cudaStream_t cs = c->cs;
   const bool timed = !M->step_timed && !multi_row;  // T_Compute = a decode step, not a prefill
   if (timed) CK(c, cudaEventRecord(M->st0, cs));
@@ -1862,6 +1965,8 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   ap.q = M->q;
   ap.addrs = dv.addrs;
   ap.units = dv.units;
+  ap.hdr = dv.hdr;
+  ap.rfirst = dv.rfirst;
   ap.n_units = n_units;
   ap.n_units_dev = nullptr;
   if (capturing) {  // replays keep the full persistent grid; the unit count comes from the metadata
@@ -2079,7 +2184,7 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
   if (c->host_only) return fail(c, MIRAGE_ERR_STATE, "host-only context has no device");
   Model* M = get_model(c, model);
   if (!M || layer < 0 || layer >= M->shp.n || B <= 0 || B > c->cfg.max_batch || !seq_ids || !q_dev ||
-      !out_dev || split_tokens_override < 0 || split_tokens_override % kBlockTokens)
+      !out_dev || split_tokens_override < -1 || (split_tokens_override > 0 && split_tokens_override % kBlockTokens))
     return fail(c, MIRAGE_ERR_RANGE, "attn_only: arguments");
   char* host;
   if (int32_t e = acquire_stage(c, &host)) return e;
@@ -2099,9 +2204,11 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
   int split_blocks = 1;
   const int n_units = build_units(hv.len, hv.seq_off, B, M->shp.Hk, M->shp.H / M->shp.Hk,
                                   mirage::attention_grid_ctas(M->shp.H, M->shp.Hk, M->shp.D),
-                                  mirage::attention_cta_warps(M->shp.Hk), split_tokens_override / kBlockTokens,
-                                  hv.units, c->max_units, &split_blocks);
+                                  mirage::attention_cta_warps(M->shp.Hk),
+                                  split_tokens_override < 0 ? -1 : split_tokens_override / kBlockTokens,
+                                  hv.units, c->max_units, &split_blocks, &hv.hdr[1], hv.rfirst);
   if (n_units < 0) return fail(c, MIRAGE_ERR_RANGE, "attn_only: too many units for the split override");
+  hv.hdr[0] = n_units;
     if (int32_t e = upload_meta(c, host, n_addr)) return e;
   CK(c, cudaEventRecord(c->stage_ev[c->stage_i], c->cs));
   M->last_units = n_units;
@@ -2114,6 +2221,8 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
   ap.addrs = dv.addrs;
   ap.layer_off = (uint64_t)layer * s.Hk * 2 * kBlockTokens * s.D * 2;
   ap.units = dv.units;
+  ap.hdr = dv.hdr;
+  ap.rfirst = dv.rfirst;
   ap.n_units = n_units;
   ap.H = s.H;
   ap.H_kv = s.Hk;

@@ -189,3 +189,12 @@ def test_full_width_prefill_vs_oracle(base):
     for i in range(B):
         if srt[i, -1] - srt[i, -2] > 2 * 3 * row_norm * err:
             assert am[i] == int(np.argmax(exact[1][1][i])), i
+
+
+def test_balanced_ranges_schedule_16x16k_all_rows():
+    """Schedule 1 (balanced ranges): 16 x 16k Llama-3-8B would be 256
+    one-per-CTA items on 296 CTAs; the planner cuts the batch's block stream into
+    37 equal ranges instead (pieces straddle sequences). Every row against c3."""
+    worst, st = run_all_rows(attn_shape(32, 32, 8, 16384), [16384 - 5 * i for i in range(16)], layer=9)
+    assert worst <= TOL, worst
+    assert st["last_split_blocks"] == 0          # the planner chose balanced ranges
