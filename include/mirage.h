@@ -458,6 +458,20 @@ int64_t mirage_kernel_launches(const mirage_ctx* ctx);
 int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
                            float* y_dev, int32_t splits, int32_t reduce, int32_t* splits_out);
 
+/* Test/bench hook: the persistent stream-K form of the tcgen05 decode GEMM
+ * (SURVEY §8(a) a6 supporting row, NEXT-4): one wave of CTAs
+ * walks the tiles x 64-wide K blocks in order, and a tile cut between CTAs is
+ * finished inside the GEMM by the CTA holding its first K block, which adds the
+ * others' parked fp32 partials in K order (deterministic). Computes
+ * y = epilogue(X W^T) for W = w_dev bf16 [N][K], X = x_dev bf16 [B][K]
+ * (row-major, device memory, K % 8 == 0, 1 <= B <= 256): + bias_dev[N] (bf16,
+ * or NULL), then max(., 0) if relu, stored to y_dev fp32 [B][N] or, if y_dev is
+ * NULL, to y16_dev bf16 [B][N]. Uses a library-owned workspace (per process,
+ * grown on demand). Enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ * stream). Errors: RANGE, CUDA. */
+int32_t mirage_sk_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
+                       float* y_dev, void* y16_dev, const void* bias_dev, int32_t relu);
+
 /* Profiling hook. With the environment variable MIRAGE_ATTN_TRACE set when the
  * ctx is created, every attention launch of mirage_attn_only records 16
  * %globaltimer slots per CTA (ns: entry, first tiles issued, first tile

@@ -115,6 +115,7 @@ def _load():
         "mirage_kernel_launches": (I64, [P]),
         "mirage_attn_trace": (I32, [P, pU64, I32, pI32]),
         "mirage_decode_gemm": (I32, [P, P, I32, I32, P, I32, P, I32, I32, pI32]),
+        "mirage_sk_gemm": (I32, [P, P, I32, I32, P, I32, P, P, P, I32]),
         "mirage_nccl_unique_id": (I32, [P]),
         "mirage_host_register": (I32, [P, U64]),
         "mirage_region_count": (I32, [P, I32, pI32]),
@@ -145,7 +146,7 @@ EXPORTED = [
     "mirage_host_register", "mirage_host_unregister", "mirage_region_count", "mirage_region_info",
     "mirage_unremap", "mirage_swap_out", "mirage_swap_in", "mirage_set_weight_source", "mirage_tp_export",
     "mirage_tp_import", "mirage_prefill", "mirage_migrate_region", "mirage_predict_stall",
-    "mirage_attn_trace", "mirage_decode_gemm"]
+    "mirage_attn_trace", "mirage_decode_gemm", "mirage_sk_gemm"]
 
 
 def model_cfg(shape):
@@ -210,6 +211,23 @@ def decode_gemm(w, x, splits=0, stream=None, reduce=False):
     if rc:
         raise MirageError(rc, "decode_gemm")
     return y[: got.value], got.value
+
+
+def sk_gemm(w, x, bias=None, relu=False, out_bf16=False, stream=None):
+    """y [B][N] = epilogue(x [B][K] @ w[N][K]^T) on the persistent stream-K tcgen05
+    GEMM (mirage_sk_gemm); bf16 CUDA tensors; fp32 output unless out_bf16."""
+    assert w.dtype == torch.bfloat16 and x.dtype == torch.bfloat16 and w.is_cuda and x.is_cuda
+    w, x = w.contiguous(), x.contiguous()
+    N, K = w.shape
+    B = x.shape[0]
+    y = torch.empty((B, N), dtype=torch.bfloat16 if out_bf16 else torch.float32, device=w.device)
+    st = stream if stream is not None else torch.cuda.current_stream(w.device)
+    rc = LIB.mirage_sk_gemm(st.cuda_stream, w.data_ptr(), N, K, x.data_ptr(), B,
+                            None if out_bf16 else y.data_ptr(), y.data_ptr() if out_bf16 else None,
+                            None if bias is None else bias.contiguous().data_ptr(), int(bool(relu)))
+    if rc:
+        raise MirageError(rc, "sk_gemm")
+    return y
 
 
 def nccl_unique_id():

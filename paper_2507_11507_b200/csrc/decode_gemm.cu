@@ -36,6 +36,7 @@ namespace {
 constexpr int kTileM = 128;  // weight rows per tile (MMA M)
 constexpr int kTileK = 64;   // K per stage: one 128-byte swizzle row of bf16
 constexpr int kMaxClusterSplits = 8;  // portable cluster size
+constexpr int kSkMinUnits = 3;        // stream-K GEMM: K blocks per CTA at least
 // ring depth: ~96-104 KB of stages per CTA, so two CTAs share an SM (two tiles
 // streaming per SM: the grid of a decode GEMM is ~1-2 waves of small tiles)
 template <int BN>
@@ -269,6 +270,239 @@ decode_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
   }
 }
 
+// ---- persistent stream-K decode GEMM ("SK") -----------------------------------
+// The grid is one wave of G resident CTAs. The tiles x K-blocks of the GEMM are
+// one stream of units (tile-major); CTA c takes the contiguous units
+// [c U / G, (c+1) U / G), i.e. the tail of one tile, whole tiles, and the head of
+// another. A tile cut between CTAs is finished by the CTA holding its K-block 0
+// (the "owner", whose head piece is the LAST segment of its range): the others
+// (whose piece is the FIRST segment of theirs, so they never wait) park their fp32
+// partial in a per-CTA workspace slot and raise a flag; the owner adds the parked
+// partials to its own in K order (deterministic) and stores the final tile once,
+// with the epilogue (bias, ReLU, bf16) and the tensor-parallel push applied.
+// Roles: warp 0 lane 0 issues the TMA loads of every segment through the stage
+// ring; warp 1 lane 0 issues the MMAs into one of two TMEM accumulators (so the
+// next segment's MMAs overlap the previous segment's epilogue); warps 2-5 drain
+// TMEM (warp w reads lanes 32 (w % 4) ..) and run the epilogue.
+struct SkArgs {
+  float* out;                  // fp32 output (or null when out16 is set)
+  __nv_bfloat16* out16;        // bf16 output
+  int ldo, N, K, B, n_kb, tiles;
+  long long U;                 // tiles * n_kb
+  const __nv_bfloat16* bias;   // [N] or null
+  int relu;
+  float* ws;                   // [G][B][128] fp32 partials
+  int* flags;                  // [G], zero between launches (the owner resets what it consumed)
+  float* const* peers;         // fused TP push (fp32 output only)
+  int n_peers;
+  long long peer_slot;
+  unsigned long long* const* cnt;
+  int n_cnt;
+};
+
+__device__ __forceinline__ void tma_2d_hint(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(su32(bar)), "l"(pol)
+      : "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(192, 2)
+sk_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, const SkArgs g) {
+  constexpr int A_BYTES = kTileM * kTileK * 2;
+  constexpr int B_BYTES = BN * kTileK * 2;
+  constexpr int STAGE = A_BYTES + B_BYTES;
+  constexpr int ACC_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  constexpr int NBUF = BN <= 128 ? 2 : 1;            // two CTAs per SM share 512 TMEM columns
+  constexpr int TMEM_COLS = ACC_COLS * NBUF;
+  constexpr int kStages = stages<BN>();
+  extern __shared__ __align__(1024) uint8_t dsmem[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[stages<BN>()], empty[stages<BN>()], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long G = gridDim.x;
+  const long long u0 = (long long)blockIdx.x * g.U / G, u1 = (long long)(blockIdx.x + 1) * g.U / G;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mb_init(&full[i], 1);
+      mb_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mb_init(&acc_full[i], 1);
+      mb_init(&acc_empty[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem0 = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer over every segment ----
+      uint64_t w_pol;  // the weights are read once per GEMM: evict them first
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(w_pol));
+      int i = 0;
+      for (long long u = u0; u < u1;) {
+        const int t = (int)(u / g.n_kb);
+        const int kb_b = (int)(u - (long long)t * g.n_kb);
+        const int kb_e = (int)min((long long)g.n_kb, u1 - (long long)t * g.n_kb);
+        for (int kb = kb_b; kb < kb_e; ++kb, ++i) {
+          const int st = i % kStages;
+          if (i >= kStages) mb_wait(&empty[st], ((i / kStages) - 1) & 1);
+          uint8_t* a = smem + st * STAGE;
+          mb_expect_tx(&full[st], STAGE);
+          tma_2d_hint(a, &tmW, kb * kTileK, t * kTileM, &full[st], w_pol);
+          tma_2d(a + A_BYTES, &tmX, kb * kTileK, 0, &full[st]);
+        }
+        u = (long long)t * g.n_kb + kb_e;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      constexpr uint32_t idesc = idesc_bf16(kTileM, BN);
+      int i = 0, seg = 0;
+      for (long long u = u0; u < u1; ++seg) {
+        const int t = (int)(u / g.n_kb);
+        const int kb_b = (int)(u - (long long)t * g.n_kb);
+        const int kb_e = (int)min((long long)g.n_kb, u1 - (long long)t * g.n_kb);
+        const int buf = seg % NBUF;
+        if (seg >= NBUF) mb_wait(&acc_empty[buf], ((seg / NBUF) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tmem_d = tmem0 + (uint32_t)(buf * ACC_COLS);
+        for (int kb = kb_b; kb < kb_e; ++kb, ++i) {
+          const int st = i % kStages;
+          mb_wait(&full[st], (i / kStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a = su32(smem + st * STAGE), b = a + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < kTileK / 16; ++k)
+            umma_f16(tmem_d, sw128_desc(a + 32 * k), sw128_desc(b + 32 * k), idesc, (kb != kb_b || k != 0));
+          umma_commit(&empty[st]);
+        }
+        umma_commit(&acc_full[buf]);
+        u = (long long)t * g.n_kb + kb_e;
+      }
+    }
+  } else {
+    // ---- epilogue warps 2..5: TMEM lanes 32 (warp % 4) .. +31 = rows of the tile ----
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int etid = threadIdx.x - 64;  // 0..127
+    auto ebar = [&]() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+    int seg = 0, finals = 0;
+    for (long long u = u0; u < u1; ++seg) {
+      const int t = (int)(u / g.n_kb);
+      const int kb_b = (int)(u - (long long)t * g.n_kb);
+      const int kb_e = (int)min((long long)g.n_kb, u1 - (long long)t * g.n_kb);
+      u = (long long)t * g.n_kb + kb_e;
+      const int buf = seg % NBUF;
+      const bool part = kb_b > 0;                       // tail / middle piece: park it
+      const bool owner = kb_b == 0 && kb_e < g.n_kb;    // head piece of a cut tile
+      // the CTAs holding the rest of an owned tile: blockIdx+1 .. last (their first segments)
+      int c_last = blockIdx.x;
+      if (owner) {
+        const long long tile_end = (long long)(t + 1) * g.n_kb;
+        while (c_last + 1 < G && (long long)(c_last + 1) * g.U / G < tile_end) ++c_last;
+        if (etid == 0) {
+          for (int c2 = blockIdx.x + 1; c2 <= c_last; ++c2) {
+            int f;
+            do {
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(g.flags + c2) : "memory");
+            } while (f == 0);
+            g.flags[c2] = 0;  // consumed: ready for the next launch (stream-ordered)
+          }
+        }
+        ebar();  // the acquires (thread 0) order every epilogue thread's partial loads below
+      }
+      mb_wait(&acc_full[buf], (seg / NBUF) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t taddr = tmem0 + (uint32_t)(buf * ACC_COLS) + ((uint32_t)(q * 32) << 16);
+      const int n = t * kTileM + row;
+      const float bv = (g.bias && n < g.N) ? __bfloat162float(g.bias[n]) : 0.f;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr + c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int nb = min(16, g.B - c0);
+        if (nb <= 0) continue;
+        if (part) {
+          float* w = g.ws + (size_t)blockIdx.x * g.B * kTileM + (size_t)c0 * kTileM + row;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < nb) w[(size_t)j * kTileM] = __uint_as_float(v[j]);
+          continue;
+        }
+        float acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = __uint_as_float(v[j]);
+        for (int c2 = blockIdx.x + 1; owner && c2 <= c_last; ++c2) {  // K order: deterministic
+          const float* w = g.ws + (size_t)c2 * g.B * kTileM + (size_t)c0 * kTileM + row;
+          float pv[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pv[j] = j < nb ? __ldcg(w + (size_t)j * kTileM) : 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] += pv[j];
+        }
+        if (n < g.N) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j >= nb) break;
+            float y = acc[j] + bv;
+            if (g.relu) y = fmaxf(y, 0.f);
+            const long long off = (long long)(c0 + j) * g.ldo + n;
+            if (g.out16) g.out16[off] = __float2bfloat16_rn(y);
+            else g.out[off] = y;
+            for (int r = 0; r < g.n_peers; ++r) g.peers[r][g.peer_slot + off] = y;
+          }
+        }
+      }
+      // every tcgen05.ld of this buffer has completed (wait::ld): hand it back
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[buf])) : "memory");
+      if (part) {  // publish the parked partial (at most one per CTA: its first segment)
+        ebar();
+        if (etid == 0) asm volatile("st.release.gpu.global.s32 [%0], 1;" ::"l"(g.flags + blockIdx.x), "r"(1) : "memory");
+      } else {
+        ++finals;
+      }
+    }
+    if (g.n_cnt && finals) {  // fused TP all-reduce: one increment per finished tile per destination
+      ebar();
+      if (etid == 0) {
+        __threadfence_system();
+        for (int r = 0; r < g.n_cnt; ++r)
+          asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(g.cnt[r]), "l"((unsigned long long)finals)
+                       : "memory");
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem0), "n"(TMEM_COLS) : "memory");
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -343,6 +577,27 @@ cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const GemmAr
   return cudaLaunchKernelEx(&cfg, decode_gemm_kernel<BN>, tw, tx, g);
 }
 
+template <int BN>
+cudaError_t launch_sk_bn(const CUtensorMap& tw, const CUtensorMap& tx, const SkArgs& g, cudaStream_t s) {
+  constexpr int SMEM = smem_of<BN>();
+  static int cap = 0;
+  if (!cap) {
+    cudaError_t e = cudaFuncSetAttribute(sk_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, dev = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sk_gemm_kernel<BN>, 192, SMEM);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = std::max(1, std::min(per_sm, 2)) * sms;
+  }
+  // one wave (the owners wait on later CTAs, so every CTA must be resident), and
+  // every CTA holds at least kSkMinUnits K blocks (>= 1, so none is empty)
+  const long long G = std::max(1LL, std::min<long long>(cap, g.U / kSkMinUnits));
+  sk_gemm_kernel<BN><<<(unsigned)G, 192, SMEM, s>>>(tw, tx, g);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 int decode_gemm_splits(int N, int K, int B, int sms) {
@@ -406,6 +661,46 @@ cudaError_t launch_decode_gemm(const __nv_bfloat16* W, int N, int K, int ldw, co
     case 64: return launch_bn<64>(tw, tx, g, tiles, splits, s);
     case 128: return launch_bn<128>(tw, tx, g, tiles, splits, s);
     default: return launch_bn<256>(tw, tx, g, tiles, splits, s);
+  }
+}
+
+int sk_gemm_max_ctas() { return 2 * 148 * 2; }
+
+cudaError_t launch_sk_gemm(const __nv_bfloat16* W, int N, int K, int ldw, const __nv_bfloat16* X, int B, int ldx,
+                           float* out, __nv_bfloat16* out16, int ldo, const __nv_bfloat16* bias, int relu, float* ws,
+                           int* flags, float* const* peers, int n_peers, long long peer_slot, cudaStream_t s,
+                           unsigned long long* const* cnt, int n_cnt) {
+  if (B <= 0 || B > 256 || N <= 0 || K <= 0 || (ldw % 8) || (ldx % 8) || (!out && !out16) || !ws || !flags ||
+      (out16 && peers))
+    return cudaErrorInvalidValue;
+  const int BN = ((B + 15) / 16) * 16;
+  const int bn = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  CUtensorMap tw, tx;
+  if (!tensor_map(&tw, W, N, K, ldw, kTileM) || !tensor_map(&tx, X, B, K, ldx, bn)) return cudaErrorInvalidValue;
+  SkArgs g{};
+  g.out = out;
+  g.out16 = out16;
+  g.ldo = ldo;
+  g.N = N;
+  g.K = K;
+  g.B = B;
+  g.n_kb = (K + kTileK - 1) / kTileK;
+  g.tiles = (N + kTileM - 1) / kTileM;
+  g.U = (long long)g.tiles * g.n_kb;
+  g.bias = bias;
+  g.relu = relu;
+  g.ws = ws;
+  g.flags = flags;
+  g.peers = peers;
+  g.n_peers = peers ? n_peers : 0;
+  g.peer_slot = peer_slot;
+  g.cnt = cnt;
+  g.n_cnt = cnt ? n_cnt : 0;
+  switch (bn) {
+    case 32: return launch_sk_bn<32>(tw, tx, g, s);
+    case 64: return launch_sk_bn<64>(tw, tx, g, s);
+    case 128: return launch_sk_bn<128>(tw, tx, g, s);
+    default: return launch_sk_bn<256>(tw, tx, g, s);
   }
 }
 

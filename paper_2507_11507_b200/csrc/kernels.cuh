@@ -77,6 +77,18 @@ cudaError_t launch_decode_gemm(const __nv_bfloat16* W, int N, int K, int ldw, co
 inline int decode_gemm_tiles(int N) { return (N + 127) / 128; }
 // K splits for a B-row decode GEMM on `sms` SMs (per-SM load model, decode_gemm.cu)
 int decode_gemm_splits(int N, int K, int B, int sms);
+// Persistent stream-K form (decode_gemm.cu, "SK"): one wave of CTAs over the
+// tiles x K-blocks stream, cut tiles finished in the GEMM (deterministic K-order
+// fixup through ws [sk_gemm_max_ctas()][B][128] fp32 and flags [sk_gemm_max_ctas()]
+// ints, zero before the first launch): ONE output, y = epilogue(x W^T) with
+// optional bias[N], ReLU, and fp32 (out) or bf16 (out16) storage at row stride
+// ldo; peers / cnt: the fused tensor-parallel push as in launch_decode_gemm
+// (fp32 only; cnt gains one increment per tile per destination).
+int sk_gemm_max_ctas();
+cudaError_t launch_sk_gemm(const __nv_bfloat16* W, int N, int K, int ldw, const __nv_bfloat16* X, int B, int ldx,
+                           float* out, __nv_bfloat16* out16, int ldo, const __nv_bfloat16* bias, int relu, float* ws,
+                           int* flags, float* const* peers, int n_peers, long long peer_slot, cudaStream_t s,
+                           unsigned long long* const* cnt = nullptr, int n_cnt = 0);
 
 // ---- dense-layer support kernels -------------------------------------------
 // h[b] = E[tok] (+ P[pos + 2] for OPT); x[b] = bf16(norm(h[b])).

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <numeric>
 #include <cmath>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -1104,6 +1105,30 @@ int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K
       (long long)B * N, splits, nullptr, 0, 0, reinterpret_cast<cudaStream_t>(stream), nullptr, 0, reduce != 0,
       &slices);
   if (splits_out) *splits_out = slices;
+  return e == cudaSuccess ? MIRAGE_OK : MIRAGE_ERR_CUDA;
+}
+
+int32_t mirage_sk_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
+                       float* y_dev, void* y16_dev, const void* bias_dev, int32_t relu) {
+  if (!w_dev || !x_dev || (!y_dev && !y16_dev) || N <= 0 || K <= 0 || K % 8 || B <= 0 || B > 256)
+    return MIRAGE_ERR_RANGE;
+  // process-wide workspace of the hook: partial slots and flags for one wave
+  static std::mutex mu;
+  static float* ws = nullptr;
+  static int* flags = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!ws) {
+      const size_t n = (size_t)mirage::sk_gemm_max_ctas() * 256 * 128;
+      if (cudaMalloc(&ws, n * 4) != cudaSuccess) return MIRAGE_ERR_CUDA;
+      if (cudaMalloc(&flags, (size_t)mirage::sk_gemm_max_ctas() * 4) != cudaSuccess) return MIRAGE_ERR_CUDA;
+      if (cudaMemset(flags, 0, (size_t)mirage::sk_gemm_max_ctas() * 4) != cudaSuccess) return MIRAGE_ERR_CUDA;
+    }
+  }
+  const cudaError_t e = mirage::launch_sk_gemm(
+      reinterpret_cast<const bf16*>(w_dev), N, K, K, reinterpret_cast<const bf16*>(x_dev), B, K, y_dev,
+      y_dev ? nullptr : reinterpret_cast<bf16*>(y16_dev), N, reinterpret_cast<const bf16*>(bias_dev), relu, ws, flags,
+      nullptr, 0, 0, reinterpret_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? MIRAGE_OK : MIRAGE_ERR_CUDA;
 }
 

@@ -70,3 +70,45 @@ def test_decode_gemm_is_deterministic():
     b, _ = _lib.decode_gemm(w, x)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+SK_SHAPES = [(5120, 5120, 64), (8192, 1024, 64), (15360, 5120, 29), (1000, 776, 37), (130, 520, 130),
+             (20480, 5120, 16), (512, 1024, 256), (128, 64, 1), (700, 2048, 200), (1280, 8192, 64),
+             (8192, 3584, 33), (256, 64, 8)]
+
+
+@pytest.mark.parametrize("N,K,B", SK_SHAPES)
+def test_sk_gemm_matches_reference(N, K, B):
+    """Persistent stream-K form: tiles cut between CTAs are finished in the GEMM
+    (owner adds the parked partials in K order). One fp32 output vs fp64 torch,
+    and bit-identical across runs (deterministic fixup)."""
+    from paper_2507_11507_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(N * 5 + K * 11 + B)
+    w = (torch.randn((N, K), generator=g, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    x = torch.randn((B, K), generator=g, device="cuda").to(torch.bfloat16)
+    y = _lib.sk_gemm(w, x)
+    y2 = _lib.sk_gemm(w, x)
+    torch.cuda.synchronize()
+    r = ref(w, x)
+    scale = r.abs().max().item()
+    assert (y.double() - r).abs().max().item() <= 2e-5 * scale + 1e-6 * K ** 0.5
+    assert torch.equal(y, y2)
+
+
+@pytest.mark.parametrize("N,K,B,relu", [(20480, 5120, 64, True), (1000, 776, 37, True), (4096, 4096, 200, False)])
+def test_sk_gemm_bias_relu_bf16_epilogue(N, K, B, relu):
+    """The column-parallel epilogue (FC1: + bias, ReLU, bf16 store) inside the GEMM."""
+    from paper_2507_11507_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(N + 3 * K + 7 * B)
+    w = (torch.randn((N, K), generator=g, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    x = torch.randn((B, K), generator=g, device="cuda").to(torch.bfloat16)
+    bias = (torch.randn((N,), generator=g, device="cuda") * 0.1).to(torch.bfloat16)
+    y32 = _lib.sk_gemm(w, x, bias=bias, relu=relu)
+    y16 = _lib.sk_gemm(w, x, bias=bias, relu=relu, out_bf16=True)
+    torch.cuda.synchronize()
+    r = ref(w, x) + bias.double()
+    if relu:
+        r = r.clamp_min(0)
+    scale = r.abs().max().item()
+    assert (y32.double() - r).abs().max().item() <= 2e-5 * scale + 1e-6 * K ** 0.5
+    assert torch.equal(y16, y32.to(torch.bfloat16))          # the same value, rounded once

@@ -1,5 +1,5 @@
-"""Decode-GEMM microbenchmark: the tcgen05 kernel (mirage_decode_gemm, fp32 split
-slices) vs cuBLASLt (torch bf16 linear) on the decode shapes of the bench models.
+"""Decode-GEMM microbenchmark: the tcgen05 kernels (mirage_decode_gemm, fp32 split
+slices; mirage_sk_gemm, persistent stream-K, one fp32 output) vs cuBLASLt (torch bf16 linear) on the decode shapes of the bench models.
 Weights are cycled over enough copies to exceed L2; CUDA events around `reps`
 launches. Reports weight-streaming GB/s (N*K*2 bytes per GEMM).
 Usage: python tools/gemm_bench.py [--batch 16 64 128 256]"""
@@ -60,15 +60,23 @@ def main():
                 _lib.LIB.mirage_decode_gemm(st.cuda_stream, ws[i % copies].data_ptr(), N, K, x.data_ptr(), B,
                                             y.data_ptr(), 0, int(a.reduce and B <= 128), C.byref(got))
 
+            y1 = torch.empty((B, N), dtype=torch.float32, device="cuda")
+
+            def sk(i):
+                _lib.LIB.mirage_sk_gemm(st.cuda_stream, ws[i % copies].data_ptr(), N, K, x.data_ptr(), B,
+                                        y1.data_ptr(), None, None, 0)
+
             def cublas(i):
                 torch.nn.functional.linear(x, ws[i % copies])
             t_o = timeit(ours, a.reps)
+            t_s = timeit(sk, a.reps)
             t_c = timeit(cublas, a.reps)
             gb = N * K * 2 / 1e9
             print(json.dumps({"shape": name, "N": N, "K": K, "B": B, "splits": got.value,
                               "tcgen05_us": round(t_o * 1e3, 2), "cublas_us": round(t_c * 1e3, 2),
                               "tcgen05_gbs": round(gb / (t_o * 1e-3)), "cublas_gbs": round(gb / (t_c * 1e-3)),
-                              "speedup": round(t_c / t_o, 3)}), flush=True)
+                              "sk_us": round(t_s * 1e3, 2), "sk_gbs": round(gb / (t_s * 1e-3)),
+                              "speedup": round(t_c / t_o, 3), "sk_speedup": round(t_c / t_s, 3)}), flush=True)
         del ws
         torch.cuda.empty_cache()
 
