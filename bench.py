@@ -51,8 +51,10 @@ def parse():
     ap.add_argument("--no-resident-arm", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--graphs", action="store_true",
-                    help="capture the step in CUDA graphs (MIRAGE_FLAG_CUDA_GRAPHS); no per-launch attention timing")
+    ap.add_argument("--graphs", action="store_true", help="(default) kept for compatibility")
+    ap.add_argument("--eager", action="store_true",
+                    help="run the headline pass eagerly with per-launch attention events (the round-1/2 default) "
+                         "instead of as CUDA graphs followed by an eager measurement pass")
     return ap.parse_args()
 
 
@@ -427,10 +429,14 @@ def ppaper_batch(shape, S, BB, seed, total_steps, extra_blocks=0):
     return out, native
 
 
-def build_workload(args, rank, total_steps, impl="mirage"):
+def build_workload(args, rank, total_steps, impl="mirage", extra=0):
+    """The config's batch. Admission (C2 P-paper, C3) counts `total_steps` decode
+    steps; `extra` untimed steps (graph priming, the eager measurement pass) get
+    their blocks on top, so the batch does not depend on the execution mode."""
     from synth import models, workload
     sz = Sizes(impl)
     cfg = args.config
+    run_steps = total_steps + extra
     if cfg in ("c2", "c2p", "c4"):
         if cfg in ("c2", "c2p"):
             shape = models.OPT_13B
@@ -439,7 +445,7 @@ def build_workload(args, rank, total_steps, impl="mirage"):
             if cfg == "c2":
                 B = args.batch or 400
                 ctxs = workload.mid_generation_contexts(B, seed=args.seed + 1000 * rank, max_ctx=shape.max_pos)
-                ctxs = [int(min(c, shape.max_pos - total_steps - 1)) for c in ctxs]
+                ctxs = [int(min(c, shape.max_pos - run_steps - 1)) for c in ctxs]
                 desc = ("C2: OPT-13B-shaped decode, ShareGPT-shaped contexts, {a} layer(s) remapped to KV "
                         "({p} placement, beta={b}); native pool sized so the batch fits only with the reclaimed "
                         "blocks")
@@ -448,6 +454,7 @@ def build_workload(args, rank, total_steps, impl="mirage"):
                 cyc0, b0 = plan_cycle(sz, shape, args.alpha, beta_pol, args.placement)
                 gained = reclaimed_blocks(S0, BB0, cyc0[b0:])
                 ctxs, native0 = ppaper_batch(shape, S0, BB0, args.seed + 1000 * rank, total_steps, gained)
+                ctxs = [int(min(c, shape.max_pos - run_steps - 1)) for c in ctxs]
                 desc = ("C2 P-paper: OPT-13B-shaped decode at the paper's KV pressure (native pool = 35%% x 96 GB - "
                         "params = %d blocks, PAPER.md:599/:635), ShareGPT-shaped trace admitted while it fits the "
                         "native + reclaimed blocks; {a} layer(s) remapped ({p} placement, beta={b}); the PCIe link "
@@ -455,7 +462,7 @@ def build_workload(args, rank, total_steps, impl="mirage"):
         else:
             shape = models.LLAMA3_8B
             B = args.batch or 32
-            L = min(args.ctx or 32768, shape.max_pos) - total_steps - 1
+            L = min(args.ctx or 32768, shape.max_pos) - run_steps - 1
             ctxs = [L] * B
             beta_pol = args.beta or 2
             desc = ("C4: Llama-3-8B-shaped GQA decode, %d x %d-token contexts, split-K paged attention; "
@@ -465,7 +472,7 @@ def build_workload(args, rank, total_steps, impl="mirage"):
         S, BB = sz.sizes(shape)
         cycle, beta = plan_cycle(sz, shape, args.alpha, beta_pol, args.placement)
         reclaimed = reclaimed_blocks(S, BB, cycle[beta:])
-        need = sum((c + total_steps + 15) // 16 for c in ctxs)
+        need = sum((c + run_steps + 15) // 16 for c in ctxs)
         tenants = [(shape, args.seed, need - reclaimed)]
         remaps = [(0, 0, cycle, beta)] if cycle else []
         compare = {"kind": "all_resident", "tenants": [(shape, args.seed, need)], "remaps": [], "ctxs": ctxs}
@@ -482,7 +489,7 @@ def build_workload(args, rank, total_steps, impl="mirage"):
         native = int((0.35 * 96e9 - (act.n_layers * Sa + weights.global_bytes(act))) // BBa)
         gained = reclaimed_blocks(Sd, BBa, range(don.n_layers))
         trace = workload.mid_generation_contexts(4096, seed=args.seed + 1000 * rank, max_ctx=act.max_pos)
-        trace = [int(min(c, act.max_pos - total_steps - 1)) for c in trace]
+        trace = [int(min(c, act.max_pos - run_steps - 1)) for c in trace]
 
         def admit(pool):
             out, used = [], 0
@@ -494,30 +501,52 @@ def build_workload(args, rank, total_steps, impl="mirage"):
                 used += nb
             return out
         ctxs, base = admit(native + gained), admit(native)
+        # blocks the extra (untimed) steps need beyond the admission horizon
+        headroom = sum((c + run_steps + 15) // 16 - (c + total_steps + 15) // 16 for c in ctxs)
+        headroom_base = sum((c + run_steps + 15) // 16 - (c + total_steps + 15) // 16 for c in base)
         desc = ("C3: OPT-13B-shaped active tenant + inactive Llama-2-7B-shaped tenant whose params are fully "
                 "remapped to KV (beta=0); ShareGPT-shaped trace admitted in order until the pool is full "
                 "(native pool = 35%% x 96 GB - params = %d blocks)" % native)
-        tenants = [(act, args.seed, native), (don, args.seed + 1, 0)]
+        tenants = [(act, args.seed, native + headroom), (don, args.seed + 1, 0)]
         remaps = [("inactive", 1), (1, 0, list(range(don.n_layers)), 0)]
-        compare = {"kind": "no_reclaim", "tenants": [(act, args.seed, native)], "remaps": [], "ctxs": base}
+        compare = {"kind": "no_reclaim", "tenants": [(act, args.seed, native + headroom_base)], "remaps": [],
+                   "ctxs": base}
         return Workload(cfg, desc, tenants, remaps, ctxs, act.max_pos, "paged_attention_kernel<128,1>", compare), \
             {"native_blocks": native, "reclaimed_blocks": gained, "batch_without_reclaim": len(base),
+             "untimed_step_headroom_blocks": headroom,
              "block_bytes": BBa, "layer_bytes": Sa}
     raise SystemExit(f"unknown config {cfg}")
 
 
-def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warmup, e2e_steps, clock=None):
+PRIME_STEPS = 4   # untimed steps that capture the CUDA graphs before the warmup (graph mode)
+
+
+def extra_steps(args):
+    """Steps a run takes beyond warmup + steps + e2e (graph priming and the eager
+    measurement pass), so the workload is sized for them."""
+    return 0 if args.eager else PRIME_STEPS + 2 + args.steps
+
+
+def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warmup, e2e_steps, clock=None,
+            measure=True):
     """One context: add the tenants, apply the remaps, fill the batch's prompt KV,
     warm up, time `steps` decode steps of tenant 0 on the device, then
-    `e2e_steps` end-to-end steps (host sync + argmax read-back each step)."""
+    `e2e_steps` end-to-end steps (host sync + argmax read-back each step).
+    Default (not --eager): the headline pass runs as CUDA graphs (no event
+    between kernels, programmatic dependent launch intact); then, if `measure`,
+    the same context switches to eager steps with CUDA events around every
+    attention launch, slot handoff and copy (MIRAGE_FLAG_TIME_ATTN) and times
+    `steps` more steps: the roofline, H2D and handoff figures come from that
+    measurement pass."""
     import ctypes as C
     import harness
     from paper_2507_11507_b200 import _lib
     from synth import workload
     B = len(ctxs)
     arena = harness.arena_for([(sh, nat) for sh, _, nat in tenants], B, max_ctx)
+    graphs = not args.eager
     ctx = _lib.Context(arena, B, max_ctx, device=dev.index,
-                       flags=_lib.FLAG_CUDA_GRAPHS if getattr(args, "graphs", False) else _lib.FLAG_TIME_ATTN)
+                       flags=_lib.FLAG_CUDA_GRAPHS if graphs else _lib.FLAG_TIME_ATTN)
     mids = [ctx.add_model(sh, blobs[(sh.name, seed)], nat) for sh, seed, nat in tenants]
     if args.weight_source == "device" and remaps:
         dev_copy = blobs[(tenants[0][0].name, tenants[0][1])].to(dev)
@@ -553,6 +582,8 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
 
     if clock:
         clock.start()   # running before the timed region; stop() keeps the samples inside it
+    for _ in range(PRIME_STEPS if graphs else 0):   # first sight (eager) and capture of each graph key
+        step(False)
     for _ in range(warmup):
         step(False)
     ctx.sync()
@@ -584,6 +615,26 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
         ctx.sync()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     st2 = ctx.query(mid)
+    meas = None
+    if graphs and measure:
+        # measurement pass: eager steps with CUDA events around every attention launch
+        ctx.set_flags(_lib.FLAG_TIME_ATTN, _lib.FLAG_TIME_ATTN | _lib.FLAG_CUDA_GRAPHS)
+        for _ in range(2):
+            step(False)
+        ctx.sync()
+        st0 = ctx.query(mid)
+        mev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        mev[0].record(cs)
+        for k in range(steps):
+            step(False)
+            mev[k + 1].record(cs)
+        ctx.sync()
+        torch.cuda.synchronize(dev)
+        st1 = ctx.query(mid)
+        meas = {"step_ms": [mev[k].elapsed_time(mev[k + 1]) for k in range(steps)],
+                "total_ms": mev[0].elapsed_time(mev[steps])}
+    elif not graphs:
+        meas = {"step_ms": step_ms, "total_ms": total_ms}
     # the same attention launch alone (after the timed region, no DMA or GEMMs around it)
     alone_gbs = None
     try:
@@ -604,6 +655,7 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
     except Exception:
         alone_gbs = None
     out = dict(step_ms=step_ms, alone_gbs=alone_gbs, total_ms=total_ms, launches=launches, clocks=clocks, e2e_ms=e2e_ms,
+               meas=meas, graphs=graphs,
                attn_ms=st1["attn_ms"] - st0["attn_ms"], attn_launches=st1["attn_launches"] - st0["attn_launches"],
                attn_bytes=st1["attn_bytes"] - st0["attn_bytes"],
                stall_ms=st1["stall_ms"] - st0["stall_ms"], stall_waits=st1["stall_waits"] - st0["stall_waits"],
@@ -623,7 +675,7 @@ def run_mirage(args, rank, world):
     dev = torch.device("cuda", int(os.environ.get("MIRAGE_BENCH_DEVICE", lr)))
     torch.cuda.set_device(dev)
     total = args.warmup + args.steps + args.e2e_steps + 1
-    wl, info = build_workload(args, rank, total)
+    wl, info = build_workload(args, rank, total, extra=extra_steps(args))
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -659,7 +711,7 @@ def run_mirage(args, rank, world):
     if not args.no_resident_arm and wl.compare and world == 1 and (wl.remaps or wl.compare["kind"] != "all_resident"):
         c = wl.compare
         r2 = run_arm(args, torch, dev, c["tenants"], c["remaps"], c["ctxs"], wl.max_ctx, blobs, args.steps,
-                     args.warmup, 0)
+                     args.warmup, 0, measure=False)
         med = statistics.median(r2["step_ms"])
         cmp = {"kind": c["kind"], "batch": len(c["ctxs"]), "step_ms": med,
                "tok_s": len(c["ctxs"]) / (sum(r2["step_ms"]) / len(r2["step_ms"]) / 1e3),
@@ -674,6 +726,7 @@ def run_mirage(args, rank, world):
     tokens = B * args.steps * world
     value = tokens / (t_all / 1e3)
     e2e_med = statistics.median(res["e2e_ms"]) if res["e2e_ms"] else None
+    meas_total = res["meas"]["total_ms"] if res.get("meas") else t_local
     attn_avg_ms = res["attn_ms"] / max(1, res["attn_launches"])
     attn_bytes_launch = res["attn_bytes"] / max(1, res["attn_launches"])
     achieved = attn_bytes_launch / (attn_avg_ms * 1e-3) / 1e9 if attn_avg_ms > 0 else None
@@ -706,6 +759,7 @@ def run_mirage(args, rank, world):
         except Exception as e:  # the CPU leg must not hide the GPU number
             cpu = {"value": None, "unit": "tok/s", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
     step_med = statistics.median(res["step_ms"])
+    meas_med = statistics.median(res["meas"]["step_ms"]) if res.get("meas") else step_med
     h2d_gbs = res["h2d_bytes"] / (res["h2d_ms"] * 1e-3) / 1e9 if res["h2d_ms"] else None
     # predicted handoff stall of this cycle (the planner's timeline, mirage_predict_stall) from the
     # measured per-layer copy time T_T and per-layer compute time T_c = (step - measured stall) / n
@@ -714,7 +768,7 @@ def run_mirage(args, rank, world):
         from paper_2507_11507_b200 import _lib as L_
         n_l = wl.tenants[0][0].n_layers
         t_t = info["layer_bytes"] / (h2d_gbs * 1e9) * 1e9
-        t_c = max(step_med - res["stall_ms"] / args.steps, 1e-3) / n_l * 1e6   # compute only, stall removed
+        t_c = max(meas_med - res["stall_ms"] / args.steps, 1e-3) / n_l * 1e6   # compute only, stall removed
         predicted_stall = L_.predict_stall(n_l, list(info["cycle"]), info["beta"], t_t, t_c) / 1e6
     config = workload_config(wl, info, world)
     line = {
@@ -727,7 +781,11 @@ def run_mirage(args, rank, world):
         "roofline": {"kernel": wl.kernel, "bound": "hbm", "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
                      "algorithmic_bytes_per_launch": attn_bytes_launch, "avg_launch_ms": attn_avg_ms,
-                     "launches": res["attn_launches"], "share_of_step": res["attn_ms"] / t_local,
+                     "launches": res["attn_launches"], "share_of_step": res["attn_ms"] / meas_total,
+                     "measured_in": ("the measurement pass: the same batch for `steps` more eager steps with CUDA "
+                                     "events around every attention launch, after the headline pass (CUDA graphs, "
+                                     "no events between kernels)") if res.get("graphs") else "the timed region",
+                     "measurement_pass_ms_per_step": meas_total / args.steps,
                      "traffic_capture": traffic_capture,
                      "kernel_alone_gbs": res.get("alone_gbs"),
                      "copy_peak_this_run_gbs": copy_peak_run,
@@ -747,6 +805,8 @@ def run_mirage(args, rank, world):
                 "h2d_bytes_per_step": res["meta_bytes"], "d2h_bytes_per_step": 4 * B,
                 "ms_per_step": e2e_med, "how": "host-timed mirage_decode_step with host token/position arrays, "
                                                "argmax read back to host and stream sync every step"},
+        "execution": ("CUDA graphs (one per batch size and slot parity; re-streaming copies as captured branches)"
+                      if res.get("graphs") else "eager launches with per-launch attention events"),
         "gpu_launches": res["launches"], "setup_blob_s": setup_blob_s,
         "kernel_plan": {"split_blocks": res["split_blocks"], "attention_units": res["units"]},
         "host_blob": blob_info,

@@ -408,6 +408,13 @@ int32_t mirage_query(mirage_ctx* ctx, int32_t model, mirage_stats* out);
  * oracle's c5 log. Errors: RANGE (cap too small; *n_out gets the length). */
 int32_t mirage_slot_log(mirage_ctx* ctx, int32_t model, int64_t* out, int32_t cap, int32_t* n_out);
 
+/* Change the measurement-mode init flags of a live ctx: the bits of `mask`
+ * among MIRAGE_FLAG_TIME_ATTN and MIRAGE_FLAG_CUDA_GRAPHS are set to their
+ * values in `flags` (other bits of mask: CONFIG). Takes effect at the next step;
+ * captured graphs are kept (they are replayed again once MIRAGE_FLAG_CUDA_GRAPHS
+ * is set and MIRAGE_FLAG_TIME_ATTN clear). Errors: CONFIG. */
+int32_t mirage_set_flags(mirage_ctx* ctx, uint32_t flags, uint32_t mask);
+
 /* Block until all work enqueued by this ctx has finished; reports sticky errors. */
 int32_t mirage_sync(mirage_ctx* ctx);
 

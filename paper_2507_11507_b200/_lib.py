@@ -116,6 +116,7 @@ def _load():
         "mirage_attn_trace": (I32, [P, pU64, I32, pI32]),
         "mirage_decode_gemm": (I32, [P, P, I32, I32, P, I32, P, I32, I32, pI32]),
         "mirage_sk_gemm": (I32, [P, P, I32, I32, P, I32, P, P, P, I32]),
+        "mirage_set_flags": (I32, [P, C.c_uint32, C.c_uint32]),
         "mirage_nccl_unique_id": (I32, [P]),
         "mirage_host_register": (I32, [P, U64]),
         "mirage_region_count": (I32, [P, I32, pI32]),
@@ -146,7 +147,7 @@ EXPORTED = [
     "mirage_host_register", "mirage_host_unregister", "mirage_region_count", "mirage_region_info",
     "mirage_unremap", "mirage_swap_out", "mirage_swap_in", "mirage_set_weight_source", "mirage_tp_export",
     "mirage_tp_import", "mirage_prefill", "mirage_migrate_region", "mirage_predict_stall",
-    "mirage_attn_trace", "mirage_decode_gemm", "mirage_sk_gemm"]
+    "mirage_attn_trace", "mirage_decode_gemm", "mirage_sk_gemm", "mirage_set_flags"]
 
 
 def model_cfg(shape):
@@ -468,6 +469,10 @@ class Context:
 
     def sync(self):
         self._check(LIB.mirage_sync(self._ctx), "sync")
+
+    def set_flags(self, flags, mask):
+        """Switch FLAG_TIME_ATTN / FLAG_CUDA_GRAPHS on a live context (mirage_set_flags)."""
+        self._check(LIB.mirage_set_flags(self._ctx, int(flags), int(mask)), "set_flags")
 
     def attn_only(self, model, layer, seq_ids, q, out, split_tokens=0):
         assert q.dtype == torch.float32 and q.is_cuda and q.is_contiguous()

@@ -1108,6 +1108,14 @@ int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K
   return e == cudaSuccess ? MIRAGE_OK : MIRAGE_ERR_CUDA;
 }
 
+int32_t mirage_set_flags(mirage_ctx* c, uint32_t flags, uint32_t mask) {
+  GUARD(c);
+  const uint32_t allowed = MIRAGE_FLAG_TIME_ATTN | MIRAGE_FLAG_CUDA_GRAPHS;
+  if (mask & ~allowed) return fail(c, MIRAGE_ERR_CONFIG, "set_flags: only TIME_ATTN / CUDA_GRAPHS may change");
+  c->cfg.flags = (c->cfg.flags & ~mask) | (flags & mask);
+  return MIRAGE_OK;
+}
+
 int32_t mirage_sk_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
                        float* y_dev, void* y16_dev, const void* bias_dev, int32_t relu) {
   if (!w_dev || !x_dev || (!y_dev && !y16_dev) || N <= 0 || K <= 0 || K % 8 || B <= 0 || B > 256)
