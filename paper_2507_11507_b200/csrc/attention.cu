@@ -415,7 +415,7 @@ paged_attention_kernel(const AttnParams p) {
             const uint32_t part = vr < 16 ? (uint32_t)vr * ROW : 2u * TILE;
             mbar_expect_tx(&bars[w][st], vr < 16 ? 2 * part : part);
             const char* src = reinterpret_cast<const char*>(ai);
-            if (p.fold_mode & 1) {
+            if (p.kv_evict_first) {
               bulk_g2s_hint(dst, src, part, &bars[w][st], kv_pol);
               if (vr < 16) bulk_g2s_hint(dst + TILE, src + TILE, part, &bars[w][st], kv_pol);
             } else {
@@ -852,10 +852,8 @@ paged_attention_kernel(const AttnParams p) {
         const float* rg = rec0 + (e / (D / 4)) * (D + 4) + (e % (D / 4)) * 4;
 #pragma unroll
         for (int k = 0; k < NB; ++k)
-          ov[c][k] = (e < NCOL && i0 + k < ns)
-                         ? ((p.fold_mode & 2) ? *reinterpret_cast<const float4*>(rg + (i0 + k) * rstride)
-                                              : __ldcg(reinterpret_cast<const float4*>(rg + (i0 + k) * rstride)))
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
+          ov[c][k] = (e < NCOL && i0 + k < ns) ? __ldcg(reinterpret_cast<const float4*>(rg + (i0 + k) * rstride))
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     };
     float* sw = sm_accf;                          // [G][kMaxSplitsDev], zero past ns

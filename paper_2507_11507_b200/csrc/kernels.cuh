@@ -45,8 +45,8 @@ struct AttnParams {
   uint64_t* trace;             // optional [grid][16] %globaltimer stamps per CTA (MIRAGE_ATTN_TRACE), else null
   int32_t pdl;                 // launch with a programmatic dependency on the previous kernel (which
                                // must call griddepcontrol.launch_dependents early, as qkv_post does)
-  int32_t fold_mode;           // experiment bits (MIRAGE_ATTN_FOLD): 1 = K|V tiles loaded with an
-                               // L2 evict_first policy, 2 = split-combine loads weak (ld.global)
+  int32_t kv_evict_first;      // K|V tiles are loaded with an L2 evict_first policy (they are read
+                               // once per launch); MIRAGE_KV_EVICT_FIRST=0 turns it off
 };
 
 cudaError_t launch_paged_attention(const AttnParams& p, cudaStream_t s);

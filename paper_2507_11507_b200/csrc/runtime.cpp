@@ -724,12 +724,6 @@ void harvest_attn_times(Model* M) {
   (void)cudaGetLastError();
 }
 
-// MIRAGE_COPY_MODE (experiment): 0 = cudaMemcpyAsync on the copy stream (default)
-int copy_mode() {
-  static const int v = getenv("MIRAGE_COPY_MODE") ? atoi(getenv("MIRAGE_COPY_MODE")) : 0;
-  return v;
-}
-
 // The captured graphs of M bake in its weight/slot pointers and copy sources:
 // drop them whenever its cycle or weight source changes.
 void drop_graphs(Model* M) {
@@ -748,9 +742,9 @@ bool ranges_enabled() {
   return v;
 }
 
-// MIRAGE_ATTN_FOLD (experiment bits, see AttnParams::fold_mode)
-int attn_fold_mode() {
-  static const int v = getenv("MIRAGE_ATTN_FOLD") ? atoi(getenv("MIRAGE_ATTN_FOLD")) : 1;
+// MIRAGE_KV_EVICT_FIRST=0 loads the attention's K|V tiles with the default L2 policy
+int kv_evict_first() {
+  static const int v = !(getenv("MIRAGE_KV_EVICT_FIRST") && atoi(getenv("MIRAGE_KV_EVICT_FIRST")) == 0);
   return v;
 }
 
@@ -1925,9 +1919,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     if (dbg_mode != 1) {  // experiment hook: 1 = events only, no DMA
       void* dst = M->w_dev + (uint64_t)M->cycle[slot] * M->sz.S;
       const void* src = M->host + (uint64_t)nl * M->sz.S;
-      {
-        CK(c, cudaMemcpyAsync(dst, src, M->sz.S, cudaMemcpyDefault, c->xs));
-      }
+      CK(c, cudaMemcpyAsync(dst, src, M->sz.S, cudaMemcpyDefault, c->xs));
     }
     if (M->slot_tag)  // same stream, after the weights: a correct tag proves they landed
       CK(c, cudaMemcpyAsync(M->slot_tag + slot, M->host_tags + nl, 4, cudaMemcpyHostToDevice, c->xs));
@@ -2017,7 +2009,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   ap.out_fp32 = 0;
   ap.qp = qp;
   ap.pdl = use_pdl();  // programmatic dependency on qkv_post (which precedes it in the stream)
-  ap.fold_mode = attn_fold_mode();
+  ap.kv_evict_first = kv_evict_first();
   const bool time_attn = c->cfg.flags & MIRAGE_FLAG_TIME_ATTN;
   uint64_t attn_bytes = 0;
   for (int i = 0; i < B; ++i) attn_bytes += (uint64_t)hv.len[i] * 2 * Hk * D * 2;
@@ -2267,7 +2259,7 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
   ap.out = out_dev;
   ap.out_fp32 = out_fp32;
   ap.pdl = use_pdl();  // programmatic dependency on q_split (or the previous repeat)
-  ap.fold_mode = attn_fold_mode();
+  ap.kv_evict_first = kv_evict_first();
   if (c->attn_trace) {
     const int ctas = mirage::attention_grid_ctas(s.H, s.Hk, s.D);
     c->attn_trace_ctas = std::min(mirage_ctx::kTraceCtas, std::min(ctas, n_units * s.Hk));
