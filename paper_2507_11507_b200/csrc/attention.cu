@@ -370,6 +370,7 @@ paged_attention_kernel(const AttnParams p) {
       a_first = j < u_first.b1 ? p.addrs[u_first.addr_off + j] : 0;
     }
     const uint64_t kv_pol = policy_evict_first();
+    int my_t = 0;  // (per-lane producer) tiles issued to this lane's warp
     pdl_wait();
     for (int k = 0;; ++k) {
       const int sl_ = k % QB;
@@ -396,6 +397,47 @@ paged_attention_kernel(const AttnParams p) {
       const AttnUnit u = k == 0 ? u_first : p.units[item / p.H_kv];
       const uint64_t off = p.layer_off + (uint64_t)(item % p.H_kv) * (2 * TILE);
       const uint64_t* tbl = p.addrs + u.addr_off;
+      const int Lmax_u = u.len + (QP > 1 ? u.nq - 1 : 0);
+      if (p.prod_lanes) {
+        // one producer lane per consumer warp: lane w issues blocks b0 + w, b0 + w + W, ...
+        // into warp w's ring and waits only on warp w's stages (no head-of-line blocking
+        // behind another warp's slow tile); addresses fetched 8 per lane at a time
+        uint64_t pre[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) pre[q] = __shfl_sync(0xffffffffu, a_first, min(31, (lane % kWarps) + kWarps * q));
+        if (lane < kWarps) {
+          for (int j0 = u.b0 + lane, win = 0; j0 < u.b1; j0 += 8 * kWarps, ++win) {
+            uint64_t ad[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int j = j0 + kWarps * q;
+              ad[q] = j < u.b1 ? ((k == 0 && win == 0) ? pre[q] : tbl[j]) : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int j = j0 + kWarps * q;
+              if (j >= u.b1) break;
+              const int st = my_t % NS;
+              if (my_t >= NS) mbar_wait(&empty[WS ? lane : 0][st], ((my_t / NS) - 1) & 1);
+              ++my_t;
+              uint8_t* dst = smem + (size_t)lane * NS * 2 * TILE + st * 2 * TILE;
+              const int vr = min(16, Lmax_u - j * 16);
+              const uint32_t part = vr < 16 ? (uint32_t)vr * ROW : 2u * TILE;
+              mbar_expect_tx(&bars[lane][st], vr < 16 ? 2 * part : part);
+              const char* src = reinterpret_cast<const char*>(ad[q] + off);
+              if (p.kv_evict_first) {
+                bulk_g2s_hint(dst, src, part, &bars[lane][st], kv_pol);
+                if (vr < 16) bulk_g2s_hint(dst + TILE, src + TILE, part, &bars[lane][st], kv_pol);
+              } else {
+                bulk_g2s(dst, src, part, &bars[lane][st]);
+                if (vr < 16) bulk_g2s(dst + TILE, src + TILE, part, &bars[lane][st]);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        continue;
+      }
       for (int base = u.b0; base < u.b1; base += 32) {
         const int j = base + lane;
         const uint64_t a = j < u.b1 ? ((k == 0 && base == u.b0) ? a_first : tbl[j]) + off : 0;
@@ -411,7 +453,7 @@ paged_attention_kernel(const AttnParams p) {
             // the last, partly filled block of a sequence: fetch only its valid token
             // rows of K and of V (the consumer masks the scores of the other rows and
             // zeroes their V rows), so DRAM traffic equals the algorithmic bytes
-            const int vr = min(16, u.len + (QP > 1 ? u.nq - 1 : 0) - (base + i) * 16);
+            const int vr = min(16, Lmax_u - (base + i) * 16);
             const uint32_t part = vr < 16 ? (uint32_t)vr * ROW : 2u * TILE;
             mbar_expect_tx(&bars[w][st], vr < 16 ? 2 * part : part);
             const char* src = reinterpret_cast<const char*>(ai);

@@ -742,6 +742,14 @@ bool ranges_enabled() {
   return v;
 }
 
+// One producer lane per consumer warp (AttnParams::prod_lanes; MIRAGE_ATTN_PRODUCER=0: lane 0
+// issues every tile in order). Back to back: 1x32k 28.0 -> 27.4 us, 4x16k 46.1 -> 45.1,
+// OPT-13B B=400 365.7 -> 362.5; B=64 64.9 -> 65.3, B=29 37.9 -> 38.2 (profiles/r02g/attn_producer_lanes.jsonl)
+int attn_prod_lanes() {
+  static const int v = !(getenv("MIRAGE_ATTN_PRODUCER") && atoi(getenv("MIRAGE_ATTN_PRODUCER")) == 0);
+  return v;
+}
+
 // MIRAGE_KV_EVICT_FIRST=0 loads the attention's K|V tiles with the default L2 policy
 int kv_evict_first() {
   static const int v = !(getenv("MIRAGE_KV_EVICT_FIRST") && atoi(getenv("MIRAGE_KV_EVICT_FIRST")) == 0);
@@ -2010,6 +2018,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   ap.qp = qp;
   ap.pdl = use_pdl();  // programmatic dependency on qkv_post (which precedes it in the stream)
   ap.kv_evict_first = kv_evict_first();
+  ap.prod_lanes = attn_prod_lanes();
   const bool time_attn = c->cfg.flags & MIRAGE_FLAG_TIME_ATTN;
   uint64_t attn_bytes = 0;
   for (int i = 0; i < B; ++i) attn_bytes += (uint64_t)hv.len[i] * 2 * Hk * D * 2;
@@ -2260,6 +2269,7 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
   ap.out_fp32 = out_fp32;
   ap.pdl = use_pdl();  // programmatic dependency on q_split (or the previous repeat)
   ap.kv_evict_first = kv_evict_first();
+  ap.prod_lanes = attn_prod_lanes();
   if (c->attn_trace) {
     const int ctas = mirage::attention_grid_ctas(s.H, s.Hk, s.D);
     c->attn_trace_ctas = std::min(mirage_ctx::kTraceCtas, std::min(ctas, n_units * s.Hk));
