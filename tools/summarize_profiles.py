@@ -74,7 +74,8 @@ if __name__ == "__main__":
                 f.write(f"  {k:62s} {v} {u}\n")
     traffic = [to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m["dram__bytes_write.sum"]) for m in ms]
     # algorithmic bytes of the captured launches (sum_s L_s * 2 * H_kv * D * 2): the
-    # first timed step of `bench.py --config cfg --steps 2 --warmup 1` attends over ctx + 2 tokens
+    # first timed step of `bench.py --config cfg --steps 2 --warmup 1` attends over ctx + 2 tokens,
+    # plus the PRIME_STEPS graph-capture steps that precede the warm-up in the default (graph) mode
     sys.path.insert(0, ROOT)
     import importlib.util
     spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
@@ -83,9 +84,10 @@ if __name__ == "__main__":
 
     class A:
         config, batch, ctx, alpha, beta, placement, seed = cfg, 0, 0, 1, 0, "uniform", 0
-    wl, _ = bm.build_workload(A, 0, 1 + 2 + 0 + 1, "reference")
+    wl, _ = bm.build_workload(A, 0, 1 + 2 + 0 + 1, "reference", extra=getattr(bm, "PRIME_STEPS", 0) + 2 + 2)
     sh = wl.tenants[0][0]
-    alg = sum(c + 2 for c in wl.ctxs) * 2 * sh.n_kv_heads * sh.head_dim * 2
+    adv = 2 + getattr(bm, "PRIME_STEPS", 0)
+    alg = sum(c + adv for c in wl.ctxs) * 2 * sh.n_kv_heads * sh.head_dim * 2
     tpath = os.path.join(prof, "attention_traffic.json")
     t = json.load(open(tpath)) if os.path.exists(tpath) else {}
     t[cfg] = {"dram_bytes_per_launch": sum(traffic) / len(traffic), "launches": len(traffic),
