@@ -886,65 +886,6 @@ paged_attention_kernel(const AttnParams p) {
     constexpr int NCOL = G * D / 4;                                // float4 columns of the G heads
     constexpr int CPT = (NCOL + kWarps * 32 - 1) / (kWarps * 32);  // columns per thread
     constexpr int NB = 8 / CPT;                                    // splits per load batch
-    float4 acc[CPT];
-    float lamc[CPT];
-    if (p.fold_online) {
-      constexpr int NBO = G == 1 ? 4 : 8 / CPT;  // (G = 1 runs at 128 registers)
-      // (experiment) online fold per column: (m_i, l_i) travel with o_i in the same
-      // double-buffered batches and each thread keeps a running max, so there is no
-      // weight pass and no barrier: acc = acc 2^(M - M') + 2^(m_i - M') o_i in split order
-      float4 ov0[CPT][NBO], ov1[CPT][NBO];
-      float2 ml0[CPT][NBO], ml1[CPT][NBO];
-      auto load2 = [&](float4 (&ov)[CPT][NBO], float2 (&ml)[CPT][NBO], int i0) {
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) {
-          const int e = threadIdx.x + c * kWarps * 32;
-          const int g = min(e / (D / 4), G - 1);
-          const float* rg = rec0 + g * (D + 4) + (e % (D / 4)) * 4;
-          const float* rm = rec0 + g * (D + 4) + D;
-#pragma unroll
-          for (int k = 0; k < NBO; ++k) {
-            const bool v = e < NCOL && i0 + k < ns;
-            ov[c][k] = v ? __ldcg(reinterpret_cast<const float4*>(rg + (i0 + k) * rstride))
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-            ml[c][k] = v ? __ldcg(reinterpret_cast<const float2*>(rm + (i0 + k) * rstride))
-                         : make_float2(-CUDART_INF_F, 0.f);
-          }
-        }
-      };
-      float Mx[CPT];
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        Mx[c] = -CUDART_INF_F;
-        lamc[c] = 0.f;
-        acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      auto fold = [&](const float4 (&ov)[CPT][NBO], const float2 (&ml)[CPT][NBO]) {
-#pragma unroll
-        for (int c = 0; c < CPT; ++c)
-#pragma unroll
-          for (int k = 0; k < NBO; ++k) {
-            const float mn = fmaxf(Mx[c], ml[c][k].x);
-            const float sc = mn == -CUDART_INF_F ? 1.f : exp2f(Mx[c] - mn);
-            const float w = mn == -CUDART_INF_F ? 0.f : exp2f(ml[c][k].x - mn);
-            acc[c].x = acc[c].x * sc + w * ov[c][k].x;
-            acc[c].y = acc[c].y * sc + w * ov[c][k].y;
-            acc[c].z = acc[c].z * sc + w * ov[c][k].z;
-            acc[c].w = acc[c].w * sc + w * ov[c][k].w;
-            lamc[c] = lamc[c] * sc + w * ml[c][k].y;
-            Mx[c] = mn;
-          }
-      };
-      load2(ov0, ml0, 0);
-      load2(ov1, ml1, NBO);
-      for (int i0 = 0; i0 < ns; i0 += 2 * NBO) {
-        fold(ov0, ml0);
-        if (i0 + 2 * NBO < ns) load2(ov0, ml0, i0 + 2 * NBO);
-        if (i0 + NBO >= ns) break;
-        fold(ov1, ml1);
-        if (i0 + 3 * NBO < ns) load2(ov1, ml1, i0 + 3 * NBO);
-      }
-    } else {
     float4 ov0[CPT][NB], ov1[CPT][NB];
     auto load_batch = [&](float4 (&ov)[CPT][NB], int i0) {
 #pragma unroll
@@ -1003,6 +944,7 @@ paged_attention_kernel(const AttnParams p) {
     if (threadIdx.x == 0) ATTN_TRACE(10, gtimer());
     csync();
     if (threadIdx.x == 0) ATTN_TRACE(14, clock64() - c9);
+    float4 acc[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
     auto fma_batch = [&](const float4 (&ov)[CPT][NB], int i0) {
@@ -1032,14 +974,11 @@ paged_attention_kernel(const AttnParams p) {
       if (i0 + 3 * NB < ns) load_batch(ov1, i0 + 3 * NB);
     }
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) lamc[c] = sLam[min((int)(threadIdx.x + c * kWarps * 32) / (D / 4), G - 1)];
-    }
-#pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const int e = threadIdx.x + c * kWarps * 32;
       if (e >= NCOL) continue;
       const int g = e / (D / 4), d = (e % (D / 4)) * 4;
-      const float lam = lamc[c];
+      const float lam = sLam[g];
       const float4 r = make_float4(acc[c].x / lam, acc[c].y / lam, acc[c].z / lam, acc[c].w / lam);
       const size_t oi = ((size_t)s * p.H + hk * G + g) * D + d;
       if (p.out_fp32) {

@@ -2019,7 +2019,6 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   ap.pdl = use_pdl();  // programmatic dependency on qkv_post (which precedes it in the stream)
   ap.kv_evict_first = kv_evict_first();
   ap.prod_lanes = attn_prod_lanes();
-  ap.fold_online = getenv("MIRAGE_ATTN_FOLD_ONLINE") ? atoi(getenv("MIRAGE_ATTN_FOLD_ONLINE")) : 0;
   const bool time_attn = c->cfg.flags & MIRAGE_FLAG_TIME_ATTN;
   uint64_t attn_bytes = 0;
   for (int i = 0; i < B; ++i) attn_bytes += (uint64_t)hv.len[i] * 2 * Hk * D * 2;
@@ -2271,7 +2270,6 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
   ap.pdl = use_pdl();  // programmatic dependency on q_split (or the previous repeat)
   ap.kv_evict_first = kv_evict_first();
   ap.prod_lanes = attn_prod_lanes();
-  ap.fold_online = getenv("MIRAGE_ATTN_FOLD_ONLINE") ? atoi(getenv("MIRAGE_ATTN_FOLD_ONLINE")) : 0;
   if (c->attn_trace) {
     const int ctas = mirage::attention_grid_ctas(s.H, s.Hk, s.D);
     c->attn_trace_ctas = std::min(mirage_ctx::kTraceCtas, std::min(ctas, n_units * s.Hk));
