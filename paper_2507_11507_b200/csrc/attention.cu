@@ -1039,7 +1039,7 @@ cudaError_t launch_v(const AttnParams& p, cudaStream_t s, bool query, int* grid_
     return cudaSuccess;
   }
   const long items = (long)p.n_units * p.H_kv;
-  const int grid = (int)std::min<long>(items, ctas);
+  const int grid = p.full_grid ? ctas : (int)std::min<long>(items, ctas);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3((W + (WS ? 1 : 0)) * 32);

@@ -45,6 +45,8 @@ struct AttnParams {
   uint64_t* trace;             // optional [grid][16] %globaltimer stamps per CTA (MIRAGE_ATTN_TRACE), else null
   int32_t pdl;                 // launch with a programmatic dependency on the previous kernel (which
                                // must call griddepcontrol.launch_dependents early, as qkv_post does)
+  int32_t full_grid;           // launch the whole persistent grid even if there are fewer items
+                               // (schedule 1: CTA b serves range b / H_kv)
   int32_t prod_lanes;          // producer warp issues through one lane per consumer warp (else lane 0 issues all)
   int32_t kv_evict_first;      // K|V tiles are loaded with an L2 evict_first policy (they are read
                                // once per launch); MIRAGE_KV_EVICT_FIRST=0 turns it off

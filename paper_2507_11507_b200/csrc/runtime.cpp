@@ -2000,6 +2000,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   ap.units = dv.units;
   ap.hdr = dv.hdr;
   ap.rfirst = dv.rfirst;
+  ap.full_grid = attn_mode == 1;
   ap.n_units = n_units;
   ap.n_units_dev = nullptr;
   if (capturing) {  // replays keep the full persistent grid; the unit count comes from the metadata
@@ -2257,6 +2258,7 @@ int32_t mirage_attn_only(mirage_ctx* c, int32_t model, int32_t layer, int32_t B,
   ap.units = dv.units;
   ap.hdr = dv.hdr;
   ap.rfirst = dv.rfirst;
+  ap.full_grid = hv.hdr[1] == 1;
   ap.n_units = n_units;
   ap.H = s.H;
   ap.H_kv = s.Hk;

@@ -237,3 +237,27 @@ def test_balanced_ranges_remap_invariance_and_oracle():
         for h in range(16):
             ref = OAT.attend(qd[i, h], kv[1, h // 4, 0], kv[1, h // 4, 1])
             assert np.abs(outs[0][i, h].double().numpy() - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("lens", [[20, 3], [1], [16, 16, 16, 1, 33]])
+def test_balanced_ranges_with_empty_ranges(lens):
+    """Forced balanced ranges on a batch with fewer blocks than ranges: most CTAs
+    get an empty range (no item) and every block is its own piece; outputs still
+    match c3 within 2e-3."""
+    shape = small_shape(16, 4, 128)
+    ctx, r, _, _ = setup_ctx(shape, 64)
+    for i, L in enumerate(lens):
+        ctx.alloc_blocks(r, i, harness.blocks_for(L))
+        ctx.write_kv(r, i, workload.logical_kv(shape.n_layers, 4, 128, L, seed=13, seq=i))
+    q = workload.queries(len(lens), 16, 128, seed=8).cuda()
+    o = torch.empty((len(lens), 16, 128), dtype=torch.float32, device="cuda")
+    ctx.attn_only(r, 0, list(range(len(lens))), q, o, split_tokens=-1)
+    ctx.sync()
+    assert ctx.query(r)["last_split_blocks"] == 0
+    qd = q.cpu().double().numpy()
+    got = o.cpu().double().numpy()
+    for i, L in enumerate(lens):
+        kv = workload.logical_kv(shape.n_layers, 4, 128, L, seed=13, seq=i).float().double().numpy()
+        for h in range(16):
+            ref = OAT.attend(qd[i, h], kv[0, h // 4, 0], kv[0, h // 4, 1])
+            assert np.abs(got[i, h] - ref).max() <= TOL
