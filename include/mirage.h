@@ -473,9 +473,10 @@ int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K
  * y = epilogue(X W^T) for W = w_dev bf16 [N][K], X = x_dev bf16 [B][K]
  * (row-major, device memory, K % 8 == 0, 1 <= B <= 256): + bias_dev[N] (bf16,
  * or NULL), then max(., 0) if relu, stored to y_dev fp32 [B][N] or, if y_dev is
- * NULL, to y16_dev bf16 [B][N]. Uses a library-owned workspace (per process,
- * grown on demand). Enqueued on `stream` (a cudaStream_t; NULL = legacy default
- * stream). Errors: RANGE, CUDA. */
+ * NULL, to y16_dev bf16 [B][N]. Uses a library-owned workspace per device
+ * (allocated on first use, kept for the process), so calls on one device must
+ * be ordered on one stream. Enqueued on `stream` (a cudaStream_t; NULL = legacy
+ * default stream) on the current device. Errors: RANGE, CUDA. */
 int32_t mirage_sk_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
                        float* y_dev, void* y16_dev, const void* bias_dev, int32_t relu);
 

@@ -1122,18 +1122,26 @@ int32_t mirage_sk_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, co
                        float* y_dev, void* y16_dev, const void* bias_dev, int32_t relu) {
   if (!w_dev || !x_dev || (!y_dev && !y16_dev) || N <= 0 || K <= 0 || K % 8 || B <= 0 || B > 256)
     return MIRAGE_ERR_RANGE;
-  // process-wide workspace of the hook: partial slots and flags for one wave
+  // process-wide workspace of the hook, one per device: partial slots and flags for
+  // one wave (calls on one device must be stream-ordered: they share it)
   static std::mutex mu;
-  static float* ws = nullptr;
-  static int* flags = nullptr;
+  static std::map<int, std::pair<float*, int*>> wsmap;
+  float* ws = nullptr;
+  int* flags = nullptr;
   {
     std::lock_guard<std::mutex> lock(mu);
-    if (!ws) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return MIRAGE_ERR_CUDA;
+    auto it = wsmap.find(dev);
+    if (it == wsmap.end()) {
       const size_t n = (size_t)mirage::sk_gemm_max_ctas() * 256 * 128;
       if (cudaMalloc(&ws, n * 4) != cudaSuccess) return MIRAGE_ERR_CUDA;
       if (cudaMalloc(&flags, (size_t)mirage::sk_gemm_max_ctas() * 4) != cudaSuccess) return MIRAGE_ERR_CUDA;
       if (cudaMemset(flags, 0, (size_t)mirage::sk_gemm_max_ctas() * 4) != cudaSuccess) return MIRAGE_ERR_CUDA;
+      it = wsmap.emplace(dev, std::make_pair(ws, flags)).first;
     }
+    ws = it->second.first;
+    flags = it->second.second;
   }
   const cudaError_t e = mirage::launch_sk_gemm(
       reinterpret_cast<const bf16*>(w_dev), N, K, K, reinterpret_cast<const bf16*>(x_dev), B, K, y_dev,
