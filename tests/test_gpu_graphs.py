@@ -104,3 +104,37 @@ def test_streaming_cycle_graph_replays_bit_identical(cycle, beta):
         assert np.array_equal(ha, hb) and aa == ab, t
     assert la_log == lb_log == [(k, st, l, sl, int(cp)) for k, st, l, sl, cp in OT.slot_log(cycle, beta, 24)]
     assert la == lb
+
+
+def test_set_flags_switches_graphs_and_timing_mid_run():
+    """bench.py's two passes on one context: graph steps, then eager steps with
+    per-launch attention events (mirage_set_flags), then graphs again -- every step
+    bit-identical to an all-eager run with the same slot log, and the timing
+    counters advance only while FLAG_TIME_ATTN is on."""
+    from paper_2507_11507_b200 import Context, _lib
+    shape = models.TOY_LLAMA.with_layers(4)
+    cycle, beta, B, steps = [0, 1, 3], 2, 4, 30
+    ref, ref_log, _ = run_cycle(0, shape, cycle, beta, steps)
+    ctx = Context(harness.arena_for([(shape, 64)], 8, 256), 8, 256, flags=_lib.FLAG_CUDA_GRAPHS)
+    mid = ctx.add_model(shape, harness.make_blob(shape, seed=4), B)
+    ctx.remap_layers(mid, mid, cycle, beta)
+    hid = torch.empty((B, shape.d_model), dtype=torch.bfloat16, device="cuda")
+    mask = _lib.FLAG_TIME_ATTN | _lib.FLAG_CUDA_GRAPHS
+    timed = []
+    for t in range(steps):
+        if t == 10:
+            ctx.set_flags(_lib.FLAG_TIME_ATTN, mask)
+        if t == 20:
+            ctx.set_flags(_lib.FLAG_CUDA_GRAPHS, mask)
+        if t % 16 == 0:
+            for s in range(B):
+                ctx.alloc_blocks(mid, s, 1)
+        am = ctx.decode_step(mid, list(range(B)), [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)],
+                             [t] * B, hidden_out=hid)
+        ctx.sync()
+        assert np.array_equal(hid.float().cpu().numpy(), ref[t][0]) and list(am) == ref[t][1], t
+        timed.append(ctx.query(mid)["attn_launches"])
+    assert ctx.slot_log(mid) == ref_log
+    assert timed[9] == 0 and timed[19] > 0 and timed[29] == timed[25]   # events only in the eager pass
+    with pytest.raises(_lib.MirageError):
+        ctx.set_flags(0, _lib.FLAG_POISON)                                # not a measurement flag
