@@ -775,6 +775,22 @@ def run_mirage(args, rank, world):
         t_c = max(meas_med - res["stall_ms"] / args.steps, 1e-3) / n_l * 1e6   # compute only, stall removed
         predicted_stall = L_.predict_stall(n_l, list(info["cycle"]), info["beta"], t_t, t_c) / 1e6
     config = workload_config(wl, info, world)
+    # whole-step HBM roofline of the headline pass (algorithmic bytes of one step of
+    # tenant 0: every layer's K|V read by attention at the timed steps' mean context,
+    # every hidden layer's weights + the LM head read by the GEMMs, the re-streamed
+    # layers written by the copy engine) against the measured copy peak
+    sh0 = wl.tenants[0][0]
+    from synth import weights as W_
+    adv = (PRIME_STEPS if res.get("graphs") else 0) + args.warmup + (args.steps + 1) / 2
+    kv_b = sum(c + adv for c in wl.ctxs) * 2 * sh0.n_kv_heads * sh0.head_dim * 2 * sh0.n_layers
+    w_b = sh0.n_layers * W_.layer_bytes(sh0) + sh0.vocab * sh0.d_model * 2
+    rs_b = res["h2d_bytes"] / args.steps if res.get("h2d_bytes") else 0.0
+    step_bytes = kv_b + w_b + rs_b
+    step_roof = {"bytes_per_step": step_bytes, "kv_bytes": kv_b, "weight_bytes": w_b, "restream_bytes": rs_b,
+                 "achieved_gbs": step_bytes / (t_all / args.steps * 1e-3) / 1e9,
+                 "frac": step_bytes / (t_all / args.steps * 1e-3) / 1e9 / hbm_peak,
+                 "note": "algorithmic HBM bytes of one whole step / headline step time; the GEMMs at this batch "
+                         "are partly tensor-bound, so 1.0 is not reachable by the step"}
     line = {
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_all / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -796,6 +812,7 @@ def run_mirage(args, rank, world):
                      "frac_of_copy_peak_this_run": achieved / copy_peak_run if achieved else None,
                      "kernel_alone_frac": (res["alone_gbs"] / hbm_peak) if res.get("alone_gbs") else None,
                      "peak_source": peak_src},
+        "step_roofline": step_roof,
         "handoff": {"stall_ms_per_step": res["stall_ms"] / args.steps, "ready_waits": res["stall_waits"],
                     "predicted_stall_ms_per_step": predicted_stall,
                     "how": "events around each slot ready-wait on the compute stream (a5)"},
