@@ -570,7 +570,7 @@ int build_units_ranges(const int32_t* lens, const int32_t* seq_off, int B, int H
   for (int r = 0; r < R; ++r) {
     const int64_t lo = T * r / R, hi = T * (r + 1) / R;
     rfirst[r] = n;
-    while (b < B && seq_start + nbs[b] <= lo) seq_start += nbs[b++];  // (only empty sequences)
+    while (b < B && seq_start + nbs[b] <= lo) seq_start += nbs[b++];  // skip sequences that end before lo
     int64_t at = lo;
     int bb = b;
     int64_t st = seq_start;
