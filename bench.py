@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--graphs", action="store_true", help="(default) kept for compatibility")
+    ap.add_argument("--tc-gemm", action="store_true",
+                    help="row-parallel projections (O-proj, FC2/down) on the tcgen05 decode GEMM (MIRAGE_FLAG_TC_GEMM)")
     ap.add_argument("--eager", action="store_true",
                     help="run the headline pass eagerly with per-launch attention events (the round-1/2 default) "
                          "instead of as CUDA graphs followed by an eager measurement pass")
@@ -546,7 +548,8 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
     arena = harness.arena_for([(sh, nat) for sh, _, nat in tenants], B, max_ctx)
     graphs = not args.eager
     ctx = _lib.Context(arena, B, max_ctx, device=dev.index,
-                       flags=_lib.FLAG_CUDA_GRAPHS if graphs else _lib.FLAG_TIME_ATTN)
+                       flags=(_lib.FLAG_CUDA_GRAPHS if graphs else _lib.FLAG_TIME_ATTN) |
+                       (_lib.FLAG_TC_GEMM if getattr(args, "tc_gemm", False) else 0))
     mids = [ctx.add_model(sh, blobs[(sh.name, seed)], nat) for sh, seed, nat in tenants]
     if args.weight_source == "device" and remaps:
         dev_copy = blobs[(tenants[0][0].name, tenants[0][1])].to(dev)
