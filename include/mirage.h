@@ -484,8 +484,10 @@ int32_t mirage_sk_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, co
  * ctx is created, every attention launch of mirage_attn_only records 16
  * %globaltimer slots per CTA (ns: entry, first tiles issued, first tile
  * landed, last tile consumed, last output written, last split combine, exit;
- * slot 7 = items processed; 8-10 = phases of the last combine: ticket taken,
- * (m, l) staged, weights). This call synchronizes the compute stream and
+ * slot 7 = items processed; 9 = every consumer warp done with the last item;
+ * 8, 10 = phases of the last combine: ticket taken, weights computed; 12-15 =
+ * SM cycles from the merge start to the ticket, the first head's max, the
+ * weights barrier and the end of the fold). This call synchronizes the compute stream and
  * copies the last launch's [n_ctas][16] uint64 slots to host_out (capacity
  * cap_ctas CTAs). Errors: STATE (tracing off), RANGE (cap too small; *n_ctas
  * still receives the count), CUDA. */
