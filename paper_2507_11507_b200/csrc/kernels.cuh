@@ -105,14 +105,17 @@ cudaError_t launch_embed_norm(int family, int B, int d, const int32_t* tokens,
 cudaError_t launch_residual_norm(int family, int B, int d, const float* y, int ldy,
                                  const __nv_bfloat16* bias, const __nv_bfloat16* g,
                                  const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
-                                 cudaStream_t s, int nsplit = 1, long long slice = 0);
+                                 cudaStream_t s, int nsplit = 1, long long slice = 0, bool pdl = false);
 // qkv [B][(H+2Hk)D] fp32 (+bias, +RoPE) -> q in the attention kernel's split
 // format (AttnParams::q, scaled by q_scale); K/V bf16 appended to the paged cache
 // at positions[b] (block address addrs[seq_off[b] + pos / 16]).
 cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float* qkv,
                             const __nv_bfloat16* bias, const int32_t* positions,
                             const int32_t* seq_off, const uint64_t* addrs, uint64_t layer_off,
-                            float rope_theta, float q_scale, uint32_t* q, cudaStream_t s);
+                            float rope_theta, float q_scale, uint32_t* q, cudaStream_t s, bool pdl = false);
+// (pdl: launched with a programmatic dependency on the preceding kernel, the GEMM
+// whose output it reads; the prologue that does not touch that output overlaps
+// the GEMM's tail, griddepcontrol.wait guards the rest)
 // Block migration (mirage_migrate_region): copy `bytes` from src[i] to dst[i]
 // for i < n (device addresses, 16-byte aligned, bytes % 16 == 0).
 struct BlockMoves {

@@ -174,9 +174,14 @@ residual_norm_kernel(int family, int d, const float* y, int ldy, int nsplit, lon
   const int e0 = threadIdx.x * 8;
   const bool own = e0 < d;
   float v[8];
+  // under programmatic dependent launch the preceding kernel is the GEMM that
+  // writes y: h (and the bias) may be read before waiting for it, y only after
+  // (without y, the preceding kernel may have written h: wait first)
+  if (!y) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (own) {
     load8(h + (size_t)b * d + e0, v);
     if (y) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       float yv[8];
       load8(y + (size_t)b * ldy + e0, yv);
       for (int s_ = 1; s_ < nsplit; ++s_) {
@@ -330,6 +335,9 @@ qkv_post_kernel(int family, int H, int Hk, int D, const float* qkv, const __nv_b
   char* kvbase = reinterpret_cast<char*>(addrs[seq_off[b] + (pos >> 4)] + layer_off);
   const int r = pos & 15;
   const int n_qk = (H + Hk) * hc, n_v = Hk * (D / 8);
+  // the rotation angles and the cache address above need only this step's
+  // metadata; the QKV GEMM's output is read from here on
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < n_qk + n_v; e += gridDim.y * blockDim.x) {
     if (e < n_qk) {
       const int hh = e / hc, c = e % hc;
@@ -557,23 +565,39 @@ cudaError_t launch_embed_norm(int family, int B, int d, const int32_t* tokens,
 cudaError_t launch_residual_norm(int family, int B, int d, const float* y, int ldy,
                                  const __nv_bfloat16* bias, const __nv_bfloat16* g,
                                  const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
-                                 cudaStream_t s, int nsplit, long long slice) {
+                                 cudaStream_t s, int nsplit, long long slice, bool pdl) {
   if (d % 8 || d > 8192 || nsplit < 1) return cudaErrorInvalidValue;
-  residual_norm_kernel<<<B, ((d / 8 + 31) / 32) * 32, 0, s>>>(family, d, y, ldy, nsplit, slice, bias, g, bta, eps,
-                                                               h, x);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(B);
+  cfg.blockDim = dim3(((d / 8 + 31) / 32) * 32);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, residual_norm_kernel, family, d, y, ldy, nsplit, slice, bias, g, bta, eps, h, x);
 }
 
 cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float* qkv,
                             const __nv_bfloat16* bias, const int32_t* positions,
                             const int32_t* seq_off, const uint64_t* addrs, uint64_t layer_off,
-                            float rope_theta, float q_scale, uint32_t* q, cudaStream_t s) {
+                            float rope_theta, float q_scale, uint32_t* q, cudaStream_t s, bool pdl) {
   // one thread per work item: all of a row's loads are in flight at once (the
   // kernel is latency-bound at decode batch sizes)
   const int items = (H + Hk) * (D / 16) + Hk * (D / 8);
-  qkv_post_kernel<<<dim3(B, (items + 255) / 256), 256, D * sizeof(float), s>>>(family, H, Hk, D, qkv, bias, positions, seq_off,
-                                                    addrs, layer_off, rope_theta, q_scale, q);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(B, (items + 255) / 256);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = D * sizeof(float);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, qkv_post_kernel, family, H, Hk, D, qkv, bias, positions, seq_off, addrs, layer_off,
+                            rope_theta, q_scale, q);
 }
 
 __global__ void block_copy_kernel(BlockMoves m, uint64_t n16) {

@@ -2040,7 +2040,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     const uint64_t layer_off = (uint64_t)l * Hk * 2 * kBlockTokens * D * 2;
     if (int32_t e = gemm_lt(c, B, qkvN, d, w.w_qkv, M->x, M->y, 0, nullptr, 0)) return e;
     KL(c, mirage::launch_qkv_post(s.family, B, H, Hk, D, M->y, opt ? w.b_qkv : nullptr, dv.pos,
-                                 dv.seq_off, dv.addrs, layer_off, s.theta, ap.scale_log2, M->q, cs));
+                                 dv.seq_off, dv.addrs, layer_off, s.theta, ap.scale_log2, M->q, cs, use_pdl()));
     ap.layer_off = layer_off;
     if (time_attn) {
       Model::AttnTiming at{pool_event(M), pool_event(M), attn_bytes};
@@ -2075,7 +2075,8 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
         return e;
       }
       KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, opt ? w.b_o : nullptr, w.n2_g,
-                                        opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs, ns_o, (long long)B * d));
+                                        opt ? w.n2_b : nullptr, s.eps, M->h, M->x, cs, ns_o, (long long)B * d,
+                                        use_pdl()));
     }
     if (opt) {
       // FC1 + bias + ReLU fused in the GEMM epilogue, bf16 out (one rounding, as before)
@@ -2111,7 +2112,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
                                              M->flags_dev, ep2, M->tp_err, bias2, g2, b2, s.eps, M->h, M->x, cs));
       } else {
         KL(c, mirage::launch_residual_norm(s.family, B, d, M->y, d, bias2, g2, b2, s.eps, M->h, M->x, cs, ns_2,
-                                          (long long)B * d));
+                                          (long long)B * d, use_pdl()));
       }
       return MIRAGE_OK;
     };
