@@ -198,3 +198,42 @@ def test_balanced_ranges_schedule_16x16k_all_rows():
     worst, st = run_all_rows(attn_shape(32, 32, 8, 16384), [16384 - 5 * i for i in range(16)], layer=9)
     assert worst <= TOL, worst
     assert st["last_split_blocks"] == 0          # the planner chose balanced ranges
+
+
+def test_decode_step_with_balanced_ranges_vs_oracle():
+    """The balanced-range schedule inside mirage_decode_step (the step uploads the
+    ranges with its metadata and launches the whole grid): 8 sequences of ~19k
+    tokens on a Llama-shaped model with 8 kv heads (G = 4) -- 9,504 blocks over 37
+    ranges -- two decode steps against oracle c4 within the derived bound."""
+    from paper_2507_11507_b200 import Context
+    shape = models.ModelShape("llama-ranges", models.LLAMA, 1, 2048, 32, 8, 64, 512, 512, 32768, 1e-5, 10000.0)
+    B = 8
+    prompt = [19000 - 7 * i for i in range(B)]
+    nb = sum(harness.blocks_for(p + 2) for p in prompt)
+    ctx = Context(harness.arena_for([(shape, nb)], B, 19100), B, 19100)
+    mid = ctx.add_model(shape, harness.make_blob(shape, seed=6), nb)
+    layers = [weights.layer_tensors(shape, 0, 6)]
+    glob = weights.global_tensors(shape, 6)
+    kvs = []
+    for i, P in enumerate(prompt):
+        kv = workload.logical_kv(1, 8, 64, P, seed=21, seq=i)
+        ctx.alloc_blocks(mid, i, harness.blocks_for(P + 2))
+        ctx.write_kv(mid, i, kv)
+        kvf = kv.float().double().numpy()
+        kvs.append([(kvf[0, :, 0], kvf[0, :, 1])])
+    hid = torch.empty((B, shape.d_model), dtype=torch.bfloat16, device="cuda")
+    toks = [[workload.teacher_tokens(i, prompt[i] + t, shape.vocab) for i in range(B)] for t in range(2)]
+    got = []
+    for t in range(2):
+        ctx.decode_step(mid, list(range(B)), toks[t], [p + t for p in prompt], hidden_out=hid)
+        ctx.sync()
+        assert ctx.query(mid)["last_split_blocks"] == 0          # balanced ranges in the step
+        got.append(hid.float().cpu().numpy().copy())
+
+    def script(dec):
+        for i in range(B):
+            dec.set_kv(i, kvs[i])
+        return [dec.step(list(range(B)), toks[t], [p + t for p in prompt])[:2] for t in range(2)]
+    exact, bounds = CB.predict(shape, layers, glob, script, draws=2)
+    for t in range(2):
+        CB.check(got[t], exact[t][0], bounds[t], t)
