@@ -237,3 +237,35 @@ def test_decode_step_with_balanced_ranges_vs_oracle():
     exact, bounds = CB.predict(shape, layers, glob, script, draws=2)
     for t in range(2):
         CB.check(got[t], exact[t][0], bounds[t], t)
+
+
+def test_balanced_ranges_in_graph_replays_bit_identical():
+    """The balanced-range schedule under CUDA graphs: the replayed attention reads
+    the schedule and the ranges from the step's uploaded metadata and launches the
+    whole grid, so graph replays equal eager steps bit for bit."""
+    from paper_2507_11507_b200 import Context, _lib
+    shape = models.ModelShape("llama-ranges", models.LLAMA, 1, 2048, 32, 8, 64, 512, 512, 32768, 1e-5, 10000.0)
+    B = 8
+    prompt = [19000 - 7 * i for i in range(B)]
+    outs = {}
+    for flags in (0, _lib.FLAG_CUDA_GRAPHS):
+        nb = sum(harness.blocks_for(p + 6) for p in prompt)
+        ctx = Context(harness.arena_for([(shape, nb)], B, 19100), B, 19100, flags=flags)
+        mid = ctx.add_model(shape, harness.make_blob(shape, seed=6), nb)
+        for i, P in enumerate(prompt):
+            ctx.alloc_blocks(mid, i, harness.blocks_for(P + 6))
+            ctx.fill_kv(mid, i, P, seed=i)
+        hid = torch.empty((B, shape.d_model), dtype=torch.bfloat16, device="cuda")
+        res = []
+        for t in range(5):
+            am = ctx.decode_step(mid, list(range(B)), [workload.teacher_tokens(i, prompt[i] + t, shape.vocab)
+                                                      for i in range(B)], [p + t for p in prompt], hidden_out=hid)
+            ctx.sync()
+            assert ctx.query(mid)["last_split_blocks"] == 0
+            res.append((hid.float().cpu().numpy().copy(), list(am)))
+        outs[flags] = res
+        ctx.close()
+        del ctx
+        torch.cuda.empty_cache()
+    for (ha, aa), (hb, ab) in zip(outs[0], outs[_lib.FLAG_CUDA_GRAPHS]):
+        assert np.array_equal(ha, hb) and aa == ab
