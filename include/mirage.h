@@ -460,10 +460,14 @@ int64_t mirage_kernel_launches(const mirage_ctx* ctx);
  * of a tile run as one thread-block cluster and are summed in split order
  * through distributed shared memory inside the kernel (at most 8 splits,
  * B <= 128), so y_dev receives ONE slice [B][N] and *splits_out is set to 1.
+ * col_groups (0 or 1 = none, at most 8): the batch rows are cut into that many
+ * groups (each rounded up to 32/64/128/256 rows; empty groups dropped), one CTA
+ * per (128-row tile, split, group), each re-reading its tile's weights (the
+ * fused tensor-parallel push GEMM runs one split this way; not with reduce).
  * Enqueued on `stream` (a cudaStream_t; NULL = legacy default stream).
  * Errors: RANGE, CUDA. */
 int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
-                           float* y_dev, int32_t splits, int32_t reduce, int32_t* splits_out);
+                           float* y_dev, int32_t splits, int32_t reduce, int32_t col_groups, int32_t* splits_out);
 
 /* Test/bench hook: the persistent stream-K form of the tcgen05 decode GEMM
  * (SURVEY §8(a) a6 supporting row, NEXT-4): one wave of CTAs

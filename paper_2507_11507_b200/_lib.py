@@ -114,7 +114,7 @@ def _load():
         "mirage_write_kv": (I32, [P, I32, I64, I32, P]),
         "mirage_kernel_launches": (I64, [P]),
         "mirage_attn_trace": (I32, [P, pU64, I32, pI32]),
-        "mirage_decode_gemm": (I32, [P, P, I32, I32, P, I32, P, I32, I32, pI32]),
+        "mirage_decode_gemm": (I32, [P, P, I32, I32, P, I32, P, I32, I32, I32, pI32]),
         "mirage_sk_gemm": (I32, [P, P, I32, I32, P, I32, P, P, P, I32]),
         "mirage_set_flags": (I32, [P, C.c_uint32, C.c_uint32]),
         "mirage_nccl_unique_id": (I32, [P]),
@@ -195,7 +195,7 @@ def predict_stall(n_layers, cycle, beta, t_transfer_ns, t_compute_layer_ns):
     return out.value
 
 
-def decode_gemm(w, x, splits=0, stream=None, reduce=False):
+def decode_gemm(w, x, splits=0, stream=None, reduce=False, col_groups=0):
     """Y slices [splits][B][N] fp32 of x [B][K] @ w[N][K]^T on the tcgen05 decode GEMM
     (mirage_decode_gemm); both bf16 CUDA tensors. reduce: the splits are summed in
     the kernel (one slice). Returns (slices, number of slices)."""
@@ -208,7 +208,7 @@ def decode_gemm(w, x, splits=0, stream=None, reduce=False):
     got = C.c_int32()
     st = stream if stream is not None else torch.cuda.current_stream(w.device)
     rc = LIB.mirage_decode_gemm(st.cuda_stream, w.data_ptr(), N, K, x.data_ptr(), B, y.data_ptr(), int(splits),
-                                int(bool(reduce)), C.byref(got))
+                                int(bool(reduce)), int(col_groups), C.byref(got))
     if rc:
         raise MirageError(rc, "decode_gemm")
     return y[: got.value], got.value

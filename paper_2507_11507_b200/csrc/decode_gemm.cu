@@ -132,6 +132,7 @@ decode_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * kTileM;
   const int split = blockIdx.y;
+  const int zb = blockIdx.z * BN;  // column group: batch rows [zb, zb + BN) of this CTA
   const int kb0 = split * g.kb_per_split;
   const int kb1 = min(g.n_kb, kb0 + g.kb_per_split);
   const int nkb = kb1 - kb0;
@@ -165,7 +166,7 @@ decode_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
       uint8_t* a = smem + st * STAGE;
       mb_expect_tx(&full[st], STAGE);
       tma_2d(a, &tmW, (kb0 + i) * kTileK, n0, &full[st]);
-      tma_2d(a + A_BYTES, &tmX, (kb0 + i) * kTileK, 0, &full[st]);
+      tma_2d(a + A_BYTES, &tmX, (kb0 + i) * kTileK, zb, &full[st]);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer (one thread) ----
@@ -244,9 +245,9 @@ decode_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr + c0));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    const int nb = min(16, g.B - c0);
+    const int nb = min(16, g.B - zb - c0);
     if (n < g.N && nb > 0) {
-      const long long off = (long long)c0 * g.ldo + n;
+      const long long off = (long long)(zb + c0) * g.ldo + n;
 #pragma unroll 1
       for (int r = -1; r < g.n_peers; ++r) {  // r = -1: the local slice; r >= 0: fused TP push to rank r
         float* d = (r < 0 ? dst : g.peers[r] + g.peer_slot + (long long)split * g.slice) + off;
@@ -550,7 +551,7 @@ constexpr int smem_of() { return stages<BN>() * (kTileM * kTileK * 2 + BN * kTil
 
 template <int BN>
 cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const GemmArgs& g, int tiles, int splits,
-                      cudaStream_t s) {
+                      int cgroups, cudaStream_t s) {
   constexpr int SMEM = smem_of<BN>();
   static bool attr = false;
   if (!attr) {
@@ -559,7 +560,7 @@ cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const GemmAr
     attr = true;
   }
   if (!g.creduce) {
-    decode_gemm_kernel<BN><<<dim3(tiles, splits), 128, SMEM, s>>>(tw, tx, g);
+    decode_gemm_kernel<BN><<<dim3(tiles, splits, cgroups), 128, SMEM, s>>>(tw, tx, g);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg{};
@@ -630,11 +631,18 @@ int decode_gemm_splits(int N, int K, int B, int sms) {
 cudaError_t launch_decode_gemm(const __nv_bfloat16* W, int N, int K, int ldw, const __nv_bfloat16* X, int B, int ldx,
                                float* out, int ldo, long long slice, int splits, float* const* peers, int n_peers,
                                long long peer_slot, cudaStream_t s, unsigned long long* const* cnt, int n_cnt,
-                               bool reduce, int* slices_out) {
-  if (B <= 0 || B > 256 || N <= 0 || K <= 0 || splits < 1 || splits > kMaxGemmSplits || (ldw % 8) || (ldx % 8))
+                               bool reduce, int* slices_out, int cgroups) {
+  if (B <= 0 || B > 256 || N <= 0 || K <= 0 || splits < 1 || splits > kMaxGemmSplits || (ldw % 8) || (ldx % 8) ||
+      cgroups < 1 || cgroups > 8)
     return cudaErrorInvalidValue;
-  const int BN = ((B + 15) / 16) * 16;
+  // column groups: the batch is cut into cgroups groups of bn rows, one CTA per
+  // (tile, split, group); every group re-reads the tile's weights (from L2 when the
+  // groups of a tile run side by side), so a GEMM with few tiles covers more SMs
+  // without cutting K
+  const int Bg = (B + cgroups - 1) / cgroups;
+  const int BN = ((Bg + 15) / 16) * 16;
   const int bn = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  cgroups = (B + bn - 1) / bn;  // groups that actually hold rows
   CUtensorMap tw, tx;
   if (!tensor_map(&tw, W, N, K, ldw, kTileM) || !tensor_map(&tx, X, B, K, ldx, bn)) return cudaErrorInvalidValue;
   GemmArgs g{};
@@ -652,16 +660,37 @@ cudaError_t launch_decode_gemm(const __nv_bfloat16* W, int N, int K, int ldw, co
   g.cnt = cnt;
   g.n_cnt = cnt ? n_cnt : 0;
   // the partial tile parks in the stage ring: B x 128 fp32 must fit there (bn <= 128)
-  g.creduce = reduce && splits > 1 && splits <= kMaxClusterSplits && bn <= 128 &&
+  g.creduce = reduce && cgroups == 1 && splits > 1 && splits <= kMaxClusterSplits && bn <= 128 &&
               B * kTileM * 4 <= smem_of<128>() - 1024;
   if (slices_out) *slices_out = g.creduce ? 1 : splits;
   const int tiles = (N + kTileM - 1) / kTileM;
   switch (bn) {
-    case 32: return launch_bn<32>(tw, tx, g, tiles, splits, s);
-    case 64: return launch_bn<64>(tw, tx, g, tiles, splits, s);
-    case 128: return launch_bn<128>(tw, tx, g, tiles, splits, s);
-    default: return launch_bn<256>(tw, tx, g, tiles, splits, s);
+    case 32: return launch_bn<32>(tw, tx, g, tiles, splits, cgroups, s);
+    case 64: return launch_bn<64>(tw, tx, g, tiles, splits, cgroups, s);
+    case 128: return launch_bn<128>(tw, tx, g, tiles, splits, cgroups, s);
+    default: return launch_bn<256>(tw, tx, g, tiles, splits, cgroups, s);
   }
+}
+
+int decode_gemm_cgroups(int N, int B, int sms) {
+  // one K split (the fused tensor-parallel push): as many column groups of >= 32
+  // rows as keep the grid within one wave of two CTAs per SM
+  const int tiles = (N + kTileM - 1) / kTileM;
+  int best = 1;
+  for (int cg = 2; cg <= 8; cg *= 2) {
+    const int Bg = (B + cg - 1) / cg;
+    if (Bg < 32 && cg > 1) break;
+    if (tiles * cg > 2 * sms) break;
+    best = cg;
+  }
+  return best;
+}
+
+int decode_gemm_ctas_per_split(int N, int B, int cgroups) {
+  const int Bg = (B + cgroups - 1) / cgroups;
+  const int BN = ((Bg + 15) / 16) * 16;
+  const int bn = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  return ((N + kTileM - 1) / kTileM) * ((B + bn - 1) / bn);
 }
 
 int sk_gemm_max_ctas() { return 2 * 148 * 2; }

@@ -72,12 +72,18 @@ constexpr int kMaxGemmSplits = 16;
 cudaError_t launch_decode_gemm(const __nv_bfloat16* W, int N, int K, int ldw, const __nv_bfloat16* X, int B, int ldx,
                                float* out, int ldo, long long slice, int splits, float* const* peers, int n_peers,
                                long long peer_slot, cudaStream_t s, unsigned long long* const* cnt = nullptr,
-                               int n_cnt = 0, bool reduce = false, int* slices_out = nullptr);
+                               int n_cnt = 0, bool reduce = false, int* slices_out = nullptr, int cgroups = 1);
 // reduce = true: up to 8 splits of a tile (batch <= 128) are summed inside the GEMM
 // through a thread-block cluster's distributed shared memory, so `out` receives
 // ONE slice (*slices_out = 1); otherwise *slices_out = splits.
 // tiles (CTAs per split) of a decode GEMM with N output rows
 inline int decode_gemm_tiles(int N) { return (N + 127) / 128; }
+// cgroups > 1 cuts the batch into column groups of >= 32 rows, one CTA per (tile,
+// split, group) (launch_decode_gemm rounds the group width up to 32/64/128/256 and
+// drops empty groups): the column-group count the fused push GEMM uses, and the
+// CTAs (= arrival-counter increments) per split for a given request
+int decode_gemm_cgroups(int N, int B, int sms);
+int decode_gemm_ctas_per_split(int N, int B, int cgroups);
 // K splits for a B-row decode GEMM on `sms` SMs (per-SM load model, decode_gemm.cu)
 int decode_gemm_splits(int N, int K, int B, int sms);
 // Persistent stream-K form (decode_gemm.cu, "SK"): one wave of CTAs over the

@@ -820,9 +820,14 @@ int32_t tp_push_gemm(mirage_ctx* c, Model* M, int B, int N, int K, const bf16* W
   // one K split, so every rank receives B x N exactly once (summing the splits in
   // the kernel through a cluster's distributed shared memory first measured slower:
   // 13.1 vs 12.4 ms per 70B-TP8 shard step, profiles/r02_tp_push_vs_pull_per_rank.jsonl)
+  // column groups (batch cut into >= 32-row groups, one CTA each) spread the one
+  // split over more SMs: each group re-reads its tile's weights, from L2
+  static const int cg_env = getenv("MIRAGE_PUSH_CG") ? atoi(getenv("MIRAGE_PUSH_CG")) : 0;
+  const int cg = cg_env > 0 ? std::min(cg_env, 8) : mirage::decode_gemm_cgroups(N, B, c->sms);
   KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, mine, N, 0, 1, M->push_dst_dev + par * (c->tp - 1),
-                                   c->tp - 1, 0, c->cs, M->push_cnt_dev, c->tp));
-  M->push_expect += (unsigned long long)mirage::decode_gemm_tiles(N);  // every CTA signals once
+                                   c->tp - 1, 0, c->cs, M->push_cnt_dev, c->tp, false, nullptr, cg));
+  // every CTA signals once
+  M->push_expect += (unsigned long long)mirage::decode_gemm_ctas_per_split(N, B, cg);
   return MIRAGE_OK;
 }
 
@@ -1090,9 +1095,9 @@ int64_t mirage_kernel_launches(const mirage_ctx* c) { return c ? c->launches : 0
 
 
 int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
-                           float* y_dev, int32_t splits, int32_t reduce, int32_t* splits_out) {
+                           float* y_dev, int32_t splits, int32_t reduce, int32_t col_groups, int32_t* splits_out) {
   if (!w_dev || !x_dev || !y_dev || N <= 0 || K <= 0 || K % 8 || B <= 0 || B > 256 || splits < 0 ||
-      splits > mirage::kMaxGemmSplits)
+      splits > mirage::kMaxGemmSplits || col_groups < 0 || col_groups > 8)
     return MIRAGE_ERR_RANGE;
   if (splits == 0) {
     int dev = 0, sms = 148;
@@ -1105,7 +1110,7 @@ int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K
   const cudaError_t e = mirage::launch_decode_gemm(
       reinterpret_cast<const bf16*>(w_dev), N, K, K, reinterpret_cast<const bf16*>(x_dev), B, K, y_dev, N,
       (long long)B * N, splits, nullptr, 0, 0, reinterpret_cast<cudaStream_t>(stream), nullptr, 0, reduce != 0,
-      &slices);
+      &slices, col_groups > 0 ? col_groups : 1);
   if (splits_out) *splits_out = slices;
   return e == cudaSuccess ? MIRAGE_OK : MIRAGE_ERR_CUDA;
 }

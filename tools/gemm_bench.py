@@ -43,6 +43,8 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--shape", nargs="*", default=list(SHAPES))
     ap.add_argument("--reduce", action="store_true", help="sum the K splits in the kernel (cluster DSMEM)")
+    ap.add_argument("--one-split-cg", type=int, nargs="*", default=[],
+                    help="also time the one-split form (the fused TP push GEMM) with these column-group counts")
     a = ap.parse_args()
     for name in a.shape:
         N, K = SHAPES[name]
@@ -58,7 +60,7 @@ def main():
 
             def ours(i):
                 _lib.LIB.mirage_decode_gemm(st.cuda_stream, ws[i % copies].data_ptr(), N, K, x.data_ptr(), B,
-                                            y.data_ptr(), 0, int(a.reduce and B <= 128), C.byref(got))
+                                            y.data_ptr(), 0, int(a.reduce and B <= 128), 0, C.byref(got))
 
             y1 = torch.empty((B, N), dtype=torch.float32, device="cuda")
 
@@ -68,6 +70,13 @@ def main():
 
             def cublas(i):
                 torch.nn.functional.linear(x, ws[i % copies])
+            one = {}
+            for cg in a.one_split_cg:
+                def one_split(i, cg=cg):
+                    _lib.LIB.mirage_decode_gemm(st.cuda_stream, ws[i % copies].data_ptr(), N, K, x.data_ptr(), B,
+                                                y.data_ptr(), 1, 0, cg, C.byref(got))
+                t1 = timeit(one_split, a.reps)
+                one["cg%d" % cg] = {"us": round(t1 * 1e3, 2), "gbs": round(N * K * 2 / 1e9 / (t1 * 1e-3))}
             t_o = timeit(ours, a.reps)
             t_s = timeit(sk, a.reps)
             t_c = timeit(cublas, a.reps)
@@ -76,7 +85,8 @@ def main():
                               "tcgen05_us": round(t_o * 1e3, 2), "cublas_us": round(t_c * 1e3, 2),
                               "tcgen05_gbs": round(gb / (t_o * 1e-3)), "cublas_gbs": round(gb / (t_c * 1e-3)),
                               "sk_us": round(t_s * 1e3, 2), "sk_gbs": round(gb / (t_s * 1e-3)),
-                              "speedup": round(t_c / t_o, 3), "sk_speedup": round(t_c / t_s, 3)}), flush=True)
+                              "speedup": round(t_c / t_o, 3), "sk_speedup": round(t_c / t_s, 3),
+                              "one_split": one}), flush=True)
         del ws
         torch.cuda.empty_cache()
 
