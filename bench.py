@@ -42,7 +42,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="0 = config default (c2: 400, c4: 32)")
     ap.add_argument("--ctx", type=int, default=0, help="c4 context length (default 32768)")
     ap.add_argument("--alpha", type=int, default=1)
-    ap.add_argument("--beta", type=int, default=0, help="0 = config default (c2: 1, c4: 2)")
+    ap.add_argument("--beta", type=int, default=0,
+                    help="0 = config default (c2: 1, c4: 1 = the planner's choice, reading #6; SURVEY's C4 "
+                         "line used 2, which is link-bound: 3 x 436 MB per step > the step)")
     ap.add_argument("--placement", default="uniform", choices=["uniform", "last"])
     ap.add_argument("--weight-source", default="host", choices=["host", "device"],
                     help="re-streaming tier: pinned host copy (paper) or a device-resident copy "
@@ -466,7 +468,11 @@ def build_workload(args, rank, total_steps, impl="mirage", extra=0):
             B = args.batch or 32
             L = min(args.ctx or 32768, shape.max_pos) - run_steps - 1
             ctxs = [L] * B
-            beta_pol = args.beta or 2
+            # reading #6 (alpha + 1 preferred): the planner's rule picks beta = 1 here,
+            # T_T = 436 MB / 55.5 GB/s = 7.9 ms <= (floor(32/2) - 1) x T_c = 15 x 0.71 ms
+            # (profiles/r02i/bench_c4_beta1_planner.json); beta = 2 re-streams 3 layers per
+            # step, 23.6 ms of link time in a 22.6 ms step (profiles/r02i/bench_c4_beta2.json)
+            beta_pol = args.beta or 1
             desc = ("C4: Llama-3-8B-shaped GQA decode, %d x %d-token contexts, split-K paged attention; "
                     "{a} layer(s) remapped ({p} placement, beta={b}); native pool sized so the batch fits only "
                     "with the reclaimed blocks" % (B, L))

@@ -97,111 +97,183 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-// Normalise one row held 8 elements per thread (thread t owns elements
-// 8t..8t+7, t < d/8) and write bf16 x. family 0: LayerNorm (two-pass
-// mean/var), 1: RMSNorm.
-__device__ __forceinline__ void norm_row8(int family, int d, bool own, float (&v)[8],
-                                          const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps,
-                                          __nv_bfloat16* x, float* red) {
-  const int e0 = threadIdx.x * 8;
-  float gv[8], bv[8], out[8];
-  if (own) {  // issue the parameter loads before the reductions (one DRAM round trip less)
-    load8bf(g + e0, gv);
-    if (family == 0) load8bf(bta + e0, bv);
+// A row of d fp32 elements is held CH float4 chunks per thread: thread t owns
+// chunks t, t + T, ..., t + (CH - 1) T (T = blockDim.x), so each load instruction
+// of a warp reads 512 consecutive bytes; chunks past d / 4 are not owned (zeros).
+// CH = 4 for d >= 4096 keeps a block at <= 512 threads, so two or three rows
+// are resident per SM at <= 64 registers and a decode batch runs in one wave.
+__device__ __forceinline__ void ld4(const float* p, float (&v)[4]) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
+__device__ __forceinline__ void ld4cg(const float* p, float (&v)[4]) {  // L2 only (peer-written slots)
+  const float4 a = __ldcg(reinterpret_cast<const float4*>(p));
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
+__device__ __forceinline__ void st4(float* p, const float (&v)[4]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void unpack4bf(uint2 u, float (&v)[4]) {
+  v[0] = __uint_as_float(u.x << 16);
+  v[1] = __uint_as_float(u.x & 0xffff0000u);
+  v[2] = __uint_as_float(u.y << 16);
+  v[3] = __uint_as_float(u.y & 0xffff0000u);
+}
+__device__ __forceinline__ uint2 ld4bfw(const __nv_bfloat16* p) { return *reinterpret_cast<const uint2*>(p); }
+__device__ __forceinline__ void ld4bf(const __nv_bfloat16* p, float (&v)[4]) { unpack4bf(ld4bfw(p), v); }
+__device__ __forceinline__ uint2 pack4bf(const float (&v)[4]) {
+  return make_uint2((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v[0])) |
+                        ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v[1])) << 16),
+                    (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v[2])) |
+                        ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v[3])) << 16));
+}
+__host__ __device__ constexpr int row_chunks(int d) { return d >= 4096 ? 4 : 2; }
+inline int row_threads(int d) { return ((d / 4 + row_chunks(d) - 1) / row_chunks(d) + 31) / 32 * 32; }
+
+// Normalise the row and write bf16 x. family 0: LayerNorm (two-pass mean/var),
+// 1: RMSNorm. Each thread sums its own elements in chunk order, then the block
+// sums the per-thread values in fixed order (deterministic).
+template <int CH>
+__device__ __forceinline__ void norm_row(int family, int d, const float (&v)[CH][4], const __nv_bfloat16* g,
+                                         const __nv_bfloat16* bta, float eps, __nv_bfloat16* x, float* red) {
+  const int T = blockDim.x, nc = d >> 2;
+  uint2 gw[CH], bw[CH];
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {  // issue the parameter loads before the reductions
+    const int c = j * T + threadIdx.x;
+    if (c < nc) {
+      gw[j] = ld4bfw(g + 4 * c);
+      if (family == 0) bw[j] = ld4bfw(bta + 4 * c);
+    }
   }
+  float mean = 0.f, q = 0.f;
   if (family == 0) {
     float sm = 0.f;
-    if (own)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) sm += v[k];
-    const float mean = block_sum(sm, red) / d;
-    float q = 0.f;
-    if (own)
+    for (int j = 0; j < CH; ++j)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) q += (v[k] - mean) * (v[k] - mean);
-    const float r = rsqrtf(block_sum(q, red) / d + eps);
-    if (own) {
+      for (int k = 0; k < 4; ++k) sm += v[j][k];  // unowned chunks are zero
+    mean = block_sum(sm, red) / d;
+  }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) out[k] = (v[k] - mean) * r * gv[k] + bv[k];
-      *reinterpret_cast<uint4*>(x + e0) = pack8bf(out);
-    }
-  } else {
-    float q = 0.f;
-    if (own)
+  for (int j = 0; j < CH; ++j)
+    if (j * T + (int)threadIdx.x < nc)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) q += v[k] * v[k];
-    const float r = rsqrtf(block_sum(q, red) / d + eps);
-    if (own) {
+      for (int k = 0; k < 4; ++k) q += (v[j][k] - mean) * (v[j][k] - mean);
+  const float r = rsqrtf(block_sum(q, red) / d + eps);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) out[k] = v[k] * r * gv[k];
-      *reinterpret_cast<uint4*>(x + e0) = pack8bf(out);
+  for (int j = 0; j < CH; ++j) {
+    const int c = j * T + threadIdx.x;
+    if (c < nc) {
+      float gv[4], out[4];
+      unpack4bf(gw[j], gv);
+      if (family == 0) {
+        float bv[4];
+        unpack4bf(bw[j], bv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) out[k] = (v[j][k] - mean) * r * gv[k] + bv[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) out[k] = v[j][k] * r * gv[k];
+      }
+      *reinterpret_cast<uint2*>(x + 4 * c) = pack4bf(out);
     }
   }
 }
 
-__global__ void __launch_bounds__(1024)
+template <int CH>
+__global__ void __launch_bounds__(512, 2)
 embed_norm_kernel(int family, int d, const int32_t* tokens, const int32_t* positions,
                   const __nv_bfloat16* embed, const __nv_bfloat16* pos_embed,
                   const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps, float* h,
                   __nv_bfloat16* x) {
   __shared__ __align__(16) float red[32];
-  const int b = blockIdx.x;
-  const int e0 = threadIdx.x * 8;
-  const bool own = e0 < d;
-  float v[8];
-  if (own) {
-    load8bf(embed + (size_t)tokens[b] * d + e0, v);
-    if (family == 0) {
-      float pv[8];
-      load8bf(pos_embed + (size_t)(positions[b] + 2) * d + e0, pv);
+  const int b = blockIdx.x, T = blockDim.x, nc = d >> 2;
+  float v[CH][4] = {};
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] += pv[k];
+  for (int j = 0; j < CH; ++j) {
+    const int c = j * T + threadIdx.x;
+    if (c < nc) {
+      ld4bf(embed + (size_t)tokens[b] * d + 4 * c, v[j]);
+      if (family == 0) {
+        float pv[4];
+        ld4bf(pos_embed + (size_t)(positions[b] + 2) * d + 4 * c, pv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[j][k] += pv[k];
+      }
+      st4(h + (size_t)b * d + 4 * c, v[j]);
     }
-    store8(h + (size_t)b * d + e0, v);
   }
-  norm_row8(family, d, own, v, g, bta, eps, x + (size_t)b * d, red);
+  norm_row<CH>(family, d, v, g, bta, eps, x + (size_t)b * d, red);
 }
 
 // h[b] += y[b] (+ bias) if y != nullptr; then x[b] = bf16(norm(h[b])) if g != nullptr.
 // y may hold nsplit split-K slices (the tcgen05 decode GEMM's output), `slice`
 // floats apart: they are summed in slice order, then added.
-__global__ void __launch_bounds__(1024)
+template <int CH>
+__global__ void __launch_bounds__(512, 2)
 residual_norm_kernel(int family, int d, const float* y, int ldy, int nsplit, long long slice,
                      const __nv_bfloat16* bias, const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps,
                      float* h, __nv_bfloat16* x) {
   __shared__ __align__(16) float red[32];
-  const int b = blockIdx.x;
-  const int e0 = threadIdx.x * 8;
-  const bool own = e0 < d;
-  float v[8];
+  const int b = blockIdx.x, T = blockDim.x, nc = d >> 2;
+  float v[CH][4] = {};
   // under programmatic dependent launch the preceding kernel is the GEMM that
   // writes y: h (and the bias) may be read before waiting for it, y only after
   // (without y, the preceding kernel may have written h: wait first)
   if (!y) asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (own) {
-    load8(h + (size_t)b * d + e0, v);
-    if (y) {
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      float yv[8];
-      load8(y + (size_t)b * ldy + e0, yv);
-      for (int s_ = 1; s_ < nsplit; ++s_) {
-        float ys[8];
-        load8(y + s_ * slice + (size_t)b * ldy + e0, ys);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) yv[k] += ys[k];
+  for (int j = 0; j < CH; ++j) {
+    const int c = j * T + threadIdx.x;
+    if (c < nc) ld4(h + (size_t)b * d + 4 * c, v[j]);
+  }
+  if (y) {
+    // every load of the row is issued before the first store (a store to h between
+    // them would serialise one DRAM round trip per chunk: the compiler cannot
+    // prove h and y apart)
+    uint2 bw[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+      if (bias && j * T + (int)threadIdx.x < nc) bw[j] = ld4bfw(bias + 4 * (j * T + threadIdx.x));
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    float yv[CH][4];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int c = j * T + threadIdx.x;
+      if (c < nc) ld4(y + (size_t)b * ldy + 4 * c, yv[j]);
+    }
+    for (int s_ = 1; s_ < nsplit; ++s_)
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int c = j * T + threadIdx.x;
+        if (c < nc) {
+          float ys[4];
+          ld4(y + s_ * slice + (size_t)b * ldy + 4 * c, ys);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) yv[j][k] += ys[k];
+        }
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] += yv[k];
-      if (bias) {
-        float bv[8];
-        load8bf(bias + e0, bv);
+    for (int j = 0; j < CH; ++j) {
+      const int c = j * T + threadIdx.x;
+      if (c < nc) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] += bv[k];
+        for (int k = 0; k < 4; ++k) v[j][k] += yv[j][k];
+        if (bias) {
+          float bv[4];
+          unpack4bf(bw[j], bv);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[j][k] += bv[k];
+        }
       }
-      store8(h + (size_t)b * d + e0, v);
+    }
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int c = j * T + threadIdx.x;
+      if (c < nc) st4(h + (size_t)b * d + 4 * c, v[j]);
     }
   }
-  if (g) norm_row8(family, d, own, v, g, bta, eps, x + (size_t)b * d, red);
+  if (g) norm_row<CH>(family, d, v, g, bta, eps, x + (size_t)b * d, red);
 }
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
@@ -213,7 +285,49 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
-__global__ void __launch_bounds__(1024)
+// h[b] += sum over ranks r (fixed order) of parts[r][b] (+ bias), then the norm
+template <int CH>
+__device__ __forceinline__ void tp_sum_norm(int family, int d, const float* const* parts, int tp, bool cg,
+                                            const __nv_bfloat16* bias, const __nv_bfloat16* g,
+                                            const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
+                                            float* red) {
+  const int b = blockIdx.x, T = blockDim.x, nc = d >> 2;
+  float v[CH][4] = {};
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int c = j * T + threadIdx.x;
+    if (c < nc) ld4(h + (size_t)b * d + 4 * c, v[j]);
+  }
+  for (int r = 0; r < tp; ++r)  // fixed order: every rank computes the same sum
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int c = j * T + threadIdx.x;
+      if (c < nc) {
+        float pv[4];
+        if (cg) ld4cg(parts[r] + (size_t)b * d + 4 * c, pv);
+        else ld4(parts[r] + (size_t)b * d + 4 * c, pv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[j][k] += pv[k];
+      }
+    }
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int c = j * T + threadIdx.x;
+    if (c < nc) {
+      if (bias) {
+        float bv[4];
+        ld4bf(bias + 4 * c, bv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[j][k] += bv[k];
+      }
+      st4(h + (size_t)b * d + 4 * c, v[j]);
+    }
+  }
+  if (g) norm_row<CH>(family, d, v, g, bta, eps, x + (size_t)b * d, red);
+}
+
+template <int CH>
+__global__ void __launch_bounds__(512, 2)
 tp_residual_norm_kernel(int family, int d, const float* const* parts, int tp, int rank,
                         unsigned long long* const* flags, unsigned long long epoch, unsigned int* err,
                         const __nv_bfloat16* bias, const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps,
@@ -238,35 +352,16 @@ tp_residual_norm_kernel(int family, int d, const float* const* parts, int tp, in
     }
   }
   __syncthreads();
-  const int e0 = threadIdx.x * 8;
-  const bool own = e0 < d;
-  float v[8];
-  if (own) {
-    load8(h + (size_t)b * d + e0, v);
-    for (int r = 0; r < tp; ++r) {  // fixed order: every rank computes the same sum
-      float pv[8];
-      load8(parts[r] + (size_t)b * d + e0, pv);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] += pv[k];
-    }
-    if (bias) {
-      float bv[8];
-      load8bf(bias + e0, bv);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] += bv[k];
-    }
-    store8(h + (size_t)b * d + e0, v);
-  }
-  if (g) norm_row8(family, d, own, v, g, bta, eps, x + (size_t)b * d, red);
+  tp_sum_norm<CH>(family, d, parts, tp, false, bias, g, bta, eps, h, x, red);
 }
 
-__global__ void __launch_bounds__(1024)
+template <int CH>
+__global__ void __launch_bounds__(512, 2)
 tp_push_residual_norm_kernel(int family, int d, const float* const* slots, int tp, const unsigned long long* cnt,
                              unsigned long long expect, unsigned int* err, const __nv_bfloat16* bias,
                              const __nv_bfloat16* g, const __nv_bfloat16* bta, float eps, float* h,
                              __nv_bfloat16* x) {
   __shared__ __align__(16) float red[32];
-  const int b = blockIdx.x;
   if (threadIdx.x == 0) {
     for (int r = 0; r < tp; ++r) {  // every rank's tiles of this GEMM have landed here
       long long n = 0;
@@ -280,29 +375,7 @@ tp_push_residual_norm_kernel(int family, int d, const float* const* slots, int t
     }
   }
   __syncthreads();
-  const int e0 = threadIdx.x * 8;
-  const bool own = e0 < d;
-  float v[8];
-  if (own) {
-    load8(h + (size_t)b * d + e0, v);
-    for (int r = 0; r < tp; ++r) {  // fixed order: every rank computes the same sum
-      float pv[8];
-      const float4* src = reinterpret_cast<const float4*>(slots[r] + (size_t)b * d + e0);
-      const float4 p0 = __ldcg(src), p1 = __ldcg(src + 1);
-      pv[0] = p0.x; pv[1] = p0.y; pv[2] = p0.z; pv[3] = p0.w;
-      pv[4] = p1.x; pv[5] = p1.y; pv[6] = p1.z; pv[7] = p1.w;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] += pv[k];
-    }
-    if (bias) {
-      float bv[8];
-      load8bf(bias + e0, bv);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] += bv[k];
-    }
-    store8(h + (size_t)b * d + e0, v);
-  }
-  if (g) norm_row8(family, d, own, v, g, bta, eps, x + (size_t)b * d, red);
+  tp_sum_norm<CH>(family, d, slots, tp, true, bias, g, bta, eps, h, x, red);
 }
 
 // One CTA per sequence. Adds the bias, applies rotate-half RoPE (Llama) with the
@@ -557,8 +630,12 @@ cudaError_t launch_embed_norm(int family, int B, int d, const int32_t* tokens,
                               const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
                               cudaStream_t s) {
   if (d % 8 || d > 8192) return cudaErrorInvalidValue;
-  embed_norm_kernel<<<B, ((d / 8 + 31) / 32) * 32, 0, s>>>(family, d, tokens, positions, embed, pos_embed, g,
-                                               bta, eps, h, x);
+  if (row_chunks(d) == 4)
+    embed_norm_kernel<4><<<B, row_threads(d), 0, s>>>(family, d, tokens, positions, embed, pos_embed, g, bta, eps,
+                                                      h, x);
+  else
+    embed_norm_kernel<2><<<B, row_threads(d), 0, s>>>(family, d, tokens, positions, embed, pos_embed, g, bta, eps,
+                                                      h, x);
   return cudaGetLastError();
 }
 
@@ -569,14 +646,17 @@ cudaError_t launch_residual_norm(int family, int B, int d, const float* y, int l
   if (d % 8 || d > 8192 || nsplit < 1) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(B);
-  cfg.blockDim = dim3(((d / 8 + 31) / 32) * 32);
+  cfg.blockDim = dim3(row_threads(d));
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, residual_norm_kernel, family, d, y, ldy, nsplit, slice, bias, g, bta, eps, h, x);
+  if (row_chunks(d) == 4)
+    return cudaLaunchKernelEx(&cfg, residual_norm_kernel<4>, family, d, y, ldy, nsplit, slice, bias, g, bta, eps, h,
+                              x);
+  return cudaLaunchKernelEx(&cfg, residual_norm_kernel<2>, family, d, y, ldy, nsplit, slice, bias, g, bta, eps, h, x);
 }
 
 cudaError_t launch_qkv_post(int family, int B, int H, int Hk, int D, const float* qkv,
@@ -641,8 +721,12 @@ cudaError_t launch_tp_push_residual_norm(int family, int B, int d, const float* 
                                          const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
                                          cudaStream_t s) {
   if (d % 8 || d > 8192) return cudaErrorInvalidValue;
-  tp_push_residual_norm_kernel<<<B, ((d / 8 + 31) / 32) * 32, 0, s>>>(family, d, slots, tp, cnt, expect, err, bias,
-                                                                       g, bta, eps, h, x);
+  if (row_chunks(d) == 4)
+    tp_push_residual_norm_kernel<4><<<B, row_threads(d), 0, s>>>(family, d, slots, tp, cnt, expect, err, bias, g,
+                                                                 bta, eps, h, x);
+  else
+    tp_push_residual_norm_kernel<2><<<B, row_threads(d), 0, s>>>(family, d, slots, tp, cnt, expect, err, bias, g,
+                                                                 bta, eps, h, x);
   return cudaGetLastError();
 }
 
@@ -652,8 +736,12 @@ cudaError_t launch_tp_residual_norm(int family, int B, int d, const float* const
                                     const __nv_bfloat16* bta, float eps, float* h, __nv_bfloat16* x,
                                     cudaStream_t s) {
   if (d % 8 || d > 8192) return cudaErrorInvalidValue;
-  tp_residual_norm_kernel<<<B, ((d / 8 + 31) / 32) * 32, 0, s>>>(family, d, parts, tp, rank, flags, epoch, err,
-                                                                 bias, g, bta, eps, h, x);
+  if (row_chunks(d) == 4)
+    tp_residual_norm_kernel<4><<<B, row_threads(d), 0, s>>>(family, d, parts, tp, rank, flags, epoch, err, bias, g,
+                                                            bta, eps, h, x);
+  else
+    tp_residual_norm_kernel<2><<<B, row_threads(d), 0, s>>>(family, d, parts, tp, rank, flags, epoch, err, bias, g,
+                                                            bta, eps, h, x);
   return cudaGetLastError();
 }
 
