@@ -454,7 +454,7 @@ int64_t mirage_kernel_launches(const mirage_ctx* ctx);
  * cores (tcgen05 + TMEM, TMA-fed; SURVEY §8(a) a6 supporting row, NEXT-4):
  * Y_s[b][n] = sum over split s's share of K of X[b][k] * W[n][k], for
  * W = w_dev bf16 [N][K] and X = x_dev bf16 [B][K] (row-major, device memory,
- * K % 8 == 0, 1 <= B <= 256), written to y_dev fp32 [splits][B][N]; the splits
+ * K % 8 == 0, 1 <= B <= 256, or <= 256 * col_groups), written to y_dev fp32 [splits][B][N]; the splits
  * partition K in order and sum to Y. splits = 0 picks the library's choice
  * (a per-SM load model) and reports it in *splits_out. reduce != 0: splits
  * of a tile run as one thread-block cluster and are summed in split order
@@ -463,7 +463,8 @@ int64_t mirage_kernel_launches(const mirage_ctx* ctx);
  * col_groups (0 or 1 = none, at most 8): the batch rows are cut into that many
  * groups (each rounded up to 32/64/128/256 rows; empty groups dropped), one CTA
  * per (128-row tile, split, group), each re-reading its tile's weights (the
- * fused tensor-parallel push GEMM runs one split this way; not with reduce).
+ * fused tensor-parallel push GEMM runs one split this way; not with reduce);
+ * B may then reach 256 * col_groups.
  * Enqueued on `stream` (a cudaStream_t; NULL = legacy default stream).
  * Errors: RANGE, CUDA. */
 int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,

@@ -632,8 +632,8 @@ cudaError_t launch_decode_gemm(const __nv_bfloat16* W, int N, int K, int ldw, co
                                float* out, int ldo, long long slice, int splits, float* const* peers, int n_peers,
                                long long peer_slot, cudaStream_t s, unsigned long long* const* cnt, int n_cnt,
                                bool reduce, int* slices_out, int cgroups) {
-  if (B <= 0 || B > 256 || N <= 0 || K <= 0 || splits < 1 || splits > kMaxGemmSplits || (ldw % 8) || (ldx % 8) ||
-      cgroups < 1 || cgroups > 8)
+  if (B <= 0 || cgroups < 1 || cgroups > 8 || B > 256 * cgroups || N <= 0 || K <= 0 || splits < 1 ||
+      splits > kMaxGemmSplits || (ldw % 8) || (ldx % 8))
     return cudaErrorInvalidValue;
   // column groups: the batch is cut into cgroups groups of bn rows, one CTA per
   // (tile, split, group); every group re-reads the tile's weights (from L2 when the
@@ -676,8 +676,8 @@ int decode_gemm_cgroups(int N, int B, int sms) {
   // one K split (the fused tensor-parallel push): as many column groups of >= 32
   // rows as keep the grid within one wave of two CTAs per SM
   const int tiles = (N + kTileM - 1) / kTileM;
-  int best = 1;
-  for (int cg = 2; cg <= 8; cg *= 2) {
+  int best = (B + 255) / 256;  // a group holds at most 256 rows (the MMA's N)
+  for (int cg = 2 * best; cg <= 8; cg *= 2) {
     const int Bg = (B + cg - 1) / cg;
     if (Bg < 32 && cg > 1) break;
     if (tiles * cg > 2 * sms) break;

@@ -823,7 +823,8 @@ int32_t tp_push_gemm(mirage_ctx* c, Model* M, int B, int N, int K, const bf16* W
   // column groups (batch cut into >= 32-row groups, one CTA each) spread the one
   // split over more SMs: each group re-reads its tile's weights, from L2
   static const int cg_env = getenv("MIRAGE_PUSH_CG") ? atoi(getenv("MIRAGE_PUSH_CG")) : 0;
-  const int cg = cg_env > 0 ? std::min(cg_env, 8) : mirage::decode_gemm_cgroups(N, B, c->sms);
+  const int cg = std::max((B + 255) / 256,
+                          cg_env > 0 ? std::min(cg_env, 8) : mirage::decode_gemm_cgroups(N, B, c->sms));
   KL(c, mirage::launch_decode_gemm(W, N, K, K, x, B, K, mine, N, 0, 1, M->push_dst_dev + par * (c->tp - 1),
                                    c->tp - 1, 0, c->cs, M->push_cnt_dev, c->tp, false, nullptr, cg));
   // every CTA signals once
@@ -1096,8 +1097,8 @@ int64_t mirage_kernel_launches(const mirage_ctx* c) { return c ? c->launches : 0
 
 int32_t mirage_decode_gemm(void* stream, const void* w_dev, int32_t N, int32_t K, const void* x_dev, int32_t B,
                            float* y_dev, int32_t splits, int32_t reduce, int32_t col_groups, int32_t* splits_out) {
-  if (!w_dev || !x_dev || !y_dev || N <= 0 || K <= 0 || K % 8 || B <= 0 || B > 256 || splits < 0 ||
-      splits > mirage::kMaxGemmSplits || col_groups < 0 || col_groups > 8)
+  if (!w_dev || !x_dev || !y_dev || N <= 0 || K <= 0 || K % 8 || B <= 0 || col_groups < 0 || col_groups > 8 ||
+      B > 256 * std::max(1, col_groups) || splits < 0 || splits > mirage::kMaxGemmSplits)
     return MIRAGE_ERR_RANGE;
   if (splits == 0) {
     int dev = 0, sms = 148;

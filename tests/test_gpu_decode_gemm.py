@@ -116,24 +116,32 @@ def test_sk_gemm_bias_relu_bf16_epilogue(N, K, B, relu):
 
 @pytest.mark.parametrize("N,K,B,splits,cg", [(8192, 1024, 64, 1, 2), (8192, 3584, 64, 1, 2), (1000, 776, 37, 1, 2),
                                              (700, 2048, 200, 1, 4), (8192, 1024, 128, 1, 4), (384, 4096, 16, 1, 2),
-                                             (5120, 5120, 100, 3, 3), (130, 520, 250, 2, 8)])
+                                             (5120, 5120, 100, 3, 3), (130, 520, 250, 2, 8),
+                                             (5120, 1024, 400, 1, 2), (1000, 776, 300, 2, 4)])
 def test_decode_gemm_column_groups_bit_identical(N, K, B, splits, cg):
     """col_groups: the batch rows are cut into groups, one CTA per (tile, split,
     group), each re-reading its tile's weights. Every output element still sums the
     same K blocks in the same MMA order, so the slices are bit-identical to the
     ungrouped launch, and within the fp64 reference's bound. Ragged groups (B not a
-    multiple of the group width) and groups that round to an empty tail included."""
+    multiple of the group width) and groups that round to an empty tail included;
+    with groups the batch may exceed one MMA's 256 columns (B = 300, 400)."""
     from paper_2507_11507_b200 import _lib
     g = torch.Generator(device="cuda").manual_seed(N * 5 + K + B * 11 + cg)
     w = (torch.randn((N, K), generator=g, device="cuda") / K ** 0.5).to(torch.bfloat16)
     x = torch.randn((B, K), generator=g, device="cuda").to(torch.bfloat16)
-    y1, n1 = _lib.decode_gemm(w, x, splits)
     yg, ng = _lib.decode_gemm(w, x, splits, col_groups=cg)
     torch.cuda.synchronize()
-    assert n1 == ng == splits
+    assert ng == splits
     r = ref(w, x)
     got = yg.double().sum(0)
     assert (got - r).abs().max().item() <= 2e-5 * r.abs().max().item() + 1e-6 * K ** 0.5
+    if B > 256:  # more rows than one MMA's N: only a grouped launch exists
+        with pytest.raises(_lib.MirageError):
+            _lib.decode_gemm(w, x, splits)
+        return
+    y1, n1 = _lib.decode_gemm(w, x, splits)
+    torch.cuda.synchronize()
+    assert n1 == splits
     # the group width is rounded to 32/64/128/256 rows, so the MMA N differs between
     # the two launches: compare element values, which tcgen05 accumulates per column
     assert torch.equal(yg, y1)
