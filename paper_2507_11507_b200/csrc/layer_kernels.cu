@@ -495,11 +495,25 @@ __global__ void __launch_bounds__(1024) argmax_kernel(int V, const float* logits
   const float* row = logits + (size_t)b * V;
   float best = -CUDART_INF_F;
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
-    const float v = row[i];
-    if (v > best) {  // i increases per thread: keeps the lowest index on ties
-      best = v;
-      bi = i;
+  // indices increase per thread, so a strict > keeps the lowest index on ties
+  if ((V & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    const int V4 = V >> 2;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < V4; i += blockDim.x) {
+      const float4 q = __ldcs(r4 + i);  // read once: stream past L1/L2
+      if (q.x > best) { best = q.x; bi = 4 * i; }
+      if (q.y > best) { best = q.y; bi = 4 * i + 1; }
+      if (q.z > best) { best = q.z; bi = 4 * i + 2; }
+      if (q.w > best) { best = q.w; bi = 4 * i + 3; }
+    }
+  } else {
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+      const float v = row[i];
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
     }
   }
 #pragma unroll

@@ -75,15 +75,17 @@ def run_ranks(tp, push, B=4):
     return res
 
 
-@pytest.mark.parametrize("push,B", [(False, 4), (True, 4), (True, 64)],
-                         ids=["pull-consumer", "fused-gemm-push", "fused-gemm-push-column-groups"])
+@pytest.mark.parametrize("push,B", [(False, 4), (True, 4), (True, 64), (True, 300)],
+                         ids=["pull-consumer", "fused-gemm-push", "fused-gemm-push-column-groups",
+                              "fused-gemm-push-b300"])
 def test_two_rank_tp_over_peer_memory_matches_oracle(push, B):
     """pull: cuBLASLt partial GEMM, then one kernel reads the peers' partials (a10).
     fused-gemm-push (MIRAGE_FLAG_TC_GEMM, NEXT-4): the tcgen05 decode GEMM's
     epilogue stores each partial tile into every rank's exchange buffer and bumps
     the rank's arrival counter; the consumer reads local memory only. At B = 64
     the push GEMM cuts the batch into two 32-row column groups (two CTAs per
-    tile, so the arrival counters expect twice the tiles)."""
+    tile, so the arrival counters expect twice the tiles); at B = 300 the batch
+    exceeds one MMA's 256 columns and only a grouped launch exists."""
     import c4_bounds as CB
     from oracle.decode import Decoder
     from synth import models, weights, workload
