@@ -825,9 +825,17 @@ def run_mirage(args, rank, world):
         "handoff": {"stall_ms_per_step": res["stall_ms"] / args.steps, "ready_waits": res["stall_waits"],
                     "predicted_stall_ms_per_step": predicted_stall,
                     "how": "events around each slot ready-wait on the compute stream (a5)"},
-        "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": h2d_peak, "frac": (h2d_gbs / h2d_peak) if h2d_gbs else None,
-                "bytes_per_step": res["h2d_bytes"] / args.steps, "copies": res["h2d_copies"],
-                "peak_source": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this run"},
+        "h2d": ({"achieved_gbs": h2d_gbs, "peak_gbs": h2d_peak, "frac": (h2d_gbs / h2d_peak) if h2d_gbs else None,
+                 "bytes_per_step": res["h2d_bytes"] / args.steps, "copies": res["h2d_copies"],
+                 "peak_source": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this run"}
+                if args.weight_source == "host" else
+                # NEXT-2 tier: the re-streaming copies are device-to-device (a peer B200's HBM over
+                # NVLink in deployment, this GPU here); their rate is not a host-link figure
+                {"source": "device", "achieved_gbs": h2d_gbs, "peak_gbs": copy_peak_run,
+                 "hbm_traffic_gbs": 2 * h2d_gbs if h2d_gbs else None,   # each copied byte is read and written
+                 "frac": (2 * h2d_gbs / copy_peak_run) if h2d_gbs and copy_peak_run else None,
+                 "bytes_per_step": res["h2d_bytes"] / args.steps, "copies": res["h2d_copies"],
+                 "peak_source": "same-GPU D2D copy peak measured in this run (read + write bytes)"}),
         "compare": cmp, "step_ms_median": step_med,
         "steps_ms": [round(x, 3) for x in res["step_ms"]],
         "cpu_baseline": cpu, "clocks": res["clocks"],
