@@ -73,9 +73,12 @@ extern "C" {
                                     * lcm(m, beta)); the re-streaming DMAs are a captured
                                     * branch forked from the slot-free events and joined
                                     * before the graph ends (captured on the second step
-                                    * of a key; ignored with MIRAGE_FLAG_TIME_ATTN,
-                                    * MIRAGE_FLAG_SLOT_TAGS, during reloads and for
-                                    * prefill steps)                                     */
+                                    * of a key; ignored with MIRAGE_FLAG_SLOT_TAGS, during
+                                    * reloads and for prefill steps). Together with
+                                    * MIRAGE_FLAG_TIME_ATTN the graphs are separate timed
+                                    * variants with an event node before and after each
+                                    * attention launch (read after each replay; handoff
+                                    * stalls and copies are timed in eager steps only) */
 #define MIRAGE_FLAG_TP_IPC 16u /* init flag: tensor parallelism without NCCL: after
                                 * mirage_tp_export/import, each partial O-/down-projection
                                 * is summed by one kernel that reads the peers' partials

@@ -224,9 +224,14 @@ struct Model {
   struct Graph {
     cudaGraphExec_t exec;
     int64_t kernels;
+    // timed graphs (MIRAGE_FLAG_CUDA_GRAPHS + MIRAGE_FLAG_TIME_ATTN): event nodes before
+    // and after each layer's attention launch, 2 per layer, read after the replay
+    std::vector<cudaEvent_t> tev;
   };
   std::map<int64_t, Graph> graphs;
   std::set<int64_t> graph_seen;  // keys run once eagerly (plans/autotune done)
+  const Graph* tpend = nullptr;  // the last timed replay whose attention times are not harvested
+  uint64_t tpend_bytes = 0;      // algorithmic bytes of each of its attention launches
   cudaEvent_t join_ev = nullptr; // the copy branch rejoins the compute stream at the end of a capture
   // slot events used inside captures (an event recorded in a capture cannot be
   // waited on outside it, so the eager ready/free events stay separate)
@@ -708,7 +713,26 @@ void harvest_stall_times(Model* M) {
   (void)cudaGetLastError();
 }
 
+// attention times of the last timed graph replay: its event pairs are re-recorded
+// by the next replay of that graph, so a new timed replay harvests (blocking) first
+void harvest_graph_attn(Model* M, bool block) {
+  if (!M->tpend) return;
+  const std::vector<cudaEvent_t>& ev = M->tpend->tev;
+  if (!block && cudaEventQuery(ev.back()) != cudaSuccess) return;
+  cudaEventSynchronize(ev.back());
+  for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+    M->attn_ms += ms;
+    M->attn_bytes += M->tpend_bytes;
+    M->attn_launches += 1;
+  }
+  M->tpend = nullptr;
+  (void)cudaGetLastError();
+}
+
 void harvest_attn_times(Model* M) {
+  harvest_graph_attn(M, false);
   while (!M->attn_pending.empty()) {
     auto& t = M->attn_pending.front();
     if (cudaEventQuery(t.t1) != cudaSuccess) break;
@@ -727,7 +751,11 @@ void harvest_attn_times(Model* M) {
 // The captured graphs of M bake in its weight/slot pointers and copy sources:
 // drop them whenever its cycle or weight source changes.
 void drop_graphs(Model* M) {
-  for (auto& g : M->graphs) cudaGraphExecDestroy(g.second.exec);
+  harvest_graph_attn(M, true);
+  for (auto& g : M->graphs) {
+    cudaGraphExecDestroy(g.second.exec);
+    for (auto e : g.second.tev) cudaEventDestroy(e);
+  }
   M->graphs.clear();
   M->graph_seen.clear();
   for (auto e : M->cap_ready_ev) cudaEventDestroy(e);
@@ -1905,7 +1933,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     // pre-capture waits and, on replays, by the previous graph's joined copy branch)
     const bool prior_copy = use_of[l] - beta < (int64_t)M->uses;
     if (!dbg_nowait && l < s.n && use_of[l] >= beta && use_of[l] >= 0 && !(capturing && prior_copy)) {
-      if (c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) {  // measured stall of this handoff
+      if ((c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) && !capturing) {  // measured stall of this handoff
         Model::AttnTiming t{pool_event(M), pool_event(M), 0};
         CK(c, cudaEventRecord(t.t0, cs));
         CK(c, cudaStreamWaitEvent(cs, M->ready_ev[use_of[l] % beta], 0));
@@ -1958,15 +1986,20 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   // CUDA graph of the step body (embed ... argmax): models without a streaming
   // cycle, one graph per batch size, captured on the second step of that size
   // (the first runs eagerly so cuBLASLt plans/autotuning happen outside capture)
+  // With MIRAGE_FLAG_TIME_ATTN too, the graphs are separate timed variants: an event
+  // node before and after each attention launch (the measurement pass of bench.py)
+  const bool time_attn = c->cfg.flags & MIRAGE_FLAG_TIME_ATTN;
+  uint64_t attn_bytes = 0;
+  for (int i = 0; i < B; ++i) attn_bytes += (uint64_t)hv.len[i] * 2 * Hk * D * 2;
   const bool graphable = (c->cfg.flags & MIRAGE_FLAG_CUDA_GRAPHS) && !reloading && qp == 1 &&
-                         !(c->cfg.flags & MIRAGE_FLAG_TIME_ATTN) && !M->tp_ready && !dbg_nowait &&
-                         prefetch_debug() == 0 && !M->slot_tag;
+                         !M->tp_ready && !dbg_nowait && prefetch_debug() == 0 && !M->slot_tag;
   if (c->tp > 1 && !c->nccl && !M->tp_ready)
     return fail(c, MIRAGE_ERR_STATE, "step: tensor parallel model without a collective (tp_import first)");
   bool body_done = false;
   int64_t l0 = 0;
   const int64_t par_period = m ? (int64_t)std::lcm(m, beta) : 1;
-  const int64_t gkey = (int64_t)B * 64 + (m ? (int64_t)(M->uses % par_period) : 0);
+  const int64_t gkey = ((int64_t)B * 64 + (m ? (int64_t)(M->uses % par_period) : 0)) * 2 + (time_attn ? 1 : 0);
+  std::vector<cudaEvent_t> cap_tev;  // a timed capture's attention event pairs
   if (graphable) {
     auto g = M->graphs.find(gkey);
     if (g != M->graphs.end() || M->graph_seen.count(gkey)) {
@@ -1974,7 +2007,12 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
       for (int sl = 0; sl < beta; ++sl) CK(c, cudaStreamWaitEvent(cs, M->ready_ev[sl], 0));
     }
     if (g != M->graphs.end()) {
+      if (time_attn) harvest_graph_attn(M, true);  // its events are about to be re-recorded
       CK(c, cudaGraphLaunch(g->second.exec, cs));
+      if (time_attn) {
+        M->tpend = &g->second;
+        M->tpend_bytes = attn_bytes;
+      }
       c->launches += g->second.kernels;
       body_done = true;
       // host bookkeeping of the replayed step: the slot log and the copy count
@@ -1992,6 +2030,11 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
         CK(c, cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
         M->cap_ready_ev.push_back(a);
         M->cap_free_ev.push_back(b);
+      }
+      if (time_attn) {
+        harvest_graph_attn(M, true);
+        cap_tev.resize(2 * (size_t)s.n, nullptr);
+        for (auto& e : cap_tev) CK(c, cudaEventCreate(&e));
       }
       CK(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
       capturing = true;
@@ -2034,10 +2077,7 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
   ap.pdl = use_pdl();  // programmatic dependency on qkv_post (which precedes it in the stream)
   ap.kv_evict_first = kv_evict_first();
   ap.prod_lanes = attn_prod_lanes();
-  const bool time_attn = c->cfg.flags & MIRAGE_FLAG_TIME_ATTN;
-  uint64_t attn_bytes = 0;
-  for (int i = 0; i < B; ++i) attn_bytes += (uint64_t)hv.len[i] * 2 * Hk * D * 2;
-  if (time_attn) {
+  if (time_attn && !capturing) {  // (no event queries inside a stream capture)
     harvest_attn_times(M);
     harvest_stall_times(M);
   }
@@ -2048,7 +2088,12 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     KL(c, mirage::launch_qkv_post(s.family, B, H, Hk, D, M->y, opt ? w.b_qkv : nullptr, dv.pos,
                                  dv.seq_off, dv.addrs, layer_off, s.theta, ap.scale_log2, M->q, cs, use_pdl()));
     ap.layer_off = layer_off;
-    if (time_attn) {
+    if (time_attn && capturing) {  // event record nodes of the timed graph (external: they
+      // record at replay time; a plain record inside a capture is only a dependency marker)
+      CK(c, cudaEventRecordWithFlags(cap_tev[2 * l], cs, cudaEventRecordExternal));
+      KL(c, mirage::launch_paged_attention(ap, cs));
+      CK(c, cudaEventRecordWithFlags(cap_tev[2 * l + 1], cs, cudaEventRecordExternal));
+    } else if (time_attn) {
       Model::AttnTiming at{pool_event(M), pool_event(M), attn_bytes};
       CK(c, cudaEventRecord(at.t0, cs));
       KL(c, mirage::launch_paged_attention(ap, cs));
@@ -2160,8 +2205,12 @@ int32_t mirage_decode_step(mirage_ctx* c, int32_t model, int32_t B, const int64_
     cudaGraphExec_t exec;
     CK(c, cudaGraphInstantiate(&exec, graph, 0));
     cudaGraphDestroy(graph);
-    M->graphs[gkey] = Model::Graph{exec, c->launches - l0};
+    M->graphs[gkey] = Model::Graph{exec, c->launches - l0, cap_tev};
     CK(c, cudaGraphLaunch(exec, cs));
+    if (time_attn) {
+      M->tpend = &M->graphs[gkey];
+      M->tpend_bytes = attn_bytes;
+    }
   }
   }  // !body_done
   if (hidden_out)

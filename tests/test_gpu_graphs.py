@@ -138,3 +138,42 @@ def test_set_flags_switches_graphs_and_timing_mid_run():
     assert timed[9] == 0 and timed[19] > 0 and timed[29] == timed[25]   # events only in the eager pass
     with pytest.raises(_lib.MirageError):
         ctx.set_flags(0, _lib.FLAG_POISON)                                # not a measurement flag
+
+
+def test_timed_graphs_bit_identical_and_count_every_attention_launch():
+    """bench.py's timed-graph pass: with FLAG_CUDA_GRAPHS and FLAG_TIME_ATTN both set
+    the step runs as separate graphs that carry an event node before and after each
+    attention launch. Every step stays bit-identical to an all-eager run (same slot
+    log), and each replay adds one timed launch per layer with that step's
+    algorithmic bytes; the untimed graphs keep running without events afterwards."""
+    from paper_2507_11507_b200 import Context, _lib
+    shape = models.TOY_LLAMA.with_layers(4)
+    cycle, beta, B, steps = [0, 1, 3], 2, 4, 36
+    ref, ref_log, _ = run_cycle(0, shape, cycle, beta, steps)
+    ctx = Context(harness.arena_for([(shape, 64)], 8, 256), 8, 256, flags=_lib.FLAG_CUDA_GRAPHS)
+    mid = ctx.add_model(shape, harness.make_blob(shape, seed=4), B)
+    ctx.remap_layers(mid, mid, cycle, beta)
+    hid = torch.empty((B, shape.d_model), dtype=torch.bfloat16, device="cuda")
+    both = _lib.FLAG_TIME_ATTN | _lib.FLAG_CUDA_GRAPHS
+    q = []
+    for t in range(steps):
+        if t == 10:
+            ctx.set_flags(both, both)                      # timed graphs
+        if t == 26:
+            ctx.set_flags(_lib.FLAG_CUDA_GRAPHS, both)     # plain graphs again
+        if t % 16 == 0:
+            for s in range(B):
+                ctx.alloc_blocks(mid, s, 1)
+        am = ctx.decode_step(mid, list(range(B)), [workload.teacher_tokens(s, t, shape.vocab) for s in range(B)],
+                             [t] * B, hidden_out=hid)
+        ctx.sync()
+        assert np.array_equal(hid.float().cpu().numpy(), ref[t][0]) and list(am) == ref[t][1], t
+        st = ctx.query(mid)
+        q.append((st["attn_launches"], st["attn_bytes"], st["attn_ms"]))
+    assert ctx.slot_log(mid) == ref_log
+    assert q[9][0] == 0
+    for t in range(10, 26):                               # eager, capture or replay: one per layer
+        assert q[t][0] - q[t - 1][0] == shape.n_layers, t
+        assert q[t][1] - q[t - 1][1] == shape.n_layers * B * (t + 1) * 2 * shape.n_kv_heads * shape.head_dim * 2, t
+        assert q[t][2] > q[t - 1][2], t
+    assert q[35] == q[26]                                 # no events in the plain graphs
