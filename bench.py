@@ -545,8 +545,9 @@ def run_arm(args, torch, dev, tenants, remaps, ctxs, max_ctx, blobs, steps, warm
     between kernels, programmatic dependent launch intact); then, if `measure`,
     the same context switches to eager steps with CUDA events around every
     attention launch, slot handoff and copy (MIRAGE_FLAG_TIME_ATTN) and times
-    `steps` more steps: the roofline, H2D and handoff figures come from that
-    measurement pass."""
+    `steps` more steps (the H2D and handoff figures and roofline.eager_pass),
+    then to timed CUDA graphs (an event node before and after every attention
+    launch) for `steps` more steps: roofline.achieved comes from that pass."""
     import ctypes as C
     import harness
     from paper_2507_11507_b200 import _lib
